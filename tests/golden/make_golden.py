@@ -1,0 +1,213 @@
+"""Generate golden vectors by running the UNMODIFIED reference (mgsmooth 0.1.0).
+
+Run in the build container only (the reference does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Outputs (committed, small):
+    net_conv.json, net_fc.json   seeded small-problem training runs:
+        train_inference_net(A31, variant, 4, TrainConfig(samples=10, max_steps=2,
+        batch_size=5, epochs=20, seed=0), k=1, seed_net=0), A31 = rotated FD
+        31x31, theta=pi/6, anisotropy=0.01; saved with smoothers.save_model.
+    net_conv_k2.json             fresh inference_net('conv', k=2, seed=5) with a
+        seeded random final layer (exercises the k>1 leaky-stage path).
+    ops.npz                      apply_stencil / restrict / prolong / galerkin /
+        coarse LU on random per-point stencils, square / lshape / cylinder masks.
+    case_<name>.npz              full hierarchies: per-level A, per-level K
+        (small cases), f, residual history, u after N cycles.
+    c1.npz                       config 1 (255^2, V(2,2), 20 cycles) history + u.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+import mgsmooth as mg                                     # noqa: E402  (reference)
+from mgsmooth import grid as rg, transfer as rt, hierarchy as rh, smoothers as rs  # noqa: E402
+from mgsmooth import problems as rp, dense as rd, training as rtr              # noqa: E402
+from mgsmooth.cli import RepeatedSmoother                  # noqa: E402
+
+from paper_2102_12071_b200 import problems as gen          # noqa: E402  (input generators only)
+
+
+def spec_of(mask, h):
+    return rg.GridSpec(mask.shape[0], mask.shape[1], h, mask)
+
+
+def make_nets():
+    out = {}
+    A31 = rp.assemble_rotated_laplacian(rg.full_spec(31), math.pi / 6, 0.01)
+    for variant in ("conv", "fc"):
+        path = os.path.join(HERE, f"net_{variant}.json")
+        if os.path.exists(path):
+            out[variant] = rs.load_model(path)
+            continue
+        t0 = time.time()
+        cfg = rtr.TrainConfig(samples=10, max_steps=2, batch_size=5, epochs=20, seed=0)
+        net, _, _ = rtr.train_inference_net(A31, variant, 4, cfg, k=1, seed_net=0)
+        rs.save_model(path, net, {"fixture": "SURVEY G4", "operator": "rotated FD 31x31 pi/6 0.01"})
+        print(f"trained {variant} net in {time.time() - t0:.1f}s")
+        out[variant] = rs.load_model(path)
+    path = os.path.join(HERE, "net_conv_k2.json")
+    if not os.path.exists(path):
+        net = rs.inference_net("conv", k=2, seed=5)
+        rng = np.random.default_rng(6)
+        net.weights[-1] = rng.standard_normal(net.weights[-1].shape) * 0.05
+        rs.save_model(path, net, {"fixture": "random k=2 conv net, seed 5/6"})
+    out["conv_k2"] = rs.load_model(path)
+    return out
+
+
+def make_ops():
+    rng = np.random.default_rng(20240817)
+    d = {}
+    for geom in ("square", "lshape", "cylinder"):
+        for n in (9, 10):
+            mask = gen.geometry_mask(geom, n) if n == 9 else np.ones((n, n + 3), bool)
+            if n == 10 and geom != "square":
+                continue
+            h = 1.0 / (n + 1)
+            spec = spec_of(mask, h)
+            A = rng.standard_normal(mask.shape + (3, 3))
+            A[:, :, 1, 1] += 8.0
+            u = np.where(mask, rng.standard_normal(mask.shape), 0.0)
+            S = rg.StencilField(spec, A)
+            U = rg.GridFunction(spec, u)
+            key = f"{geom}{n}"
+            d[f"{key}_mask"] = mask
+            d[f"{key}_A"] = A
+            d[f"{key}_u"] = u
+            d[f"{key}_Au"] = rg.apply_stencil(S, U).values
+            tp = rt.coarsen_full(spec)
+            d[f"{key}_rc"] = rt.restrict(tp, U).values
+            ec = np.where(tp.coarse.mask, rng.standard_normal(tp.coarse.mask.shape), 0.0)
+            d[f"{key}_ec"] = ec
+            d[f"{key}_Pe"] = rt.prolong(tp, rg.GridFunction(tp.coarse, ec)).values
+            Ac = rt.galerkin_product(S, tp)
+            d[f"{key}_Ac"] = Ac.data
+            d[f"{key}_maskc"] = tp.coarse.mask
+            lu, perm = rd.lu_factor(rg.materialize_stencil(Ac))
+            d[f"{key}_lu"] = lu
+            d[f"{key}_perm"] = perm
+            b = rng.standard_normal(tp.coarse.n_active)
+            d[f"{key}_lub"] = b
+            d[f"{key}_lux"] = rd.lu_solve(lu, perm, b)
+    np.savez_compressed(os.path.join(HERE, "ops.npz"), **d)
+
+
+def run_case(name, A, mask, levels, smoother, nu, cycles, f, h, store_levels=True):
+    """Reference hierarchy + fixed-count V(nu, nu) cycle loop."""
+    spec = spec_of(mask, h)
+    S = rg.StencilField(spec, A)
+    hier = rh.build_hierarchy(S, levels)
+    if smoother == "jacobi":
+        rh.equip_classical(hier, "jacobi")
+    else:
+        rh.equip_inferred(hier, smoother)
+    if nu > 1:
+        for lev in hier.levels[:-1]:
+            lev.smoother = RepeatedSmoother(lev.smoother, lev.operator, nu)
+    F = rg.GridFunction(spec, f)
+    u = rg.zeros(spec)
+    denom = F.norm() if F.norm() > 0 else 1.0
+    hist = [(F - rg.apply_stencil(S, u)).norm() / denom]
+    for _ in range(cycles):
+        u = rh.v_cycle(hier, 0, F, u)
+        hist.append((F - rg.apply_stencil(S, u)).norm() / denom)
+    d = {"u": u.values, "history": np.array(hist),
+         "levels": levels, "nu": nu, "cycles": cycles, "h": h}
+    if store_levels:                       # large cases regenerate A0 / f from their seeds
+        d.update({"A0": A, "mask": mask, "f": F.values})
+    if store_levels:
+        for l, lev in enumerate(hier.levels):
+            d[f"A{l}"] = lev.operator.data
+            d[f"mask{l}"] = lev.spec.mask
+            sm = lev.smoother
+            if sm is not None:
+                inner = sm.inner if isinstance(sm, RepeatedSmoother) else sm
+                if isinstance(inner, rs.InferredSmoother):
+                    d[f"K{l}"] = inner.kernels
+        d["coarse_lu"] = hier.coarse_lu
+        d["coarse_perm"] = hier.coarse_perm
+    else:
+        for l, lev in enumerate(hier.levels):
+            d[f"Asum{l}"] = np.array([lev.operator.data.sum(), np.abs(lev.operator.data).sum()])
+            sm = lev.smoother
+            if sm is not None:
+                inner = sm.inner if isinstance(sm, RepeatedSmoother) else sm
+                if isinstance(inner, rs.InferredSmoother):
+                    K = inner.kernels
+                    d[f"Ksum{l}"] = np.array([K.sum(), np.abs(K).sum()])
+                    d[f"Kmid{l}"] = K[K.shape[0] // 2, K.shape[1] // 2]
+                    d[f"Kcorner{l}"] = K[0, 0]
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+    print(f"{name}: hist[-1]={hist[-1]:.3e}")
+
+
+def make_problem_pins():
+    """Reference assembly tables that pin the host-side generators."""
+    d = {}
+    for i, (n, th, ep) in enumerate([(7, math.pi / 6, 100.0), (255, math.pi / 6, 0.01),
+                                      (4095, math.pi / 4, 1e-3), (511, 1.234, 0.05)]):
+        S = rp.assemble_rotated_laplacian(rg.full_spec(n), th, ep)
+        d[f"rot{i}"] = S.data[0, 0]
+        d[f"rot{i}_params"] = np.array([n, th, ep])
+    np.savez_compressed(os.path.join(HERE, "problems.npz"), **d)
+
+
+def main():
+    make_problem_pins()
+    nets = make_nets()
+    make_ops()
+    # small structural cases (all-level A and K stored)
+    n = 15
+    A = gen.rotated_fd(n, math.pi / 6, 0.01)
+    f = gen.uniform_rhs(n, 0)
+    run_case("case_rot15_conv_v22", A, np.ones((n, n), bool), 3, nets["conv"], 2, 10, f, 1 / (n + 1))
+    run_case("case_rot15_jacobi_v11", A, np.ones((n, n), bool), 3, "jacobi", 1, 10, f, 1 / (n + 1))
+    run_case("case_rot15_convk2_v11", A, np.ones((n, n), bool), 3, nets["conv_k2"], 1, 6, f, 1 / (n + 1))
+    n = 31
+    A = gen.rotated_fd(n, math.pi / 4, 0.001)
+    f = gen.uniform_rhs(n, 1)
+    run_case("case_rot31_fc_v22", A, np.ones((n, n), bool), 4, nets["fc"], 2, 8, f, 1 / (n + 1))
+    mask = gen.geometry_mask("lshape", n)
+    fm = np.where(mask, f, 0.0)
+    run_case("case_lshape31_conv_v11", A, mask, 4, nets["conv"], 1, 8, fm, 1 / (n + 1))
+    mask = gen.geometry_mask("cylinder", n)
+    fm = np.where(mask, f, 0.0)
+    run_case("case_cyl31_fc_v11", A, mask, 3, nets["fc"], 1, 6, fm, 1 / (n + 1))
+    # variable coefficient (reference bilinear-FE assembly) and config-3 style 5-point GRF
+    spec = rg.full_spec(31)
+    Av = rp.assemble_variable_diffusion(spec, 10.0).data
+    run_case("case_var31_conv_v22", Av, np.ones((31, 31), bool), 4, nets["conv"], 2, 8, gen.uniform_rhs(31, 2), spec.spacing)
+    Ag = gen.grf_diffusion_5pt(63, seed=2)
+    run_case("case_grf63_conv_v22", Ag, np.ones((63, 63), bool), 5, nets["conv"], 2, 8, gen.uniform_rhs(63, 2), 1 / 63)
+    # non-square + even sizes
+    Ar = gen.rotated_fd(20, math.pi / 3, 0.01, cols=27)
+    run_case("case_rect20x27_conv_v11", Ar, np.ones((20, 27), bool), 3, nets["conv"], 1, 6,
+             gen.uniform_rhs(20, 3, cols=27), 1 / 21)
+    # config 1: 255^2 rotated FD eps=0.01 theta=pi/6, V(2,2), 20 cycles, conv net
+    n = 255
+    run_case("c1_fd_conv", gen.rotated_fd(n, math.pi / 6, 0.01), np.ones((n, n), bool), 7, nets["conv"], 2, 20,
+             gen.uniform_rhs(n, 0), 1 / (n + 1), store_levels=False)
+    run_case("c1_q1_conv", gen.rotated_q1(n, math.pi / 6, 0.01), np.ones((n, n), bool), 7, nets["conv"], 2, 20,
+             gen.uniform_rhs(n, 0), 1 / (n + 1), store_levels=False)
+    # config 4 sample: first two problems of the batch, 511^2, V(1,1), 10 cycles
+    eps, theta = gen.batch_parameters(256, seed=3)
+    n = 511
+    for i in range(2):
+        run_case(f"c4_p{i}", gen.rotated_fd(n, theta[i], eps[i]), np.ones((n, n), bool), 8, nets["conv"], 1, 10,
+                 gen.uniform_rhs(n, [4, i]), 1 / (n + 1), store_levels=False)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,111 @@
+"""Pin the CPU oracle (oracle/mg_oracle.py) to golden vectors produced by the
+unmodified reference (tests/golden/make_golden.py).  CPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import mg_oracle as mo
+from paper_2102_12071_b200 import problems as gen
+
+from cases import LARGE, SMALL, load
+from conftest import golden, rel_err
+
+KEYS = ["square9", "lshape9", "cylinder9", "square10"]
+
+
+@pytest.mark.parametrize("key", KEYS)
+def test_apply_stencil_bit_exact(ops_golden, key):
+    g = ops_golden
+    out = mo.apply_stencil(g[f"{key}_A"], g[f"{key}_u"], g[f"{key}_mask"])
+    assert np.array_equal(out, g[f"{key}_Au"])
+
+
+@pytest.mark.parametrize("key", KEYS)
+def test_restrict_prolong_bit_exact(ops_golden, key):
+    g = ops_golden
+    mask, mc = g[f"{key}_mask"], g[f"{key}_maskc"]
+    assert np.array_equal(mo.coarse_mask(mask), mc)
+    assert np.array_equal(mo.restrict(g[f"{key}_u"], mc), g[f"{key}_rc"])
+    assert np.array_equal(mo.prolong(g[f"{key}_ec"], mask.shape, mask), g[f"{key}_Pe"])
+
+
+@pytest.mark.parametrize("key", KEYS)
+def test_galerkin_bit_exact(ops_golden, key):
+    g = ops_golden
+    Ac = mo.galerkin(g[f"{key}_A"], g[f"{key}_mask"], g[f"{key}_maskc"])
+    assert np.array_equal(Ac, g[f"{key}_Ac"])
+
+
+@pytest.mark.parametrize("key", KEYS)
+def test_lu(ops_golden, key):
+    g = ops_golden
+    M = mo.materialize(g[f"{key}_Ac"], g[f"{key}_maskc"])
+    lu, perm = mo.lu_factor(M)
+    assert np.array_equal(perm, g[f"{key}_perm"])
+    assert rel_err(lu, g[f"{key}_lu"]) < 1e-14
+    assert rel_err(mo.lu_solve(lu, perm, g[f"{key}_lub"]), g[f"{key}_lux"]) < 1e-13
+
+
+def test_lu_singular_raises():
+    M = np.array([[1.0, 2.0], [2.0, 4.0]])
+    with pytest.raises(mo.OracleError) as ei:
+        mo.lu_factor(M)
+    assert ei.value.kind == "SingularMatrixError" and ei.value.pivot_index == 1
+
+
+def test_problem_generators_match_reference_assembly():
+    g = golden("problems.npz")
+    for i in range(4):
+        n, th, ep = g[f"rot{i}_params"]
+        A = gen.rotated_fd(int(n), th, ep)
+        assert np.array_equal(A[0, 0], g[f"rot{i}"])
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_hierarchy_and_kernels(name, nets):
+    c = load(name)
+    g = c["golden"]
+    h = mo.build_hierarchy(c["A0"], c["levels"], c["mask"])
+    for l in range(h.depth):
+        assert np.array_equal(h.masks[l], g[f"mask{l}"])
+        assert h.ops[l].shape == g[f"A{l}"].shape
+        assert rel_err(h.ops[l], g[f"A{l}"]) <= 1e-15
+    assert np.array_equal(h.perm, g["coarse_perm"])
+    if c["smoother"] == "jacobi":
+        mo.equip_jacobi(h)
+    else:
+        mo.equip_inferred(h, nets[c["smoother"]])
+        for l in range(h.depth - 1):
+            assert rel_err(h.kernels[l], g[f"K{l}"]) < 1e-13
+    u, hist = mo.run_cycles(h, c["f"], c["cycles"], c["nu"], c["nu"])
+    gh = g["history"]
+    assert np.all(np.abs(hist - gh) <= 1e-12 * np.abs(gh) + 1e-300)
+    assert rel_err(u, g["u"]) < 1e-11
+
+
+def test_v_cycle_nu1_equals_reference_v_cycle(nets):
+    """solve() with V(1,1) reproduces the golden V(1,1) history prefix."""
+    c = load("case_rot15_jacobi_v11")
+    h = mo.equip_jacobi(mo.build_hierarchy(c["A0"], c["levels"], c["mask"]))
+    u, hist, it, conv = mo.solve(h, c["f"], tol=1e-30, max_iter=4, raise_on_divergence=False)
+    assert it == 4 and not conv
+    assert np.allclose(hist, c["golden"]["history"][:5], rtol=1e-12, atol=0)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1_fd_conv", "c1_q1_conv"])
+def test_config1_history(name, nets):
+    c = load(name)
+    g = c["golden"]
+    h = mo.equip_inferred(mo.build_hierarchy(c["A0"], c["levels"]), nets["conv"])
+    for l in range(h.depth):
+        assert rel_err(g[f"Asum{l}"], [h.ops[l].sum(), np.abs(h.ops[l]).sum()]) < 1e-12
+    for l in range(h.depth - 1):
+        K = h.kernels[l]
+        assert rel_err(K[K.shape[0] // 2, K.shape[1] // 2], g[f"Kmid{l}"]) < 1e-13
+        assert rel_err(K[0, 0], g[f"Kcorner{l}"]) < 1e-13
+    u, hist = mo.run_cycles(h, c["f"], c["cycles"], c["nu"], c["nu"])
+    assert np.all(np.abs(hist - g["history"]) <= 1e-10 * np.abs(g["history"]))
+    assert rel_err(u, g["u"]) < 1e-10
