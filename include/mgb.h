@@ -1,0 +1,202 @@
+/*
+ * mgb.h — C-ABI of the B200-native learned-smoother multigrid hot path.
+ *
+ * Drop-in boundary for the reference's Python solver API (mgsmooth 0.1.0,
+ * /root/reference/pkg/src/mgsmooth).  The reference has no FFI; its "plugin"
+ * surface is the Python module API re-exported by __init__.py:9-35 plus the
+ * duck-typed smoother protocol obj.apply(r) (hierarchy.py:107,111).  Each
+ * entry point below names the reference function it replaces.  The Python
+ * facade paper_2102_12071_b200/ binds these through ctypes.
+ *
+ * Conventions
+ *  - All fp64.  Grid arrays are dense row-major (rows, cols) with i = row = y,
+ *    j = col = x (grid.py:3-13).  Batched calls stack `batch` problems of the
+ *    same shape contiguously: (batch, rows, cols).
+ *  - Stencil tables in the reference layout ("AoS"): (rows, cols, 3, 3), entry
+ *    [di+1][dj+1] multiplies u(i+di, j+dj) (cross-correlation, zero outside).
+ *    Smoother kernels: (rows, cols, k, 3, 3) (smoothers.py:291-300).
+ *  - Masks are uint8 (rows, cols), 1 = active; NULL means every point active.
+ *  - Pointers documented "dev" are CUDA device pointers; "host" are host
+ *    pointers.  `stream` is a cudaStream_t passed as void* (NULL = legacy).
+ *  - Every function returns an mgb_status.  Non-zero statuses map onto the
+ *    reference's exception classes (errors.py:8-42); the message is available
+ *    from mgb_last_error() (thread-local), and for MGB_SINGULAR the failing
+ *    elimination step from mgb_last_pivot() (dense.py:38-40).
+ *  - Compute functions never fall back to the CPU.  Without a usable sm_100
+ *    device they return MGB_CUDA.
+ */
+#ifndef MGB_H
+#define MGB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  MGB_OK = 0,
+  MGB_CONFIG = 1,       /* ConfigError            errors.py:16 */
+  MGB_NUMERIC = 2,      /* NumericError           errors.py:20 */
+  MGB_NONCONVERGED = 3, /* NonConvergedError      errors.py:40 */
+  MGB_CONTRACT = 4,     /* ContractError          errors.py:12 */
+  MGB_SINGULAR = 5,     /* SingularMatrixError    errors.py:24 */
+  MGB_CUDA = 6,         /* RuntimeError (CUDA failure / no device) */
+  MGB_NCCL = 7          /* RuntimeError (collective failure) */
+} mgb_status;
+
+enum { MGB_NET_CONV = 0, MGB_NET_FC = 1 };          /* smoothers.py:213-214 */
+
+typedef struct mgb_hier mgb_hier;   /* device MultigridHierarchy (hierarchy.py:38) */
+typedef struct mgb_work mgb_work;   /* per-solve workspace: concurrent solves on one hierarchy are safe */
+
+/* ---- library / errors ---------------------------------------------------- */
+int         mgb_version(void);
+const char* mgb_last_error(void);
+int         mgb_last_pivot(void);
+int         mgb_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- stateless grid ops on reference layouts (device pointers) ----------- */
+
+/* grid.apply_stencil (grid.py:216-226): out = A u, zero outside, masked. k odd (1 or 3). */
+int mgb_apply_stencil(int batch, int rows, int cols, int k, const double* A_dev,
+                      const uint8_t* mask_dev, const double* u_dev, double* out_dev, void* stream);
+
+/* transfer.restrict for full coarsening (transfer.py:108-121, coarsen_full :50-61):
+   coarse = FW/16 gather about fine anchor 2c+1; coarse shape (rows/2, cols/2);
+   mask_c_dev is the COARSE mask (= fine mask[1::2,1::2]). */
+int mgb_restrict(int batch, int rows, int cols, const uint8_t* mask_c_dev,
+                 const double* fine_dev, double* coarse_dev, void* stream);
+
+/* transfer.prolong (transfer.py:124-147): fine = (2 FW/16) scatter of coarse; masked by the fine mask. */
+int mgb_prolong(int batch, int rows, int cols, const uint8_t* mask_f_dev,
+                const double* coarse_dev, double* fine_dev, void* stream);
+
+/* transfer.galerkin_product (transfer.py:150-209) for full coarsening and k = 3 or 1 fine
+   stencils: Ac (rows/2, cols/2, 3, 3) = R A P per coarse point; masks may be NULL.
+   *k_out receives the trimmed stencil size (_trim, transfer.py:212-222): 3, or 1 when
+   the outer ring is zero everywhere. */
+int mgb_galerkin_product(int batch, int rows, int cols, int k, const double* A_dev,
+                         const uint8_t* mask_f_dev, const uint8_t* mask_c_dev,
+                         double* Ac_dev, int* k_out, void* stream);
+
+/* smoothers.inferred_apply (smoothers.py:325-343): out = M(r), kernels (rows, cols, kst, 3, 3),
+   leaky(slope) between stages. */
+int mgb_smoother_apply(int batch, int rows, int cols, int kst, const double* K_dev,
+                       const uint8_t* mask_dev, double slope, const double* r_dev,
+                       double* out_dev, void* stream);
+
+/* smoothers.infer_kernels (smoothers.py:302-322, net_forward :273-288, features :184-210):
+   K_dev (rows, cols, kst, 3, 3) from A_dev (rows, cols, 3, 3).  weights_host is the
+   concatenation of the net's weight arrays in row-major order (conv: (7,3,3),(5,3,3),
+   (3,3,3),(27,9k); fc: (81,40),(40,40),(40,40),(40,9k)).  precision 64 = fp64 network
+   (parity), 32 = fp32 network with fp64 diagonal normalisation. */
+int mgb_infer_kernels(int batch, int rows, int cols, const double* A_dev, const uint8_t* mask_dev,
+                      int variant, int kst, const double* weights_host, int64_t n_weights,
+                      double slope, int precision, double* K_dev, void* stream);
+
+/* dense.lu_factor / lu_solve (dense.py:21-63) on the device, n <= 4096.
+   lu_dev (n, n) row-major is overwritten in place; perm_dev (n) int32. */
+int mgb_lu_factor(int n, double* lu_dev, int32_t* perm_dev, void* stream);
+int mgb_lu_solve(int n, const double* lu_dev, const int32_t* perm_dev, const double* b_dev,
+                 double* x_dev, void* stream);
+
+/* ---- hierarchy (hierarchy.py:70-214) -------------------------------------- */
+
+/* build_hierarchy (hierarchy.py:70-88): Galerkin chain on the device, materialise and
+   LU-factor the coarsest operator.  A0 is (batch, rows, cols, 3, 3) in the reference
+   layout, on the host (a0_on_device = 0) or the device (1).  mask_host may be NULL
+   (all active); it is shared by the batch.  The hierarchy lives on `device`. */
+int mgb_hier_build(int device, int batch, int rows, int cols, double spacing,
+                   const double* A0, int a0_on_device, const uint8_t* mask_host,
+                   int levels, void* stream, mgb_hier** out);
+void mgb_hier_destroy(mgb_hier* h);
+int mgb_hier_depth(const mgb_hier* h, int* depth, int* batch);
+/* level geometry; k = trimmed operator size; ks = installed smoother stages (0 = none) */
+int mgb_hier_level_info(const mgb_hier* h, int level, int* rows, int* cols, int* k, int* ks,
+                        double* spacing);
+/* copy level operator / smoother kernels / mask out (host pointers, reference layouts;
+   the operator is written as (batch, rows, cols, k, k) with the trimmed k). */
+int mgb_hier_get_operator(const mgb_hier* h, int level, double* out_host);
+int mgb_hier_get_kernels(const mgb_hier* h, int level, double* out_host);
+int mgb_hier_get_mask(const mgb_hier* h, int level, uint8_t* out_host);
+/* device pointer to the level operator in the internal layout (9 planes of
+   batch*rows*cols each, plane o = (di+1)*3 + (dj+1)). */
+int mgb_hier_operator_planes(const mgb_hier* h, int level, const double** planes_dev);
+
+/* equip_inferred (hierarchy.py:207-214): per-level CNN inference on levels 0..L-2. */
+int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const double* weights_host,
+                            int64_t n_weights, double slope, int precision, void* stream);
+/* equip_classical(kind="jacobi") (hierarchy.py:152-161, smoothers.py:29-50). */
+int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream);
+/* install explicit kernels on one level: (batch, rows, cols, kst, 3, 3) host or device. */
+int mgb_hier_set_kernels(mgb_hier* h, int level, int kst, const double* K, int on_device,
+                         double slope, void* stream);
+
+/* coarse_solve (hierarchy.py:91-93): x = A_L^{-1} f on the coarsest level (device). */
+int mgb_coarse_solve(const mgb_hier* h, const double* f_dev, double* x_dev, void* stream);
+
+/* ---- per-level fused passes on a hierarchy (device pointers, dense layout) ---- */
+/* r = f - A_l u (masked); optionally (norm2_dev != NULL) per-problem sum of squares. */
+int mgb_residual(const mgb_hier* h, int level, const double* f_dev, const double* u_dev,
+                 double* r_dev, double* norm2_dev, void* stream);
+/* u <- u + M(f - A u), `sweeps` times (u in/out; uses the workspace). */
+int mgb_smooth(const mgb_hier* h, mgb_work* w, int level, const double* f_dev, double* u_dev,
+               int sweeps, void* stream);
+/* rc = R (f - A_l u) on level l -> l+1 (fused residual + full weighting). */
+int mgb_restrict_residual(const mgb_hier* h, int level, const double* f_dev, const double* u_dev,
+                          double* rc_dev, void* stream);
+/* u <- u + P ec on level l (fused prolongation + coarse-grid correction). */
+int mgb_prolong_correct(const mgb_hier* h, int level, const double* ec_dev, double* u_dev,
+                        void* stream);
+
+/* ---- cycles and solve ------------------------------------------------------ */
+int  mgb_work_create(const mgb_hier* h, mgb_work** out);
+void mgb_work_destroy(mgb_work* w);
+
+/* v_cycle (hierarchy.py:96-111) from level `level`, V(nu1, nu2) (RepeatedSmoother,
+   cli.py:365-377); u_dev in/out. */
+int mgb_vcycle(const mgb_hier* h, mgb_work* w, int level, const double* f_dev, double* u_dev,
+               int nu1, int nu2, void* stream);
+
+/* Fixed-count cycle loop with the per-cycle residual history kept on the device:
+   history_dev (batch, cycles + 1) receives ||f - A u_i|| / ||f|| (0 if ||f|| = 0 uses
+   denominator 1, hierarchy.py:125-133).  No host synchronisation; the launch sequence
+   is replayed from a CUDA graph after the first call with the same arguments.
+   u_zero != 0 starts from u = 0 without reading u_dev. */
+int mgb_run_cycles(const mgb_hier* h, mgb_work* w, const double* f_dev, double* u_dev,
+                   int nu1, int nu2, int cycles, int u_zero, double* history_dev, void* stream);
+
+/* Host-buffer variant of mgb_run_cycles (the drop-in call for callers holding host
+   arrays): copies f (and u unless u_zero) host->device, runs the graph-replayed cycle
+   loop, copies u and the history device->host and synchronises `stream`.  Pinned host
+   memory gives asynchronous full-bandwidth copies; pageable memory also works. */
+int mgb_run_cycles_host(const mgb_hier* h, mgb_work* w, const double* f_host, double* u_host,
+                        int nu1, int nu2, int cycles, int u_zero, double* history_host,
+                        void* stream);
+
+/* solve (hierarchy.py:119-146) for batch == 1: loop until history < tol or max_iter,
+   NonConvergedError (MGB_NONCONVERGED) when rr is non-finite or > 1e6 max(r0, tol).
+   history_host has room for max_iter + 1 entries; *n_history receives its length. */
+int mgb_solve(const mgb_hier* h, mgb_work* w, const double* f_dev, double* u_dev,
+              int nu1, int nu2, double tol, int max_iter, double* history_host,
+              int* n_history, int* iterations, int* converged, double* loop_seconds,
+              void* stream);
+
+/* instrumentation for bench.py: number of kernel launches issued by the last
+   mgb_run_cycles / mgb_vcycle call (graph replays count their nodes). */
+int64_t mgb_last_launch_count(const mgb_work* w);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGB_H */

@@ -1,0 +1,22 @@
+"""B200-native learned-smoother multigrid (hot path of arXiv 2102.12071).
+
+Drop-in facade for the reference package's solver API (mgsmooth 0.1.0,
+__init__.py:9-35) restricted to the hot path: grids and stencil fields, full
+coarsening transfers and Galerkin products, the stencil -> smoother CNN, the
+per-point smoother, the V-cycle and the solve loop.  Everything numeric runs
+in hand-written sm_100a CUDA kernels behind the C-ABI in include/mgb.h
+(libmgb.so, built by ``python -m paper_2102_12071_b200.build``).
+"""
+
+from .errors import (ConfigError, ContractError, MgError, NonConvergedError, NumericError,
+                     SingularMatrixError, TrainingError, UnsupportedOperationError)
+from .grid import (GridFunction, GridSpec, StencilField, apply_stencil, constant_stencil, from_active,
+                   full_spec, to_active, zeros)
+from .transfer import TransferPair, coarsen_full, galerkin_product, prolong, restrict
+from .smoothers import (InferredSmoother, JacobiSmoother, KernelInferenceNet, infer_kernels, inference_net,
+                        jacobi, load_model, save_model)
+from .hierarchy import (Level, MultigridHierarchy, RepeatedSmoother, SolveReport, build_hierarchy,
+                        build_hierarchy_batch, coarse_solve, cycle_correction, equip_classical,
+                        equip_inferred, solve, v_cycle)
+
+__version__ = "0.1.0"

@@ -1,0 +1,974 @@
+// C-ABI (include/mgb.h): hierarchy objects, workspaces, cycle driver, CUDA graphs.
+//
+// Reference map: hierarchy.py build_hierarchy :70-88, coarse_solve :91-93,
+// v_cycle :96-111, solve :119-146, equip_classical :152-161, equip_inferred
+// :207-214; cli.py RepeatedSmoother :365-377 (V(nu1, nu2)); errors.py.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mgb_internal.h"
+
+namespace mgb {
+
+static thread_local std::string g_err;
+static thread_local int g_pivot = -1;
+
+void set_error(int status, const std::string& msg, int pivot) {
+  (void)status;
+  g_err = msg;
+  g_pivot = pivot;
+}
+int fail(int status, const std::string& msg) {
+  set_error(status, msg);
+  return status;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what;
+  return MGB_CUDA;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return cudaSuccess;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+template <typename T>
+static void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+}  // namespace mgb
+
+using namespace mgb;
+
+// ---------------------------------------------------------------------------
+// objects
+
+struct LevelD {
+  int rows = 0, cols = 0, k = 3, ks = 0;
+  double h = 0.0;
+  int64_t n = 0;
+  double* A = nullptr;     // batch x 9 planes of n
+  double* K = nullptr;     // batch x ks x 9 planes of n
+  uint8_t* mask = nullptr; // null = all active
+  std::vector<uint8_t> hmask;
+  int64_t nact = 0;
+};
+
+struct mgb_hier {
+  int device = 0, batch = 1;
+  std::vector<LevelD> lv;
+  int nc = 0;               // active unknowns on the coarsest level
+  double* lu = nullptr;     // batch x nc x nc
+  int32_t* perm = nullptr;  // batch x nc
+  int32_t* actp = nullptr;  // nc flat indices of active coarsest points
+  double slope = 0.01;
+  ~mgb_hier() {
+    DeviceGuard dg(device);
+    for (auto& l : lv) {
+      dfree(l.A);
+      dfree(l.K);
+      dfree(l.mask);
+    }
+    dfree(lu);
+    dfree(perm);
+    dfree(actp);
+  }
+  Grid grid(int l) const { return Grid{batch, lv[l].rows, lv[l].cols}; }
+  int depth() const { return (int)lv.size(); }
+};
+
+struct GraphKey {
+  const double* f;
+  double* u;
+  int nu1, nu2, cycles, u_zero, mode;
+  double* hist;
+  bool operator==(const GraphKey& o) const {
+    return f == o.f && u == o.u && nu1 == o.nu1 && nu2 == o.nu2 && cycles == o.cycles &&
+           u_zero == o.u_zero && mode == o.mode && hist == o.hist;
+  }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+};
+
+struct mgb_work {
+  const mgb_hier* h = nullptr;
+  cudaStream_t cap = nullptr;
+  std::vector<double*> u, t, f, r, v;
+  double* partials = nullptr;
+  int max_nblk = 0;
+  double* fnorm2 = nullptr;   // batch
+  double* scratch = nullptr;  // batch x 4 (solve history slots)
+  double *hf = nullptr, *hu = nullptr, *hh = nullptr;  // host-call staging (level 0 f, u, history)
+  int64_t hh_cap = 0;
+  std::vector<GraphEntry> graphs;
+  int64_t last_launches = 0;
+  ~mgb_work() {
+    DeviceGuard dg(h ? h->device : -1);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto* vec : {&u, &t, &f, &r, &v})
+      for (auto*& p : *vec) dfree(p);
+    dfree(partials);
+    dfree(fnorm2);
+    dfree(scratch);
+    dfree(hf);
+    dfree(hu);
+    dfree(hh);
+    if (cap) cudaStreamDestroy(cap);
+  }
+};
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// library / errors
+
+extern "C" int mgb_version(void) { return 1; }
+extern "C" const char* mgb_last_error(void) { return g_err.c_str(); }
+extern "C" int mgb_last_pivot(void) { return g_pivot; }
+
+extern "C" int mgb_device_info(int device, int* sm_count, int* cc_major, int* cc_minor) {
+  int cnt = 0;
+  cudaError_t e = cudaGetDeviceCount(&cnt);
+  if (e != cudaSuccess || cnt == 0) return fail(MGB_CUDA, "no CUDA device available");
+  if (device < 0 || device >= cnt) return fail(MGB_CONFIG, "device index out of range");
+  cudaDeviceProp pr;
+  MGB_CUDA_TRY(cudaGetDeviceProperties(&pr, device));
+  if (sm_count) *sm_count = pr.multiProcessorCount;
+  if (cc_major) *cc_major = pr.major;
+  if (cc_minor) *cc_minor = pr.minor;
+  return MGB_OK;
+}
+
+static int check_dims(int batch, int rows, int cols) {
+  if (batch < 1) return fail(MGB_CONTRACT, "batch must be positive");
+  if (rows < 1 || cols < 1) return fail(MGB_CONTRACT, "grid dimensions must be positive");
+  if ((int64_t)rows * cols > (int64_t)1 << 34) return fail(MGB_CONTRACT, "grid too large");
+  return MGB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stateless ops (reference layouts)
+
+extern "C" int mgb_apply_stencil(int batch, int rows, int cols, int k, const double* A_dev,
+                                 const uint8_t* mask_dev, const double* u_dev, double* out_dev,
+                                 void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (k != 1 && k != 3) return fail(MGB_CONTRACT, "apply_stencil supports k = 1 or 3");
+  Grid g{batch, rows, cols};
+  Tab A = k == 3 ? tab_aos(A_dev, g.n(), 1) : Tab{A_dev, g.n(), 1, 0, 1};
+  MGB_CUDA_TRY(launch_apply(g, k, A, mask_dev, u_dev, out_dev, S(stream)));
+  return MGB_OK;
+}
+
+extern "C" int mgb_restrict(int batch, int rows, int cols, const uint8_t* mask_c_dev,
+                            const double* fine_dev, double* coarse_dev, void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (rows / 2 < 1 || cols / 2 < 1) return fail(MGB_CONFIG, "grid cannot be coarsened further");
+  Grid g{batch, rows, cols};
+  MGB_CUDA_TRY(launch_restrict(g, mask_c_dev, fine_dev, coarse_dev, S(stream)));
+  return MGB_OK;
+}
+
+extern "C" int mgb_prolong(int batch, int rows, int cols, const uint8_t* mask_f_dev,
+                           const double* coarse_dev, double* fine_dev, void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (rows / 2 < 1 || cols / 2 < 1) return fail(MGB_CONFIG, "grid cannot be coarsened further");
+  Grid g{batch, rows, cols};
+  MGB_CUDA_TRY(launch_prolong(g, mask_f_dev, coarse_dev, fine_dev, false, S(stream)));
+  return MGB_OK;
+}
+
+extern "C" int mgb_galerkin_product(int batch, int rows, int cols, int k, const double* A_dev,
+                                    const uint8_t* mask_f_dev, const uint8_t* mask_c_dev,
+                                    double* Ac_dev, int* k_out, void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (k != 3) return fail(MGB_CONTRACT, "galerkin_product supports 3x3 fine stencils");
+  if (rows / 2 < 1 || cols / 2 < 1) return fail(MGB_CONFIG, "grid cannot be coarsened further");
+  Grid g{batch, rows, cols};
+  const int64_t nc = (int64_t)(rows / 2) * (cols / 2);
+  int* ring = nullptr;
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ring), sizeof(int), S(stream)));
+  MGB_CUDA_TRY(cudaMemsetAsync(ring, 0, sizeof(int), S(stream)));
+  MGB_CUDA_TRY(launch_galerkin(g, tab_aos(A_dev, g.n(), 1), mask_f_dev, mask_c_dev,
+                               tabw_aos(Ac_dev, nc, 1), ring, S(stream)));
+  int hr = 0;
+  MGB_CUDA_TRY(cudaMemcpyAsync(&hr, ring, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
+  MGB_CUDA_TRY(cudaFreeAsync(ring, S(stream)));
+  MGB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  if (k_out) *k_out = hr ? 3 : 1;
+  return MGB_OK;
+}
+
+// out = M(r) for a kst-stage smoother whose kernels are in table K
+static int smoother_apply_tab(const Grid& g, int kst, Tab K, const uint8_t* mask, double slope,
+                              const double* r, double* out, double* tmp1, double* tmp2,
+                              const double* base, cudaStream_t s) {
+  const double* in = r;
+  for (int st = 0; st < kst; ++st) {
+    const bool last = st == kst - 1;
+    double* dst = last ? out : ((st & 1) ? tmp2 : tmp1);
+    MGB_CUDA_TRY(launch_pointwise(g, K, st, mask, in, st > 0, slope, last ? base : nullptr, dst, s));
+    in = dst;
+  }
+  return MGB_OK;
+}
+
+extern "C" int mgb_smoother_apply(int batch, int rows, int cols, int kst, const double* K_dev,
+                                  const uint8_t* mask_dev, double slope, const double* r_dev,
+                                  double* out_dev, void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (kst < 1) return fail(MGB_CONTRACT, "smoother needs at least one stage");
+  Grid g{batch, rows, cols};
+  double *t1 = nullptr, *t2 = nullptr;
+  const size_t bytes = sizeof(double) * g.n() * batch;
+  if (kst > 1) {
+    MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t1), bytes, S(stream)));
+    MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t2), bytes, S(stream)));
+  }
+  int st = smoother_apply_tab(g, kst, tab_aos(K_dev, g.n(), kst), mask_dev, slope, r_dev, out_dev,
+                              t1, t2, nullptr, S(stream));
+  if (t1) cudaFreeAsync(t1, S(stream));
+  if (t2) cudaFreeAsync(t2, S(stream));
+  return st;
+}
+
+static int upload_weights(int variant, int kst, const double* w_host, int64_t nw, double** w_dev,
+                          cudaStream_t s) {
+  if (variant != MGB_NET_CONV && variant != MGB_NET_FC)
+    return fail(MGB_CONFIG, "unknown net variant");
+  if (kst < 1 || kst > 4) return fail(MGB_CONFIG, "inference supports 1 <= k <= 4 stages");
+  if (nw != net_weight_count(variant, kst))
+    return fail(MGB_CONFIG, "weight count does not match the net architecture");
+  for (int64_t q = 0; q < nw; ++q)
+    if (!std::isfinite(w_host[q])) return fail(MGB_NUMERIC, "non-finite net weights");
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(w_dev), sizeof(double) * nw, s));
+  MGB_CUDA_TRY(cudaMemcpyAsync(*w_dev, w_host, sizeof(double) * nw, cudaMemcpyHostToDevice, s));
+  return MGB_OK;
+}
+
+extern "C" int mgb_infer_kernels(int batch, int rows, int cols, const double* A_dev,
+                                 const uint8_t* mask_dev, int variant, int kst,
+                                 const double* weights_host, int64_t n_weights, double slope,
+                                 int precision, double* K_dev, void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (precision != 32 && precision != 64) return fail(MGB_CONFIG, "precision must be 32 or 64");
+  double* w = nullptr;
+  if (int st = upload_weights(variant, kst, weights_host, n_weights, &w, S(stream))) return st;
+  Grid g{batch, rows, cols};
+  cudaError_t e = launch_infer(g, tab_aos(A_dev, g.n(), 1), mask_dev, variant, kst, w, slope,
+                               precision, tabw_aos(K_dev, g.n(), kst), S(stream));
+  cudaFreeAsync(w, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "launch_infer");
+  return MGB_OK;
+}
+
+extern "C" int mgb_lu_factor(int n, double* lu_dev, int32_t* perm_dev, void* stream) {
+  if (n < 1 || n > 4096) return fail(MGB_CONFIG, "dense LU supports 1 <= n <= 4096");
+  int* st = nullptr;
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&st), sizeof(int), S(stream)));
+  MGB_CUDA_TRY(launch_lu_factor(1, n, lu_dev, perm_dev, st, S(stream)));
+  int hs = -1;
+  MGB_CUDA_TRY(cudaMemcpyAsync(&hs, st, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
+  MGB_CUDA_TRY(cudaFreeAsync(st, S(stream)));
+  MGB_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  if (hs >= 0) {
+    set_error(MGB_SINGULAR, "singular to working precision at pivot " + std::to_string(hs), hs);
+    return MGB_SINGULAR;
+  }
+  return MGB_OK;
+}
+
+extern "C" int mgb_lu_solve(int n, const double* lu_dev, const int32_t* perm_dev,
+                            const double* b_dev, double* x_dev, void* stream) {
+  if (n < 1 || n > 4096) return fail(MGB_CONFIG, "dense LU supports 1 <= n <= 4096");
+  MGB_CUDA_TRY(launch_lu_solve_vec(n, lu_dev, perm_dev, b_dev, x_dev, S(stream)));
+  return MGB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// hierarchy
+
+static int64_t count_active(const std::vector<uint8_t>& m) {
+  int64_t c = 0;
+  for (uint8_t x : m) c += x != 0;
+  return c;
+}
+
+extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double spacing,
+                              const double* A0, int a0_on_device, const uint8_t* mask_host,
+                              int levels, void* stream, mgb_hier** out) {
+  if (!out) return fail(MGB_CONTRACT, "null output handle");
+  *out = nullptr;
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (!(spacing > 0.0)) return fail(MGB_CONTRACT, "grid spacing must be positive");
+  if (levels < 2) return fail(MGB_CONFIG, "a hierarchy needs at least two levels");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0)
+    return fail(MGB_CUDA, "no CUDA device available");
+  if (device < 0 || device >= cnt) return fail(MGB_CONFIG, "device index out of range");
+  DeviceGuard dg(device);
+  cudaStream_t s = S(stream);
+
+  std::unique_ptr<mgb_hier> h(new mgb_hier());
+  h->device = device;
+  h->batch = batch;
+  // level geometry + masks on the host (coarsen_full, transfer.py:50-61)
+  const bool has_mask = mask_host != nullptr;
+  {
+    LevelD l0;
+    l0.rows = rows;
+    l0.cols = cols;
+    l0.h = spacing;
+    l0.n = (int64_t)rows * cols;
+    l0.k = 3;
+    l0.hmask.assign(mask_host ? mask_host : nullptr, mask_host ? mask_host + l0.n : nullptr);
+    if (!has_mask) l0.hmask.assign(l0.n, 1);
+    l0.nact = count_active(l0.hmask);
+    if (l0.nact == 0) return fail(MGB_CONTRACT, "grid has no active points");
+    h->lv.push_back(std::move(l0));
+  }
+  for (int step = 0; step < levels - 1; ++step) {
+    const LevelD& f = h->lv.back();
+    LevelD c;
+    c.rows = f.rows / 2;
+    c.cols = f.cols / 2;
+    if (c.rows < 1 || c.cols < 1)
+      return fail(MGB_CONFIG, "level " + std::to_string(step) + ": " + std::to_string(f.rows) + "x" +
+                                  std::to_string(f.cols) + " grid cannot be coarsened further");
+    c.h = 2.0 * f.h;
+    c.n = (int64_t)c.rows * c.cols;
+    c.hmask.resize(c.n);
+    for (int i = 0; i < c.rows; ++i)
+      for (int j = 0; j < c.cols; ++j)
+        c.hmask[(int64_t)i * c.cols + j] = f.hmask[(int64_t)(2 * i + 1) * f.cols + (2 * j + 1)];
+    c.nact = count_active(c.hmask);
+    if (c.nact == 0)
+      return fail(MGB_CONFIG, "level " + std::to_string(step) + ": coarsening left no active points");
+    if (c.nact >= f.nact)
+      return fail(MGB_CONFIG, "level " + std::to_string(step) + ": coarsening does not shrink the active set");
+    h->lv.push_back(std::move(c));
+  }
+  const int L = h->depth();
+  const LevelD& lc = h->lv[L - 1];
+  if (lc.nact > 4096)
+    return fail(MGB_CONFIG, "coarsest level has " + std::to_string(lc.nact) +
+                                " unknowns; the dense direct solve supports at most 4096 (add levels)");
+  // non-finite input check (StencilField, grid.py:182-183)
+  if (!a0_on_device) {
+    const int64_t tot = (int64_t)batch * h->lv[0].n * 9;
+    for (int64_t q = 0; q < tot; ++q)
+      if (!std::isfinite(A0[q])) return fail(MGB_NUMERIC, "non-finite stencil weights");
+  }
+  // device allocations
+  for (auto& l : h->lv) {
+    MGB_CUDA_TRY(dalloc(&l.A, (size_t)batch * 9 * l.n));
+    if (has_mask) {
+      MGB_CUDA_TRY(dalloc(&l.mask, (size_t)l.n));
+      MGB_CUDA_TRY(cudaMemcpyAsync(l.mask, l.hmask.data(), l.n, cudaMemcpyHostToDevice, s));
+    }
+  }
+  // level 0: reference AoS -> planes
+  {
+    LevelD& l0 = h->lv[0];
+    const double* src = A0;
+    double* tmp = nullptr;
+    if (!a0_on_device) {
+      MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * batch * 9 * l0.n, s));
+      MGB_CUDA_TRY(cudaMemcpyAsync(tmp, A0, sizeof(double) * batch * 9 * l0.n, cudaMemcpyHostToDevice, s));
+      src = tmp;
+    }
+    MGB_CUDA_TRY(launch_convert(h->grid(0), 1, tab_aos(src, l0.n, 1), tabw_soa(l0.A, l0.n, 1), s));
+    if (tmp) MGB_CUDA_TRY(cudaFreeAsync(tmp, s));
+  }
+  // Galerkin chain (transfer.py:150-209) with the _trim ring test
+  int* ring = nullptr;
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ring), sizeof(int) * L, s));
+  MGB_CUDA_TRY(cudaMemsetAsync(ring, 0, sizeof(int) * L, s));
+  for (int l = 0; l + 1 < L; ++l) {
+    LevelD& f = h->lv[l];
+    LevelD& c = h->lv[l + 1];
+    MGB_CUDA_TRY(launch_galerkin(h->grid(l), tab_soa(f.A, f.n, 1), f.mask, c.mask,
+                                 tabw_soa(c.A, c.n, 1), ring + l + 1, s));
+  }
+  std::vector<int> hring(L, 1);
+  MGB_CUDA_TRY(cudaMemcpyAsync(hring.data(), ring, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaFreeAsync(ring, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int l = 1; l < L; ++l) h->lv[l].k = hring[l] ? 3 : 1;
+  // coarsest: materialise over active points and LU-factor (hierarchy.py:87)
+  {
+    LevelD& c = h->lv[L - 1];
+    const int nc = (int)c.nact;
+    h->nc = nc;
+    std::vector<int32_t> idx(c.n, -1), actp(nc);
+    int a = 0;
+    for (int64_t p = 0; p < c.n; ++p)
+      if (c.hmask[p]) { idx[p] = a; actp[a] = (int32_t)p; ++a; }
+    int32_t* didx = nullptr;
+    int* dst = nullptr;
+    MGB_CUDA_TRY(dalloc(&h->actp, nc));
+    MGB_CUDA_TRY(dalloc(&h->lu, (size_t)batch * nc * nc));
+    MGB_CUDA_TRY(dalloc(&h->perm, (size_t)batch * nc));
+    MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&didx), sizeof(int32_t) * c.n, s));
+    MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dst), sizeof(int) * batch, s));
+    MGB_CUDA_TRY(cudaMemcpyAsync(didx, idx.data(), sizeof(int32_t) * c.n, cudaMemcpyHostToDevice, s));
+    MGB_CUDA_TRY(cudaMemcpyAsync(h->actp, actp.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, s));
+    MGB_CUDA_TRY(cudaMemsetAsync(h->lu, 0, sizeof(double) * batch * nc * nc, s));
+    MGB_CUDA_TRY(launch_materialize(h->grid(L - 1), tab_soa(c.A, c.n, 1), didx, nc, h->actp, h->lu, s));
+    MGB_CUDA_TRY(launch_lu_factor(batch, nc, h->lu, h->perm, dst, s));
+    std::vector<int> hs(batch);
+    MGB_CUDA_TRY(cudaMemcpyAsync(hs.data(), dst, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
+    MGB_CUDA_TRY(cudaFreeAsync(didx, s));
+    MGB_CUDA_TRY(cudaFreeAsync(dst, s));
+    MGB_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int b = 0; b < batch; ++b)
+      if (hs[b] >= 0) {
+        set_error(MGB_SINGULAR, "coarsest operator singular to working precision at pivot " +
+                                    std::to_string(hs[b]) + " (problem " + std::to_string(b) + ")",
+                  hs[b]);
+        return MGB_SINGULAR;
+      }
+  }
+  *out = h.release();
+  return MGB_OK;
+}
+
+extern "C" void mgb_hier_destroy(mgb_hier* h) { delete h; }
+
+extern "C" int mgb_hier_depth(const mgb_hier* h, int* depth, int* batch) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (depth) *depth = h->depth();
+  if (batch) *batch = h->batch;
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_level_info(const mgb_hier* h, int level, int* rows, int* cols, int* k,
+                                   int* ks, double* spacing) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  const LevelD& l = h->lv[level];
+  if (rows) *rows = l.rows;
+  if (cols) *cols = l.cols;
+  if (k) *k = l.k;
+  if (ks) *ks = l.ks;
+  if (spacing) *spacing = l.h;
+  return MGB_OK;
+}
+
+static int download_table(const mgb_hier* h, const LevelD& l, const double* planes, int kst,
+                          double* out_host) {
+  DeviceGuard dg(h->device);
+  double* tmp = nullptr;
+  const size_t cnt = (size_t)h->batch * kst * 9 * l.n;
+  MGB_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&tmp), cnt * sizeof(double)));
+  Grid g{h->batch, l.rows, l.cols};
+  cudaError_t e = launch_convert(g, kst, tab_soa(planes, l.n, kst), tabw_aos(tmp, l.n, kst), nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(out_host, tmp, cnt * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "download_table");
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_get_operator(const mgb_hier* h, int level, double* out_host) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  const LevelD& l = h->lv[level];
+  if (l.k == 3) return download_table(h, l, l.A, 1, out_host);
+  std::vector<double> full((size_t)h->batch * 9 * l.n);
+  if (int st = download_table(h, l, l.A, 1, full.data())) return st;
+  for (size_t q = 0; q < (size_t)h->batch * l.n; ++q) out_host[q] = full[q * 9 + 4];
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_get_kernels(const mgb_hier* h, int level, double* out_host) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  const LevelD& l = h->lv[level];
+  if (!l.K) return fail(MGB_CONFIG, "level " + std::to_string(level) + " has no smoother installed");
+  return download_table(h, l, l.K, l.ks, out_host);
+}
+
+extern "C" int mgb_hier_get_mask(const mgb_hier* h, int level, uint8_t* out_host) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  std::memcpy(out_host, h->lv[level].hmask.data(), h->lv[level].n);
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_operator_planes(const mgb_hier* h, int level, const double** planes_dev) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  *planes_dev = h->lv[level].A;
+  return MGB_OK;
+}
+
+static int alloc_kernels(mgb_hier* h, LevelD& l, int kst) {
+  if (l.K && l.ks == kst) return MGB_OK;
+  dfree(l.K);
+  l.ks = 0;
+  MGB_CUDA_TRY(dalloc(&l.K, (size_t)h->batch * kst * 9 * l.n));
+  l.ks = kst;
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const double* weights_host,
+                                       int64_t n_weights, double slope, int precision, void* stream) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (precision != 32 && precision != 64) return fail(MGB_CONFIG, "precision must be 32 or 64");
+  for (int l = 0; l + 1 < h->depth(); ++l)
+    if (h->lv[l].k != 3) return fail(MGB_CONFIG, "kernel inference needs 3x3 stencils on every level");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  double* w = nullptr;
+  if (int st = upload_weights(variant, kst, weights_host, n_weights, &w, s)) return st;
+  for (int l = 0; l + 1 < h->depth(); ++l) {
+    LevelD& lv = h->lv[l];
+    if (int st = alloc_kernels(h, lv, kst)) return st;
+    cudaError_t e = launch_infer(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, variant, kst, w, slope,
+                                 precision, tabw_soa(lv.K, lv.n, kst), s);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(w, s);
+      return cuda_fail(e, "launch_infer");
+    }
+  }
+  h->slope = slope;
+  MGB_CUDA_TRY(cudaFreeAsync(w, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (!(omega > 0.0 && omega < 2.0)) return fail(MGB_CONFIG, "jacobi weight out of range");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  int* flag = nullptr;
+  const int L = h->depth();
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int) * L, s));
+  MGB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int) * L, s));
+  for (int l = 0; l + 1 < L; ++l) {
+    LevelD& lv = h->lv[l];
+    if (int st = alloc_kernels(h, lv, 1)) return st;
+    MGB_CUDA_TRY(launch_jacobi(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, omega,
+                               tabw_soa(lv.K, lv.n, 1), flag + l, s));
+  }
+  std::vector<int> hf(L);
+  MGB_CUDA_TRY(cudaMemcpyAsync(hf.data(), flag, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaFreeAsync(flag, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int l = 0; l + 1 < L; ++l)
+    if (hf[l]) return fail(MGB_CONFIG, "jacobi: operator has zero diagonal entries");
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_set_kernels(mgb_hier* h, int level, int kst, const double* K, int on_device,
+                                    double slope, void* stream) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level + 1 >= h->depth()) return fail(MGB_CONFIG, "no smoother on this level");
+  if (kst < 1) return fail(MGB_CONTRACT, "smoother needs at least one stage");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  LevelD& lv = h->lv[level];
+  if (int st = alloc_kernels(h, lv, kst)) return st;
+  const size_t cnt = (size_t)h->batch * kst * 9 * lv.n;
+  const double* src = K;
+  double* tmp = nullptr;
+  if (!on_device) {
+    for (size_t q = 0; q < cnt; ++q)
+      if (!std::isfinite(K[q])) return fail(MGB_NUMERIC, "non-finite smoother kernels");
+    MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), cnt * sizeof(double), s));
+    MGB_CUDA_TRY(cudaMemcpyAsync(tmp, K, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
+    src = tmp;
+  }
+  MGB_CUDA_TRY(launch_convert(h->grid(level), kst, tab_aos(src, lv.n, kst), tabw_soa(lv.K, lv.n, kst), s));
+  if (tmp) MGB_CUDA_TRY(cudaFreeAsync(tmp, s));
+  h->slope = slope;
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  return MGB_OK;
+}
+
+extern "C" int mgb_coarse_solve(const mgb_hier* h, const double* f_dev, double* x_dev, void* stream) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  DeviceGuard dg(h->device);
+  const int L = h->depth();
+  MGB_CUDA_TRY(launch_lu_solve_grid(h->grid(L - 1), h->nc, h->lu, h->perm, h->actp, f_dev, x_dev, S(stream)));
+  return MGB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// per-level passes
+
+static int check_level(const mgb_hier* h, int level, bool smoothed) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  if (smoothed && level == h->depth() - 1) return fail(MGB_CONFIG, "the coarsest level has no smoother");
+  return MGB_OK;
+}
+
+extern "C" int mgb_residual(const mgb_hier* h, int level, const double* f_dev, const double* u_dev,
+                            double* r_dev, double* norm2_dev, void* stream) {
+  if (int st = check_level(h, level, false)) return st;
+  DeviceGuard dg(h->device);
+  const LevelD& l = h->lv[level];
+  const Grid g = h->grid(level);
+  cudaStream_t s = S(stream);
+  double* part = nullptr;
+  int nblk = residual_blocks(g);
+  if (norm2_dev) MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * nblk * g.batch, s));
+  MGB_CUDA_TRY(launch_residual(g, tab_soa(l.A, l.n, 1), l.mask, f_dev, u_dev, r_dev, part, &nblk, s));
+  if (norm2_dev) {
+    MGB_CUDA_TRY(launch_finalize(g.batch, nblk, part, norm2_dev, nullptr, nullptr, 0, s));
+    MGB_CUDA_TRY(cudaFreeAsync(part, s));
+  }
+  return MGB_OK;
+}
+
+extern "C" int mgb_restrict_residual(const mgb_hier* h, int level, const double* f_dev,
+                                     const double* u_dev, double* rc_dev, void* stream) {
+  if (int st = check_level(h, level, true)) return st;
+  DeviceGuard dg(h->device);
+  const LevelD& l = h->lv[level];
+  MGB_CUDA_TRY(launch_resid_restrict(h->grid(level), tab_soa(l.A, l.n, 1), l.mask, h->lv[level + 1].mask,
+                                     f_dev, u_dev, rc_dev, S(stream)));
+  return MGB_OK;
+}
+
+extern "C" int mgb_prolong_correct(const mgb_hier* h, int level, const double* ec_dev, double* u_dev,
+                                   void* stream) {
+  if (int st = check_level(h, level, true)) return st;
+  DeviceGuard dg(h->device);
+  MGB_CUDA_TRY(launch_prolong(h->grid(level), h->lv[level].mask, ec_dev, u_dev, true, S(stream)));
+  return MGB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// workspace + cycle driver
+
+extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
+  if (!h || !out) return fail(MGB_CONTRACT, "null argument");
+  *out = nullptr;
+  DeviceGuard dg(h->device);
+  std::unique_ptr<mgb_work> w(new mgb_work());
+  w->h = h;
+  const int L = h->depth();
+  w->u.assign(L, nullptr);
+  w->t.assign(L, nullptr);
+  w->f.assign(L, nullptr);
+  w->r.assign(L, nullptr);
+  w->v.assign(L, nullptr);
+  for (int l = 0; l < L; ++l) {
+    const size_t cnt = (size_t)h->batch * h->lv[l].n;
+    if (l > 0) {
+      MGB_CUDA_TRY(dalloc(&w->u[l], cnt));
+      MGB_CUDA_TRY(dalloc(&w->f[l], cnt));
+    }
+    if (l + 1 < L) MGB_CUDA_TRY(dalloc(&w->t[l], cnt));
+  }
+  w->max_nblk = residual_blocks(h->grid(0));
+  MGB_CUDA_TRY(dalloc(&w->partials, (size_t)w->max_nblk * h->batch));
+  MGB_CUDA_TRY(dalloc(&w->fnorm2, (size_t)h->batch));
+  MGB_CUDA_TRY(dalloc(&w->scratch, (size_t)h->batch * 4));
+  MGB_CUDA_TRY(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
+  *out = w.release();
+  return MGB_OK;
+}
+
+extern "C" void mgb_work_destroy(mgb_work* w) { delete w; }
+
+extern "C" int64_t mgb_last_launch_count(const mgb_work* w) { return w ? w->last_launches : 0; }
+
+static int ensure_generic(mgb_work* w, int l) {
+  const mgb_hier* h = w->h;
+  const size_t cnt = (size_t)h->batch * h->lv[l].n;
+  if (!w->r[l]) MGB_CUDA_TRY(dalloc(&w->r[l], cnt));
+  if (!w->v[l]) MGB_CUDA_TRY(dalloc(&w->v[l], cnt));
+  return MGB_OK;
+}
+
+// one smoothing sweep on level l: out = in + M(f - A in); in == null means in = 0
+static int sweep(mgb_work* w, int l, const double* f, const double* in, double* out, cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  const LevelD& lv = h->lv[l];
+  const Grid g = h->grid(l);
+  if (lv.ks == 1) {
+    MGB_CUDA_TRY(launch_sweep(g, tab_soa(lv.A, lv.n, 1), tab_soa(lv.K, lv.n, 1), lv.mask, f, in, out, s));
+    return MGB_OK;
+  }
+  // multi-stage (nonlinear) smoother: residual, then k stages with leaky between
+  if (int st = ensure_generic(w, l)) return st;
+  const double* r = f;
+  if (in) {
+    MGB_CUDA_TRY(launch_residual(g, tab_soa(lv.A, lv.n, 1), lv.mask, f, in, w->r[l], nullptr, nullptr, s));
+    r = w->r[l];
+  }
+  return smoother_apply_tab(g, lv.ks, tab_soa(lv.K, lv.n, lv.ks), lv.mask, h->slope, r, out, w->v[l],
+                            w->r[l], in, s);
+}
+
+// V(nu1, nu2) from level l; u_in == null means a zero initial guess.  Returns the
+// buffer holding the result (u_l or the level's ping-pong partner).
+static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero, int nu1, int nu2,
+                      cudaStream_t s, double** result) {
+  const mgb_hier* h = w->h;
+  const int L = h->depth();
+  if (l == L - 1) {
+    MGB_CUDA_TRY(launch_lu_solve_grid(h->grid(l), h->nc, h->lu, h->perm, h->actp, f, u, s));
+    *result = u;
+    return MGB_OK;
+  }
+  const LevelD& lv = h->lv[l];
+  if (!lv.K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+  double* cur = u;
+  double* oth = w->t[l];
+  if (zero && nu1 == 0) MGB_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(double) * h->batch * lv.n, s));
+  for (int q = 0; q < nu1; ++q) {
+    if (int st = sweep(w, l, f, (zero && q == 0) ? nullptr : cur, oth, s)) return st;
+    std::swap(cur, oth);
+  }
+  MGB_CUDA_TRY(launch_resid_restrict(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, h->lv[l + 1].mask, f, cur,
+                                     w->f[l + 1], s));
+  double* ec = nullptr;
+  if (int st = vcycle_rec(w, l + 1, w->f[l + 1], w->u[l + 1], true, nu1, nu2, s, &ec)) return st;
+  MGB_CUDA_TRY(launch_prolong(h->grid(l), lv.mask, ec, cur, true, s));
+  for (int q = 0; q < nu2; ++q) {
+    if (int st = sweep(w, l, f, cur, oth, s)) return st;
+    std::swap(cur, oth);
+  }
+  *result = cur;
+  return MGB_OK;
+}
+
+static int enqueue_vcycle(mgb_work* w, int l, const double* f, double* u, int nu1, int nu2, cudaStream_t s) {
+  double* res = nullptr;
+  if (int st = vcycle_rec(w, l, f, u, false, nu1, nu2, s, &res)) return st;
+  if (res != u)
+    MGB_CUDA_TRY(cudaMemcpyAsync(u, res, sizeof(double) * w->h->batch * w->h->lv[l].n,
+                                 cudaMemcpyDeviceToDevice, s));
+  return MGB_OK;
+}
+
+// hist[b * hstride] = ||f - A u|| / ||f|| on level 0 (fnorm2 must be current)
+static int enqueue_resnorm(mgb_work* w, const double* f, const double* u, double* hist, int64_t hstride,
+                           cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  const LevelD& l0 = h->lv[0];
+  int nblk = 0;
+  MGB_CUDA_TRY(launch_residual(h->grid(0), tab_soa(l0.A, l0.n, 1), l0.mask, f, u, nullptr, w->partials, &nblk, s));
+  MGB_CUDA_TRY(launch_finalize(h->batch, nblk, w->partials, nullptr, w->fnorm2, hist, hstride, s));
+  return MGB_OK;
+}
+
+static int enqueue_fnorm(mgb_work* w, const double* f, cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  const LevelD& l0 = h->lv[0];
+  int nblk = 0;
+  MGB_CUDA_TRY(launch_residual(h->grid(0), tab_soa(l0.A, l0.n, 1), l0.mask, f, nullptr, nullptr, w->partials,
+                               &nblk, s));
+  MGB_CUDA_TRY(launch_finalize(h->batch, nblk, w->partials, w->fnorm2, nullptr, nullptr, 0, s));
+  return MGB_OK;
+}
+
+static int check_equipped(const mgb_hier* h) {
+  for (int l = 0; l + 1 < h->depth(); ++l)
+    if (!h->lv[l].K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+  return MGB_OK;
+}
+
+extern "C" int mgb_vcycle(const mgb_hier* h, mgb_work* w, int level, const double* f_dev, double* u_dev,
+                          int nu1, int nu2, void* stream) {
+  if (!h || !w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  if (nu1 < 0 || nu2 < 0) return fail(MGB_CONFIG, "sweep counts must be non-negative");
+  DeviceGuard dg(h->device);
+  for (int l = level; l + 1 < h->depth(); ++l)
+    if (!h->lv[l].K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+  const int64_t l0 = g_launches;
+  int st = enqueue_vcycle(w, level, f_dev, u_dev, nu1, nu2, S(stream));
+  w->last_launches = g_launches - l0;
+  return st;
+}
+
+extern "C" int mgb_smooth(const mgb_hier* h, mgb_work* w, int level, const double* f_dev, double* u_dev,
+                          int sweeps, void* stream) {
+  if (int st = check_level(h, level, true)) return st;
+  if (!w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
+  if (!h->lv[level].K) return fail(MGB_CONFIG, "level " + std::to_string(level) + " has no smoother installed");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  double* cur = u_dev;
+  double* oth = w->t[level];
+  for (int q = 0; q < sweeps; ++q) {
+    if (int st = sweep(w, level, f_dev, cur, oth, s)) return st;
+    std::swap(cur, oth);
+  }
+  if (cur != u_dev)
+    MGB_CUDA_TRY(cudaMemcpyAsync(u_dev, cur, sizeof(double) * h->batch * h->lv[level].n,
+                                 cudaMemcpyDeviceToDevice, s));
+  return MGB_OK;
+}
+
+// Capture (once per key) and launch a graph.  mode 0: run_cycles; mode 1: one
+// solve iteration (cycle + residual norm into scratch).
+static int get_graph(mgb_work* w, const GraphKey& key, GraphEntry** out) {
+  GraphEntry* ent = nullptr;
+  for (auto& g : w->graphs)
+    if (g.key == key) ent = &g;
+  if (!ent) {
+    const int64_t l0 = g_launches;
+    cudaGraph_t graph = nullptr;
+    MGB_CUDA_TRY(cudaStreamBeginCapture(w->cap, cudaStreamCaptureModeThreadLocal));
+    int st = MGB_OK;
+    const int64_t nb = w->h->batch * (int64_t)w->h->lv[0].n;
+    if (key.mode == 0) {
+      if (key.u_zero) {
+        cudaError_t e = cudaMemsetAsync(key.u, 0, sizeof(double) * nb, w->cap);
+        if (e != cudaSuccess) st = cuda_fail(e, "memset");
+      }
+      if (!st) st = enqueue_fnorm(w, key.f, w->cap);
+      if (!st) st = enqueue_resnorm(w, key.f, key.u, key.hist, key.cycles + 1, w->cap);
+      for (int c = 0; c < key.cycles && !st; ++c) {
+        st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap);
+        if (!st) st = enqueue_resnorm(w, key.f, key.u, key.hist + c + 1, key.cycles + 1, w->cap);
+      }
+    } else {
+      st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap);
+      if (!st) st = enqueue_resnorm(w, key.f, key.u, w->scratch, 4, w->cap);
+    }
+    cudaError_t e = cudaStreamEndCapture(w->cap, &graph);
+    if (st) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    GraphEntry ge;
+    ge.key = key;
+    ge.launches = g_launches - l0;
+    e = cudaGraphInstantiate(&ge.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    if (w->graphs.size() >= 8) {
+      cudaGraphExecDestroy(w->graphs.front().exec);
+      w->graphs.erase(w->graphs.begin());
+    }
+    w->graphs.push_back(ge);
+    ent = &w->graphs.back();
+  }
+  *out = ent;
+  return MGB_OK;
+}
+
+static int launch_graph(mgb_work* w, const GraphKey& key, cudaStream_t s) {
+  GraphEntry* ent = nullptr;
+  if (int st = get_graph(w, key, &ent)) return st;
+  MGB_CUDA_TRY(cudaGraphLaunch(ent->exec, s));
+  w->last_launches = ent->launches;
+  return MGB_OK;
+}
+
+extern "C" int mgb_run_cycles(const mgb_hier* h, mgb_work* w, const double* f_dev, double* u_dev, int nu1,
+                              int nu2, int cycles, int u_zero, double* history_dev, void* stream) {
+  if (!h || !w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
+  if (cycles < 0 || nu1 < 0 || nu2 < 0) return fail(MGB_CONFIG, "counts must be non-negative");
+  if (!history_dev) return fail(MGB_CONTRACT, "history buffer required");
+  if (int st = check_equipped(h)) return st;
+  DeviceGuard dg(h->device);
+  GraphKey key{f_dev, u_dev, nu1, nu2, cycles, u_zero ? 1 : 0, 0, history_dev};
+  return launch_graph(w, key, S(stream));
+}
+
+extern "C" int mgb_run_cycles_host(const mgb_hier* h, mgb_work* w, const double* f_host, double* u_host,
+                                   int nu1, int nu2, int cycles, int u_zero, double* history_host,
+                                   void* stream) {
+  if (!h || !w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
+  if (!f_host || !u_host || !history_host) return fail(MGB_CONTRACT, "null host buffer");
+  if (cycles < 0 || nu1 < 0 || nu2 < 0) return fail(MGB_CONFIG, "counts must be non-negative");
+  if (int st = check_equipped(h)) return st;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  const size_t cnt = (size_t)h->batch * h->lv[0].n;
+  if (!w->hf) MGB_CUDA_TRY(dalloc(&w->hf, cnt));
+  if (!w->hu) MGB_CUDA_TRY(dalloc(&w->hu, cnt));
+  const int64_t nh = (int64_t)h->batch * (cycles + 1);
+  if (nh > w->hh_cap) {
+    dfree(w->hh);
+    MGB_CUDA_TRY(dalloc(&w->hh, (size_t)nh));
+    w->hh_cap = nh;
+  }
+  MGB_CUDA_TRY(cudaMemcpyAsync(w->hf, f_host, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (!u_zero) MGB_CUDA_TRY(cudaMemcpyAsync(w->hu, u_host, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
+  GraphKey key{w->hf, w->hu, nu1, nu2, cycles, u_zero ? 1 : 0, 0, w->hh};
+  if (int st = launch_graph(w, key, s)) return st;
+  MGB_CUDA_TRY(cudaMemcpyAsync(u_host, w->hu, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaMemcpyAsync(history_host, w->hh, nh * sizeof(double), cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  return MGB_OK;
+}
+
+extern "C" int mgb_solve(const mgb_hier* h, mgb_work* w, const double* f_dev, double* u_dev, int nu1, int nu2,
+                         double tol, int max_iter, double* history_host, int* n_history, int* iterations,
+                         int* converged, double* loop_seconds, void* stream) {
+  if (!h || !w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
+  if (!(tol > 0.0)) return fail(MGB_CONFIG, "tolerance must be positive");
+  if (h->batch != 1) return fail(MGB_CONTRACT, "mgb_solve handles one problem; use mgb_run_cycles for batches");
+  if (max_iter < 0) return fail(MGB_CONFIG, "max_iter must be non-negative");
+  if (int st = check_equipped(h)) return st;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  // r0 (hierarchy.py:125-133)
+  if (int st = enqueue_fnorm(w, f_dev, s)) return st;
+  if (int st = enqueue_resnorm(w, f_dev, u_dev, w->scratch, 4, s)) return st;
+  double rr = 0.0;
+  MGB_CUDA_TRY(cudaMemcpyAsync(&rr, w->scratch, sizeof(double), cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  const double r0 = rr;
+  int nh = 0;
+  history_host[nh++] = r0;
+  int it = 0;
+  GraphKey key{f_dev, u_dev, nu1, nu2, 1, 0, 1, nullptr};
+  GraphEntry* pre = nullptr;
+  if (int st = get_graph(w, key, &pre)) return st;  // capture outside the timed loop
+  const auto t0 = std::chrono::steady_clock::now();
+  while (history_host[nh - 1] >= tol && it < max_iter) {
+    if (int st = launch_graph(w, key, s)) return st;
+    MGB_CUDA_TRY(cudaMemcpyAsync(&rr, w->scratch, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MGB_CUDA_TRY(cudaStreamSynchronize(s));
+    ++it;
+    history_host[nh++] = rr;
+    if (!std::isfinite(rr) || rr > 1e6 * std::max(r0, tol)) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "diverged at iteration %d: relative residual %.3e", it, rr);
+      if (n_history) *n_history = nh;
+      if (iterations) *iterations = it;
+      return fail(MGB_NONCONVERGED, buf);
+    }
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  if (n_history) *n_history = nh;
+  if (iterations) *iterations = it;
+  if (converged) *converged = history_host[nh - 1] < tol ? 1 : 0;
+  if (loop_seconds) *loop_seconds = std::chrono::duration<double>(t1 - t0).count();
+  return MGB_OK;
+}

@@ -1,0 +1,431 @@
+"""Multigrid hierarchy, V-cycle and solve — facade over the B200 C-ABI.
+
+Mirrors the reference's hierarchy.py:26-214 (same names, arguments, return
+types and exceptions).  The hierarchy (Galerkin operators, smoother kernels,
+coarsest LU) lives on the GPU; ``v_cycle`` / ``solve`` upload the right-hand
+side, run the whole cycle on the device (one CUDA graph per cycle) and copy
+the result back.  ``run_cycles`` / ``solve_device`` are the device-resident
+entry points used for throughput measurements (torch CUDA tensors in/out).
+
+V(nu1, nu2) follows the reference convention of wrapping every level's
+smoother in ``RepeatedSmoother(inner, A, steps=nu)`` (cli.py:365-377):
+``v_cycle`` reads ``steps`` from such wrappers, or takes ``nu1``/``nu2``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, device as dv
+from .errors import ConfigError, ContractError, UnsupportedOperationError
+from .grid import GridFunction, GridSpec, StencilField, apply_stencil, zeros
+from .smoothers import (LEAKY_SLOPE, VARIANT_ID, InferredSmoother, JacobiSmoother, KernelInferenceNet)
+from .transfer import TransferPair, coarsen_full
+
+
+@dataclass
+class SolveReport:
+    """hierarchy.py:54-59."""
+    iterations: int
+    residual_history: list
+    converged: bool
+    wall_time: float
+
+
+@dataclass
+class RepeatedSmoother:
+    """cli.py:365-377: `steps` sweeps of `inner` per smoothing application.
+    On the device this is exactly `steps` fused sweeps u <- u + M(f - A u)."""
+    inner: object
+    operator: StencilField
+    steps: int
+
+    def apply(self, r: GridFunction) -> GridFunction:
+        u = self.inner.apply(r)
+        for _ in range(self.steps - 1):
+            u = u + self.inner.apply(r - apply_stencil(self.operator, u))
+        return u
+
+
+class Level:
+    """hierarchy.py:26-35; the operator is fetched from the device on first use."""
+
+    def __init__(self, hier, index: int, spec: GridSpec, transfer: TransferPair | None,
+                 operator: StencilField | None = None):
+        self._hier = hier
+        self.index = index
+        self._spec = spec
+        self.transfer = transfer
+        self.smoother = None
+        self.scheme = "full"
+        self._operator = operator
+
+    @property
+    def spec(self) -> GridSpec:
+        return self._spec
+
+    @property
+    def operator(self) -> StencilField:
+        if self._operator is None:
+            self._operator = self._hier._download_operator(self.index)
+        return self._operator
+
+
+class DeviceSmoother:
+    """Smoother installed in a device hierarchy (per-point kernels on the GPU).
+    ``kernels`` downloads the (rows, cols, k, 3, 3) table on first use."""
+
+    def __init__(self, hier, level: int, k: int, slope: float, kind: str, omega: float | None = None):
+        self._hier = hier
+        self.level = level
+        self.k = k
+        self.slope = slope
+        self.kind = kind
+        self.omega = omega
+        self._kernels = None
+
+    @property
+    def spec(self) -> GridSpec:
+        return self._hier.levels[self.level].spec
+
+    @property
+    def kernels(self) -> np.ndarray:
+        if self._kernels is None:
+            self._kernels = self._hier._download_kernels(self.level, self.k)
+        return self._kernels
+
+    def apply(self, r: GridFunction) -> GridFunction:
+        return InferredSmoother(self.spec, self.kernels, self.k, self.slope).apply(r)
+
+
+class MultigridHierarchy:
+    """hierarchy.py:38-51 backed by an mgb_hier handle on one GPU."""
+
+    def __init__(self, handle: C.c_void_p, device: int, batch: int, specs: list, transfers: list,
+                 A0: StencilField | None):
+        self._h = handle
+        self.device = device
+        self.batch = batch
+        self.scheme = "full"
+        self.levels = [Level(self, l, specs[l], transfers[l], A0 if l == 0 else None)
+                       for l in range(len(specs))]
+        self._installed = [None] * len(specs)
+        self._pool = []
+        self._lock = threading.Lock()
+        self.coarse_lu = None
+        self.coarse_perm = None
+
+    # -- lifetime ----------------------------------------------------------
+    def __del__(self):
+        try:
+            for w in self._pool:
+                _lib.lib().mgb_work_destroy(w)
+            if self._h:
+                _lib.lib().mgb_hier_destroy(self._h)
+        except Exception:
+            pass
+        self._h = None
+
+    @property
+    def depth(self) -> int:
+        return len(self.levels)
+
+    @property
+    def finest(self) -> Level:
+        return self.levels[0]
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- workspaces: one per concurrent solve -----------------
+    def acquire_work(self):
+        with self._lock:
+            if self._pool:
+                return self._pool.pop()
+        w = C.c_void_p()
+        _lib.call("mgb_work_create", self._h, C.byref(w))
+        return w
+
+    def release_work(self, w):
+        with self._lock:
+            self._pool.append(w)
+
+    # -- level data ----------------------------------------------------------
+    def level_info(self, l: int):
+        r, c, k, ks = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        h = C.c_double()
+        _lib.call("mgb_hier_level_info", self._h, l, C.byref(r), C.byref(c), C.byref(k), C.byref(ks), C.byref(h))
+        return r.value, c.value, k.value, ks.value, h.value
+
+    def _download_operator(self, l: int) -> StencilField:
+        rows, cols, k, _, _ = self.level_info(l)
+        out = np.empty((self.batch, rows, cols, k, k))
+        _lib.call("mgb_hier_get_operator", self._h, l, out.ctypes.data_as(_lib.P))
+        return StencilField(self.levels[l].spec, out[0] if self.batch == 1 else out[0])
+
+    def operator_batch(self, l: int) -> np.ndarray:
+        rows, cols, k, _, _ = self.level_info(l)
+        out = np.empty((self.batch, rows, cols, k, k))
+        _lib.call("mgb_hier_get_operator", self._h, l, out.ctypes.data_as(_lib.P))
+        return out
+
+    def _download_kernels(self, l: int, k: int) -> np.ndarray:
+        rows, cols, _, ks, _ = self.level_info(l)
+        out = np.empty((self.batch, rows, cols, ks, 3, 3))
+        _lib.call("mgb_hier_get_kernels", self._h, l, out.ctypes.data_as(_lib.P))
+        return out[0]
+
+    def kernels_batch(self, l: int) -> np.ndarray:
+        rows, cols, _, ks, _ = self.level_info(l)
+        out = np.empty((self.batch, rows, cols, ks, 3, 3))
+        _lib.call("mgb_hier_get_kernels", self._h, l, out.ctypes.data_as(_lib.P))
+        return out
+
+    # -- smoother bookkeeping ------------------------------------------------
+    def _sweeps(self, nu1, nu2):
+        """Resolve (nu1, nu2) and make sure the device holds each level's smoother."""
+        steps = set()
+        for lev in self.levels[:-1]:
+            sm = lev.smoother
+            if sm is None:
+                raise ConfigError(f"level {lev.index} has no smoother installed")
+            base = sm
+            if hasattr(sm, "inner") and hasattr(sm, "steps"):
+                steps.add(int(sm.steps))
+                base = sm.inner
+            else:
+                steps.add(1)
+            if base is not self._installed[lev.index]:
+                self._install(lev.index, base)
+        if nu1 is None or nu2 is None:
+            if len(steps) != 1:
+                raise ConfigError("levels use different sweep counts; pass nu1/nu2 explicitly")
+            nu = steps.pop()
+            nu1 = nu if nu1 is None else nu1
+            nu2 = nu if nu2 is None else nu2
+        return int(nu1), int(nu2)
+
+    def _install(self, l: int, sm):
+        """Upload an arbitrary per-point smoother (InferredSmoother / JacobiSmoother)."""
+        if isinstance(sm, DeviceSmoother) and sm._hier is self:
+            self._installed[l] = sm
+            return
+        if isinstance(sm, JacobiSmoother):
+            K, k, slope = sm.kernels(), 1, LEAKY_SLOPE
+        elif isinstance(sm, InferredSmoother) or hasattr(sm, "kernels"):
+            K, k, slope = np.asarray(sm.kernels, dtype=float), int(sm.k), float(sm.slope)
+        else:
+            raise UnsupportedOperationError(
+                f"smoother {type(sm).__name__} on level {l} has no per-point kernels for the B200 path")
+        if sm.spec != self.levels[l].spec:
+            raise ContractError(f"smoother on level {l} is bound to a different grid")
+        K = np.ascontiguousarray(np.broadcast_to(K, (self.batch,) + K.shape))
+        _lib.call("mgb_hier_set_kernels", self._h, l, k, K.ctypes.data_as(_lib.P), 0, slope, None)
+        self._installed[l] = sm
+
+    # -- device-resident entry points (torch CUDA tensors) -------------------
+    def run_cycles(self, f, u, cycles: int, nu1: int | None = None, nu2: int | None = None,
+                   history=None, u_zero: bool = False):
+        """Fixed-count V(nu1, nu2) loop entirely on the device: f, u are
+        (batch, rows, cols) or (rows, cols) fp64 CUDA tensors; returns the
+        (batch, cycles + 1) relative-residual history tensor (no host sync)."""
+        nu1, nu2 = self._sweeps(nu1, nu2)
+        t = dv.torch()
+        if history is None:
+            history = t.empty((self.batch, cycles + 1), dtype=t.float64, device=f.device)
+        w = self.acquire_work()
+        try:
+            _lib.call("mgb_run_cycles", self._h, w, dv.ptr(f), dv.ptr(u), nu1, nu2, int(cycles),
+                      1 if u_zero else 0, dv.ptr(history), dv.stream(f))
+            self.last_launches = int(_lib.lib().mgb_last_launch_count(w))
+        finally:
+            self.release_work(w)
+        return history
+
+    def run_cycles_host(self, f_host: np.ndarray, u_host: np.ndarray, cycles: int, nu1: int | None = None,
+                        nu2: int | None = None, history_host: np.ndarray | None = None, u_zero: bool = False,
+                        stream=None) -> np.ndarray:
+        """Host-buffer cycle loop through mgb_run_cycles_host: f_host / u_host are
+        C-contiguous fp64 arrays (pinned for full-speed copies); u_host is updated
+        in place; returns the (batch, cycles + 1) history."""
+        nu1, nu2 = self._sweeps(nu1, nu2)
+        if history_host is None:
+            history_host = np.empty((self.batch, cycles + 1))
+        for a in (f_host, u_host, history_host):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ContractError("host buffers must be C-contiguous float64")
+        w = self.acquire_work()
+        try:
+            _lib.call("mgb_run_cycles_host", self._h, w, f_host.ctypes.data_as(_lib.P),
+                      u_host.ctypes.data_as(_lib.P), nu1, nu2, int(cycles), 1 if u_zero else 0,
+                      history_host.ctypes.data_as(_lib.P), stream)
+            self.last_launches = int(_lib.lib().mgb_last_launch_count(w))
+        finally:
+            self.release_work(w)
+        return history_host
+
+    def solve_device(self, f, u, tol: float = 1e-6, max_iter: int = 100, nu1=None, nu2=None) -> SolveReport:
+        nu1, nu2 = self._sweeps(nu1, nu2)
+        hist = np.zeros(max_iter + 1)
+        nh, it, conv, secs = C.c_int(), C.c_int(), C.c_int(), C.c_double()
+        w = self.acquire_work()
+        try:
+            _lib.call("mgb_solve", self._h, w, dv.ptr(f), dv.ptr(u), nu1, nu2, float(tol), int(max_iter),
+                      hist.ctypes.data_as(_lib.PD), C.byref(nh), C.byref(it), C.byref(conv), C.byref(secs),
+                      dv.stream(f))
+        finally:
+            self.release_work(w)
+        return SolveReport(it.value, hist[:nh.value].tolist(), bool(conv.value), secs.value)
+
+
+# ---------------------------------------------------------------------------
+# module API (hierarchy.py:62-214)
+
+def _level_specs(spec: GridSpec, levels: int):
+    specs, transfers = [spec], []
+    for step in range(levels - 1):
+        try:
+            tp = coarsen_full(specs[-1])
+        except ConfigError as exc:
+            raise ConfigError(f"level {step}: {exc}") from exc
+        if tp.coarse.n_active >= specs[-1].n_active:
+            raise ConfigError(f"level {step}: coarsening does not shrink the active set")
+        transfers.append(tp)
+        specs.append(tp.coarse)
+    transfers.append(None)
+    return specs, transfers
+
+
+def build_hierarchy(A: StencilField, levels: int, scheme: str = "full", device: int | None = None) -> MultigridHierarchy:
+    """hierarchy.py:70-88: Galerkin chain + coarsest LU, built on the GPU."""
+    if levels < 2:
+        raise ConfigError("a hierarchy needs at least two levels")
+    if scheme == "redblack":
+        raise UnsupportedOperationError("red-black coarsening is not on the B200 path")
+    if scheme != "full":
+        raise ConfigError(f"unknown coarsening scheme {scheme!r}")
+    if A.k != 3:
+        raise UnsupportedOperationError("the device hierarchy takes 3x3 fine-level stencils")
+    specs, transfers = _level_specs(A.spec, levels)
+    return _build(np.ascontiguousarray(A.data)[None], A.spec, levels, specs, transfers, A, device)
+
+
+def build_hierarchy_batch(A_batch: np.ndarray, levels: int, spec: GridSpec | None = None,
+                          device: int | None = None) -> MultigridHierarchy:
+    """A batch of independent problems on one grid (config 4): A_batch is
+    (batch, rows, cols, 3, 3); every kernel runs over the batch in one launch."""
+    A_batch = np.ascontiguousarray(np.asarray(A_batch, dtype=float))
+    if A_batch.ndim != 5 or A_batch.shape[3:] != (3, 3):
+        raise ContractError("batched operators must be (batch, rows, cols, 3, 3)")
+    if not np.isfinite(A_batch).all():
+        from .errors import NumericError
+        raise NumericError("non-finite stencil weights")
+    if levels < 2:
+        raise ConfigError("a hierarchy needs at least two levels")
+    rows, cols = A_batch.shape[1:3]
+    if spec is None:
+        spec = GridSpec(rows, cols, 1.0 / (rows + 1), np.ones((rows, cols), bool))
+    specs, transfers = _level_specs(spec, levels)
+    return _build(A_batch, spec, levels, specs, transfers, None, device)
+
+
+def _build(A_host, spec, levels, specs, transfers, A0, device):
+    dev = dv.current_device() if device is None else device
+    dv.require_cuda(dev)
+    mask = None if spec.all_active else np.ascontiguousarray(spec.mask.astype(np.uint8))
+    h = C.c_void_p()
+    _lib.call("mgb_hier_build", dev, A_host.shape[0], spec.rows, spec.cols, float(spec.spacing),
+              A_host.ctypes.data_as(_lib.P), 0, None if mask is None else mask.ctypes.data_as(_lib.P),
+              int(levels), None, C.byref(h))
+    return MultigridHierarchy(h, dev, A_host.shape[0], specs, transfers, A0)
+
+
+def coarse_solve(hier: MultigridHierarchy, f: GridFunction) -> GridFunction:
+    """hierarchy.py:91-93 (LU solve on the device)."""
+    x = dv.to_dev(f.values)
+    out = dv.empty(x.shape)
+    _lib.call("mgb_coarse_solve", hier.handle, dv.ptr(x), dv.ptr(out), dv.stream(out))
+    return GridFunction(f.spec, dv.host(out))
+
+
+def v_cycle(hier: MultigridHierarchy, level: int, f: GridFunction, u: GridFunction,
+            nu1: int | None = None, nu2: int | None = None) -> GridFunction:
+    """hierarchy.py:96-111; V(nu1, nu2) from RepeatedSmoother wrappers or the arguments."""
+    if level < 0 or level >= hier.depth:
+        raise ConfigError(f"v_cycle: level {level} out of range")
+    lev = hier.levels[level]
+    if f.spec != lev.spec or u.spec != lev.spec:
+        raise ConfigError(f"v_cycle: data not on level-{level} spec")
+    if level == hier.depth - 1:
+        return coarse_solve(hier, f)
+    nu1, nu2 = hier._sweeps(nu1, nu2)
+    fd = dv.to_dev(f.values)
+    ud = dv.to_dev(u.values)
+    w = hier.acquire_work()
+    try:
+        _lib.call("mgb_vcycle", hier.handle, w, level, dv.ptr(fd), dv.ptr(ud), nu1, nu2, dv.stream(ud))
+    finally:
+        hier.release_work(w)
+    return GridFunction(lev.spec, dv.host(ud))
+
+
+def cycle_correction(hier: MultigridHierarchy, r: GridFunction) -> GridFunction:
+    """hierarchy.py:114-116."""
+    return v_cycle(hier, 0, r, zeros(hier.finest.spec))
+
+
+def solve(hier: MultigridHierarchy, f: GridFunction, u0: GridFunction | None = None, tol: float = 1e-6,
+          max_iter: int = 100, nu1: int | None = None, nu2: int | None = None):
+    """hierarchy.py:119-146: returns (u, SolveReport); NonConvergedError on divergence."""
+    if tol <= 0.0:
+        raise ConfigError("tolerance must be positive")
+    if hier.batch != 1:
+        raise ContractError("solve() takes a single-problem hierarchy; use run_cycles for batches")
+    spec = hier.finest.spec
+    if f.spec != spec:
+        raise ConfigError("solve: right-hand side not on the finest spec")
+    fd = dv.to_dev(f.values)
+    ud = dv.zeros(fd.shape) if u0 is None else dv.to_dev(u0.values)
+    rep = hier.solve_device(fd, ud, tol, max_iter, nu1, nu2)
+    return GridFunction(spec, dv.host(ud)), rep
+
+
+def equip_classical(hier: MultigridHierarchy, kind: str = "jacobi", omega: float = 2.0 / 3.0) -> MultigridHierarchy:
+    """hierarchy.py:152-161 (jacobi on the device)."""
+    if kind == "gauss-seidel":
+        raise UnsupportedOperationError("Gauss-Seidel (sequential sweep) is not on the B200 path")
+    if kind != "jacobi":
+        raise ConfigError(f"unknown classical smoother {kind!r}")
+    _lib.call("mgb_hier_equip_jacobi", hier.handle, float(omega), None)
+    for lev in hier.levels[:-1]:
+        sm = DeviceSmoother(hier, lev.index, 1, LEAKY_SLOPE, "jacobi", omega)
+        lev.smoother = sm
+        hier._installed[lev.index] = sm
+    return hier
+
+
+def equip_inferred(hier: MultigridHierarchy, net: KernelInferenceNet, precision: int = 64) -> MultigridHierarchy:
+    """hierarchy.py:207-214: CNN inference of every smoothed level on the device."""
+    for lev in hier.levels[:-1]:
+        if hier.level_info(lev.index)[2] != 3:
+            raise ConfigError("kernel inference needs 3x3 stencils on every level")
+    W = net.flat_weights()
+    _lib.call("mgb_hier_equip_inferred", hier.handle, VARIANT_ID[net.variant], int(net.k),
+              W.ctypes.data_as(_lib.P), W.size, float(net.slope), int(precision), None)
+    for lev in hier.levels[:-1]:
+        sm = DeviceSmoother(hier, lev.index, net.k, net.slope, f"inferred-{net.variant}")
+        lev.smoother = sm
+        hier._installed[lev.index] = sm
+    return hier
+
+
+def equip_conv_init(*a, **k):
+    raise UnsupportedOperationError("shared-kernel ConvSmoother training is not on the B200 path")
+
+
+retarget = equip_trained = equip_conv_init

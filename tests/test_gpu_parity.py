@@ -1,0 +1,333 @@
+"""GPU parity of the CUDA path (through the C-ABI via the facade) against the
+golden vectors produced by the unmodified reference and against the CPU
+oracle.  Tolerances:
+  * stencil / transfer / Galerkin: bit-exact (same operation order, no FMA);
+  * hierarchy operators: bit-exact; level sizes, masks, k: exact;
+  * fp64 CNN kernels: max|dK| / max|K| <= 1e-13 per level;
+  * V-cycle histories and u: 1e-10 relative (+1e-14 absolute on histories);
+  * fp32 CNN inference: max|dK| / max|K| <= 1e-5 per level.
+"""
+
+import math
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2102_12071_b200 as mg
+from oracle import mg_oracle as mo
+from paper_2102_12071_b200 import problems as gen
+
+from cases import LARGE, SMALL, load
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ["square9", "lshape9", "cylinder9", "square10"]
+HIST_RTOL, HIST_ATOL = 1e-10, 1e-14
+
+
+def spec_of(mask, h):
+    return mg.GridSpec(mask.shape[0], mask.shape[1], h, mask)
+
+
+def net_of(name, nets_dir=None):
+    import os
+    from conftest import GOLDEN
+    return mg.load_model(os.path.join(GOLDEN, f"net_{name}.json"))
+
+
+def assert_hist(h, g):
+    h = np.asarray(h)
+    g = np.asarray(g)
+    assert h.shape == g.shape
+    assert np.all(np.abs(h - g) <= HIST_RTOL * np.abs(g) + HIST_ATOL), (h, g)
+
+
+# ---------------------------------------------------------------------------
+# stateless ops: bit-exact against the reference
+
+@pytest.mark.parametrize("key", KEYS)
+def test_apply_stencil_bit_exact(ops_golden, key):
+    g = ops_golden
+    spec = spec_of(g[f"{key}_mask"], 0.1)
+    out = mg.apply_stencil(mg.StencilField(spec, g[f"{key}_A"]), mg.GridFunction(spec, g[f"{key}_u"]))
+    assert np.array_equal(out.values, g[f"{key}_Au"])
+
+
+@pytest.mark.parametrize("key", KEYS)
+def test_transfers_bit_exact(ops_golden, key):
+    g = ops_golden
+    spec = spec_of(g[f"{key}_mask"], 0.1)
+    tp = mg.coarsen_full(spec)
+    assert np.array_equal(tp.coarse.mask, g[f"{key}_maskc"])
+    rc = mg.restrict(tp, mg.GridFunction(spec, g[f"{key}_u"]))
+    assert np.array_equal(rc.values, g[f"{key}_rc"])
+    pe = mg.prolong(tp, mg.GridFunction(tp.coarse, g[f"{key}_ec"]))
+    assert np.array_equal(pe.values, g[f"{key}_Pe"])
+
+
+@pytest.mark.parametrize("key", KEYS)
+def test_galerkin_bit_exact(ops_golden, key):
+    g = ops_golden
+    spec = spec_of(g[f"{key}_mask"], 0.1)
+    Ac = mg.galerkin_product(mg.StencilField(spec, g[f"{key}_A"]), mg.coarsen_full(spec))
+    assert np.array_equal(Ac.data, g[f"{key}_Ac"])
+
+
+def test_constant_prolongs_to_half():
+    """tests/test_transfer.py:50 of the reference: P(1) = 0.5 at odd/odd points."""
+    spec = mg.full_spec(15)
+    tp = mg.coarsen_full(spec)
+    pe = mg.prolong(tp, mg.GridFunction(tp.coarse, np.ones((7, 7))))
+    assert np.all(pe.values[1::2, 1::2] == 0.5)
+
+
+@pytest.mark.parametrize("key", KEYS)
+def test_device_lu(ops_golden, key):
+    import ctypes as C
+    from paper_2102_12071_b200 import _lib, device as dv
+    g = ops_golden
+    M = mo.materialize(g[f"{key}_Ac"], g[f"{key}_maskc"])
+    n = M.shape[0]
+    lu = dv.to_dev(M)
+    perm = dv.to_dev(np.zeros(n, np.int32))
+    _lib.call("mgb_lu_factor", n, dv.ptr(lu), dv.ptr(perm), dv.stream(lu))
+    assert np.array_equal(dv.host(perm), g[f"{key}_perm"])
+    assert np.array_equal(dv.host(lu), g[f"{key}_lu"])
+    b = dv.to_dev(g[f"{key}_lub"])
+    x = dv.empty((n,))
+    _lib.call("mgb_lu_solve", n, dv.ptr(lu), dv.ptr(perm), dv.ptr(b), dv.ptr(x), dv.stream(x))
+    assert np.array_equal(dv.host(x), g[f"{key}_lux"])
+
+
+def test_singular_coarsest_raises_with_pivot():
+    from paper_2102_12071_b200 import _lib, device as dv
+    M = np.array([[1.0, 2.0], [2.0, 4.0]])
+    lu = dv.to_dev(M)
+    perm = dv.to_dev(np.zeros(2, np.int32))
+    with pytest.raises(mg.SingularMatrixError) as ei:
+        _lib.call("mgb_lu_factor", 2, dv.ptr(lu), dv.ptr(perm), dv.stream(lu))
+    assert ei.value.pivot_index == 1
+    # a zero operator makes the hierarchy's coarsest LU singular
+    spec = mg.full_spec(7)
+    with pytest.raises(mg.SingularMatrixError):
+        mg.build_hierarchy(mg.StencilField(spec, np.zeros((7, 7, 3, 3))), 2)
+
+
+# ---------------------------------------------------------------------------
+# hierarchies: operators, kernels, cycles
+
+def _equip(h, smoother, precision=64):
+    if smoother == "jacobi":
+        return mg.equip_classical(h, "jacobi")
+    return mg.equip_inferred(h, net_of(smoother), precision)
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_hierarchy_operators_and_kernels(name):
+    c = load(name)
+    g = c["golden"]
+    spec = spec_of(c["mask"], float(g["h"]))
+    h = mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"])
+    assert h.depth == c["levels"]
+    for l in range(h.depth):
+        lev = h.levels[l]
+        assert np.array_equal(lev.spec.mask, g[f"mask{l}"])
+        assert np.array_equal(lev.operator.data, g[f"A{l}"]), f"level {l}"
+    _equip(h, c["smoother"])
+    for l in range(h.depth - 1):
+        if f"K{l}" in g:
+            assert rel_err(h.levels[l].smoother.kernels, g[f"K{l}"]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", sorted(SMALL) + sorted(LARGE))
+def test_cycles_match_reference_history(name):
+    c = load(name)
+    g = c["golden"]
+    spec = spec_of(c["mask"], float(g["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), c["smoother"])
+    from paper_2102_12071_b200 import device as dv
+    f = dv.to_dev(np.where(c["mask"], c["f"], 0.0))
+    u = dv.zeros(f.shape)
+    hist = h.run_cycles(f, u, c["cycles"], c["nu"], c["nu"], u_zero=True)
+    assert_hist(dv.host(hist)[0], g["history"])
+    assert rel_err(dv.host(u), g["u"]) <= 1e-10
+
+
+def test_v_cycle_facade_with_repeated_smoother():
+    """The reference's V(2,2) convention (RepeatedSmoother) maps to 2 device sweeps."""
+    c = load("case_rot15_conv_v22")
+    g = c["golden"]
+    spec = spec_of(c["mask"], float(g["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), "conv")
+    for lev in h.levels[:-1]:
+        lev.smoother = mg.RepeatedSmoother(lev.smoother, lev.operator, 2)
+    F = mg.GridFunction(spec, c["f"])
+    u = mg.zeros(spec)
+    for _ in range(c["cycles"]):
+        u = mg.v_cycle(h, 0, F, u)
+    assert rel_err(u.values, g["u"]) <= 1e-10
+
+
+def test_solve_report_contract():
+    """tests/test_hierarchy.py:68 of the reference: history[0] = 1 from u0 = 0,
+    len = iterations + 1, certified residual, converged flag."""
+    c = load("case_var31_conv_v22")
+    spec = spec_of(c["mask"], float(c["golden"]["h"]))
+    A = mg.StencilField(spec, c["A0"])
+    h = _equip(mg.build_hierarchy(A, c["levels"]), "conv")
+    F = mg.GridFunction(spec, c["f"])
+    u, rep = mg.solve(h, F, tol=1e-8, max_iter=50)
+    assert rep.converged and rep.residual_history[0] == 1.0
+    assert len(rep.residual_history) == rep.iterations + 1
+    r = (F - mg.apply_stencil(A, u)).norm() / F.norm()
+    assert abs(r - rep.residual_history[-1]) <= 1e-12 * max(r, 1e-300) + 1e-15
+    # oracle cross-check of the whole history (V(1,1), solve semantics)
+    ho = mo.equip_inferred(mo.build_hierarchy(c["A0"], c["levels"]), mo.load_net_json(
+        __import__("os").path.join(__import__("conftest").GOLDEN, "net_conv.json")))
+    _, hist, it, conv = mo.solve(ho, c["f"], tol=1e-8, max_iter=50)
+    assert it == rep.iterations and conv
+    assert_hist(rep.residual_history, hist)
+    # non-converged flag at a tiny max_iter
+    _, rep2 = mg.solve(h, F, tol=1e-30, max_iter=2)
+    assert rep2.iterations == 2 and not rep2.converged
+
+
+def test_solve_divergence_raises():
+    """the pi/6-trained net diverges on a pi/3 operator -> NonConvergedError."""
+    n = 63
+    spec = mg.full_spec(n)
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, gen.rotated_fd(n, math.pi / 3, 0.01)), 5), "conv")
+    F = mg.GridFunction(spec, gen.uniform_rhs(n, 0))
+    try:
+        mg.solve(h, F, tol=1e-12, max_iter=200)
+    except mg.NonConvergedError:
+        return
+    pytest.skip("did not diverge at this size")
+
+
+def test_coarse_solve_exact():
+    c = load("case_rot15_conv_v22")
+    spec = spec_of(c["mask"], float(c["golden"]["h"]))
+    h = mg.build_hierarchy(mg.StencilField(spec, c["A0"]), 2)
+    Ac = h.levels[1].operator
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(Ac.data.shape[:2])
+    x = mg.coarse_solve(h, mg.GridFunction(Ac.spec, b))
+    want = np.linalg.solve(mo.materialize(Ac.data, Ac.spec.mask), b.ravel())
+    assert np.max(np.abs(x.values.ravel() - want)) < 1e-10
+
+
+def test_batched_hierarchy_matches_single_problems():
+    """Config 4 path: two 511^2 problems in one batched hierarchy."""
+    from paper_2102_12071_b200 import device as dv
+    cs = [load("c4_p0"), load("c4_p1")]
+    A = np.stack([c["A0"] for c in cs])
+    h = mg.build_hierarchy_batch(A, 8)
+    mg.equip_inferred(h, net_of("conv"))
+    f = dv.to_dev(np.stack([c["f"] for c in cs]))
+    u = dv.zeros(f.shape)
+    hist = dv.host(h.run_cycles(f, u, 10, 1, 1, u_zero=True))
+    U = dv.host(u)
+    for b, c in enumerate(cs):
+        assert_hist(hist[b], c["golden"]["history"])
+        assert rel_err(U[b], c["golden"]["u"]) <= 1e-10
+
+
+def test_fp32_inference_within_tolerance():
+    c = load("c1_fd_conv")
+    spec = mg.full_spec(255)
+    A = mg.StencilField(spec, c["A0"])
+    h64 = _equip(mg.build_hierarchy(A, 7), "conv", 64)
+    h32 = _equip(mg.build_hierarchy(A, 7), "conv", 32)
+    for l in range(6):
+        K64 = h64.levels[l].smoother.kernels
+        K32 = h32.levels[l].smoother.kernels
+        assert rel_err(K32, K64) <= 1e-5
+    hf = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), 7), "fc", 32)
+    hd = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), 7), "fc", 64)
+    for l in range(6):
+        assert rel_err(hf.levels[l].smoother.kernels, hd.levels[l].smoother.kernels) <= 1e-5
+
+
+# ---------------------------------------------------------------------------
+# oracle cross-checks at sizes without golden vectors (masks, rectangles, k>1)
+
+@pytest.mark.parametrize("rows,cols,geom,nu,variant", [
+    (48, 64, "square", 1, "fc"),
+    (63, 63, "cylinder", 2, "conv"),
+    (33, 45, "square", 2, "conv_k2"),
+    (127, 127, "lshape", 1, "conv"),
+])
+def test_random_operators_vs_oracle(rows, cols, geom, nu, variant):
+    from paper_2102_12071_b200 import device as dv
+    rng = np.random.default_rng(rows * cols)
+    mask = gen.geometry_mask(geom, rows) if rows == cols else np.ones((rows, cols), bool)
+    A = gen.rotated_fd(rows, 0.7, 0.05, cols=cols)
+    A = A * (1.0 + 0.3 * rng.random((rows, cols, 1, 1)))   # per-point variation
+    f = np.where(mask, rng.uniform(-1, 1, (rows, cols)), 0.0)
+    levels = 4
+    spec = spec_of(mask, 1.0 / (rows + 1))
+    net = net_of(variant)
+    h = mg.equip_inferred(mg.build_hierarchy(mg.StencilField(spec, A), levels), net)
+    fd = dv.to_dev(f)
+    u = dv.zeros(f.shape)
+    hist = dv.host(h.run_cycles(fd, u, 5, nu, nu, u_zero=True))[0]
+    ho = mo.equip_inferred(mo.build_hierarchy(A, levels, mask), mo.load_net_json(
+        __import__("os").path.join(__import__("conftest").GOLDEN, f"net_{variant}.json")))
+    uo, ho_hist = mo.run_cycles(ho, f, 5, nu, nu)
+    assert_hist(hist, ho_hist)
+    assert rel_err(dv.host(u), uo) <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# properties at full benchmark size (config 2: 4095^2)
+
+@pytest.mark.slow
+def test_config2_properties_full_size():
+    """Size-independent checks at 4095^2: (1) runs are bitwise reproducible,
+    (2) the Jacobi-smoothed V-cycle is linear in f (V(f1+f2) = V(f1)+V(f2) from
+    u = 0, to round-off), (3) the learned-smoother history decreases."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    n = 4095
+    A = gen.rotated_fd(n, math.pi / 4, 1e-3)
+    h = mg.equip_inferred(mg.build_hierarchy(mg.StencilField(mg.full_spec(n), A), 11), net_of("conv"))
+    f = dv.to_dev(gen.uniform_rhs(n, 1))
+    u1, u2 = dv.zeros(f.shape), dv.zeros(f.shape)
+    h1 = h.run_cycles(f, u1, 3, 2, 2, u_zero=True).clone()
+    h2 = h.run_cycles(f, u2, 3, 2, 2, u_zero=True).clone()
+    assert t.equal(u1, u2) and t.equal(h1, h2)
+    hh = dv.host(h1)[0]
+    assert np.all(np.diff(hh) < 0)
+    hj = mg.equip_classical(mg.build_hierarchy(mg.StencilField(mg.full_spec(n), A), 11), "jacobi")
+    fa = dv.to_dev(gen.uniform_rhs(n, 5))
+    fb = dv.to_dev(gen.uniform_rhs(n, 6))
+    ua, ub, uab = dv.zeros(f.shape), dv.zeros(f.shape), dv.zeros(f.shape)
+    hj.run_cycles(fa, ua, 1, 1, 1, u_zero=True)
+    hj.run_cycles(fb, ub, 1, 1, 1, u_zero=True)
+    hj.run_cycles(fa + fb, uab, 1, 1, 1, u_zero=True)
+    err = (uab - ua - ub).abs().max().item() / uab.abs().max().item()
+    assert err < 1e-12
+
+
+def test_concurrent_solves_share_one_hierarchy():
+    """a built hierarchy is immutable; concurrent solves are safe."""
+    c = load("case_var31_conv_v22")
+    spec = spec_of(c["mask"], float(c["golden"]["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), "conv")
+    F = mg.GridFunction(spec, c["f"])
+    ref = mg.solve(h, F, tol=1e-8)[1].residual_history
+    out = {}
+
+    def run(i):
+        import torch
+        with torch.cuda.stream(torch.cuda.Stream()):
+            out[i] = mg.solve(h, F, tol=1e-8)[1].residual_history
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    for i in range(4):
+        assert out[i] == ref
