@@ -5,7 +5,8 @@
 Workload (N = 1): BASELINE.json config 2 — rotated anisotropic Laplacian
 (reference FD stencil, eps = 1e-3, theta = pi/4) on a 4095^2 interior grid,
 11 levels, Galerkin coarse operators, per-point smoother kernels from the
-seeded conv inference net (tests/golden/net_conv.json = SURVEY G4 fixture),
+seeded conv inference net (tests/golden/net_conv_c2.json: the reference's own
+SURVEY-G4 training recipe run at the config's theta/eps),
 b ~ U[-1, 1] (seed 1), u0 = 0.  One step = one 10-cycle V(2,2) solve including
 the per-cycle residual history (as hierarchy.solve times it).  Multi-GPU (torchrun):
 every rank solves its own copy of the problem (weak scaling, no data-path
@@ -36,6 +37,9 @@ CONFIGS = {
     "c2": (4095, math.pi / 4, 1e-3, 11, 2, 10, 1),
     "c1": (255, math.pi / 6, 0.01, 7, 2, 20, 0),
 }
+# inference net per config: the SURVEY G4 training recipe run by the reference at the
+# config's own (theta, eps) (tests/golden/make_golden.py)
+NETS = {"c2": "net_conv_c2.json", "c1": "net_conv.json"}
 # algorithmic bytes of one pass, per-point fp64 model
 SWEEP_BYTES_PER_POINT = 168          # read u, f, A(9), M(9); write u
 CPU_SAMPLE_N = 1023                  # bounded CPU sample: same operator family at 1023^2
@@ -143,7 +147,7 @@ def build_problem(cfg_name, device):
     n, theta, eps, levels, nu, cycles, seed = CONFIGS[cfg_name]
     A = gen.rotated_fd(n, theta, eps)
     f = gen.uniform_rhs(n, seed)
-    net = mg.load_model(os.path.join(ROOT, "paper_2102_12071_b200", "data", "net_conv.json"))
+    net = mg.load_model(os.path.join(ROOT, "paper_2102_12071_b200", "data", NETS[cfg_name]))
     import torch
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -171,7 +175,7 @@ def cpu_sample(cfg_name, steps=1, warmup=0):
     f = gen.uniform_rhs(n, seed)
     t0 = time.perf_counter()
     h = mo.build_hierarchy(A, levels)
-    mo.equip_inferred(h, mo.load_net_json(os.path.join(ROOT, "paper_2102_12071_b200", "data", "net_conv.json")))
+    mo.equip_inferred(h, mo.load_net_json(os.path.join(ROOT, "paper_2102_12071_b200", "data", NETS[cfg_name])))
     setup = time.perf_counter() - t0
     u = np.zeros((n, n))
     fn = float(np.linalg.norm(f))

@@ -81,6 +81,7 @@ struct mgb_hier {
   int32_t* perm = nullptr;  // batch x nc
   int32_t* actp = nullptr;  // nc flat indices of active coarsest points
   double slope = 0.01;
+  int version = 0;          // bumped whenever smoother kernels are (re)installed
   ~mgb_hier() {
     DeviceGuard dg(device);
     for (auto& l : lv) {
@@ -123,6 +124,7 @@ struct mgb_work {
   double *hf = nullptr, *hu = nullptr, *hh = nullptr;  // host-call staging (level 0 f, u, history)
   int64_t hh_cap = 0;
   std::vector<GraphEntry> graphs;
+  int graph_version = -1;   // hierarchy version the cached graphs were captured against
   int64_t last_launches = 0;
   ~mgb_work() {
     DeviceGuard dg(h ? h->device : -1);
@@ -526,6 +528,7 @@ extern "C" int mgb_hier_operator_planes(const mgb_hier* h, int level, const doub
 }
 
 static int alloc_kernels(mgb_hier* h, LevelD& l, int kst) {
+  ++h->version;
   if (l.K && l.ks == kst) return MGB_OK;
   dfree(l.K);
   l.ks = 0;
@@ -832,11 +835,26 @@ extern "C" int mgb_smooth(const mgb_hier* h, mgb_work* w, int level, const doubl
 
 // Capture (once per key) and launch a graph.  mode 0: run_cycles; mode 1: one
 // solve iteration (cycle + residual norm into scratch).
+// allocations are not allowed while capturing: size the workspace first
+static int prepare_work(mgb_work* w) {
+  for (int l = 0; l + 1 < w->h->depth(); ++l)
+    if (w->h->lv[l].ks > 1)
+      if (int st = ensure_generic(w, l)) return st;
+  return MGB_OK;
+}
+
 static int get_graph(mgb_work* w, const GraphKey& key, GraphEntry** out) {
+  if (w->graph_version != w->h->version) {
+    for (auto& g : w->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    w->graphs.clear();
+    w->graph_version = w->h->version;
+  }
   GraphEntry* ent = nullptr;
   for (auto& g : w->graphs)
     if (g.key == key) ent = &g;
   if (!ent) {
+    if (int st = prepare_work(w)) return st;
     const int64_t l0 = g_launches;
     cudaGraph_t graph = nullptr;
     MGB_CUDA_TRY(cudaStreamBeginCapture(w->cap, cudaStreamCaptureModeThreadLocal));

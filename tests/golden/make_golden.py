@@ -57,6 +57,14 @@ def make_nets():
         rs.save_model(path, net, {"fixture": "SURVEY G4", "operator": "rotated FD 31x31 pi/6 0.01"})
         print(f"trained {variant} net in {time.time() - t0:.1f}s")
         out[variant] = rs.load_model(path)
+    # the same recipe at config 2's parameters (theta = pi/4, anisotropy = 1e-3): the bench net
+    path = os.path.join(HERE, "net_conv_c2.json")
+    if not os.path.exists(path):
+        A31c2 = rp.assemble_rotated_laplacian(rg.full_spec(31), math.pi / 4, 1e-3)
+        cfg = rtr.TrainConfig(samples=10, max_steps=2, batch_size=5, epochs=20, seed=0)
+        net, _, _ = rtr.train_inference_net(A31c2, "conv", 4, cfg, k=1, seed_net=0)
+        rs.save_model(path, net, {"fixture": "SURVEY G4 recipe at config-2 parameters"})
+    out["conv_c2"] = rs.load_model(path)
     path = os.path.join(HERE, "net_conv_k2.json")
     if not os.path.exists(path):
         net = rs.inference_net("conv", k=2, seed=5)
