@@ -129,6 +129,14 @@ int mgb_hier_get_mask(const mgb_hier* h, int level, uint8_t* out_host);
    batch*rows*cols each, plane o = (di+1)*3 + (dj+1)). */
 int mgb_hier_operator_planes(const mgb_hier* h, int level, const double** planes_dev);
 
+/* Storage of operator / smoother tables in the hot loop: mode 0 (default) keeps, per
+   level and table, an exact 25-entry band-class representation when the table is
+   constant away from the boundary (constant-coefficient problems); mode 1 forces
+   per-point planes everywhere.  Results are bit-identical in both modes.
+   mgb_hier_storage_info reports whether level `level`'s A / M tables are class-compact. */
+int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream);
+int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_classed);
+
 /* equip_inferred (hierarchy.py:207-214): per-level CNN inference on levels 0..L-2. */
 int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const double* weights_host,
                             int64_t n_weights, double slope, int precision, void* stream);

@@ -3,13 +3,16 @@
 // Reference map: hierarchy.py build_hierarchy :70-88, coarse_solve :91-93,
 // v_cycle :96-111, solve :119-146, equip_classical :152-161, equip_inferred
 // :207-214; cli.py RepeatedSmoother :365-377 (V(nu1, nu2)); errors.py.
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
+#include "mgb_cycle.h"
 #include "mgb_internal.h"
 
 namespace mgb {
@@ -69,8 +72,12 @@ struct LevelD {
   double* A = nullptr;     // batch x 9 planes of n
   double* K = nullptr;     // batch x ks x 9 planes of n
   uint8_t* mask = nullptr; // null = all active
+  double* Acls = nullptr;  // band-class tables (batch x 25 x 9) when A is class-constant
+  double* Kcls = nullptr;  // band-class tables (batch x 25 x ks x 9) when M is class-constant
   std::vector<uint8_t> hmask;
   int64_t nact = 0;
+  Op opA() const { return Op{A, Acls, n, 1}; }
+  Op opK() const { return Op{K, Kcls, n, ks}; }
 };
 
 struct mgb_hier {
@@ -82,12 +89,15 @@ struct mgb_hier {
   int32_t* actp = nullptr;  // nc flat indices of active coarsest points
   double slope = 0.01;
   int version = 0;          // bumped whenever smoother kernels are (re)installed
+  int compact = 1;          // use band-class tables where they represent a table exactly
   ~mgb_hier() {
     DeviceGuard dg(device);
     for (auto& l : lv) {
       dfree(l.A);
       dfree(l.K);
       dfree(l.mask);
+      dfree(l.Acls);
+      dfree(l.Kcls);
     }
     dfree(lu);
     dfree(perm);
@@ -319,6 +329,55 @@ static int64_t count_active(const std::vector<uint8_t>& m) {
   return c;
 }
 
+// Band-class compaction (mgb_cycle.cu): if every point of the table equals its
+// class representative, keep the 25 class tables (exact) for the hot loop.
+static int classify_table(mgb_hier* h, int l, const double* planes, int ks, double** cls_out, cudaStream_t s) {
+  dfree(*cls_out);
+  LevelD& lv = h->lv[l];
+  if (!h->compact || lv.mask || !planes) return MGB_OK;
+  int64_t rep[25];
+  for (int c = 0; c < 25; ++c) rep[c] = -1;
+  for (int i = 0; i < lv.rows; ++i)
+    for (int j = 0; j < lv.cols; ++j) {
+      const int c = host_band(i, lv.rows) * 5 + host_band(j, lv.cols);
+      if (rep[c] < 0) rep[c] = (int64_t)i * lv.cols + j;
+      if (i > 2 && i < lv.rows - 3 && j > 2) j = std::max(j, lv.cols - 4);  // skip the interior
+    }
+  int64_t* drep = nullptr;
+  int* flag = nullptr;
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&drep), sizeof(rep), s));
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), s));
+  MGB_CUDA_TRY(cudaMemcpyAsync(drep, rep, sizeof(rep), cudaMemcpyHostToDevice, s));
+  MGB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  const Op T{planes, nullptr, lv.n, ks};
+  MGB_CUDA_TRY(launch_classify(h->grid(l), T, drep, flag, s));
+  int hf = 1;
+  MGB_CUDA_TRY(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (!hf) {
+    MGB_CUDA_TRY(dalloc(cls_out, (size_t)h->batch * 25 * ks * 9));
+    MGB_CUDA_TRY(launch_gather_cls(h->grid(l), T, drep, *cls_out, s));
+  }
+  MGB_CUDA_TRY(cudaFreeAsync(drep, s));
+  MGB_CUDA_TRY(cudaFreeAsync(flag, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  return MGB_OK;
+}
+
+static int classify_all(mgb_hier* h, cudaStream_t s) {
+  for (int l = 0; l < h->depth(); ++l) {
+    LevelD& lv = h->lv[l];
+    if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s)) return st;
+    if (lv.K) {
+      if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s)) return st;
+    } else {
+      dfree(lv.Kcls);
+    }
+  }
+  ++h->version;
+  return MGB_OK;
+}
+
 extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double spacing,
                               const double* A0, int a0_on_device, const uint8_t* mask_host,
                               int levels, void* stream, mgb_hier** out) {
@@ -454,7 +513,25 @@ extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double 
         return MGB_SINGULAR;
       }
   }
+  if (const char* e = getenv("MGB_STORAGE")) h->compact = std::string(e) != "planes";
+  if (int st = classify_all(h.get(), s)) return st;
   *out = h.release();
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (mode != 0 && mode != 1) return fail(MGB_CONFIG, "storage mode must be 0 (auto) or 1 (per-point planes)");
+  DeviceGuard dg(h->device);
+  h->compact = mode == 0;
+  return classify_all(h, S(stream));
+}
+
+extern "C" int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_classed) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  if (a_classed) *a_classed = h->lv[level].Acls != nullptr;
+  if (k_classed) *k_classed = h->lv[level].Kcls != nullptr;
   return MGB_OK;
 }
 
@@ -560,7 +637,7 @@ extern "C" int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const 
   h->slope = slope;
   MGB_CUDA_TRY(cudaFreeAsync(w, s));
   MGB_CUDA_TRY(cudaStreamSynchronize(s));
-  return MGB_OK;
+  return classify_all(h, s);
 }
 
 extern "C" int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream) {
@@ -584,7 +661,7 @@ extern "C" int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream) {
   MGB_CUDA_TRY(cudaStreamSynchronize(s));
   for (int l = 0; l + 1 < L; ++l)
     if (hf[l]) return fail(MGB_CONFIG, "jacobi: operator has zero diagonal entries");
-  return MGB_OK;
+  return classify_all(h, s);
 }
 
 extern "C" int mgb_hier_set_kernels(mgb_hier* h, int level, int kst, const double* K, int on_device,
@@ -610,7 +687,7 @@ extern "C" int mgb_hier_set_kernels(mgb_hier* h, int level, int kst, const doubl
   if (tmp) MGB_CUDA_TRY(cudaFreeAsync(tmp, s));
   h->slope = slope;
   MGB_CUDA_TRY(cudaStreamSynchronize(s));
-  return MGB_OK;
+  return classify_all(h, s);
 }
 
 extern "C" int mgb_coarse_solve(const mgb_hier* h, const double* f_dev, double* x_dev, void* stream) {
@@ -654,8 +731,8 @@ extern "C" int mgb_restrict_residual(const mgb_hier* h, int level, const double*
   if (int st = check_level(h, level, true)) return st;
   DeviceGuard dg(h->device);
   const LevelD& l = h->lv[level];
-  MGB_CUDA_TRY(launch_resid_restrict(h->grid(level), tab_soa(l.A, l.n, 1), l.mask, h->lv[level + 1].mask,
-                                     f_dev, u_dev, rc_dev, S(stream)));
+  MGB_CUDA_TRY(launch_resid_restrict2(h->grid(level), l.opA(), l.mask, h->lv[level + 1].mask,
+                                      f_dev, u_dev, rc_dev, S(stream)));
   return MGB_OK;
 }
 
@@ -690,7 +767,8 @@ extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
     }
     if (l + 1 < L) MGB_CUDA_TRY(dalloc(&w->t[l], cnt));
   }
-  w->max_nblk = residual_blocks(h->grid(0));
+  w->max_nblk = std::max(std::max(residual_blocks(h->grid(0)), resnorm_blocks(h->grid(0))),
+                         sweep_blocks(h->grid(0)));
   MGB_CUDA_TRY(dalloc(&w->partials, (size_t)w->max_nblk * h->batch));
   MGB_CUDA_TRY(dalloc(&w->fnorm2, (size_t)h->batch));
   MGB_CUDA_TRY(dalloc(&w->scratch, (size_t)h->batch * 4));
@@ -717,7 +795,7 @@ static int sweep(mgb_work* w, int l, const double* f, const double* in, double* 
   const LevelD& lv = h->lv[l];
   const Grid g = h->grid(l);
   if (lv.ks == 1) {
-    MGB_CUDA_TRY(launch_sweep(g, tab_soa(lv.A, lv.n, 1), tab_soa(lv.K, lv.n, 1), lv.mask, f, in, out, s));
+    MGB_CUDA_TRY(launch_sweep2(g, lv.opA(), lv.opK(), lv.mask, f, in, out, nullptr, s));
     return MGB_OK;
   }
   // multi-stage (nonlinear) smoother: residual, then k stages with leaky between
@@ -731,10 +809,35 @@ static int sweep(mgb_work* w, int l, const double* f, const double* in, double* 
                             w->r[l], in, s);
 }
 
-// V(nu1, nu2) from level l; u_in == null means a zero initial guess.  Returns the
-// buffer holding the result (u_l or the level's ping-pong partner).
+// hist[b * hstride] = sqrt(partials sum) / ||f|| (fnorm2 must be current)
+static int enqueue_finalize(mgb_work* w, int nblk, double* hist, int64_t hstride, cudaStream_t s) {
+  MGB_CUDA_TRY(launch_finalize(w->h->batch, nblk, w->partials, nullptr, w->fnorm2, hist, hstride, s));
+  return MGB_OK;
+}
+
+// hist[b * hstride] = ||f - A u|| / ||f|| on level 0
+static int enqueue_resnorm(mgb_work* w, const double* f, const double* u, double* hist, int64_t hstride,
+                           cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  const LevelD& l0 = h->lv[0];
+  MGB_CUDA_TRY(launch_resnorm(h->grid(0), l0.opA(), l0.mask, f, u, w->partials, s));
+  return enqueue_finalize(w, resnorm_blocks(h->grid(0)), hist, hstride, s);
+}
+
+static int enqueue_fnorm(mgb_work* w, const double* f, cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  const LevelD& l0 = h->lv[0];
+  MGB_CUDA_TRY(launch_resnorm(h->grid(0), l0.opA(), l0.mask, f, nullptr, w->partials, s));
+  MGB_CUDA_TRY(launch_finalize(h->batch, resnorm_blocks(h->grid(0)), w->partials, w->fnorm2, nullptr, nullptr, 0, s));
+  return MGB_OK;
+}
+
+// V(nu1, nu2) from level l; zero means a zero initial guess (u not read).  Returns
+// the buffer holding the result (u_l or the level's ping-pong partner).  With
+// hist != null (level 0 only) the relative residual of the INPUT u is written to
+// hist[b * hstride], folded into the first pre-sweep when it is a fused sweep.
 static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero, int nu1, int nu2,
-                      cudaStream_t s, double** result) {
+                      cudaStream_t s, double** result, double* hist = nullptr, int64_t hstride = 0) {
   const mgb_hier* h = w->h;
   const int L = h->depth();
   if (l == L - 1) {
@@ -746,16 +849,26 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   if (!lv.K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
   double* cur = u;
   double* oth = w->t[l];
+  const Grid g = h->grid(l);
+  const bool fuse_norm = hist && nu1 > 0 && lv.ks == 1;
+  if (hist && !fuse_norm) {
+    if (int st = enqueue_resnorm(w, f, zero ? nullptr : u, hist, hstride, s)) return st;
+  }
   if (zero && nu1 == 0) MGB_CUDA_TRY(cudaMemsetAsync(cur, 0, sizeof(double) * h->batch * lv.n, s));
   for (int q = 0; q < nu1; ++q) {
-    if (int st = sweep(w, l, f, (zero && q == 0) ? nullptr : cur, oth, s)) return st;
+    const double* in = (zero && q == 0) ? nullptr : cur;
+    if (q == 0 && fuse_norm) {
+      MGB_CUDA_TRY(launch_sweep2(g, lv.opA(), lv.opK(), lv.mask, f, in, oth, w->partials, s));
+      if (int st = enqueue_finalize(w, sweep_blocks(g), hist, hstride, s)) return st;
+    } else {
+      if (int st = sweep(w, l, f, in, oth, s)) return st;
+    }
     std::swap(cur, oth);
   }
-  MGB_CUDA_TRY(launch_resid_restrict(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, h->lv[l + 1].mask, f, cur,
-                                     w->f[l + 1], s));
+  MGB_CUDA_TRY(launch_resid_restrict2(g, lv.opA(), lv.mask, h->lv[l + 1].mask, f, cur, w->f[l + 1], s));
   double* ec = nullptr;
   if (int st = vcycle_rec(w, l + 1, w->f[l + 1], w->u[l + 1], true, nu1, nu2, s, &ec)) return st;
-  MGB_CUDA_TRY(launch_prolong(h->grid(l), lv.mask, ec, cur, true, s));
+  MGB_CUDA_TRY(launch_prolong(g, lv.mask, ec, cur, true, s));
   for (int q = 0; q < nu2; ++q) {
     if (int st = sweep(w, l, f, cur, oth, s)) return st;
     std::swap(cur, oth);
@@ -764,33 +877,13 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   return MGB_OK;
 }
 
-static int enqueue_vcycle(mgb_work* w, int l, const double* f, double* u, int nu1, int nu2, cudaStream_t s) {
+static int enqueue_vcycle(mgb_work* w, int l, const double* f, double* u, int nu1, int nu2, cudaStream_t s,
+                          bool zero = false, double* hist = nullptr, int64_t hstride = 0) {
   double* res = nullptr;
-  if (int st = vcycle_rec(w, l, f, u, false, nu1, nu2, s, &res)) return st;
+  if (int st = vcycle_rec(w, l, f, u, zero, nu1, nu2, s, &res, hist, hstride)) return st;
   if (res != u)
     MGB_CUDA_TRY(cudaMemcpyAsync(u, res, sizeof(double) * w->h->batch * w->h->lv[l].n,
                                  cudaMemcpyDeviceToDevice, s));
-  return MGB_OK;
-}
-
-// hist[b * hstride] = ||f - A u|| / ||f|| on level 0 (fnorm2 must be current)
-static int enqueue_resnorm(mgb_work* w, const double* f, const double* u, double* hist, int64_t hstride,
-                           cudaStream_t s) {
-  const mgb_hier* h = w->h;
-  const LevelD& l0 = h->lv[0];
-  int nblk = 0;
-  MGB_CUDA_TRY(launch_residual(h->grid(0), tab_soa(l0.A, l0.n, 1), l0.mask, f, u, nullptr, w->partials, &nblk, s));
-  MGB_CUDA_TRY(launch_finalize(h->batch, nblk, w->partials, nullptr, w->fnorm2, hist, hstride, s));
-  return MGB_OK;
-}
-
-static int enqueue_fnorm(mgb_work* w, const double* f, cudaStream_t s) {
-  const mgb_hier* h = w->h;
-  const LevelD& l0 = h->lv[0];
-  int nblk = 0;
-  MGB_CUDA_TRY(launch_residual(h->grid(0), tab_soa(l0.A, l0.n, 1), l0.mask, f, nullptr, nullptr, w->partials,
-                               &nblk, s));
-  MGB_CUDA_TRY(launch_finalize(h->batch, nblk, w->partials, w->fnorm2, nullptr, nullptr, 0, s));
   return MGB_OK;
 }
 
@@ -861,16 +954,17 @@ static int get_graph(mgb_work* w, const GraphKey& key, GraphEntry** out) {
     int st = MGB_OK;
     const int64_t nb = w->h->batch * (int64_t)w->h->lv[0].n;
     if (key.mode == 0) {
-      if (key.u_zero) {
+      // history entry c (residual of the input of cycle c) is folded into cycle c's
+      // first pre-sweep; the last entry needs its own residual pass
+      if (key.u_zero && key.cycles == 0) {
         cudaError_t e = cudaMemsetAsync(key.u, 0, sizeof(double) * nb, w->cap);
         if (e != cudaSuccess) st = cuda_fail(e, "memset");
       }
       if (!st) st = enqueue_fnorm(w, key.f, w->cap);
-      if (!st) st = enqueue_resnorm(w, key.f, key.u, key.hist, key.cycles + 1, w->cap);
-      for (int c = 0; c < key.cycles && !st; ++c) {
-        st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap);
-        if (!st) st = enqueue_resnorm(w, key.f, key.u, key.hist + c + 1, key.cycles + 1, w->cap);
-      }
+      for (int c = 0; c < key.cycles && !st; ++c)
+        st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap, key.u_zero && c == 0,
+                            key.hist + c, key.cycles + 1);
+      if (!st) st = enqueue_resnorm(w, key.f, key.u, key.hist + key.cycles, key.cycles + 1, w->cap);
     } else {
       st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap);
       if (!st) st = enqueue_resnorm(w, key.f, key.u, w->scratch, 4, w->cap);

@@ -92,32 +92,40 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return t;  // valid in thread 0
 }
 
-// r = f - A u, masked.  Optional r output and per-block sum of squares.
+// r = f - A u, masked.  Optional r output and per-block sum of squares.  Each
+// block covers 32 columns x (8 * RES_RPT) rows so the partials stay few.
+constexpr int RES_RPT = 8;
 __global__ void __launch_bounds__(NT) k_residual(Grid g, Tab A, const uint8_t* __restrict__ mask,
                                                  const double* __restrict__ f,
                                                  const double* __restrict__ u,
                                                  double* __restrict__ r,
                                                  double* __restrict__ partials) {
   __shared__ double sh[32];
-  const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+  const int j = blockIdx.x * BX + threadIdx.x, b = blockIdx.z;
   const int64_t n = g.n();
-  double v = 0.0;
-  if (i < g.rows && j < g.cols) {
-    const int64_t p = (int64_t)i * g.cols + j;
-    if (act(mask, p))
-      v = u ? __ldg(f + b * n + p) - stencil3(A, b, u + b * n, i, j, g.rows, g.cols)
-            : __ldg(f + b * n + p) - 0.0;
-    if (r) r[b * n + p] = v;
+  double acc = 0.0;
+#pragma unroll 2
+  for (int q = 0; q < RES_RPT; ++q) {
+    const int i = (blockIdx.y * RES_RPT + q) * BY + threadIdx.y;
+    if (i < g.rows && j < g.cols) {
+      const int64_t p = (int64_t)i * g.cols + j;
+      double v = 0.0;
+      if (act(mask, p))
+        v = u ? __ldg(f + b * n + p) - stencil3(A, b, u + b * n, i, j, g.rows, g.cols)
+              : __ldg(f + b * n + p) - 0.0;
+      if (r) r[b * n + p] = v;
+      acc += v * v;
+    }
   }
   if (partials) {
-    const double t = block_sum(v * v, sh);
+    const double t = block_sum(acc, sh);
     if (threadIdx.x == 0 && threadIdx.y == 0)
       partials[(int64_t)b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
 }
 
 // one block per problem: out2[b] = fixed-order sum of partials; optional history entry
-__global__ void __launch_bounds__(256) k_finalize(int nblk, const double* __restrict__ partials,
+__global__ void __launch_bounds__(1024) k_finalize(int nblk, const double* __restrict__ partials,
                                                   double* __restrict__ out2,
                                                   const double* __restrict__ fnorm2,
                                                   double* __restrict__ hist, int64_t hstride) {
@@ -541,8 +549,13 @@ cudaError_t launch_apply(const Grid& g, int k, Tab A, const uint8_t* mask, const
   return cudaGetLastError();
 }
 
+static dim3 resgrid(const Grid& g) {
+  return dim3((g.cols + BX - 1) / BX, (g.rows + BY * RES_RPT - 1) / (BY * RES_RPT), g.batch);
+}
+
 int residual_blocks(const Grid& g) {
-  return ((g.cols + BX - 1) / BX) * ((g.rows + BY - 1) / BY);
+  const dim3 d = resgrid(g);
+  return (int)(d.x * d.y);
 }
 
 cudaError_t launch_residual(const Grid& g, Tab A, const uint8_t* mask, const double* f,
@@ -550,14 +563,14 @@ cudaError_t launch_residual(const Grid& g, Tab A, const uint8_t* mask, const dou
                             cudaStream_t s) {
   ++g_launches;
   if (nblk) *nblk = residual_blocks(g);
-  k_residual<<<pgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask, f, u, r, partials);
+  k_residual<<<resgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask, f, u, r, partials);
   return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(int batch, int nblk, const double* partials, double* out2,
                             const double* fnorm2, double* hist, int64_t hstride, cudaStream_t s) {
   ++g_launches;
-  k_finalize<<<batch, 256, 0, s>>>(nblk, partials, out2, fnorm2, hist, hstride);
+  k_finalize<<<batch, 1024, 0, s>>>(nblk, partials, out2, fnorm2, hist, hstride);
   return cudaGetLastError();
 }
 

@@ -186,6 +186,18 @@ class MultigridHierarchy:
         _lib.call("mgb_hier_get_kernels", self._h, l, out.ctypes.data_as(_lib.P))
         return out
 
+    # -- table storage ---------------------------------------------------------
+    def set_storage(self, mode: str = "auto"):
+        """'auto': exact band-class tables where a level's table allows it (default);
+        'planes': per-point planes everywhere.  Results are bit-identical."""
+        _lib.call("mgb_hier_set_storage", self._h, {"auto": 0, "planes": 1}[mode], None)
+
+    def storage_info(self, l: int):
+        """(A class-compact, M class-compact) for level l."""
+        a, k = C.c_int(), C.c_int()
+        _lib.call("mgb_hier_storage_info", self._h, l, C.byref(a), C.byref(k))
+        return bool(a.value), bool(k.value)
+
     # -- smoother bookkeeping ------------------------------------------------
     def _sweeps(self, nu1, nu2):
         """Resolve (nu1, nu2) and make sure the device holds each level's smoother."""
