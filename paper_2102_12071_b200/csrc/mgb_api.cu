@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "mgb_cycle.h"
+#include "mgb_stream.h"
 #include "mgb_internal.h"
 
 namespace mgb {
@@ -90,6 +91,7 @@ struct mgb_hier {
   double slope = 0.01;
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
+  int fused = 1;            // row-streaming PRE/POST passes (mgb_stream.cu) where applicable
   ~mgb_hier() {
     DeviceGuard dg(device);
     for (auto& l : lv) {
@@ -514,6 +516,7 @@ extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double 
       }
   }
   if (const char* e = getenv("MGB_STORAGE")) h->compact = std::string(e) != "planes";
+  if (const char* e = getenv("MGB_FUSED")) h->fused = std::string(e) != "0";
   if (int st = classify_all(h.get(), s)) return st;
   *out = h.release();
   return MGB_OK;
@@ -525,6 +528,13 @@ extern "C" int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream) {
   DeviceGuard dg(h->device);
   h->compact = mode == 0;
   return classify_all(h, S(stream));
+}
+
+extern "C" int mgb_hier_set_fused(mgb_hier* h, int enable) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  h->fused = enable ? 1 : 0;
+  ++h->version;
+  return MGB_OK;
 }
 
 extern "C" int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_classed) {
@@ -768,7 +778,8 @@ extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
     if (l + 1 < L) MGB_CUDA_TRY(dalloc(&w->t[l], cnt));
   }
   w->max_nblk = std::max(std::max(residual_blocks(h->grid(0)), resnorm_blocks(h->grid(0))),
-                         sweep_blocks(h->grid(0)));
+                         std::max(sweep_blocks(h->grid(0)),
+                                  std::max(stream_blocks(h->grid(0), 1, true), stream_blocks(h->grid(0), 2, true))));
   MGB_CUDA_TRY(dalloc(&w->partials, (size_t)w->max_nblk * h->batch));
   MGB_CUDA_TRY(dalloc(&w->fnorm2, (size_t)h->batch));
   MGB_CUDA_TRY(dalloc(&w->scratch, (size_t)h->batch * 4));
@@ -851,6 +862,38 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   double* oth = w->t[l];
   const Grid g = h->grid(l);
   const bool fuse_norm = hist && nu1 > 0 && lv.ks == 1;
+  if (h->fused && lv.ks == 1 && (nu1 == 1 || nu1 == 2) && (nu2 == 1 || nu2 == 2)) {
+    // PRE: [history norm] + nu1 sweeps + residual + restriction in one streaming pass
+    StreamArgs a{};
+    a.g = g;
+    a.A = lv.opA();
+    a.K = lv.opK();
+    a.mask = lv.mask;
+    a.mask_c = h->lv[l + 1].mask;
+    a.f = f;
+    a.u = zero ? nullptr : cur;
+    a.uo = oth;
+    a.rc = w->f[l + 1];
+    a.partials = fuse_norm ? w->partials : nullptr;
+    a.stream = s;
+    MGB_CUDA_TRY(launch_stream(a, nu1, true, false, fuse_norm));
+    if (fuse_norm) {
+      if (int st = enqueue_finalize(w, stream_blocks(g, nu1, true), hist, hstride, s)) return st;
+    }
+    std::swap(cur, oth);
+    double* ec = nullptr;
+    if (int st = vcycle_rec(w, l + 1, w->f[l + 1], w->u[l + 1], true, nu1, nu2, s, &ec)) return st;
+    // POST: coarse-grid correction + nu2 sweeps in one streaming pass
+    a.u = cur;
+    a.uo = oth;
+    a.ec = ec;
+    a.rc = nullptr;
+    a.partials = nullptr;
+    MGB_CUDA_TRY(launch_stream(a, nu2, false, true, false));
+    std::swap(cur, oth);
+    *result = cur;
+    return MGB_OK;
+  }
   if (hist && !fuse_norm) {
     if (int st = enqueue_resnorm(w, f, zero ? nullptr : u, hist, hstride, s)) return st;
   }

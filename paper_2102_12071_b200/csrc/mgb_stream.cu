@@ -1,0 +1,350 @@
+// Row-streaming, temporally blocked V-cycle passes (the level-l hot kernels).
+//
+//   PRE(l)  = [history norm of the input u] + NSW sweeps u <- u + M (f - A u)
+//             + residual + full-weighting restriction   -> u_out, rc
+//   POST(l) = prolongation/coarse-grid correction u <- u + P ec + NSW sweeps -> u_out
+//
+// One CTA owns a strip of SWOUT columns (plus a halo of H columns on each side,
+// one column per thread) and a segment of rows, and marches down the rows: at
+// step t it brings in row t of u and f (cp.async prefetch ring, D rows ahead)
+// and advances every pipeline stage by one row.  Stage k (k = 1..S, odd =
+// residual, even = smoother update) produces row t - 2k, so every stage reads
+// only rows that earlier steps published and one __syncthreads per step is
+// enough.  Each stage keeps the 3x3 window of its input field in registers
+// (own column + left/right neighbours, exchanged through a double-buffered
+// shared-memory row); the own-column residual and update values never leave
+// registers.  u and f are read from HBM once per pass and u is written once,
+// so a V(2,2) cycle level costs ~2 x (16 + 8) B per point instead of
+// 4 x 24 + 18 + 18 + 16 for separate passes.
+//
+// A, M: band-class tables (constant-coefficient levels; 25 x 9 in shared
+// memory, the interior class in registers) or per-point planes (read through
+// L1/L2).  Arithmetic uses fused multiply-add; results agree with the separate
+// passes and with the reference to rounding (SURVEY §8(c) gate: 1e-10).
+//
+// Reference: v_cycle hierarchy.py:96-111 (with RepeatedSmoother cli.py:365-377),
+// apply_stencil grid.py:216-226, inferred_apply smoothers.py:325-343, restrict
+// transfer.py:108-121, prolong transfer.py:124-147, history hierarchy.py:129-141.
+#include "mgb_stream.h"
+
+namespace mgb {
+namespace {
+
+constexpr int SWT = 128;   // threads (= columns incl. halo) per CTA
+constexpr int PD = 16;     // prefetch ring depth (rows) for u
+constexpr int PDF = 32;    // ring depth for f (also read by the later residual stages)
+constexpr int DIST = 8;    // prefetch distance (rows ahead)
+constexpr int NCLS = 25;
+constexpr int CINT = 12;   // interior band class (2 * 5 + 2)
+
+__device__ __forceinline__ int bandc(int i, int n) { return i < 2 ? i : (i >= n - 2 ? 4 - (n - 1 - i) : 2); }
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int NSW, bool RES, bool PRO>
+struct SP {
+  static constexpr int S = 2 * NSW + (RES ? 1 : 0);  // stencil stages after the input field
+  static constexpr int H = 2 * NSW + 2;              // column halo per side
+  static constexpr int WOUT = SWT - 2 * H;           // owned columns per strip (even)
+  static constexpr int NF = S;                       // fields with a window (F_0 .. F_{S-1})
+};
+
+struct Win {
+  double v[3][3];  // [row: oldest..newest][col: left, own, right]
+};
+
+// Stage weights: classed (registers for the interior class, shared table for the
+// boundary bands) or per-point planes.
+template <bool CLS>
+struct W9 {
+  __device__ __forceinline__ static void get(const Op& t, const double* tab, const double* reg, int b, int64_t p,
+                                             int cls, double* w) {
+    if (CLS) {
+      if (cls == CINT) {
+#pragma unroll
+        for (int o = 0; o < 9; ++o) w[o] = reg[o];
+      } else {
+#pragma unroll
+        for (int o = 0; o < 9; ++o) w[o] = tab[cls * 9 + o];
+      }
+    } else {
+      const double* base = t.planes + (int64_t)b * 9 * t.n + p;
+#pragma unroll
+      for (int o = 0; o < 9; ++o) w[o] = __ldg(base + (int64_t)o * t.n);
+    }
+  }
+};
+
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool CA, bool CK>
+__global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
+  using P = SP<NSW, RES, PRO>;
+  constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
+  extern __shared__ double smem[];
+  double* ring_u = smem;                               // PD x SWT (unused when ZU)
+  double* ring_f = ring_u + PD * SWT;                  // PDF x SWT
+  double* xch = ring_f + PDF * SWT;                    // NF x 2 x SWT neighbour exchange rows
+  double* rlast = xch + NF * 2 * SWT;                  // 4 x SWT last-residual ring (RES)
+  double* tA = rlast + 4 * SWT;                        // 25 x 9
+  double* tK = tA + NCLS * 9;                          // 25 x 9
+  double* red = tK + NCLS * 9;                         // 32
+
+  const Grid g = a.g;
+  const int tid = threadIdx.x;
+  const int b = blockIdx.z;
+  const int64_t n = g.n();
+  const int j0 = blockIdx.x * WOUT;        // first owned column (even)
+  const int col = j0 - H + tid;
+  const bool cin = col >= 0 && col < g.cols;
+  const bool owned_c = tid >= H && tid < H + WOUT && cin;
+  const int R0 = blockIdx.y * a.seg, R1 = min(g.rows, R0 + a.seg);
+  const double* fb = a.f + b * n;
+  const double* ub = ZU ? nullptr : a.u + b * n;
+  double* uob = a.uo + b * n;
+  const int colL = max(tid - 1, 0), colR = min(tid + 1, SWT - 1);
+
+  double rA[9], rK[9];
+  if (CA) {
+    for (int q = tid; q < NCLS * 9; q += SWT) tA[q] = a.A.cls[(int64_t)b * NCLS * 9 + q];
+  }
+  if (CK) {
+    for (int q = tid; q < NCLS * 9; q += SWT) tK[q] = a.K.cls[(int64_t)b * NCLS * 9 + q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int o = 0; o < 9; ++o) {
+    rA[o] = CA ? tA[CINT * 9 + o] : 0.0;
+    rK[o] = CK ? tK[CINT * 9 + o] : 0.0;
+  }
+
+  Win w[NF];
+#pragma unroll
+  for (int k = 0; k < NF; ++k)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[k].v[r][c] = 0.0;
+  // own-column history one row older than the window for the u-fields F_0, F_2
+  double hold[NSW];
+#pragma unroll
+  for (int m = 0; m < NSW; ++m) hold[m] = 0.0;
+  double acc = 0.0;
+
+  const int t0 = R0 - S - 1;
+  const int t1 = R1 + 2 * S;
+  // prefetch rows t0 .. t0 + DIST - 1
+  auto issue = [&](int row) {
+    const bool rv = row >= 0 && row < g.rows && cin;
+    const int64_t off = rv ? (int64_t)row * g.cols + col : 0;
+    const int slot = row & (PD - 1);
+    if (!ZU) cp_async8(&ring_u[slot * SWT + tid], ub + off, rv);
+    cp_async8(&ring_f[(row & (PDF - 1)) * SWT + tid], fb + off, rv);
+    cp_commit();
+  };
+  for (int q = 0; q < DIST; ++q) issue(t0 + q);
+
+  for (int t = t0; t <= t1; ++t) {
+    issue(t + DIST);
+    cp_wait<DIST>();  // row t has landed (own element; neighbours come via xch)
+    // ---- input field F_0 = u (+ P ec) at row t
+    double u0 = 0.0;
+    {
+      const bool rv = t >= 0 && t < g.rows && cin;
+      if (rv) {
+        const int64_t p = (int64_t)t * g.cols + col;
+        const bool act = a.mask == nullptr || a.mask[p];
+        if (!ZU) u0 = ring_u[(t & (PD - 1)) * SWT + tid];
+        if (PRO) {
+          const int rc_ = g.rows / 2, cc_ = g.cols / 2;
+          const double* eb = a.ec + b * (int64_t)rc_ * cc_;
+          double s = 0.0;
+#pragma unroll
+          for (int di = -1; di <= 1; ++di) {
+            const int tt = t - 1 - di;
+            if (tt < 0 || (tt & 1)) continue;
+            const int ci = tt >> 1;
+            if (ci >= rc_) continue;
+#pragma unroll
+            for (int dj = -1; dj <= 1; ++dj) {
+              const int uu = col - 1 - dj;
+              if (uu < 0 || (uu & 1)) continue;
+              const int cj = uu >> 1;
+              if (cj >= cc_) continue;
+              const double wgt = (di == 0 ? 2.0 : 1.0) * (dj == 0 ? 2.0 : 1.0) * 0.125;
+              s = fma(wgt, __ldg(eb + (int64_t)ci * cc_ + cj), s);
+            }
+          }
+          u0 = act ? u0 + s : 0.0;
+        }
+        if (!act) u0 = 0.0;
+      }
+    }
+    // ---- stages: k odd = residual of F_{k-1}, k even = update
+    double nv[NF + 1];
+    nv[0] = u0;
+#pragma unroll
+    for (int k = 1; k <= S; ++k) {
+      const int row = t - 2 * k;
+      double val = 0.0;
+      if (row >= 0 && row < g.rows && cin) {
+        const int64_t p = (int64_t)row * g.cols + col;
+        const bool act = a.mask == nullptr || a.mask[p];
+        if (act) {
+          const int cls = (CA || CK) ? bandc(row, g.rows) * 5 + bandc(col, g.cols) : 0;
+          double wt[9];
+          const Win& in = w[k - 1];
+          if (k & 1) {
+            W9<CA>::get(a.A, tA, rA, b, p, cls, wt);
+            double s = 0.0;
+#pragma unroll
+            for (int di = 0; di < 3; ++di)
+#pragma unroll
+              for (int dj = 0; dj < 3; ++dj) s = fma(wt[di * 3 + dj], in.v[di][dj], s);
+            val = ring_f[(row & (PDF - 1)) * SWT + tid] - s;
+            if (NORM && k == 1 && row >= R0 && row < R1 && owned_c) acc = fma(val, val, acc);
+          } else {
+            W9<CK>::get(a.K, tK, rK, b, p, cls, wt);
+            double s = 0.0;
+#pragma unroll
+            for (int di = 0; di < 3; ++di)
+#pragma unroll
+              for (int dj = 0; dj < 3; ++dj) s = fma(wt[di * 3 + dj], in.v[di][dj], s);
+            val = hold[k / 2 - 1] + s;   // own u of the previous u-field at this row
+          }
+        }
+      }
+      nv[k] = val;
+      if (k == 2 * NSW && row >= R0 && row < R1 && owned_c && row >= 0) uob[(int64_t)row * g.cols + col] = val;
+    }
+    // ---- publish the new rows
+    const int sl = t & 1;
+#pragma unroll
+    for (int k = 0; k < NF; ++k) xch[(k * 2 + sl) * SWT + tid] = nv[k];
+    if (RES) rlast[((t - 2 * S) & 3) * SWT + tid] = nv[S];
+    __syncthreads();
+    // ---- restriction of the last residual: coarse row ci needs fine rows 2ci..2ci+2
+    if (RES) {
+      const int top = t - 2 * S;  // newest residual row
+      if (top >= 2 && !(top & 1)) {
+        const int ci = (top - 2) >> 1;
+        const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+        const int cj = (j0 >> 1) + tid;
+        if (tid < WOUT / 2 && ci >= (R0 >> 1) && 2 * ci + 1 < R1 && ci < rows_c && cj < cols_c) {
+          double s = 0.0;
+          const int base = H + 2 * tid;  // thread column of fine col 2cj = j0 + 2 tid
+#pragma unroll
+          for (int di = 0; di < 3; ++di) {
+            const double* rr = &rlast[((top - 2 + di) & 3) * SWT];
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj) {
+              const double wgt = (di == 1 ? 2.0 : 1.0) * (dj == 1 ? 2.0 : 1.0) * 0.0625;
+              s = fma(wgt, rr[base + dj], s);
+            }
+          }
+          const int64_t pc = (int64_t)ci * cols_c + cj;
+          const bool actc = a.mask_c == nullptr || a.mask_c[pc];
+          a.rc[b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
+        }
+      }
+    }
+    // ---- slide the windows: newest row of F_k = the value just published
+#pragma unroll
+    for (int k = 0; k < NF; ++k) {
+      if (!(k & 1) && k / 2 < NSW) hold[k / 2] = w[k].v[0][1];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        w[k].v[0][c] = w[k].v[1][c];
+        w[k].v[1][c] = w[k].v[2][c];
+      }
+      w[k].v[2][0] = xch[(k * 2 + sl) * SWT + colL];
+      w[k].v[2][1] = nv[k];
+      w[k].v[2][2] = xch[(k * 2 + sl) * SWT + colR];
+    }
+  }
+  cp_wait<0>();
+  if (NORM) {
+    // block reduction (deterministic order)
+    double v = acc;
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int q = 0; q < SWT / 32; ++q) s += red[q];
+      a.partials[(int64_t)b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+}  // namespace
+
+int stream_seg(const Grid& g) {
+  // rows per CTA segment (even): long segments amortise the pipeline fill,
+  // enough segments keep ~2 CTAs per SM busy
+  const int strips = (g.cols + 115) / 116;
+  int seg = 256;
+  while (seg > 32 && (int64_t)strips * ((g.rows + seg - 1) / seg) * g.batch < 2 * 148) seg /= 2;
+  return seg;
+}
+
+dim3 stream_grid(const Grid& g, int nsw, bool res) {
+  const int H = 2 * nsw + 2;
+  const int wout = SWT - 2 * H;
+  const int seg = stream_seg(g);
+  return dim3((g.cols + wout - 1) / wout, (g.rows + seg - 1) / seg, g.batch);
+}
+
+int stream_blocks(const Grid& g, int nsw, bool res) {
+  const dim3 d = stream_grid(g, nsw, res);
+  return (int)(d.x * d.y);
+}
+
+static size_t stream_smem(int nsw, bool res) {
+  const int nf = 2 * nsw + (res ? 1 : 0);
+  return sizeof(double) * ((size_t)(PD + PDF + 2 * nf + 4) * SWT + 2 * NCLS * 9 + 32);
+}
+
+template <typename KF>
+static cudaError_t run_k(KF kern, dim3 grid, size_t smem, cudaStream_t s, const StreamArgs& a) {
+  static thread_local bool attr_set = false;
+  (void)attr_set;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, SWT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stream(const StreamArgs& a0, int nsw, bool res, bool pro, bool norm) {
+  StreamArgs a = a0;
+  a.seg = stream_seg(a.g);
+  const dim3 grid = stream_grid(a.g, nsw, res);
+  const bool zu = a.u == nullptr, ca = a.A.cls != nullptr, ck = a.K.cls != nullptr;
+  cudaStream_t s = a.stream;
+  const size_t sm = stream_smem(nsw, res);
+  ++g_launches;
+#define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
+  if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
+    if (ca && ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, true>, grid, sm, s, a);   \
+    if (ca) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, false>, grid, sm, s, a);        \
+    if (ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, true>, grid, sm, s, a);        \
+    return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, false>, grid, sm, s, a);               \
+  }
+  // PRE: restriction, optional norm, optional zero start; POST: prolongation, no norm
+  MGB_ST(1, true, false, false, false) MGB_ST(1, true, false, true, false)
+  MGB_ST(1, true, false, false, true)  MGB_ST(1, true, false, true, true)
+  MGB_ST(2, true, false, false, false) MGB_ST(2, true, false, true, false)
+  MGB_ST(2, true, false, false, true)  MGB_ST(2, true, false, true, true)
+  MGB_ST(1, false, true, false, false) MGB_ST(2, false, true, false, false)
+#undef MGB_ST
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mgb

@@ -1,0 +1,28 @@
+// Row-streaming fused V-cycle passes (mgb_stream.cu).
+#pragma once
+
+#include "mgb_cycle.h"
+
+namespace mgb {
+
+struct StreamArgs {
+  Grid g;
+  Op A, K;                 // operator / smoother tables (planes or band classes), ks == 1
+  const uint8_t* mask;     // fine mask (null = all active)
+  const uint8_t* mask_c;   // coarse mask (restriction output)
+  const double* f;         // right-hand side
+  const double* u;         // input u (null = zero)
+  double* uo;              // output u (must not alias u)
+  const double* ec;        // coarse correction (POST)
+  double* rc;              // restricted residual (PRE)
+  double* partials;        // per-CTA sums of the input residual squared (history)
+  int seg;                 // rows per CTA segment (set by the launcher)
+  cudaStream_t stream;
+};
+
+// PRE: res = true, pro = false (norm optional, u null = zero start);
+// POST: res = false, pro = true.  nsw in {1, 2}.
+cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm);
+int stream_blocks(const Grid& g, int nsw, bool res);
+
+}  // namespace mgb

@@ -355,3 +355,21 @@ def test_storage_modes_bit_identical(name):
     h2 = h.run_cycles(f, u2, 4, c["nu"], c["nu"], u_zero=True).clone()
     assert t.equal(u1, u2)
     assert np.allclose(dv.host(h1), dv.host(h2), rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("name", ["c1_fd_conv", "case_var31_conv_v22", "case_lshape31_conv_v11", "c4_p0",
+                                  "case_rect20x27_conv_v11"])
+def test_fused_and_separate_passes_agree(name):
+    """Row-streaming PRE/POST passes vs separate sweep/restrict/prolong passes."""
+    from paper_2102_12071_b200 import device as dv
+    c = load(name)
+    g = c["golden"]
+    spec = spec_of(c["mask"], float(g["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), c["smoother"])
+    f = dv.to_dev(np.where(c["mask"], c["f"], 0.0))
+    u1, u2 = dv.zeros(f.shape), dv.zeros(f.shape)
+    h1 = dv.host(h.run_cycles(f, u1, c["cycles"], c["nu"], c["nu"], u_zero=True))[0]
+    h.set_fused(False)
+    h2 = dv.host(h.run_cycles(f, u2, c["cycles"], c["nu"], c["nu"], u_zero=True))[0]
+    assert_hist(h1, h2)
+    assert rel_err(dv.host(u1), dv.host(u2)) <= 1e-12
