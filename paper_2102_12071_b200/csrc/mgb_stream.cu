@@ -56,33 +56,24 @@ struct SP {
   static constexpr int NF = S;                       // fields with a window (F_0 .. F_{S-1})
 };
 
-struct Win {
-  double v[3][3];  // [row: oldest..newest][col: left, own, right]
-};
+// compile-time positive modulo 3
+__host__ __device__ constexpr int m3(int x) { return ((x % 3) + 3) % 3; }
 
-// Stage weights: classed (registers for the interior class, shared table for the
-// boundary bands) or per-point planes.
-template <bool CLS>
-struct W9 {
-  __device__ __forceinline__ static void get(const Op& t, const double* tab, const double* reg, int b, int64_t p,
-                                             int cls, double* w) {
-    if (CLS) {
-      if (cls == CINT) {
-#pragma unroll
-        for (int o = 0; o < 9; ++o) w[o] = reg[o];
-      } else {
-#pragma unroll
-        for (int o = 0; o < 9; ++o) w[o] = tab[cls * 9 + o];
-      }
-    } else {
-      const double* base = t.planes + (int64_t)b * 9 * t.n + p;
-#pragma unroll
-      for (int o = 0; o < 9; ++o) w[o] = __ldg(base + (int64_t)o * t.n);
-    }
-  }
-};
+// 3x3 dot product with three independent accumulation chains
+__device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][3], int s0, int s1, int s2) {
+  double a0 = wt[0] * x[s0][0];
+  double a1 = wt[3] * x[s1][0];
+  double a2 = wt[6] * x[s2][0];
+  a0 = fma(wt[1], x[s0][1], a0);
+  a1 = fma(wt[4], x[s1][1], a1);
+  a2 = fma(wt[7], x[s2][1], a2);
+  a0 = fma(wt[2], x[s0][2], a0);
+  a1 = fma(wt[5], x[s1][2], a1);
+  a2 = fma(wt[8], x[s2][2], a2);
+  return (a0 + a1) + a2;
+}
 
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool CA, bool CK>
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool CA, bool CK, bool MSK>
 __global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
   using P = SP<NSW, RES, PRO>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
@@ -103,19 +94,22 @@ __global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
   const int col = j0 - H + tid;
   const bool cin = col >= 0 && col < g.cols;
   const bool owned_c = tid >= H && tid < H + WOUT && cin;
+  const int ccls = bandc(col, g.cols);
+  // the whole strip is interior in x: the interior-class weights apply to every
+  // thread whenever the row is interior too (a CTA-uniform test)
+  const bool cta_cint = j0 - H >= 2 && j0 - H + SWT - 1 <= g.cols - 3;
   const int R0 = blockIdx.y * a.seg, R1 = min(g.rows, R0 + a.seg);
   const double* fb = a.f + b * n;
   const double* ub = ZU ? nullptr : a.u + b * n;
   double* uob = a.uo + b * n;
   const int colL = max(tid - 1, 0), colR = min(tid + 1, SWT - 1);
+  const uint8_t* mk = MSK ? a.mask : nullptr;
 
   double rA[9], rK[9];
-  if (CA) {
+  if (CA)
     for (int q = tid; q < NCLS * 9; q += SWT) tA[q] = a.A.cls[(int64_t)b * NCLS * 9 + q];
-  }
-  if (CK) {
+  if (CK)
     for (int q = tid; q < NCLS * 9; q += SWT) tK[q] = a.K.cls[(int64_t)b * NCLS * 9 + q];
-  }
   __syncthreads();
 #pragma unroll
   for (int o = 0; o < 9; ++o) {
@@ -123,153 +117,153 @@ __global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
     rK[o] = CK ? tK[CINT * 9 + o] : 0.0;
   }
 
-  Win w[NF];
+  // circular register windows: field k row x lives in slot x mod 3
+  double w[NF][3][3];
 #pragma unroll
   for (int k = 0; k < NF; ++k)
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) w[k].v[r][c] = 0.0;
-  // own-column history one row older than the window for the u-fields F_0, F_2
+      for (int c = 0; c < 3; ++c) w[k][r][c] = 0.0;
   double hold[NSW];
 #pragma unroll
   for (int m = 0; m < NSW; ++m) hold[m] = 0.0;
   double acc = 0.0;
 
-  const int t0 = R0 - S - 1;
+  // steps t in [t0, t1], t0 aligned to a multiple of 3 (extra leading steps only
+  // compute rows nobody needs)
+  int t0 = R0 - S - 1;
+  t0 -= m3(t0);
   const int t1 = R1 + 2 * S;
-  // prefetch rows t0 .. t0 + DIST - 1
-  auto issue = [&](int row) {
-    const bool rv = row >= 0 && row < g.rows && cin;
-    const int64_t off = rv ? (int64_t)row * g.cols + col : 0;
-    const int slot = row & (PD - 1);
-    if (!ZU) cp_async8(&ring_u[slot * SWT + tid], ub + off, rv);
-    cp_async8(&ring_f[(row & (PDF - 1)) * SWT + tid], fb + off, rv);
+  // prefetch rows t0 .. t0 + DIST - 1; pointers advance one row per issue
+  int prow = t0;
+  const int64_t cstride = g.cols;
+  const double* pu = ZU ? nullptr : ub + (int64_t)prow * cstride + col;
+  const double* pf = fb + (int64_t)prow * cstride + col;
+  auto issue = [&]() {
+    const bool rv = prow >= 0 && prow < g.rows && cin;
+    if (!ZU) cp_async8(&ring_u[(prow & (PD - 1)) * SWT + tid], rv ? pu : ub, rv);
+    cp_async8(&ring_f[(prow & (PDF - 1)) * SWT + tid], rv ? pf : fb, rv);
     cp_commit();
+    ++prow;
+    if (!ZU) pu += cstride;
+    pf += cstride;
   };
-  for (int q = 0; q < DIST; ++q) issue(t0 + q);
+  for (int q = 0; q < DIST; ++q) issue();
 
-  for (int t = t0; t <= t1; ++t) {
-    issue(t + DIST);
-    cp_wait<DIST>();  // row t has landed (own element; neighbours come via xch)
-    // ---- input field F_0 = u (+ P ec) at row t
-    double u0 = 0.0;
-    {
-      const bool rv = t >= 0 && t < g.rows && cin;
-      if (rv) {
-        const int64_t p = (int64_t)t * g.cols + col;
-        const bool act = a.mask == nullptr || a.mask[p];
+  for (int tb = t0; tb <= t1; tb += 3) {
+#pragma unroll
+    for (int ph = 0; ph < 3; ++ph) {
+      const int t = tb + ph;
+      issue();
+      cp_wait<DIST>();
+      double nv[NF + 1];
+      // ---- F_0 = u (+ P ec) at row t
+      {
+        double u0 = 0.0;
+        const bool rv = (unsigned)t < (unsigned)g.rows && cin;
         if (!ZU) u0 = ring_u[(t & (PD - 1)) * SWT + tid];
-        if (PRO) {
+        if (PRO && rv) {
           const int rc_ = g.rows / 2, cc_ = g.cols / 2;
           const double* eb = a.ec + b * (int64_t)rc_ * cc_;
           double s = 0.0;
 #pragma unroll
           for (int di = -1; di <= 1; ++di) {
             const int tt = t - 1 - di;
-            if (tt < 0 || (tt & 1)) continue;
-            const int ci = tt >> 1;
-            if (ci >= rc_) continue;
+            if (tt < 0 || (tt & 1) || (tt >> 1) >= rc_) continue;
+            const double* er = eb + (int64_t)(tt >> 1) * cc_;
 #pragma unroll
             for (int dj = -1; dj <= 1; ++dj) {
               const int uu = col - 1 - dj;
-              if (uu < 0 || (uu & 1)) continue;
-              const int cj = uu >> 1;
-              if (cj >= cc_) continue;
+              if (uu < 0 || (uu & 1) || (uu >> 1) >= cc_) continue;
               const double wgt = (di == 0 ? 2.0 : 1.0) * (dj == 0 ? 2.0 : 1.0) * 0.125;
-              s = fma(wgt, __ldg(eb + (int64_t)ci * cc_ + cj), s);
+              s = fma(wgt, __ldg(er + (uu >> 1)), s);
             }
           }
-          u0 = act ? u0 + s : 0.0;
+          u0 += s;
         }
-        if (!act) u0 = 0.0;
+        if (MSK && rv && !mk[(int64_t)t * g.cols + col]) u0 = 0.0;
+        nv[0] = rv ? u0 : 0.0;
       }
-    }
-    // ---- stages: k odd = residual of F_{k-1}, k even = update
-    double nv[NF + 1];
-    nv[0] = u0;
+      // ---- stages k = 1..S at row t - 2k (row is CTA-uniform)
 #pragma unroll
-    for (int k = 1; k <= S; ++k) {
-      const int row = t - 2 * k;
-      double val = 0.0;
-      if (row >= 0 && row < g.rows && cin) {
-        const int64_t p = (int64_t)row * g.cols + col;
-        const bool act = a.mask == nullptr || a.mask[p];
-        if (act) {
-          const int cls = (CA || CK) ? bandc(row, g.rows) * 5 + bandc(col, g.cols) : 0;
-          double wt[9];
-          const Win& in = w[k - 1];
+      for (int k = 1; k <= S; ++k) {
+        const int row = t - 2 * k;
+        const int s0 = m3(ph - 2 * k - 1), s1 = m3(ph - 2 * k), s2 = m3(ph - 2 * k + 1);
+        double val = 0.0;
+        if ((unsigned)row < (unsigned)g.rows) {
+          const bool CL = (k & 1) ? CA : CK;
+          const Op& op = (k & 1) ? a.A : a.K;
+          const double* tab = (k & 1) ? tA : tK;
+          const double* reg = (k & 1) ? rA : rK;
+          double sdot;
+          if (!CL) {
+            const double* base = op.planes + (int64_t)b * 9 * op.n + ((int64_t)row * g.cols + (cin ? col : 0));
+            double wt[9];
+#pragma unroll
+            for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
+            sdot = dot9(wt, w[k - 1], s0, s1, s2);
+          } else if (cta_cint && row >= 2 && row < g.rows - 2) {
+            sdot = dot9(reg, w[k - 1], s0, s1, s2);
+          } else {
+            sdot = dot9(tab + (bandc(row, g.rows) * 5 + ccls) * 9, w[k - 1], s0, s1, s2);
+          }
           if (k & 1) {
-            W9<CA>::get(a.A, tA, rA, b, p, cls, wt);
-            double s = 0.0;
-#pragma unroll
-            for (int di = 0; di < 3; ++di)
-#pragma unroll
-              for (int dj = 0; dj < 3; ++dj) s = fma(wt[di * 3 + dj], in.v[di][dj], s);
-            val = ring_f[(row & (PDF - 1)) * SWT + tid] - s;
+            val = ring_f[(row & (PDF - 1)) * SWT + tid] - sdot;
             if (NORM && k == 1 && row >= R0 && row < R1 && owned_c) acc = fma(val, val, acc);
           } else {
-            W9<CK>::get(a.K, tK, rK, b, p, cls, wt);
-            double s = 0.0;
+            val = hold[k / 2 - 1] + sdot;
+          }
+          if (MSK && cin && !mk[(int64_t)row * g.cols + col]) val = 0.0;
+          val = cin ? val : 0.0;
+          if (k == 2 * NSW && row >= R0 && row < R1 && owned_c) uob[(int64_t)row * g.cols + col] = val;
+        }
+        nv[k] = val;
+      }
+      // ---- publish, then slide the windows (slot of the evicted row)
+      const int sl = t & 1;
 #pragma unroll
-            for (int di = 0; di < 3; ++di)
-#pragma unroll
-              for (int dj = 0; dj < 3; ++dj) s = fma(wt[di * 3 + dj], in.v[di][dj], s);
-            val = hold[k / 2 - 1] + s;   // own u of the previous u-field at this row
+      for (int k = 0; k < NF; ++k) xch[(k * 2 + sl) * SWT + tid] = nv[k];
+      if (RES) rlast[((t - 2 * S) & 3) * SWT + tid] = nv[S];
+      __syncthreads();
+      if (RES) {
+        const int top = t - 2 * S;
+        if (top >= 2 && !(top & 1)) {
+          const int ci = (top - 2) >> 1;
+          const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+          const int cj = (j0 >> 1) + tid;
+          if (tid < WOUT / 2 && ci >= (R0 >> 1) && 2 * ci + 1 < R1 && ci < rows_c && cj < cols_c) {
+            const int base = H + 2 * tid;
+            const double* r0p = &rlast[((top - 2) & 3) * SWT + base];
+            const double* r1p = &rlast[((top - 1) & 3) * SWT + base];
+            const double* r2p = &rlast[(top & 3) * SWT + base];
+            double s = 0.0625 * r0p[0];
+            s = fma(0.125, r0p[1], s);
+            s = fma(0.0625, r0p[2], s);
+            s = fma(0.125, r1p[0], s);
+            s = fma(0.25, r1p[1], s);
+            s = fma(0.125, r1p[2], s);
+            s = fma(0.0625, r2p[0], s);
+            s = fma(0.125, r2p[1], s);
+            s = fma(0.0625, r2p[2], s);
+            const int64_t pc = (int64_t)ci * cols_c + cj;
+            const bool actc = a.mask_c == nullptr || a.mask_c[pc];
+            a.rc[b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
           }
         }
       }
-      nv[k] = val;
-      if (k == 2 * NSW && row >= R0 && row < R1 && owned_c && row >= 0) uob[(int64_t)row * g.cols + col] = val;
-    }
-    // ---- publish the new rows
-    const int sl = t & 1;
 #pragma unroll
-    for (int k = 0; k < NF; ++k) xch[(k * 2 + sl) * SWT + tid] = nv[k];
-    if (RES) rlast[((t - 2 * S) & 3) * SWT + tid] = nv[S];
-    __syncthreads();
-    // ---- restriction of the last residual: coarse row ci needs fine rows 2ci..2ci+2
-    if (RES) {
-      const int top = t - 2 * S;  // newest residual row
-      if (top >= 2 && !(top & 1)) {
-        const int ci = (top - 2) >> 1;
-        const int rows_c = g.rows / 2, cols_c = g.cols / 2;
-        const int cj = (j0 >> 1) + tid;
-        if (tid < WOUT / 2 && ci >= (R0 >> 1) && 2 * ci + 1 < R1 && ci < rows_c && cj < cols_c) {
-          double s = 0.0;
-          const int base = H + 2 * tid;  // thread column of fine col 2cj = j0 + 2 tid
-#pragma unroll
-          for (int di = 0; di < 3; ++di) {
-            const double* rr = &rlast[((top - 2 + di) & 3) * SWT];
-#pragma unroll
-            for (int dj = 0; dj < 3; ++dj) {
-              const double wgt = (di == 1 ? 2.0 : 1.0) * (dj == 1 ? 2.0 : 1.0) * 0.0625;
-              s = fma(wgt, rr[base + dj], s);
-            }
-          }
-          const int64_t pc = (int64_t)ci * cols_c + cj;
-          const bool actc = a.mask_c == nullptr || a.mask_c[pc];
-          a.rc[b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
-        }
+      for (int k = 0; k < NF; ++k) {
+        const int sn = m3(ph - 2 * k);  // slot of the new row t - 2k (evicts row t - 2k - 3)
+        if (!(k & 1) && k / 2 < NSW) hold[k / 2] = w[k][sn][1];
+        w[k][sn][0] = xch[(k * 2 + sl) * SWT + colL];
+        w[k][sn][1] = nv[k];
+        w[k][sn][2] = xch[(k * 2 + sl) * SWT + colR];
       }
-    }
-    // ---- slide the windows: newest row of F_k = the value just published
-#pragma unroll
-    for (int k = 0; k < NF; ++k) {
-      if (!(k & 1) && k / 2 < NSW) hold[k / 2] = w[k].v[0][1];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        w[k].v[0][c] = w[k].v[1][c];
-        w[k].v[1][c] = w[k].v[2][c];
-      }
-      w[k].v[2][0] = xch[(k * 2 + sl) * SWT + colL];
-      w[k].v[2][1] = nv[k];
-      w[k].v[2][2] = xch[(k * 2 + sl) * SWT + colR];
     }
   }
   cp_wait<0>();
   if (NORM) {
-    // block reduction (deterministic order)
     double v = acc;
     const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -314,8 +308,6 @@ static size_t stream_smem(int nsw, bool res) {
 
 template <typename KF>
 static cudaError_t run_k(KF kern, dim3 grid, size_t smem, cudaStream_t s, const StreamArgs& a) {
-  static thread_local bool attr_set = false;
-  (void)attr_set;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, SWT, smem, s>>>(a);
@@ -327,15 +319,17 @@ cudaError_t launch_stream(const StreamArgs& a0, int nsw, bool res, bool pro, boo
   a.seg = stream_seg(a.g);
   const dim3 grid = stream_grid(a.g, nsw, res);
   const bool zu = a.u == nullptr, ca = a.A.cls != nullptr, ck = a.K.cls != nullptr;
+  const bool msk = a.mask != nullptr;
   cudaStream_t s = a.stream;
   const size_t sm = stream_smem(nsw, res);
   ++g_launches;
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
-    if (ca && ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, true>, grid, sm, s, a);   \
-    if (ca) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, false>, grid, sm, s, a);        \
-    if (ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, true>, grid, sm, s, a);        \
-    return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, false>, grid, sm, s, a);               \
+    if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, false, true>, grid, sm, s, a); \
+    if (ca && ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, true, false>, grid, sm, s, a); \
+    if (ca) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, false, false>, grid, sm, s, a);  \
+    if (ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, true, false>, grid, sm, s, a);  \
+    return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, false, false>, grid, sm, s, a);         \
   }
   // PRE: restriction, optional norm, optional zero start; POST: prolongation, no norm
   MGB_ST(1, true, false, false, false) MGB_ST(1, true, false, true, false)
