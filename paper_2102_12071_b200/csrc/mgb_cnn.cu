@@ -188,7 +188,7 @@ cudaError_t launch_k(KF kern, const Grid& g, size_t smem, Tab A, const uint8_t* 
   ++g_launches;
   dim3 grid((unsigned)((g.n() + 127) / 128), g.batch);
   kern<<<grid, 128, smem, s>>>(g, A, mask, kst, W, slope, K);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 }  // namespace

@@ -309,7 +309,7 @@ cudaError_t launch_sweep2(const Grid& g, const Op& A, const Op& K, const uint8_t
 #define MGB_SW(ZU_, CA_, CK_, NM_) \
   if (zu == ZU_ && ca == CA_ && ck == CK_ && nm == NM_) { \
     k_sweep_t<ZU_, CA_, CK_, NM_><<<grid, blk, 0, s>>>(g, A, K, mask, f, u, uo, partials); \
-    return cudaGetLastError(); }
+    return MGB_DBG(__func__); }
   MGB_SW(false, false, false, false) MGB_SW(false, false, false, true)
   MGB_SW(false, false, true, false)  MGB_SW(false, false, true, true)
   MGB_SW(false, true, false, false)  MGB_SW(false, true, false, true)
@@ -333,7 +333,7 @@ cudaError_t launch_resid_restrict2(const Grid& g, const Op& A, const uint8_t* ma
   else if (zu) k_resid_restrict_t<true, false><<<grid, blk, 0, s>>>(g, A, mask_f, mask_c, f, u, rc);
   else if (ca) k_resid_restrict_t<false, true><<<grid, blk, 0, s>>>(g, A, mask_f, mask_c, f, u, rc);
   else k_resid_restrict_t<false, false><<<grid, blk, 0, s>>>(g, A, mask_f, mask_c, f, u, rc);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 int resnorm_blocks(const Grid& g) {
@@ -349,20 +349,20 @@ cudaError_t launch_resnorm(const Grid& g, const Op& A, const uint8_t* mask, cons
   if (zu) k_resnorm_t<true, false><<<grid, blk, 0, s>>>(g, A, mask, f, u, partials);
   else if (ca) k_resnorm_t<false, true><<<grid, blk, 0, s>>>(g, A, mask, f, u, partials);
   else k_resnorm_t<false, false><<<grid, blk, 0, s>>>(g, A, mask, f, u, partials);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_classify(const Grid& g, const Op& T, const int64_t* rep, int* flag, cudaStream_t s) {
   ++g_launches;
   dim3 grid((g.cols + BX - 1) / BX, (g.rows + BY - 1) / BY, g.batch);
   k_classify<<<grid, dim3(BX, BY), 0, s>>>(g, T, rep, flag);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_gather_cls(const Grid& g, const Op& T, const int64_t* rep, double* out, cudaStream_t s) {
   ++g_launches;
   k_gather_cls<<<g.batch, 256, 0, s>>>(g, T, rep, out);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 int host_band(int i, int n) { return i < 2 ? i : (i >= n - 2 ? 4 - (n - 1 - i) : 2); }

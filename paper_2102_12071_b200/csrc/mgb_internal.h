@@ -25,6 +25,11 @@ int cuda_fail(cudaError_t e, const char* what);
 // Counts kernel launches issued by the wrappers below (bench instrumentation).
 extern thread_local int64_t g_launches;
 
+// MGB_DEBUG_SYNC=1: synchronise after every launch and report the failing kernel
+// (debug aid; never set in measurements).
+cudaError_t debug_sync(const char* what);
+#define MGB_DBG(name) ::mgb::debug_sync(name)
+
 // ---- stencil storage descriptors --------------------------------------------
 // Operators and smoother kernels are addressed per problem b of a batch as
 //   value(p, s, o) = base[b * bstride + s * sstride + o * ostride + p * pstride]

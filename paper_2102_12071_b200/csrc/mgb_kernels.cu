@@ -14,11 +14,23 @@
 //   LU factor / solve     dense.py:21-63, coarse_solve hierarchy.py:91-93
 //   materialize           grid.py:269-292
 //   jacobi                smoothers.py:29-50
+#include <cstdio>
+#include <cstdlib>
+
 #include "mgb_internal.h"
 
 namespace mgb {
 
 thread_local int64_t g_launches = 0;
+
+cudaError_t debug_sync(const char* what) {
+  static const bool on = getenv("MGB_DEBUG_SYNC") && getenv("MGB_DEBUG_SYNC")[0] == '1';
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !on) return e;
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) fprintf(stderr, "[mgb debug] %s failed: %s\n", what, cudaGetErrorString(e));
+  return e;
+}
 
 namespace {
 
@@ -546,7 +558,7 @@ cudaError_t launch_apply(const Grid& g, int k, Tab A, const uint8_t* mask, const
   ++g_launches;
   if (k == 3) k_apply<3><<<pgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask, u, out);
   else k_apply<1><<<pgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask, u, out);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 static dim3 resgrid(const Grid& g) {
@@ -564,14 +576,14 @@ cudaError_t launch_residual(const Grid& g, Tab A, const uint8_t* mask, const dou
   ++g_launches;
   if (nblk) *nblk = residual_blocks(g);
   k_residual<<<resgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask, f, u, r, partials);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_finalize(int batch, int nblk, const double* partials, double* out2,
                             const double* fnorm2, double* hist, int64_t hstride, cudaStream_t s) {
   ++g_launches;
   k_finalize<<<batch, 1024, 0, s>>>(nblk, partials, out2, fnorm2, hist, hstride);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 constexpr int SW_TX = 32, SW_TY = 32;
@@ -582,7 +594,7 @@ cudaError_t launch_sweep(const Grid& g, Tab A, Tab K, const uint8_t* mask, const
   dim3 grid((g.cols + SW_TX - 1) / SW_TX, (g.rows + SW_TY - 1) / SW_TY, g.batch);
   if (u) k_sweep<SW_TX, SW_TY, false><<<grid, dim3(BX, BY), 0, s>>>(g, A, K, mask, f, u, uo);
   else k_sweep<SW_TX, SW_TY, true><<<grid, dim3(BX, BY), 0, s>>>(g, A, K, mask, f, u, uo);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_pointwise(const Grid& g, Tab K, int stage, const uint8_t* mask,
@@ -590,7 +602,7 @@ cudaError_t launch_pointwise(const Grid& g, Tab K, int stage, const uint8_t* mas
                              double* out, cudaStream_t s) {
   ++g_launches;
   k_pointwise<<<pgrid(g), dim3(BX, BY), 0, s>>>(g, K, stage, mask, in, lk ? 1 : 0, slope, base, out);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 constexpr int RS_CTX = 32, RS_CTY = 16;
@@ -606,7 +618,7 @@ cudaError_t launch_resid_restrict(const Grid& g, Tab A, const uint8_t* mask_f,
   ++g_launches;
   if (u) k_restrict<RS_CTX, RS_CTY, 0><<<rgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask_f, mask_c, f, u, rc);
   else k_restrict<RS_CTX, RS_CTY, 1><<<rgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask_f, mask_c, f, u, rc);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_restrict(const Grid& g, const uint8_t* mask_c, const double* fine,
@@ -614,7 +626,7 @@ cudaError_t launch_restrict(const Grid& g, const uint8_t* mask_c, const double* 
   ++g_launches;
   Tab none{nullptr, 0, 0, 0, 0};
   k_restrict<RS_CTX, RS_CTY, 2><<<rgrid(g), dim3(BX, BY), 0, s>>>(g, none, nullptr, mask_c, fine, nullptr, coarse);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_prolong(const Grid& g, const uint8_t* mask_f, const double* coarse,
@@ -622,7 +634,7 @@ cudaError_t launch_prolong(const Grid& g, const uint8_t* mask_f, const double* c
   ++g_launches;
   if (add) k_prolong<true><<<pgrid(g), dim3(BX, BY), 0, s>>>(g, mask_f, coarse, fine);
   else k_prolong<false><<<pgrid(g), dim3(BX, BY), 0, s>>>(g, mask_f, coarse, fine);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_galerkin(const Grid& g, Tab A, const uint8_t* mask_f, const uint8_t* mask_c,
@@ -631,7 +643,7 @@ cudaError_t launch_galerkin(const Grid& g, Tab A, const uint8_t* mask_f, const u
   const int rows_c = g.rows / 2, cols_c = g.cols / 2;
   dim3 grid((cols_c + BX - 1) / BX, (rows_c + BY - 1) / BY, g.batch);
   k_galerkin<<<grid, dim3(BX, BY), 0, s>>>(g, A, mask_f, mask_c, Ac, ring_flag);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_materialize(const Grid& g, Tab A, const int32_t* index_map, int nact,
@@ -639,14 +651,14 @@ cudaError_t launch_materialize(const Grid& g, Tab A, const int32_t* index_map, i
   ++g_launches;
   dim3 grid((nact + 127) / 128, g.batch);
   k_materialize<<<grid, 128, 0, s>>>(g, A, index_map, nact, actp, M);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_lu_factor(int batch, int n, double* lu, int32_t* perm, int* status,
                              cudaStream_t s) {
   ++g_launches;
   k_lu_factor<<<batch, 256, 0, s>>>(n, lu, perm, status);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 static cudaError_t lu_solve_smem(int n) {
@@ -668,7 +680,7 @@ cudaError_t launch_lu_solve_grid(const Grid& g, int n, const double* lu, const i
     if (e != cudaSuccess) return e;
   }
   k_lu_solve<<<g.batch, 256, sizeof(double) * n, s>>>(n, lu, perm, actp, f, g.n(), x, g.n());
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_lu_solve_vec(int n, const double* lu, const int32_t* perm, const double* b,
@@ -677,20 +689,20 @@ cudaError_t launch_lu_solve_vec(int n, const double* lu, const int32_t* perm, co
   if (e != cudaSuccess) return e;
   ++g_launches;
   k_lu_solve<<<1, 256, sizeof(double) * n, s>>>(n, lu, perm, nullptr, b, n, x, n);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_jacobi(const Grid& g, Tab A, const uint8_t* mask, double omega, TabW K,
                           int* zero_diag_flag, cudaStream_t s) {
   ++g_launches;
   k_jacobi<<<pgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask, omega, K, zero_diag_flag);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_convert(const Grid& g, int kst, Tab src, TabW dst, cudaStream_t s) {
   ++g_launches;
   k_convert<<<pgrid(g), dim3(BX, BY), 0, s>>>(g, kst, src, dst);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 }  // namespace mgb

@@ -311,7 +311,7 @@ static cudaError_t run_k(KF kern, dim3 grid, size_t smem, cudaStream_t s, const 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, SWT, smem, s>>>(a);
-  return cudaGetLastError();
+  return MGB_DBG(__func__);
 }
 
 cudaError_t launch_stream(const StreamArgs& a0, int nsw, bool res, bool pro, bool norm) {
