@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
   const int col = j0 - H + tid;
   const bool cin = col >= 0 && col < g.cols;
   const bool owned_c = tid >= H && tid < H + WOUT && cin;
-  const int ccls = bandc(col, g.cols);
+  const int ccls = cin ? bandc(col, g.cols) : 2;  // out-of-grid columns are zeroed anyway
   // the whole strip is interior in x: the interior-class weights apply to every
   // thread whenever the row is interior too (a CTA-uniform test)
   const bool cta_cint = j0 - H >= 2 && j0 - H + SWT - 1 <= g.cols - 3;
