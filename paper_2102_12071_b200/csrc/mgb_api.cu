@@ -75,6 +75,7 @@ struct LevelD {
   uint8_t* mask = nullptr; // null = all active
   double* Acls = nullptr;  // band-class tables (batch x 25 x 9) when A is class-constant
   double* Kcls = nullptr;  // band-class tables (batch x 25 x ks x 9) when M is class-constant
+  double hAint[9] = {0}, hKint[9] = {0};  // interior-class weights (host copy, batch 0)
   std::vector<uint8_t> hmask;
   int64_t nact = 0;
   Op opA() const { return Op{A, Acls, n, 1}; }
@@ -333,7 +334,8 @@ static int64_t count_active(const std::vector<uint8_t>& m) {
 
 // Band-class compaction (mgb_cycle.cu): if every point of the table equals its
 // class representative, keep the 25 class tables (exact) for the hot loop.
-static int classify_table(mgb_hier* h, int l, const double* planes, int ks, double** cls_out, cudaStream_t s) {
+static int classify_table(mgb_hier* h, int l, const double* planes, int ks, double** cls_out, cudaStream_t s,
+                          double* interior_host = nullptr) {
   dfree(*cls_out);
   LevelD& lv = h->lv[l];
   if (!h->compact || lv.mask || !planes) return MGB_OK;
@@ -359,6 +361,8 @@ static int classify_table(mgb_hier* h, int l, const double* planes, int ks, doub
   if (!hf) {
     MGB_CUDA_TRY(dalloc(cls_out, (size_t)h->batch * 25 * ks * 9));
     MGB_CUDA_TRY(launch_gather_cls(h->grid(l), T, drep, *cls_out, s));
+    if (interior_host && ks == 1)
+      MGB_CUDA_TRY(cudaMemcpyAsync(interior_host, *cls_out + 12 * 9, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
   }
   MGB_CUDA_TRY(cudaFreeAsync(drep, s));
   MGB_CUDA_TRY(cudaFreeAsync(flag, s));
@@ -369,9 +373,9 @@ static int classify_table(mgb_hier* h, int l, const double* planes, int ks, doub
 static int classify_all(mgb_hier* h, cudaStream_t s) {
   for (int l = 0; l < h->depth(); ++l) {
     LevelD& lv = h->lv[l];
-    if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s)) return st;
+    if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s, lv.hAint)) return st;
     if (lv.K) {
-      if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s)) return st;
+      if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s, lv.hKint)) return st;
     } else {
       dfree(lv.Kcls);
     }
@@ -876,6 +880,11 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
     a.rc = w->f[l + 1];
     a.partials = fuse_norm ? w->partials : nullptr;
     a.stream = s;
+    a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
+    for (int o = 0; o < 9; ++o) {
+      a.ci[o] = lv.hAint[o];
+      a.ci[9 + o] = lv.hKint[o];
+    }
     MGB_CUDA_TRY(launch_stream(a, nu1, true, false, fuse_norm));
     if (fuse_norm) {
       if (int st = enqueue_finalize(w, stream_blocks(g, nu1, true), hist, hstride, s)) return st;

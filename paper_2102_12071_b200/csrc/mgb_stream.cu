@@ -31,9 +31,11 @@ namespace mgb {
 namespace {
 
 constexpr int SWT = 128;   // threads (= columns incl. halo) per CTA
-constexpr int PD = 16;     // prefetch ring depth (rows) for u
-constexpr int PDF = 32;    // ring depth for f (also read by the later residual stages)
-constexpr int DIST = 8;    // prefetch distance (rows ahead)
+constexpr int PD = 8;      // prefetch ring depth (rows) for u (power of two)
+constexpr int PDF = 24;    // ring depth for f (also read by the later residual stages): rows t-10 .. t+DIST
+constexpr int DIST = 6;    // prefetch distance (rows ahead)
+constexpr int MINB = 4;    // CTAs per SM the register budget is sized for
+__device__ __forceinline__ int fslot(int row) { return (row + 4 * PDF) % PDF; }  // rows >= -4 PDF
 constexpr int NCLS = 25;
 constexpr int CINT = 12;   // interior band class (2 * 5 + 2)
 
@@ -73,8 +75,12 @@ __device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][3]
   return (a0 + a1) + a2;
 }
 
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool CA, bool CK, bool MSK>
-__global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
+// CM: 0 = per-point planes for A and M; 1 = band-class tables in shared memory;
+// 2 = band-class tables with the interior class read from the kernel parameters
+// (constant-bank operands: no registers, no shared-memory traffic).
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool MSK>
+__global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
+  constexpr bool CA = CM != 0, CK = CM != 0;
   using P = SP<NSW, RES, PRO>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
   extern __shared__ double smem[];
@@ -105,17 +111,15 @@ __global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
   const int colL = max(tid - 1, 0), colR = min(tid + 1, SWT - 1);
   const uint8_t* mk = MSK ? a.mask : nullptr;
 
-  double rA[9], rK[9];
   if (CA)
     for (int q = tid; q < NCLS * 9; q += SWT) tA[q] = a.A.cls[(int64_t)b * NCLS * 9 + q];
   if (CK)
     for (int q = tid; q < NCLS * 9; q += SWT) tK[q] = a.K.cls[(int64_t)b * NCLS * 9 + q];
   __syncthreads();
-#pragma unroll
-  for (int o = 0; o < 9; ++o) {
-    rA[o] = CA ? tA[CINT * 9 + o] : 0.0;
-    rK[o] = CK ? tK[CINT * 9 + o] : 0.0;
-  }
+  // interior-class weights: kernel parameters (constant-bank operands, no registers)
+  // for a single problem, else the shared class table
+  const double* rA = CM == 2 ? a.ci : tA + CINT * 9;
+  const double* rK = CM == 2 ? a.ci + 9 : tK + CINT * 9;
 
   // circular register windows: field k row x lives in slot x mod 3
   double w[NF][3][3];
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
   auto issue = [&]() {
     const bool rv = prow >= 0 && prow < g.rows && cin;
     if (!ZU) cp_async8(&ring_u[(prow & (PD - 1)) * SWT + tid], rv ? pu : ub, rv);
-    cp_async8(&ring_f[(prow & (PDF - 1)) * SWT + tid], rv ? pf : fb, rv);
+    cp_async8(&ring_f[fslot(prow) * SWT + tid], rv ? pf : fb, rv);
     cp_commit();
     ++prow;
     if (!ZU) pu += cstride;
@@ -208,14 +212,11 @@ __global__ void __launch_bounds__(SWT) k_stream(StreamArgs a) {
           } else {
             sdot = dot9(tab + (bandc(row, g.rows) * 5 + ccls) * 9, w[k - 1], s0, s1, s2);
           }
-          if (k & 1) {
-            val = ring_f[(row & (PDF - 1)) * SWT + tid] - sdot;
-            if (NORM && k == 1 && row >= R0 && row < R1 && owned_c) acc = fma(val, val, acc);
-          } else {
-            val = hold[k / 2 - 1] + sdot;
-          }
+          if (k & 1) val = ring_f[fslot(row) * SWT + tid] - sdot;
+          else val = hold[k / 2 - 1] + sdot;
           if (MSK && cin && !mk[(int64_t)row * g.cols + col]) val = 0.0;
           val = cin ? val : 0.0;
+          if (NORM && k == 1 && row >= R0 && row < R1 && owned_c) acc = fma(val, val, acc);
           if (k == 2 * NSW && row >= R0 && row < R1 && owned_c) uob[(int64_t)row * g.cols + col] = val;
         }
         nv[k] = val;
@@ -318,18 +319,18 @@ cudaError_t launch_stream(const StreamArgs& a0, int nsw, bool res, bool pro, boo
   StreamArgs a = a0;
   a.seg = stream_seg(a.g);
   const dim3 grid = stream_grid(a.g, nsw, res);
-  const bool zu = a.u == nullptr, ca = a.A.cls != nullptr, ck = a.K.cls != nullptr;
+  const bool zu = a.u == nullptr;
   const bool msk = a.mask != nullptr;
+  const int cm = (a.A.cls != nullptr && a.K.cls != nullptr && !msk) ? (a.ci_valid ? 2 : 1) : 0;
   cudaStream_t s = a.stream;
   const size_t sm = stream_smem(nsw, res);
   ++g_launches;
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
-    if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, false, true>, grid, sm, s, a); \
-    if (ca && ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, true, false>, grid, sm, s, a); \
-    if (ca) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, true, false, false>, grid, sm, s, a);  \
-    if (ck) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, true, false>, grid, sm, s, a);  \
-    return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, false, false, false>, grid, sm, s, a);         \
+    if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, true>, grid, sm, s, a);           \
+    if (cm == 2) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 2, false>, grid, sm, s, a);      \
+    if (cm == 1) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 1, false>, grid, sm, s, a);      \
+    return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, false>, grid, sm, s, a);                   \
   }
   // PRE: restriction, optional norm, optional zero start; POST: prolongation, no norm
   MGB_ST(1, true, false, false, false) MGB_ST(1, true, false, true, false)

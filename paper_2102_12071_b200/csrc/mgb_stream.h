@@ -17,6 +17,8 @@ struct StreamArgs {
   double* rc;              // restricted residual (PRE)
   double* partials;        // per-CTA sums of the input residual squared (history)
   int seg;                 // rows per CTA segment (set by the launcher)
+  int ci_valid;            // 1: ci holds the interior-class weights (batch == 1, classed A and M)
+  double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
   cudaStream_t stream;
 };
 
