@@ -32,10 +32,9 @@ namespace {
 
 constexpr int SWT = 128;   // threads (= columns incl. halo) per CTA
 constexpr int PD = 8;      // prefetch ring depth (rows) for u (power of two)
-constexpr int PDF = 24;    // ring depth for f (also read by the later residual stages): rows t-10 .. t+DIST
-constexpr int DIST = 6;    // prefetch distance (rows ahead)
+constexpr int PDF = 16;    // ring depth for f (also read by the later residual stages): rows t-10 .. t+DIST
+constexpr int DIST = 5;    // prefetch distance (rows ahead)
 constexpr int MINB = 4;    // CTAs per SM the register budget is sized for
-__device__ __forceinline__ int fslot(int row) { return (row + 4 * PDF) % PDF; }  // rows >= -4 PDF
 constexpr int NCLS = 25;
 constexpr int CINT = 12;   // interior band class (2 * 5 + 2)
 
@@ -75,60 +74,192 @@ __device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][3]
   return (a0 + a1) + a2;
 }
 
+// Per-CTA constants of a streaming pass.
+struct Ctx {
+  Grid g;
+  int b, tid, j0, col, colL, colR, R0, R1;
+  bool cin, owned_c;
+  int ccls;
+  const double* fb;
+  const double* ub;
+  double* uob;
+  double* ring_u;
+  double* ring_f;
+  double* xch;
+  double* rlast;
+  const double* tA;
+  const double* tK;
+  const uint8_t* mk;
+};
+
+// One pipeline step (row t).  FAST: every row the step touches is an interior
+// row, every column of the CTA is an interior in-grid column, so no bounds,
+// band-class or column tests are needed.  PH = t mod 3 (window slots).
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool MSK, bool FAST, int PH>
+__device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, const int t,
+                                            double (&w)[SP<NSW, RES, PRO>::NF][3][3], double (&hold)[NSW],
+                                            double& acc) {
+  using P = SP<NSW, RES, PRO>;
+  constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
+  constexpr bool CL = CM != 0;
+  const Grid& g = c.g;
+  double nv[NF + 1];
+  // ---- F_0 = u (+ P ec) at row t
+  {
+    double u0 = 0.0;
+    const bool rv = FAST || ((unsigned)t < (unsigned)g.rows && c.cin);
+    if (!ZU) u0 = c.ring_u[(t & (PD - 1)) * SWT + c.tid];
+    if (PRO && rv) {
+      const int rc_ = g.rows / 2, cc_ = g.cols / 2;
+      const double* eb = a.ec + c.b * (int64_t)rc_ * cc_;
+      double s = 0.0;
+#pragma unroll
+      for (int di = -1; di <= 1; ++di) {
+        const int tt = t - 1 - di;
+        if ((tt & 1) || (!FAST && (tt < 0 || (tt >> 1) >= rc_))) continue;
+        const double* er = eb + (int64_t)(tt >> 1) * cc_;
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) {
+          const int uu = c.col - 1 - dj;
+          if ((uu & 1) || (!FAST && (uu < 0 || (uu >> 1) >= cc_))) continue;
+          const double wgt = (di == 0 ? 2.0 : 1.0) * (dj == 0 ? 2.0 : 1.0) * 0.125;
+          s = fma(wgt, __ldg(er + (uu >> 1)), s);
+        }
+      }
+      u0 += s;
+    }
+    if (MSK && rv && !c.mk[(int64_t)t * g.cols + c.col]) u0 = 0.0;
+    nv[0] = (FAST || rv) ? u0 : 0.0;
+  }
+  // ---- stages k = 1..S at row t - 2k (rows are CTA-uniform)
+#pragma unroll
+  for (int k = 1; k <= S; ++k) {
+    const int row = t - 2 * k;
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int s0 = m3(PH - 2 * k - 1), s1 = m3(PH - 2 * k), s2 = m3(PH - 2 * k + 1);
+    double val = 0.0;
+    if (FAST || (unsigned)row < (unsigned)g.rows) {
+      const Op& op = (k & 1) ? a.A : a.K;
+      double sdot;
+      if (!CL) {
+        const double* base = op.planes + (int64_t)c.b * 9 * op.n + ((int64_t)row * g.cols + (c.cin ? c.col : 0));
+        double wt[9];
+#pragma unroll
+        for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
+        sdot = dot9(wt, w[k - 1], s0, s1, s2);
+      } else if (FAST) {
+        const double* reg = CM == 2 ? ((k & 1) ? a.ci : a.ci + 9) : (((k & 1) ? c.tA : c.tK) + CINT * 9);
+        sdot = dot9(reg, w[k - 1], s0, s1, s2);
+      } else {
+        const double* tab = (k & 1) ? c.tA : c.tK;
+        sdot = dot9(tab + (bandc(row, g.rows) * 5 + c.ccls) * 9, w[k - 1], s0, s1, s2);
+      }
+      if (k & 1) val = c.ring_f[(row & (PDF - 1)) * SWT + c.tid] - sdot;
+      else val = hold[k / 2 - 1] + sdot;
+      if (MSK && c.cin && !c.mk[(int64_t)row * g.cols + c.col]) val = 0.0;
+      if (!FAST) val = c.cin ? val : 0.0;
+      if (NORM && k == 1 && c.owned_c && row >= c.R0 && row < c.R1) acc = fma(val, val, acc);
+      if (k == 2 * NSW && c.owned_c && row >= c.R0 && row < c.R1) c.uob[(int64_t)row * g.cols + c.col] = val;
+    }
+    nv[k] = val;
+  }
+  // ---- publish, then slide the windows (slot of the evicted row)
+  const int sl = t & 1;
+#pragma unroll
+  for (int k = 0; k < NF; ++k) c.xch[(k * 2 + sl) * SWT + c.tid] = nv[k];
+  if (RES) c.rlast[((t - 2 * S) & 3) * SWT + c.tid] = nv[S];
+  __syncthreads();
+  if (RES) {
+    const int top = t - 2 * S;
+    if (top >= 2 && !(top & 1)) {
+      const int ci = (top - 2) >> 1;
+      const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+      const int cj = (c.j0 >> 1) + c.tid;
+      if (c.tid < WOUT / 2 && ci >= (c.R0 >> 1) && 2 * ci + 1 < c.R1 && ci < rows_c && cj < cols_c) {
+        const int base = H + 2 * c.tid;
+        const double* r0p = &c.rlast[((top - 2) & 3) * SWT + base];
+        const double* r1p = &c.rlast[((top - 1) & 3) * SWT + base];
+        const double* r2p = &c.rlast[(top & 3) * SWT + base];
+        double s = 0.0625 * r0p[0];
+        s = fma(0.125, r0p[1], s);
+        s = fma(0.0625, r0p[2], s);
+        s = fma(0.125, r1p[0], s);
+        s = fma(0.25, r1p[1], s);
+        s = fma(0.125, r1p[2], s);
+        s = fma(0.0625, r2p[0], s);
+        s = fma(0.125, r2p[1], s);
+        s = fma(0.0625, r2p[2], s);
+        const int64_t pc = (int64_t)ci * cols_c + cj;
+        const bool actc = a.mask_c == nullptr || a.mask_c[pc];
+        a.rc[c.b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int sn = m3(PH - 2 * k);  // slot of the new row t - 2k (evicts row t - 2k - 3)
+    if (!(k & 1) && k / 2 < NSW) hold[k / 2] = w[k][sn][1];
+    w[k][sn][0] = c.xch[(k * 2 + sl) * SWT + c.colL];
+    w[k][sn][1] = nv[k];
+    w[k][sn][2] = c.xch[(k * 2 + sl) * SWT + c.colR];
+  }
+}
+
 // CM: 0 = per-point planes for A and M; 1 = band-class tables in shared memory;
 // 2 = band-class tables with the interior class read from the kernel parameters
 // (constant-bank operands: no registers, no shared-memory traffic).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool MSK>
 __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
-  constexpr bool CA = CM != 0, CK = CM != 0;
   using P = SP<NSW, RES, PRO>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
   extern __shared__ double smem[];
-  double* ring_u = smem;                               // PD x SWT (unused when ZU)
-  double* ring_f = ring_u + PD * SWT;                  // PDF x SWT
-  double* xch = ring_f + PDF * SWT;                    // NF x 2 x SWT neighbour exchange rows
-  double* rlast = xch + NF * 2 * SWT;                  // 4 x SWT last-residual ring (RES)
-  double* tA = rlast + 4 * SWT;                        // 25 x 9
-  double* tK = tA + NCLS * 9;                          // 25 x 9
-  double* red = tK + NCLS * 9;                         // 32
-
-  const Grid g = a.g;
-  const int tid = threadIdx.x;
-  const int b = blockIdx.z;
+  Ctx c;
+  c.g = a.g;
+  const Grid& g = c.g;
+  c.ring_u = smem;                               // PD x SWT (unused when ZU)
+  c.ring_f = c.ring_u + PD * SWT;                // PDF x SWT
+  c.xch = c.ring_f + PDF * SWT;                  // NF x 2 x SWT neighbour exchange rows
+  c.rlast = c.xch + NF * 2 * SWT;                // 4 x SWT last-residual ring (RES)
+  double* tA = c.rlast + 4 * SWT;                // 25 x 9
+  double* tK = tA + NCLS * 9;                    // 25 x 9
+  double* red = tK + NCLS * 9;                   // 32
+  c.tA = tA;
+  c.tK = tK;
+  c.tid = threadIdx.x;
+  c.b = blockIdx.z;
   const int64_t n = g.n();
-  const int j0 = blockIdx.x * WOUT;        // first owned column (even)
-  const int col = j0 - H + tid;
-  const bool cin = col >= 0 && col < g.cols;
-  const bool owned_c = tid >= H && tid < H + WOUT && cin;
-  const int ccls = cin ? bandc(col, g.cols) : 2;  // out-of-grid columns are zeroed anyway
-  // the whole strip is interior in x: the interior-class weights apply to every
-  // thread whenever the row is interior too (a CTA-uniform test)
-  const bool cta_cint = j0 - H >= 2 && j0 - H + SWT - 1 <= g.cols - 3;
-  const int R0 = blockIdx.y * a.seg, R1 = min(g.rows, R0 + a.seg);
-  const double* fb = a.f + b * n;
-  const double* ub = ZU ? nullptr : a.u + b * n;
-  double* uob = a.uo + b * n;
-  const int colL = max(tid - 1, 0), colR = min(tid + 1, SWT - 1);
-  const uint8_t* mk = MSK ? a.mask : nullptr;
+  c.j0 = blockIdx.x * WOUT;                      // first owned column (even)
+  c.col = c.j0 - H + c.tid;
+  c.cin = c.col >= 0 && c.col < g.cols;
+  c.owned_c = c.tid >= H && c.tid < H + WOUT && c.cin;
+  c.ccls = c.cin ? bandc(c.col, g.cols) : 2;     // out-of-grid columns are zeroed anyway
+  c.R0 = blockIdx.y * a.seg;
+  c.R1 = min(g.rows, c.R0 + a.seg);
+  c.fb = a.f + c.b * n;
+  c.ub = ZU ? nullptr : a.u + c.b * n;
+  c.uob = a.uo + c.b * n;
+  c.colL = max(c.tid - 1, 0);
+  c.colR = min(c.tid + 1, SWT - 1);
+  c.mk = MSK ? a.mask : nullptr;
+  // fast steps need every CTA column interior (band class 2) and in the grid
+  const bool cta_fast = c.j0 - H >= 2 && c.j0 - H + SWT - 1 <= g.cols - 3;
 
-  if (CA)
-    for (int q = tid; q < NCLS * 9; q += SWT) tA[q] = a.A.cls[(int64_t)b * NCLS * 9 + q];
-  if (CK)
-    for (int q = tid; q < NCLS * 9; q += SWT) tK[q] = a.K.cls[(int64_t)b * NCLS * 9 + q];
+  if (CM != 0) {
+    for (int q = c.tid; q < NCLS * 9; q += SWT) {
+      tA[q] = a.A.cls[(int64_t)c.b * NCLS * 9 + q];
+      tK[q] = a.K.cls[(int64_t)c.b * NCLS * 9 + q];
+    }
+  }
   __syncthreads();
-  // interior-class weights: kernel parameters (constant-bank operands, no registers)
-  // for a single problem, else the shared class table
-  const double* rA = CM == 2 ? a.ci : tA + CINT * 9;
-  const double* rK = CM == 2 ? a.ci + 9 : tK + CINT * 9;
 
-  // circular register windows: field k row x lives in slot x mod 3
   double w[NF][3][3];
 #pragma unroll
   for (int k = 0; k < NF; ++k)
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) w[k][r][c] = 0.0;
+      for (int q = 0; q < 3; ++q) w[k][r][q] = 0.0;
   double hold[NSW];
 #pragma unroll
   for (int m = 0; m < NSW; ++m) hold[m] = 0.0;
@@ -136,18 +267,17 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
 
   // steps t in [t0, t1], t0 aligned to a multiple of 3 (extra leading steps only
   // compute rows nobody needs)
-  int t0 = R0 - S - 1;
+  int t0 = c.R0 - S - 1;
   t0 -= m3(t0);
-  const int t1 = R1 + 2 * S;
-  // prefetch rows t0 .. t0 + DIST - 1; pointers advance one row per issue
+  const int t1 = c.R1 + 2 * S;
   int prow = t0;
   const int64_t cstride = g.cols;
-  const double* pu = ZU ? nullptr : ub + (int64_t)prow * cstride + col;
-  const double* pf = fb + (int64_t)prow * cstride + col;
+  const double* pu = ZU ? nullptr : c.ub + (int64_t)prow * cstride + c.col;
+  const double* pf = c.fb + (int64_t)prow * cstride + c.col;
   auto issue = [&]() {
-    const bool rv = prow >= 0 && prow < g.rows && cin;
-    if (!ZU) cp_async8(&ring_u[(prow & (PD - 1)) * SWT + tid], rv ? pu : ub, rv);
-    cp_async8(&ring_f[fslot(prow) * SWT + tid], rv ? pf : fb, rv);
+    const bool rv = (unsigned)prow < (unsigned)g.rows && c.cin;
+    if (!ZU) cp_async8(&c.ring_u[(prow & (PD - 1)) * SWT + c.tid], rv ? pu : c.ub, rv);
+    cp_async8(&c.ring_f[(prow & (PDF - 1)) * SWT + c.tid], rv ? pf : c.fb, rv);
     cp_commit();
     ++prow;
     if (!ZU) pu += cstride;
@@ -155,126 +285,34 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   };
   for (int q = 0; q < DIST; ++q) issue();
 
-  for (int tb = t0; tb <= t1; tb += 3) {
-#pragma unroll
-    for (int ph = 0; ph < 3; ++ph) {
-      const int t = tb + ph;
-      issue();
-      cp_wait<DIST>();
-      double nv[NF + 1];
-      // ---- F_0 = u (+ P ec) at row t
-      {
-        double u0 = 0.0;
-        const bool rv = (unsigned)t < (unsigned)g.rows && cin;
-        if (!ZU) u0 = ring_u[(t & (PD - 1)) * SWT + tid];
-        if (PRO && rv) {
-          const int rc_ = g.rows / 2, cc_ = g.cols / 2;
-          const double* eb = a.ec + b * (int64_t)rc_ * cc_;
-          double s = 0.0;
-#pragma unroll
-          for (int di = -1; di <= 1; ++di) {
-            const int tt = t - 1 - di;
-            if (tt < 0 || (tt & 1) || (tt >> 1) >= rc_) continue;
-            const double* er = eb + (int64_t)(tt >> 1) * cc_;
-#pragma unroll
-            for (int dj = -1; dj <= 1; ++dj) {
-              const int uu = col - 1 - dj;
-              if (uu < 0 || (uu & 1) || (uu >> 1) >= cc_) continue;
-              const double wgt = (di == 0 ? 2.0 : 1.0) * (dj == 0 ? 2.0 : 1.0) * 0.125;
-              s = fma(wgt, __ldg(er + (uu >> 1)), s);
-            }
-          }
-          u0 += s;
-        }
-        if (MSK && rv && !mk[(int64_t)t * g.cols + col]) u0 = 0.0;
-        nv[0] = rv ? u0 : 0.0;
-      }
-      // ---- stages k = 1..S at row t - 2k (row is CTA-uniform)
-#pragma unroll
-      for (int k = 1; k <= S; ++k) {
-        const int row = t - 2 * k;
-        const int s0 = m3(ph - 2 * k - 1), s1 = m3(ph - 2 * k), s2 = m3(ph - 2 * k + 1);
-        double val = 0.0;
-        if ((unsigned)row < (unsigned)g.rows) {
-          const bool CL = (k & 1) ? CA : CK;
-          const Op& op = (k & 1) ? a.A : a.K;
-          const double* tab = (k & 1) ? tA : tK;
-          const double* reg = (k & 1) ? rA : rK;
-          double sdot;
-          if (!CL) {
-            const double* base = op.planes + (int64_t)b * 9 * op.n + ((int64_t)row * g.cols + (cin ? col : 0));
-            double wt[9];
-#pragma unroll
-            for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
-            sdot = dot9(wt, w[k - 1], s0, s1, s2);
-          } else if (cta_cint && row >= 2 && row < g.rows - 2) {
-            sdot = dot9(reg, w[k - 1], s0, s1, s2);
-          } else {
-            sdot = dot9(tab + (bandc(row, g.rows) * 5 + ccls) * 9, w[k - 1], s0, s1, s2);
-          }
-          if (k & 1) val = ring_f[fslot(row) * SWT + tid] - sdot;
-          else val = hold[k / 2 - 1] + sdot;
-          if (MSK && cin && !mk[(int64_t)row * g.cols + col]) val = 0.0;
-          val = cin ? val : 0.0;
-          if (NORM && k == 1 && row >= R0 && row < R1 && owned_c) acc = fma(val, val, acc);
-          if (k == 2 * NSW && row >= R0 && row < R1 && owned_c) uob[(int64_t)row * g.cols + col] = val;
-        }
-        nv[k] = val;
-      }
-      // ---- publish, then slide the windows (slot of the evicted row)
-      const int sl = t & 1;
-#pragma unroll
-      for (int k = 0; k < NF; ++k) xch[(k * 2 + sl) * SWT + tid] = nv[k];
-      if (RES) rlast[((t - 2 * S) & 3) * SWT + tid] = nv[S];
-      __syncthreads();
-      if (RES) {
-        const int top = t - 2 * S;
-        if (top >= 2 && !(top & 1)) {
-          const int ci = (top - 2) >> 1;
-          const int rows_c = g.rows / 2, cols_c = g.cols / 2;
-          const int cj = (j0 >> 1) + tid;
-          if (tid < WOUT / 2 && ci >= (R0 >> 1) && 2 * ci + 1 < R1 && ci < rows_c && cj < cols_c) {
-            const int base = H + 2 * tid;
-            const double* r0p = &rlast[((top - 2) & 3) * SWT + base];
-            const double* r1p = &rlast[((top - 1) & 3) * SWT + base];
-            const double* r2p = &rlast[(top & 3) * SWT + base];
-            double s = 0.0625 * r0p[0];
-            s = fma(0.125, r0p[1], s);
-            s = fma(0.0625, r0p[2], s);
-            s = fma(0.125, r1p[0], s);
-            s = fma(0.25, r1p[1], s);
-            s = fma(0.125, r1p[2], s);
-            s = fma(0.0625, r2p[0], s);
-            s = fma(0.125, r2p[1], s);
-            s = fma(0.0625, r2p[2], s);
-            const int64_t pc = (int64_t)ci * cols_c + cj;
-            const bool actc = a.mask_c == nullptr || a.mask_c[pc];
-            a.rc[b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < NF; ++k) {
-        const int sn = m3(ph - 2 * k);  // slot of the new row t - 2k (evicts row t - 2k - 3)
-        if (!(k & 1) && k / 2 < NSW) hold[k / 2] = w[k][sn][1];
-        w[k][sn][0] = xch[(k * 2 + sl) * SWT + colL];
-        w[k][sn][1] = nv[k];
-        w[k][sn][2] = xch[(k * 2 + sl) * SWT + colR];
-      }
-    }
+#define MGB_STEP(PH_)                                                                                  \
+  {                                                                                                    \
+    const int t = tb + PH_;                                                                            \
+    issue();                                                                                           \
+    cp_wait<DIST>();                                                                                   \
+    if (cta_fast && t - 2 * S >= 2 && t <= g.rows - 3)                                                 \
+      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, true, PH_>(a, c, t, w, hold, acc);                 \
+    else                                                                                               \
+      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, false, PH_>(a, c, t, w, hold, acc);                \
   }
+  for (int tb = t0; tb <= t1; tb += 3) {
+    MGB_STEP(0)
+    MGB_STEP(1)
+    MGB_STEP(2)
+  }
+#undef MGB_STEP
   cp_wait<0>();
   if (NORM) {
     double v = acc;
-    const int lane = tid & 31, wid = tid >> 5;
+    const int lane = c.tid & 31, wid = c.tid >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if (lane == 0) red[wid] = v;
     __syncthreads();
-    if (tid == 0) {
+    if (c.tid == 0) {
       double s = 0.0;
       for (int q = 0; q < SWT / 32; ++q) s += red[q];
-      a.partials[(int64_t)b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = s;
+      a.partials[(int64_t)c.b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = s;
     }
   }
 }
