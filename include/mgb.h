@@ -136,8 +136,10 @@ int mgb_hier_operator_planes(const mgb_hier* h, int level, const double** planes
    mgb_hier_storage_info reports whether level `level`'s A / M tables are class-compact. */
 int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream);
 int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_classed);
-/* 1 (default): fused row-streaming PRE/POST passes for V(1|2, 1|2) with 1-stage
-   smoothers; 0: separate sweep / restriction / prolongation passes. */
+/* Cycle pass structure for V(1|2, 1|2) with 1-stage smoothers: 2 (default) one
+   row-streaming pass per smoothing phase (sweeps + restriction, prolongation +
+   sweeps); 1: one streaming pass per sweep; 0: separate sweep / restriction /
+   prolongation kernels. */
 int mgb_hier_set_fused(mgb_hier* h, int enable);
 
 /* equip_inferred (hierarchy.py:207-214): per-level CNN inference on levels 0..L-2. */

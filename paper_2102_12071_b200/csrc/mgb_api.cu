@@ -92,7 +92,8 @@ struct mgb_hier {
   double slope = 0.01;
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
-  int fused = 1;            // row-streaming PRE/POST passes (mgb_stream.cu) where applicable
+  int fused = 2;            // 2: one streaming pass per smoothing phase; 1: single-sweep streaming
+                            // passes; 0: separate sweep / restriction / prolongation kernels
   ~mgb_hier() {
     DeviceGuard dg(device);
     for (auto& l : lv) {
@@ -520,7 +521,7 @@ extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double 
       }
   }
   if (const char* e = getenv("MGB_STORAGE")) h->compact = std::string(e) != "planes";
-  if (const char* e = getenv("MGB_FUSED")) h->fused = std::string(e) != "0";
+  if (const char* e = getenv("MGB_FUSED")) h->fused = atoi(e);
   if (int st = classify_all(h.get(), s)) return st;
   *out = h.release();
   return MGB_OK;
@@ -536,7 +537,7 @@ extern "C" int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream) {
 
 extern "C" int mgb_hier_set_fused(mgb_hier* h, int enable) {
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
-  h->fused = enable ? 1 : 0;
+  h->fused = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
   ++h->version;
   return MGB_OK;
 }
@@ -782,8 +783,7 @@ extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
     if (l + 1 < L) MGB_CUDA_TRY(dalloc(&w->t[l], cnt));
   }
   w->max_nblk = std::max(std::max(residual_blocks(h->grid(0)), resnorm_blocks(h->grid(0))),
-                         std::max(sweep_blocks(h->grid(0)),
-                                  std::max(stream_blocks(h->grid(0), 1, true), stream_blocks(h->grid(0), 2, true))));
+                         std::max(sweep_blocks(h->grid(0)), stream_max_blocks(h->grid(0))));
   MGB_CUDA_TRY(dalloc(&w->partials, (size_t)w->max_nblk * h->batch));
   MGB_CUDA_TRY(dalloc(&w->fnorm2, (size_t)h->batch));
   MGB_CUDA_TRY(dalloc(&w->scratch, (size_t)h->batch * 4));
@@ -867,7 +867,8 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   const Grid g = h->grid(l);
   const bool fuse_norm = hist && nu1 > 0 && lv.ks == 1;
   if (h->fused && lv.ks == 1 && (nu1 == 1 || nu1 == 2) && (nu2 == 1 || nu2 == 2)) {
-    // PRE: [history norm] + nu1 sweeps + residual + restriction in one streaming pass
+    // PRE: [history norm] + nu1 sweeps + residual + restriction in streaming passes
+    // (fused = 2: one pass per phase; fused = 1: single-sweep passes)
     StreamArgs a{};
     a.g = g;
     a.A = lv.opA();
@@ -875,31 +876,53 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
     a.mask = lv.mask;
     a.mask_c = h->lv[l + 1].mask;
     a.f = f;
-    a.u = zero ? nullptr : cur;
-    a.uo = oth;
-    a.rc = w->f[l + 1];
-    a.partials = fuse_norm ? w->partials : nullptr;
     a.stream = s;
     a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
     for (int o = 0; o < 9; ++o) {
       a.ci[o] = lv.hAint[o];
       a.ci[9 + o] = lv.hKint[o];
     }
-    MGB_CUDA_TRY(launch_stream(a, nu1, true, false, fuse_norm));
-    if (fuse_norm) {
-      if (int st = enqueue_finalize(w, stream_blocks(g, nu1, true), hist, hstride, s)) return st;
+    const bool split = h->fused == 1;
+    int nb = 0;
+    const double* in = zero ? nullptr : cur;
+    if (split && nu1 == 2) {
+      a.u = in;
+      a.uo = oth;
+      a.partials = fuse_norm ? w->partials : nullptr;
+      MGB_CUDA_TRY(launch_stream(a, 1, false, false, fuse_norm, &nb));
+      if (fuse_norm) {
+        if (int st = enqueue_finalize(w, nb, hist, hstride, s)) return st;
+      }
+      std::swap(cur, oth);
+      in = cur;
+    }
+    const bool norm2 = fuse_norm && !(split && nu1 == 2);
+    a.u = in;
+    a.uo = oth;
+    a.rc = w->f[l + 1];
+    a.partials = norm2 ? w->partials : nullptr;
+    MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu1, true, false, norm2, &nb));
+    if (norm2) {
+      if (int st = enqueue_finalize(w, nb, hist, hstride, s)) return st;
     }
     std::swap(cur, oth);
     double* ec = nullptr;
     if (int st = vcycle_rec(w, l + 1, w->f[l + 1], w->u[l + 1], true, nu1, nu2, s, &ec)) return st;
-    // POST: coarse-grid correction + nu2 sweeps in one streaming pass
+    // POST: coarse-grid correction + nu2 sweeps
     a.u = cur;
     a.uo = oth;
     a.ec = ec;
     a.rc = nullptr;
     a.partials = nullptr;
-    MGB_CUDA_TRY(launch_stream(a, nu2, false, true, false));
+    MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu2, false, true, false, &nb));
     std::swap(cur, oth);
+    if (split && nu2 == 2) {
+      a.u = cur;
+      a.uo = oth;
+      a.ec = nullptr;
+      MGB_CUDA_TRY(launch_stream(a, 1, false, false, false, &nb));
+      std::swap(cur, oth);
+    }
     *result = cur;
     return MGB_OK;
   }

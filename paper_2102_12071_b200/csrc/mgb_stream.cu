@@ -25,18 +25,22 @@
 // Reference: v_cycle hierarchy.py:96-111 (with RepeatedSmoother cli.py:365-377),
 // apply_stencil grid.py:216-226, inferred_apply smoothers.py:325-343, restrict
 // transfer.py:108-121, prolong transfer.py:124-147, history hierarchy.py:129-141.
+#include <utility>
+#include <vector>
+#include <algorithm>
+
 #include "mgb_stream.h"
 
 namespace mgb {
 namespace {
 
-constexpr int SWC = 128;   // columns (incl. halo) per CTA
-constexpr int CPT = 2;     // columns per thread
-constexpr int SWT = SWC / CPT;  // threads per CTA
+constexpr int SWT = 128;   // threads (= columns incl. halo) per CTA
 constexpr int PD = 8;      // prefetch ring depth (rows) for u (power of two)
-constexpr int PDF = 16;    // ring depth for f (rows t-10 .. t+DIST; power of two)
+constexpr int PDF = 16;    // ring depth for f (also read by the later residual stages): rows t-10 .. t+DIST
 constexpr int DIST = 5;    // prefetch distance (rows ahead)
-constexpr int MINB = 5;    // CTAs per SM the register budget is sized for
+constexpr int MINB = 4;    // CTAs per SM the register budget is sized for
+constexpr int PE = 8;      // ring of coarse rows (POST prolongation), power of two
+constexpr int EW = SWT / 2 + 4;  // coarse columns staged per CTA
 constexpr int NCLS = 25;
 constexpr int CINT = 12;   // interior band class (2 * 5 + 2)
 
@@ -54,46 +58,41 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 template <int NSW, bool RES, bool PRO>
 struct SP {
   static constexpr int S = 2 * NSW + (RES ? 1 : 0);  // stencil stages after the input field
-  static constexpr int H = 2 * NSW + 2;              // column halo per side (even)
-  static constexpr int WOUT = SWC - 2 * H;           // owned columns per strip (even)
+  static constexpr int H = 2 * NSW + 2;              // column halo per side
+  static constexpr int WOUT = SWT - 2 * H;           // owned columns per strip (even)
   static constexpr int NF = S;                       // fields with a window (F_0 .. F_{S-1})
 };
 
 // compile-time positive modulo 3
 __host__ __device__ constexpr int m3(int x) { return ((x % 3) + 3) % 3; }
 
-// 3x3 dot product of weights with window columns c0..c0+2 of rows s0, s1, s2,
-// three independent accumulation chains, the first seeded with `init`:
-//   returns init + sgn * sum(w * x)
-template <bool NEG>
-__device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][4], int s0, int s1, int s2, int c0,
-                                       double init) {
-  double a0 = NEG ? fma(-wt[0], x[s0][c0], init) : fma(wt[0], x[s0][c0], init);
-  double a1 = wt[3] * x[s1][c0];
-  double a2 = wt[6] * x[s2][c0];
-  a0 = fma(wt[1], x[s0][c0 + 1], NEG ? -a0 : a0);
-  a1 = fma(wt[4], x[s1][c0 + 1], a1);
-  a2 = fma(wt[7], x[s2][c0 + 1], a2);
-  a0 = fma(wt[2], x[s0][c0 + 2], a0);
-  a1 = fma(wt[5], x[s1][c0 + 2], a1);
-  a2 = fma(wt[8], x[s2][c0 + 2], a2);
-  const double t = (a0 + a1) + a2;
-  return NEG ? -t : t;
+// 3x3 dot product with three independent accumulation chains
+__device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][3], int s0, int s1, int s2) {
+  double a0 = wt[0] * x[s0][0];
+  double a1 = wt[3] * x[s1][0];
+  double a2 = wt[6] * x[s2][0];
+  a0 = fma(wt[1], x[s0][1], a0);
+  a1 = fma(wt[4], x[s1][1], a1);
+  a2 = fma(wt[7], x[s2][1], a2);
+  a0 = fma(wt[2], x[s0][2], a0);
+  a1 = fma(wt[5], x[s1][2], a1);
+  a2 = fma(wt[8], x[s2][2], a2);
+  return (a0 + a1) + a2;
 }
 
 // Per-CTA constants of a streaming pass.
 struct Ctx {
   Grid g;
-  int b, tid, j0, R0, R1;
-  int col[CPT];
-  bool cin[CPT], owned_c[CPT];
-  int ccls[CPT];
-  int lL, lR;   // exchange-row indices of the left / right neighbour columns
+  int b, tid, j0, col, colL, colR, R0, R1;
+  bool cin, owned_c;
+  int ccls;
   const double* fb;
   const double* ub;
   double* uob;
   double* ring_u;
   double* ring_f;
+  double* ring_e;   // PE x EW coarse correction rows (POST)
+  int cjb;          // coarse column of ring_e entry 0
   double* xch;
   double* rlast;
   const double* tA;
@@ -102,85 +101,81 @@ struct Ctx {
 };
 
 // One pipeline step (row t).  FAST: every row the step touches is an interior
-// row and every column of the CTA an interior in-grid column, so no bounds,
+// row, every column of the CTA is an interior in-grid column, so no bounds,
 // band-class or column tests are needed.  PH = t mod 3 (window slots).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool MSK, bool FAST, int PH>
 __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, const int t,
-                                            double (&w)[SP<NSW, RES, PRO>::NF][3][4],
-                                            double (&hold)[NSW][CPT], double& acc) {
+                                            double (&w)[SP<NSW, RES, PRO>::NF][3][3], double (&hold)[NSW],
+                                            double& acc) {
   using P = SP<NSW, RES, PRO>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
   constexpr bool CL = CM != 0;
   const Grid& g = c.g;
-  double nv[NF + 1][CPT];
-  const int tc = CPT * c.tid;  // first exchange column of this thread
+  double nv[NF + 1];
   // ---- F_0 = u (+ P ec) at row t
-#pragma unroll
-  for (int q = 0; q < CPT; ++q) {
+  {
     double u0 = 0.0;
-    const bool rv = FAST || ((unsigned)t < (unsigned)g.rows && c.cin[q]);
-    if (!ZU) u0 = c.ring_u[(t & (PD - 1)) * SWC + tc + q];
+    const bool rv = FAST || ((unsigned)t < (unsigned)g.rows && c.cin);
+    if (!ZU) u0 = c.ring_u[(t & (PD - 1)) * SWT + c.tid];
     if (PRO && rv) {
-      const int rc_ = g.rows / 2, cc_ = g.cols / 2;
-      const double* eb = a.ec + c.b * (int64_t)rc_ * cc_;
+      // u += P ec with the coarse rows staged in shared memory (ring_e)
       double s = 0.0;
 #pragma unroll
       for (int di = -1; di <= 1; ++di) {
         const int tt = t - 1 - di;
-        if ((tt & 1) || (!FAST && (tt < 0 || (tt >> 1) >= rc_))) continue;
-        const double* er = eb + (int64_t)(tt >> 1) * cc_;
+        if (tt & 1) continue;
+        const double* er = c.ring_e + ((tt >> 1) & (PE - 1)) * EW;  // out-of-range rows were zero-filled
 #pragma unroll
         for (int dj = -1; dj <= 1; ++dj) {
-          const int uu = c.col[q] - 1 - dj;
-          if ((uu & 1) || (!FAST && (uu < 0 || (uu >> 1) >= cc_))) continue;
+          const int uu = c.col - 1 - dj;
+          if (uu & 1) continue;
           const double wgt = (di == 0 ? 2.0 : 1.0) * (dj == 0 ? 2.0 : 1.0) * 0.125;
-          s = fma(wgt, __ldg(er + (uu >> 1)), s);
+          s = fma(wgt, er[(uu >> 1) - c.cjb], s);
         }
       }
       u0 += s;
     }
-    if (MSK && rv && !c.mk[(int64_t)t * g.cols + c.col[q]]) u0 = 0.0;
-    nv[0][q] = (FAST || rv) ? u0 : 0.0;
+    if (MSK && rv && !c.mk[(int64_t)t * g.cols + c.col]) u0 = 0.0;
+    nv[0] = (FAST || rv) ? u0 : 0.0;
   }
   // ---- stages k = 1..S at row t - 2k (rows are CTA-uniform)
 #pragma unroll
   for (int k = 1; k <= S; ++k) {
     const int row = t - 2 * k;
+    constexpr int dummy = 0;
+    (void)dummy;
     const int s0 = m3(PH - 2 * k - 1), s1 = m3(PH - 2 * k), s2 = m3(PH - 2 * k + 1);
-    const bool rowv = FAST || (unsigned)row < (unsigned)g.rows;
+    double val = 0.0;
+    if (FAST || (unsigned)row < (unsigned)g.rows) {
+      const Op& op = (k & 1) ? a.A : a.K;
+      double sdot;
+      if (!CL) {
+        const double* base = op.planes + (int64_t)c.b * 9 * op.n + ((int64_t)row * g.cols + (c.cin ? c.col : 0));
+        double wt[9];
 #pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-      double val = 0.0;
-      if (rowv) {
-        const Op& op = (k & 1) ? a.A : a.K;
-        const double init = (k & 1) ? c.ring_f[(row & (PDF - 1)) * SWC + tc + q] : hold[k / 2 - 1][q];
-        if (!CL) {
-          const double* base = op.planes + (int64_t)c.b * 9 * op.n +
-                               ((int64_t)row * g.cols + (c.cin[q] ? c.col[q] : 0));
-          double wt[9];
-#pragma unroll
-          for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
-          val = (k & 1) ? dot9<true>(wt, w[k - 1], s0, s1, s2, q, init) : dot9<false>(wt, w[k - 1], s0, s1, s2, q, init);
-        } else {
-          const double* wt = FAST ? (CM == 2 ? ((k & 1) ? a.ci : a.ci + 9) : (((k & 1) ? c.tA : c.tK) + CINT * 9))
-                                  : (((k & 1) ? c.tA : c.tK) + (bandc(row, g.rows) * 5 + c.ccls[q]) * 9);
-          val = (k & 1) ? dot9<true>(wt, w[k - 1], s0, s1, s2, q, init) : dot9<false>(wt, w[k - 1], s0, s1, s2, q, init);
-        }
-        if (MSK && c.cin[q] && !c.mk[(int64_t)row * g.cols + c.col[q]]) val = 0.0;
-        if (!FAST) val = c.cin[q] ? val : 0.0;
-        if (NORM && k == 1 && c.owned_c[q] && row >= c.R0 && row < c.R1) acc = fma(val, val, acc);
-        if (k == 2 * NSW && c.owned_c[q] && row >= c.R0 && row < c.R1)
-          c.uob[(int64_t)row * g.cols + c.col[q]] = val;
+        for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
+        sdot = dot9(wt, w[k - 1], s0, s1, s2);
+      } else if (FAST) {
+        const double* reg = CM == 2 ? ((k & 1) ? a.ci : a.ci + 9) : (((k & 1) ? c.tA : c.tK) + CINT * 9);
+        sdot = dot9(reg, w[k - 1], s0, s1, s2);
+      } else {
+        const double* tab = (k & 1) ? c.tA : c.tK;
+        sdot = dot9(tab + (bandc(row, g.rows) * 5 + c.ccls) * 9, w[k - 1], s0, s1, s2);
       }
-      nv[k][q] = val;
+      if (k & 1) val = c.ring_f[(row & (PDF - 1)) * SWT + c.tid] - sdot;
+      else val = hold[k / 2 - 1] + sdot;
+      if (MSK && c.cin && !c.mk[(int64_t)row * g.cols + c.col]) val = 0.0;
+      if (!FAST) val = c.cin ? val : 0.0;
+      if (NORM && k == 1 && c.owned_c && row >= c.R0 && row < c.R1) acc = fma(val, val, acc);
+      if (k == 2 * NSW && c.owned_c && row >= c.R0 && row < c.R1) c.uob[(int64_t)row * g.cols + c.col] = val;
     }
+    nv[k] = val;
   }
-  // ---- publish (one 16-byte store per field), then slide the windows
+  // ---- publish, then slide the windows (slot of the evicted row)
   const int sl = t & 1;
 #pragma unroll
-  for (int k = 0; k < NF; ++k)
-    *reinterpret_cast<double2*>(&c.xch[(k * 2 + sl) * SWC + tc]) = make_double2(nv[k][0], nv[k][1]);
-  if (RES) *reinterpret_cast<double2*>(&c.rlast[((t - 2 * S) & 3) * SWC + tc]) = make_double2(nv[S][0], nv[S][1]);
+  for (int k = 0; k < NF; ++k) c.xch[(k * 2 + sl) * SWT + c.tid] = nv[k];
+  if (RES) c.rlast[((t - 2 * S) & 3) * SWT + c.tid] = nv[S];
   __syncthreads();
   if (RES) {
     const int top = t - 2 * S;
@@ -190,9 +185,9 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
       const int cj = (c.j0 >> 1) + c.tid;
       if (c.tid < WOUT / 2 && ci >= (c.R0 >> 1) && 2 * ci + 1 < c.R1 && ci < rows_c && cj < cols_c) {
         const int base = H + 2 * c.tid;
-        const double* r0p = &c.rlast[((top - 2) & 3) * SWC + base];
-        const double* r1p = &c.rlast[((top - 1) & 3) * SWC + base];
-        const double* r2p = &c.rlast[(top & 3) * SWC + base];
+        const double* r0p = &c.rlast[((top - 2) & 3) * SWT + base];
+        const double* r1p = &c.rlast[((top - 1) & 3) * SWT + base];
+        const double* r2p = &c.rlast[(top & 3) * SWT + base];
         double s = 0.0625 * r0p[0];
         s = fma(0.125, r0p[1], s);
         s = fma(0.0625, r0p[2], s);
@@ -211,14 +206,10 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
 #pragma unroll
   for (int k = 0; k < NF; ++k) {
     const int sn = m3(PH - 2 * k);  // slot of the new row t - 2k (evicts row t - 2k - 3)
-    if (!(k & 1) && k / 2 < NSW) {
-      hold[k / 2][0] = w[k][sn][1];
-      hold[k / 2][1] = w[k][sn][2];
-    }
-    w[k][sn][0] = c.xch[(k * 2 + sl) * SWC + c.lL];
-    w[k][sn][1] = nv[k][0];
-    w[k][sn][2] = nv[k][1];
-    w[k][sn][3] = c.xch[(k * 2 + sl) * SWC + c.lR];
+    if (!(k & 1) && k / 2 < NSW) hold[k / 2] = w[k][sn][1];
+    w[k][sn][0] = c.xch[(k * 2 + sl) * SWT + c.colL];
+    w[k][sn][1] = nv[k];
+    w[k][sn][2] = c.xch[(k * 2 + sl) * SWT + c.colR];
   }
 }
 
@@ -233,11 +224,12 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   Ctx c;
   c.g = a.g;
   const Grid& g = c.g;
-  c.ring_u = smem;                               // PD x SWC (unused when ZU)
-  c.ring_f = c.ring_u + PD * SWC;                // PDF x SWC
-  c.xch = c.ring_f + PDF * SWC;                  // NF x 2 x SWC neighbour exchange rows
-  c.rlast = c.xch + NF * 2 * SWC;                // 4 x SWC last-residual ring (RES)
-  double* tA = c.rlast + 4 * SWC;                // 25 x 9
+  c.ring_u = smem;                               // PD x SWT (unused when ZU)
+  c.ring_f = c.ring_u + PD * SWT;                // PDF x SWT
+  c.ring_e = c.ring_f + PDF * SWT;               // PE x EW (POST only; allocated always)
+  c.xch = c.ring_e + PE * EW;                    // NF x 2 x SWT neighbour exchange rows
+  c.rlast = c.xch + NF * 2 * SWT;                // 4 x SWT last-residual ring (RES)
+  double* tA = c.rlast + 4 * SWT;                // 25 x 9
   double* tK = tA + NCLS * 9;                    // 25 x 9
   double* red = tK + NCLS * 9;                   // 32
   c.tA = tA;
@@ -246,24 +238,21 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   c.b = blockIdx.z;
   const int64_t n = g.n();
   c.j0 = blockIdx.x * WOUT;                      // first owned column (even)
-#pragma unroll
-  for (int q = 0; q < CPT; ++q) {
-    const int lc = CPT * c.tid + q;
-    c.col[q] = c.j0 - H + lc;
-    c.cin[q] = c.col[q] >= 0 && c.col[q] < g.cols;
-    c.owned_c[q] = lc >= H && lc < H + WOUT && c.cin[q];
-    c.ccls[q] = c.cin[q] ? bandc(c.col[q], g.cols) : 2;  // out-of-grid columns are zeroed anyway
-  }
-  c.lL = max(CPT * c.tid - 1, 0);
-  c.lR = min(CPT * c.tid + CPT, SWC - 1);
+  c.col = c.j0 - H + c.tid;
+  c.cin = c.col >= 0 && c.col < g.cols;
+  c.owned_c = c.tid >= H && c.tid < H + WOUT && c.cin;
+  c.ccls = c.cin ? bandc(c.col, g.cols) : 2;     // out-of-grid columns are zeroed anyway
+  c.cjb = ((c.j0 - H) >> 1) - 1;
   c.R0 = blockIdx.y * a.seg;
   c.R1 = min(g.rows, c.R0 + a.seg);
   c.fb = a.f + c.b * n;
   c.ub = ZU ? nullptr : a.u + c.b * n;
   c.uob = a.uo + c.b * n;
+  c.colL = max(c.tid - 1, 0);
+  c.colR = min(c.tid + 1, SWT - 1);
   c.mk = MSK ? a.mask : nullptr;
   // fast steps need every CTA column interior (band class 2) and in the grid
-  const bool cta_fast = c.j0 - H >= 2 && c.j0 - H + SWC - 1 <= g.cols - 3;
+  const bool cta_fast = c.j0 - H >= 2 && c.j0 - H + SWT - 1 <= g.cols - 3;
 
   if (CM != 0) {
     for (int q = c.tid; q < NCLS * 9; q += SWT) {
@@ -273,16 +262,16 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   }
   __syncthreads();
 
-  double w[NF][3][4];
+  double w[NF][3][3];
 #pragma unroll
   for (int k = 0; k < NF; ++k)
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[k][r][q] = 0.0;
-  double hold[NSW][CPT];
+      for (int q = 0; q < 3; ++q) w[k][r][q] = 0.0;
+  double hold[NSW];
 #pragma unroll
-  for (int m = 0; m < NSW; ++m) hold[m][0] = hold[m][1] = 0.0;
+  for (int m = 0; m < NSW; ++m) hold[m] = 0.0;
   double acc = 0.0;
 
   // steps t in [t0, t1], t0 aligned to a multiple of 3 (extra leading steps only
@@ -292,22 +281,40 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   const int t1 = c.R1 + 2 * S;
   int prow = t0;
   const int64_t cstride = g.cols;
-  const int tc = CPT * c.tid;
-  const double* pu = ZU ? nullptr : c.ub + (int64_t)prow * cstride + c.col[0];
-  const double* pf = c.fb + (int64_t)prow * cstride + c.col[0];
+  const double* pu = ZU ? nullptr : c.ub + (int64_t)prow * cstride + c.col;
+  const double* pf = c.fb + (int64_t)prow * cstride + c.col;
+  const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+  const double* ecb = PRO ? a.ec + c.b * (int64_t)rows_c * cols_c : nullptr;
   auto issue = [&]() {
-    const bool rok = (unsigned)prow < (unsigned)g.rows;
-#pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-      const bool rv = rok && c.cin[q];
-      if (!ZU) cp_async8(&c.ring_u[(prow & (PD - 1)) * SWC + tc + q], rv ? pu + q : c.ub, rv);
-      cp_async8(&c.ring_f[(prow & (PDF - 1)) * SWC + tc + q], rv ? pf + q : c.fb, rv);
+    const bool rv = (unsigned)prow < (unsigned)g.rows && c.cin;
+    if (!ZU) cp_async8(&c.ring_u[(prow & (PD - 1)) * SWT + c.tid], rv ? pu : c.ub, rv);
+    cp_async8(&c.ring_f[(prow & (PDF - 1)) * SWT + c.tid], rv ? pf : c.fb, rv);
+    if (PRO && !(prow & 1) && c.tid < EW) {
+      // coarse row ci is first needed by fine row 2ci (as di = -1); stage it with the
+      // group of fine row 2ci - 2 so every thread's copy is complete and published by
+      // the barrier of step 2ci - 2.  Out-of-range coarse points read as zero.
+      const int ci = (prow >> 1) + 1, cj = c.cjb + c.tid;
+      const bool ev = ci >= 0 && ci < rows_c && cj >= 0 && cj < cols_c;
+      cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + c.tid], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
     }
     cp_commit();
     ++prow;
     if (!ZU) pu += cstride;
     pf += cstride;
   };
+  if (PRO) {
+    // coarse rows needed before the first regular issue can stage them
+    for (int ci = (t0 >> 1) - 1; ci <= (t0 >> 1) + 1; ++ci) {
+      const int cj = c.cjb + c.tid;
+      if (c.tid < EW) {
+        const bool ev = ci >= 0 && ci < rows_c && cj >= 0 && cj < cols_c;
+        cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + c.tid], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
+      }
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+  }
   for (int q = 0; q < DIST; ++q) issue();
 
 #define MGB_STEP(PH_)                                                                                  \
@@ -344,65 +351,87 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
 
 }  // namespace
 
-int stream_seg(const Grid& g) {
-  // rows per CTA segment (even): long segments amortise the pipeline fill,
-  // enough segments keep ~2 CTAs per SM busy
-  const int strips = (g.cols + (SWC - 12) - 1) / (SWC - 12);
-  int seg = 256;
-  while (seg > 32 && (int64_t)strips * ((g.rows + seg - 1) / seg) * g.batch < 2 * 148) seg /= 2;
-  return seg;
-}
-
-dim3 stream_grid(const Grid& g, int nsw, bool res) {
-  const int H = 2 * nsw + 2;
-  const int wout = SWC - 2 * H;
-  const int seg = stream_seg(g);
-  return dim3((g.cols + wout - 1) / wout, (g.rows + seg - 1) / seg, g.batch);
-}
-
-int stream_blocks(const Grid& g, int nsw, bool res) {
-  const dim3 d = stream_grid(g, nsw, res);
-  return (int)(d.x * d.y);
-}
-
 static size_t stream_smem(int nsw, bool res) {
   const int nf = 2 * nsw + (res ? 1 : 0);
-  return sizeof(double) * ((size_t)(PD + PDF + 2 * nf + 4) * SWC + 2 * NCLS * 9 + 32);
+  return sizeof(double) * ((size_t)(PD + PDF + 2 * nf + 4) * SWT + PE * EW + 2 * NCLS * 9 + 32);
+}
+
+// Rows per CTA segment: minimise waves x (segment + pipeline fill) for the
+// kernel's measured occupancy (the whole grid runs ~one row step per CTA at a time).
+static int choose_seg(const Grid& g, int nsw, bool res, int occ) {
+  const int H = 2 * nsw + 2, wout = SWT - 2 * H, S = 2 * nsw + (res ? 1 : 0);
+  const int64_t strips = (g.cols + wout - 1) / wout;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t slots = (int64_t)sms * std::max(occ, 1);
+  int best = 256;
+  double best_t = 1e300;
+  for (int seg = 512; seg >= 16; seg /= 2) {
+    const int64_t ctas = strips * ((g.rows + seg - 1) / seg) * g.batch;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    // a partial last wave still costs a full CTA time; fill = 3S + 3 steps
+    const double t = (double)waves * (seg + 3 * S + 3) + 1e-3 * seg;
+    if (t < best_t) { best_t = t; best = seg; }
+  }
+  return best;
 }
 
 template <typename KF>
-static cudaError_t run_k(KF kern, dim3 grid, size_t smem, cudaStream_t s, const StreamArgs& a) {
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, SWT, smem, s>>>(a);
+static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks) {
+  static thread_local std::vector<std::pair<const void*, int>> occ_cache;
+  const size_t smem = stream_smem(nsw, res);
+  int occ = -1;
+  for (auto& e : occ_cache)
+    if (e.first == (const void*)kern) occ = e.second;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SWT, smem);
+    if (e != cudaSuccess) return e;
+    occ_cache.push_back({(const void*)kern, occ});
+  }
+  a.seg = choose_seg(a.g, nsw, res, occ);
+  const int H = 2 * nsw + 2, wout = SWT - 2 * H;
+  const dim3 grid((a.g.cols + wout - 1) / wout, (a.g.rows + a.seg - 1) / a.seg, a.g.batch);
+  if (nblocks) *nblocks = (int)(grid.x * grid.y);
+  kern<<<grid, SWT, smem, a.stream>>>(a);
   return MGB_DBG(__func__);
 }
 
-cudaError_t launch_stream(const StreamArgs& a0, int nsw, bool res, bool pro, bool norm) {
-  StreamArgs a = a0;
-  a.seg = stream_seg(a.g);
-  const dim3 grid = stream_grid(a.g, nsw, res);
+cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks) {
   const bool zu = a.u == nullptr;
   const bool msk = a.mask != nullptr;
   const int cm = (a.A.cls != nullptr && a.K.cls != nullptr && !msk) ? (a.ci_valid ? 2 : 1) : 0;
-  cudaStream_t s = a.stream;
-  const size_t sm = stream_smem(nsw, res);
   ++g_launches;
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
-    if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, true>, grid, sm, s, a);           \
-    if (cm == 2) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 2, false>, grid, sm, s, a);      \
-    if (cm == 1) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 1, false>, grid, sm, s, a);      \
-    return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, false>, grid, sm, s, a);                   \
+    if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, true>, nsw, res, a, nblocks);     \
+    if (cm == 2) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 2, false>, nsw, res, a, nblocks); \
+    if (cm == 1) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 1, false>, nsw, res, a, nblocks); \
+    return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, false>, nsw, res, a, nblocks);             \
   }
-  // PRE: restriction, optional norm, optional zero start; POST: prolongation, no norm
+  // PRE (restriction, optional history norm, optional zero start), plain sweeps,
+  // POST (prolongation)
   MGB_ST(1, true, false, false, false) MGB_ST(1, true, false, true, false)
   MGB_ST(1, true, false, false, true)  MGB_ST(1, true, false, true, true)
   MGB_ST(2, true, false, false, false) MGB_ST(2, true, false, true, false)
   MGB_ST(2, true, false, false, true)  MGB_ST(2, true, false, true, true)
+  MGB_ST(1, false, false, false, false) MGB_ST(1, false, false, true, false)
+  MGB_ST(1, false, false, false, true)  MGB_ST(1, false, false, true, true)
   MGB_ST(1, false, true, false, false) MGB_ST(2, false, true, false, false)
 #undef MGB_ST
   return cudaErrorInvalidValue;
+}
+
+int stream_max_blocks(const Grid& g) {
+  // upper bound on the CTAs of any streaming pass over g (seg >= 16, nsw >= 1)
+  const int wout = SWT - 2 * 4 - 4;
+  return (int)(((g.cols + wout - 1) / wout) * ((g.rows + 15) / 16));
 }
 
 }  // namespace mgb

@@ -23,8 +23,10 @@ struct StreamArgs {
 };
 
 // PRE: res = true, pro = false (norm optional, u null = zero start);
-// POST: res = false, pro = true.  nsw in {1, 2}.
-cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm);
-int stream_blocks(const Grid& g, int nsw, bool res);
+// plain sweeps: res = pro = false, nsw = 1 (norm optional);
+// POST: res = false, pro = true.  nsw in {1, 2}.  *nblocks receives the CTA count
+// (the number of history partials written when norm is set).
+cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
+int stream_max_blocks(const Grid& g);
 
 }  // namespace mgb

@@ -192,9 +192,10 @@ class MultigridHierarchy:
         'planes': per-point planes everywhere.  Results are bit-identical."""
         _lib.call("mgb_hier_set_storage", self._h, {"auto": 0, "planes": 1}[mode], None)
 
-    def set_fused(self, enable: bool = True):
-        """Fused row-streaming PRE/POST passes (default) or separate passes."""
-        _lib.call("mgb_hier_set_fused", self._h, 1 if enable else 0)
+    def set_fused(self, mode=2):
+        """Pass structure: 2 (default) one streaming pass per smoothing phase, 1 one
+        streaming pass per sweep, 0 / False separate sweep, restriction, prolongation."""
+        _lib.call("mgb_hier_set_fused", self._h, int(mode))
 
     def storage_info(self, l: int):
         """(A class-compact, M class-compact) for level l."""

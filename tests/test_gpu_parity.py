@@ -369,7 +369,9 @@ def test_fused_and_separate_passes_agree(name):
     f = dv.to_dev(np.where(c["mask"], c["f"], 0.0))
     u1, u2 = dv.zeros(f.shape), dv.zeros(f.shape)
     h1 = dv.host(h.run_cycles(f, u1, c["cycles"], c["nu"], c["nu"], u_zero=True))[0]
-    h.set_fused(False)
-    h2 = dv.host(h.run_cycles(f, u2, c["cycles"], c["nu"], c["nu"], u_zero=True))[0]
-    assert_hist(h1, h2)
-    assert rel_err(dv.host(u1), dv.host(u2)) <= 1e-12
+    for mode in (1, 0):
+        h.set_fused(mode)
+        u2 = dv.zeros(f.shape)
+        h2 = dv.host(h.run_cycles(f, u2, c["cycles"], c["nu"], c["nu"], u_zero=True))[0]
+        assert_hist(h1, h2)
+        assert rel_err(dv.host(u1), dv.host(u2)) <= 1e-12
