@@ -13,7 +13,7 @@ import os
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmgb.so")
+LIB_PATH = os.environ.get("MGB_LIB_PATH") or os.path.join(HERE, "libmgb.so")  # override: experiments only
 
 MGB_OK, MGB_CONFIG, MGB_NUMERIC, MGB_NONCONVERGED, MGB_CONTRACT, MGB_SINGULAR, MGB_CUDA, MGB_NCCL = range(8)
 NET_CONV, NET_FC = 0, 1

@@ -92,6 +92,8 @@ struct mgb_hier {
   double slope = 0.01;
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
+  int64_t stream_min = 1500000;  // streaming passes on levels with at least this many points
+                                   // (smaller levels are latency-bound: separate tile kernels win)
   int fused = 2;            // 2: one streaming pass per smoothing phase; 1: single-sweep streaming
                             // passes; 0: separate sweep / restriction / prolongation kernels
   ~mgb_hier() {
@@ -522,6 +524,7 @@ extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double 
   }
   if (const char* e = getenv("MGB_STORAGE")) h->compact = std::string(e) != "planes";
   if (const char* e = getenv("MGB_FUSED")) h->fused = atoi(e);
+  if (const char* e = getenv("MGB_STREAM_MIN")) h->stream_min = atoll(e);
   if (int st = classify_all(h.get(), s)) return st;
   *out = h.release();
   return MGB_OK;
@@ -866,7 +869,8 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   double* oth = w->t[l];
   const Grid g = h->grid(l);
   const bool fuse_norm = hist && nu1 > 0 && lv.ks == 1;
-  if (h->fused && lv.ks == 1 && (nu1 == 1 || nu1 == 2) && (nu2 == 1 || nu2 == 2)) {
+  if (h->fused && lv.ks == 1 && (nu1 == 1 || nu1 == 2) && (nu2 == 1 || nu2 == 2) &&
+      (int64_t)lv.n * h->batch >= h->stream_min) {
     // PRE: [history norm] + nu1 sweeps + residual + restriction in streaming passes
     // (fused = 2: one pass per phase; fused = 1: single-sweep passes)
     StreamArgs a{};

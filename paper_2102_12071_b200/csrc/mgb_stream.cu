@@ -38,7 +38,10 @@ constexpr int SWT = 128;   // threads (= columns incl. halo) per CTA
 constexpr int PD = 8;      // prefetch ring depth (rows) for u (power of two)
 constexpr int PDF = 16;    // ring depth for f (also read by the later residual stages): rows t-10 .. t+DIST
 constexpr int DIST = 5;    // prefetch distance (rows ahead)
-constexpr int MINB = 4;    // CTAs per SM the register budget is sized for
+#ifndef MGB_MINB
+#define MGB_MINB 3
+#endif
+constexpr int MINB = MGB_MINB;  // CTAs per SM the register budget is sized for
 constexpr int PE = 8;      // ring of coarse rows (POST prolongation), power of two
 constexpr int EW = SWT / 2 + 4;  // coarse columns staged per CTA
 constexpr int NCLS = 25;

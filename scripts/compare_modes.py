@@ -7,7 +7,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 h, f_host, info = bench.build_problem(cfg, 0)
 f = torch.from_numpy(f_host).cuda()
 u = torch.zeros_like(f)
-for mode in (2, 1, 0):
+for mode in [int(m) for m in os.environ.get("MODES", "2,1,0").split(",")]:
     h.set_fused(mode)
     for _ in range(3):
         hist = h.run_cycles(f, u, info["cycles"], info["nu"], info["nu"], u_zero=True)
