@@ -201,6 +201,14 @@ int mgb_solve(const mgb_hier* h, mgb_work* w, const double* f_dev, double* u_dev
               int* n_history, int* iterations, int* converged, double* loop_seconds,
               void* stream);
 
+/* Average device time (ms, CUDA events on `stream`) of one smoothing phase of the
+   cycle on `level` over `reps` back-to-back repetitions: pass 0 = PRE (nu sweeps +
+   residual + restriction), pass 1 = POST (prolongation + nu sweeps), in whatever
+   pass structure the hierarchy uses (mgb_hier_set_fused).  f_dev / u_dev are
+   level-sized device arrays; u_dev is overwritten. */
+int mgb_time_pass(const mgb_hier* h, mgb_work* w, int level, int pass, int nu, const double* f_dev,
+                  double* u_dev, int reps, double* ms, void* stream);
+
 /* instrumentation for bench.py: number of kernel launches issued by the last
    mgb_run_cycles / mgb_vcycle call (graph replays count their nodes). */
 int64_t mgb_last_launch_count(const mgb_work* w);

@@ -64,6 +64,7 @@ SIGNATURES = {
     "mgb_run_cycles": (I, [P, P, P, P, I, I, I, I, P, P]),
     "mgb_run_cycles_host": (I, [P, P, P, P, I, I, I, I, P, P]),
     "mgb_solve": (I, [P, P, P, P, I, I, D, I, PD, PI, PI, PI, PD, P]),
+    "mgb_time_pass": (I, [P, P, I, I, I, P, P, I, PD, P]),
     "mgb_last_launch_count": (I64, [P]),
 }
 

@@ -850,6 +850,84 @@ static int enqueue_fnorm(mgb_work* w, const double* f, cudaStream_t s) {
   return MGB_OK;
 }
 
+// ---- row-streaming passes (mgb_stream.cu) -----------------------------------
+
+static bool use_stream(const mgb_hier* h, int l, int nu1, int nu2) {
+  const LevelD& lv = h->lv[l];
+  return h->fused && lv.ks == 1 && (nu1 == 1 || nu1 == 2) && (nu2 == 1 || nu2 == 2) &&
+         (int64_t)lv.n * h->batch >= h->stream_min;
+}
+
+static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  const LevelD& lv = h->lv[l];
+  StreamArgs a{};
+  a.g = h->grid(l);
+  a.A = lv.opA();
+  a.K = lv.opK();
+  a.mask = lv.mask;
+  a.mask_c = h->lv[l + 1].mask;
+  a.f = f;
+  a.stream = s;
+  a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
+  for (int o = 0; o < 9; ++o) {
+    a.ci[o] = lv.hAint[o];
+    a.ci[9 + o] = lv.hKint[o];
+  }
+  return a;
+}
+
+// PRE on level l: [history norm of the input] + nu1 sweeps + residual + restriction
+// into w->f[l+1].  in == null: zero initial guess.  *cur / *oth: ping-pong buffers
+// (the result ends in *cur).  hist != null: relative residual of the input.
+static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, double** cur, double** oth, int nu1,
+                       double* hist, int64_t hstride, cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  StreamArgs a = stream_args(w, l, f, s);
+  const bool split = h->fused == 1;
+  int nb = 0;
+  if (split && nu1 == 2) {
+    a.u = in;
+    a.uo = *oth;
+    a.partials = hist ? w->partials : nullptr;
+    MGB_CUDA_TRY(launch_stream(a, 1, false, false, hist != nullptr, &nb));
+    if (hist) MGB_CUDA_TRY(launch_finalize(h->batch, nb, w->partials, nullptr, w->fnorm2, hist, hstride, s));
+    std::swap(*cur, *oth);
+    in = *cur;
+    hist = nullptr;
+  }
+  a.u = in;
+  a.uo = *oth;
+  a.rc = w->f[l + 1];
+  a.partials = hist ? w->partials : nullptr;
+  MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu1, true, false, hist != nullptr, &nb));
+  if (hist) MGB_CUDA_TRY(launch_finalize(h->batch, nb, w->partials, nullptr, w->fnorm2, hist, hstride, s));
+  std::swap(*cur, *oth);
+  return MGB_OK;
+}
+
+// POST on level l: u <- u + P ec, then nu2 sweeps (result ends in *cur)
+static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, double** cur, double** oth, int nu2,
+                        cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  StreamArgs a = stream_args(w, l, f, s);
+  const bool split = h->fused == 1;
+  int nb = 0;
+  a.u = *cur;
+  a.uo = *oth;
+  a.ec = ec;
+  MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu2, false, true, false, &nb));
+  std::swap(*cur, *oth);
+  if (split && nu2 == 2) {
+    a.u = *cur;
+    a.uo = *oth;
+    a.ec = nullptr;
+    MGB_CUDA_TRY(launch_stream(a, 1, false, false, false, &nb));
+    std::swap(*cur, *oth);
+  }
+  return MGB_OK;
+}
+
 // V(nu1, nu2) from level l; zero means a zero initial guess (u not read).  Returns
 // the buffer holding the result (u_l or the level's ping-pong partner).  With
 // hist != null (level 0 only) the relative residual of the INPUT u is written to
@@ -869,64 +947,12 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   double* oth = w->t[l];
   const Grid g = h->grid(l);
   const bool fuse_norm = hist && nu1 > 0 && lv.ks == 1;
-  if (h->fused && lv.ks == 1 && (nu1 == 1 || nu1 == 2) && (nu2 == 1 || nu2 == 2) &&
-      (int64_t)lv.n * h->batch >= h->stream_min) {
-    // PRE: [history norm] + nu1 sweeps + residual + restriction in streaming passes
-    // (fused = 2: one pass per phase; fused = 1: single-sweep passes)
-    StreamArgs a{};
-    a.g = g;
-    a.A = lv.opA();
-    a.K = lv.opK();
-    a.mask = lv.mask;
-    a.mask_c = h->lv[l + 1].mask;
-    a.f = f;
-    a.stream = s;
-    a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
-    for (int o = 0; o < 9; ++o) {
-      a.ci[o] = lv.hAint[o];
-      a.ci[9 + o] = lv.hKint[o];
-    }
-    const bool split = h->fused == 1;
-    int nb = 0;
-    const double* in = zero ? nullptr : cur;
-    if (split && nu1 == 2) {
-      a.u = in;
-      a.uo = oth;
-      a.partials = fuse_norm ? w->partials : nullptr;
-      MGB_CUDA_TRY(launch_stream(a, 1, false, false, fuse_norm, &nb));
-      if (fuse_norm) {
-        if (int st = enqueue_finalize(w, nb, hist, hstride, s)) return st;
-      }
-      std::swap(cur, oth);
-      in = cur;
-    }
-    const bool norm2 = fuse_norm && !(split && nu1 == 2);
-    a.u = in;
-    a.uo = oth;
-    a.rc = w->f[l + 1];
-    a.partials = norm2 ? w->partials : nullptr;
-    MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu1, true, false, norm2, &nb));
-    if (norm2) {
-      if (int st = enqueue_finalize(w, nb, hist, hstride, s)) return st;
-    }
-    std::swap(cur, oth);
+  if (use_stream(h, l, nu1, nu2)) {
+    if (int st = enqueue_pre(w, l, f, zero ? nullptr : cur, &cur, &oth, nu1, fuse_norm ? hist : nullptr, hstride, s))
+      return st;
     double* ec = nullptr;
     if (int st = vcycle_rec(w, l + 1, w->f[l + 1], w->u[l + 1], true, nu1, nu2, s, &ec)) return st;
-    // POST: coarse-grid correction + nu2 sweeps
-    a.u = cur;
-    a.uo = oth;
-    a.ec = ec;
-    a.rc = nullptr;
-    a.partials = nullptr;
-    MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu2, false, true, false, &nb));
-    std::swap(cur, oth);
-    if (split && nu2 == 2) {
-      a.u = cur;
-      a.uo = oth;
-      a.ec = nullptr;
-      MGB_CUDA_TRY(launch_stream(a, 1, false, false, false, &nb));
-      std::swap(cur, oth);
-    }
+    if (int st = enqueue_post(w, l, f, ec, &cur, &oth, nu2, s)) return st;
     *result = cur;
     return MGB_OK;
   }
@@ -1190,4 +1216,62 @@ extern "C" int mgb_solve(const mgb_hier* h, mgb_work* w, const double* f_dev, do
   if (converged) *converged = history_host[nh - 1] < tol ? 1 : 0;
   if (loop_seconds) *loop_seconds = std::chrono::duration<double>(t1 - t0).count();
   return MGB_OK;
+}
+
+// Average device time of one PRE (pass 0) or POST (pass 1) phase on `level`,
+// measured with CUDA events on `stream` around `reps` back-to-back launches
+// (bench.py's roofline of the dominant kernel).  f_dev / u_dev: level arrays.
+extern "C" int mgb_time_pass(const mgb_hier* h, mgb_work* w, int level, int pass, int nu, const double* f_dev,
+                             double* u_dev, int reps, double* ms, void* stream) {
+  if (!h || !w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
+  if (level < 0 || level + 1 >= h->depth()) return fail(MGB_CONFIG, "level has no smoothing phase");
+  if (pass != 0 && pass != 1) return fail(MGB_CONFIG, "pass must be 0 (PRE) or 1 (POST)");
+  if (reps < 1) return fail(MGB_CONFIG, "reps must be positive");
+  if (int st = check_equipped(h)) return st;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  if (int st = prepare_work(w)) return st;
+  cudaEvent_t e0, e1;
+  MGB_CUDA_TRY(cudaEventCreate(&e0));
+  MGB_CUDA_TRY(cudaEventCreate(&e1));
+  const bool stream_pass = use_stream(h, level, nu, nu);
+  double* bufs[2] = {u_dev, w->t[level]};
+  int st = MGB_OK;
+  auto one = [&](int r) -> int {
+    double* cur = bufs[r & 1];
+    double* oth = bufs[(r + 1) & 1];
+    if (stream_pass) {
+      if (pass == 0) return enqueue_pre(w, level, f_dev, cur, &cur, &oth, nu, nullptr, 0, s);
+      return enqueue_post(w, level, f_dev, w->u[level + 1], &cur, &oth, nu, s);
+    }
+    // separate passes: the same work as the fused phase
+    const LevelD& lv = h->lv[level];
+    const Grid g = h->grid(level);
+    if (pass == 0) {
+      for (int q = 0; q < nu; ++q) {
+        if (int e = sweep(w, level, f_dev, cur, oth, s)) return e;
+        std::swap(cur, oth);
+      }
+      MGB_CUDA_TRY(launch_resid_restrict2(g, lv.opA(), lv.mask, h->lv[level + 1].mask, f_dev, cur, w->f[level + 1], s));
+    } else {
+      MGB_CUDA_TRY(launch_prolong(g, lv.mask, w->u[level + 1], cur, true, s));
+      for (int q = 0; q < nu; ++q) {
+        if (int e = sweep(w, level, f_dev, cur, oth, s)) return e;
+        std::swap(cur, oth);
+      }
+    }
+    return MGB_OK;
+  };
+  MGB_CUDA_TRY(cudaMemsetAsync(w->u[level + 1], 0, sizeof(double) * h->batch * h->lv[level + 1].n, s));
+  st = one(0);  // warm
+  if (!st) MGB_CUDA_TRY(cudaEventRecord(e0, s));
+  for (int r = 0; r < reps && !st; ++r) st = one(r);
+  if (!st) MGB_CUDA_TRY(cudaEventRecord(e1, s));
+  if (!st) MGB_CUDA_TRY(cudaEventSynchronize(e1));
+  float t = 0.f;
+  if (!st) MGB_CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ms) *ms = (double)t / reps;
+  return st;
 }
