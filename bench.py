@@ -70,12 +70,12 @@ def measured_peak():
 
 
 def ncu_traffic():
-    """DRAM bytes per launch of the sweep kernel from the committed ncu capture."""
+    """DRAM bytes per launch of the level-0 PRE pass from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         try:
             d = json.load(open(p))
-            return d.get("sweep_dram_bytes_per_launch"), d
+            return d.get("pre_dram_bytes_per_launch"), d
         except Exception:
             pass
     return None, None
