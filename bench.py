@@ -2,18 +2,24 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
 
-Workload (N = 1): BASELINE.json config 2 — rotated anisotropic Laplacian
+Default workload (N = 1): BASELINE.json config 2 — rotated anisotropic Laplacian
 (reference FD stencil, eps = 1e-3, theta = pi/4) on a 4095^2 interior grid,
 11 levels, Galerkin coarse operators, per-point smoother kernels from the
 seeded conv inference net (tests/golden/net_conv_c2.json: the reference's own
-SURVEY-G4 training recipe run at the config's theta/eps),
-b ~ U[-1, 1] (seed 1), u0 = 0.  One step = one 10-cycle V(2,2) solve including
-the per-cycle residual history (as hierarchy.solve times it).  Multi-GPU (torchrun):
-every rank solves its own copy of the problem (weak scaling, no data-path
-collective); the job value is the sum over ranks of unknowns / max-over-ranks time.
+SURVEY-G4 training recipe run at the config's theta/eps), b ~ U[-1, 1] (seed 1),
+u0 = 0.  One step = one 10-cycle V(2,2) solve including the per-cycle residual
+history (as hierarchy.solve times it).
+
+Other configs: c1 (255^2, V(2,2) x 20), c3 (8191^2 GRF 5-point variable
+coefficients, per-point tables, V(2,2) x 10), c4 (256 problems at 511^2 with
+random (eps, theta), V(1,1) x 10, batched hierarchy).
+
+Multi-GPU (torchrun): c1-c3 place one replica per rank (weak scaling, no
+data-path collective); c4 splits its 256 problems across ranks (strong scaling).
+The value is the job's unknowns / max-over-ranks device time.
 
 `--impl reference` times the CPU oracle port of the reference algorithm (NumPy,
-oracle/mg_oracle.py) on a bounded sample of the same workload (see cpu_sample()).
+oracle/mg_oracle.py) on a bounded sample of the same workload (cpu_sample()).
 """
 
 from __future__ import annotations
@@ -32,17 +38,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# name: dict(n, levels, nu, cycles, net, batch, kind, ...)
 CONFIGS = {
-    # name: (n, theta, eps, levels, nu, cycles, rhs seed)
-    "c2": (4095, math.pi / 4, 1e-3, 11, 2, 10, 1),
-    "c1": (255, math.pi / 6, 0.01, 7, 2, 20, 0),
+    "c1": dict(n=255, op="rot", theta=math.pi / 6, eps=0.01, levels=7, nu=2, cycles=20, seed=0, batch=1,
+               net="net_conv.json", desc="rotated FD eps=0.01 theta=pi/6"),
+    "c2": dict(n=4095, op="rot", theta=math.pi / 4, eps=1e-3, levels=11, nu=2, cycles=10, seed=1, batch=1,
+               net="net_conv_c2.json", desc="rotated FD Laplacian eps=0.001 theta=pi/4"),
+    "c3": dict(n=8191, op="grf", levels=12, nu=2, cycles=10, seed=2, batch=1, net="net_conv_c3.json",
+               desc="-div(exp(GRF) grad u), 5-point cell-centred, corr. length 1/32, per-point tables"),
+    "c4": dict(n=511, op="batch", levels=8, nu=1, cycles=10, seed=3, batch=256, net="net_conv.json",
+               desc="256 rotated FD problems, log-uniform eps in [1e-3,1], theta ~ U[0,pi)"),
 }
-# inference net per config: the SURVEY G4 training recipe run by the reference at the
-# config's own (theta, eps) (tests/golden/make_golden.py)
-NETS = {"c2": "net_conv_c2.json", "c1": "net_conv.json"}
-# algorithmic bytes of one pass, per-point fp64 model
-SWEEP_BYTES_PER_POINT = 168          # read u, f, A(9), M(9); write u
-CPU_SAMPLE_N = 1023                  # bounded CPU sample: same operator family at 1023^2
+CPU_SAMPLE_N = 1023                  # bounded CPU sample: same operator family at <= 1023^2
 
 
 def cycle_bytes_per_fine_unknown(n, levels, nu1, nu2):
@@ -69,10 +76,10 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
+def ncu_traffic(cfg_name):
     """DRAM bytes per launch of the level-0 PRE pass from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(p):
+    if os.path.exists(p) and cfg_name == "c2":
         try:
             d = json.load(open(p))
             return d.get("pre_dram_bytes_per_launch"), d
@@ -134,48 +141,69 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_init():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
-
-
-def build_problem(cfg_name, device):
-    import paper_2102_12071_b200 as mg
+def operators(cfg, lo=0, hi=None):
+    """Host inputs of a config: (A (batch, n, n, 3, 3), f (batch, n, n)) for problems [lo, hi)."""
     from paper_2102_12071_b200 import problems as gen
-    n, theta, eps, levels, nu, cycles, seed = CONFIGS[cfg_name]
-    A = gen.rotated_fd(n, theta, eps)
-    f = gen.uniform_rhs(n, seed)
-    net = mg.load_model(os.path.join(ROOT, "paper_2102_12071_b200", "data", NETS[cfg_name]))
+    n = cfg["n"]
+    if cfg["op"] == "rot":
+        return gen.rotated_fd(n, cfg["theta"], cfg["eps"])[None], gen.uniform_rhs(n, cfg["seed"])[None]
+    if cfg["op"] == "grf":
+        return gen.grf_diffusion_5pt(n, seed=cfg["seed"])[None], gen.uniform_rhs(n, cfg["seed"])[None]
+    hi = cfg["batch"] if hi is None else hi
+    eps, theta = gen.batch_parameters(cfg["batch"], seed=cfg["seed"])
+    A = np.empty((hi - lo, n, n, 3, 3))
+    f = np.empty((hi - lo, n, n))
+    for k, i in enumerate(range(lo, hi)):
+        A[k] = gen.rotated_fd(n, theta[i], eps[i])
+        f[k] = gen.uniform_rhs(n, [4, i])
+    return A, f
+
+
+def build_problem(cfg_name, device, lo=0, hi=None):
     import torch
+    import paper_2102_12071_b200 as mg
+    cfg = CONFIGS[cfg_name]
+    A, f = operators(cfg, lo, hi)
+    n = cfg["n"]
+    net = mg.load_model(os.path.join(ROOT, "paper_2102_12071_b200", "data", cfg["net"]))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    h = mg.build_hierarchy(mg.StencilField(mg.full_spec(n), A), levels, device=device)
+    if cfg["batch"] == 1:
+        spec = mg.GridSpec(n, n, 1.0 / n if cfg["op"] == "grf" else 1.0 / (n + 1), np.ones((n, n), bool))
+        h = mg.build_hierarchy(mg.StencilField(spec, A[0]), cfg["levels"], device=device)
+    else:
+        h = mg.build_hierarchy_batch(A, cfg["levels"], device=device)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     mg.equip_inferred(h, net)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     del A
-    return h, f, dict(n=n, theta=theta, eps=eps, levels=levels, nu=nu, cycles=cycles, seed=seed,
-                      setup_rap_lu_s=t1 - t0, setup_infer_s=t2 - t1)
+    info = dict(cfg, setup_rap_lu_s=t1 - t0, setup_infer_s=t2 - t1, local_batch=f.shape[0])
+    return h, f, info
 
 
 def cpu_sample(cfg_name, steps=1, warmup=0):
-    """Oracle port (NumPy, single thread) on a bounded sample: the config's operator
-    family at CPU_SAMPLE_N^2 (levels scaled to reach 3x3), V(nu, nu) cycles with
-    the history residual, timed like hierarchy.solve (setup excluded)."""
+    """Oracle port (NumPy, single thread) on a bounded sample of the config: its
+    operator family at min(n, CPU_SAMPLE_N)^2 (levels scaled to reach 3x3), one
+    problem, V(nu, nu) cycles with the history residual, timed like
+    hierarchy.solve (setup excluded)."""
     from oracle import mg_oracle as mo
     from paper_2102_12071_b200 import problems as gen
-    n0, theta, eps, levels0, nu, cycles, seed = CONFIGS[cfg_name]
-    n = min(n0, CPU_SAMPLE_N)
+    cfg = CONFIGS[cfg_name]
+    n = min(cfg["n"], CPU_SAMPLE_N)
     levels = gen.levels_for(n)
-    A = gen.rotated_fd(n, theta, eps)
-    f = gen.uniform_rhs(n, seed)
+    nu = cfg["nu"]
+    if cfg["op"] == "rot":
+        A, f = gen.rotated_fd(n, cfg["theta"], cfg["eps"]), gen.uniform_rhs(n, cfg["seed"])
+    elif cfg["op"] == "grf":
+        A, f = gen.grf_diffusion_5pt(n, seed=cfg["seed"]), gen.uniform_rhs(n, cfg["seed"])
+    else:
+        eps, theta = gen.batch_parameters(cfg["batch"], seed=cfg["seed"])
+        A, f = gen.rotated_fd(n, theta[0], eps[0]), gen.uniform_rhs(n, [4, 0])
     t0 = time.perf_counter()
     h = mo.build_hierarchy(A, levels)
-    mo.equip_inferred(h, mo.load_net_json(os.path.join(ROOT, "paper_2102_12071_b200", "data", NETS[cfg_name])))
+    mo.equip_inferred(h, mo.load_net_json(os.path.join(ROOT, "paper_2102_12071_b200", "data", cfg["net"])))
     setup = time.perf_counter() - t0
     u = np.zeros((n, n))
     fn = float(np.linalg.norm(f))
@@ -190,7 +218,7 @@ def cpu_sample(cfg_name, steps=1, warmup=0):
     per_cycle = float(np.mean(times))
     return {"value": n * n / per_cycle, "unit": "unknowns/s", "cores": 1, "kind": "port",
             "sample": f"oracle/mg_oracle.py (NumPy, 1 thread) V({nu},{nu}) cycle + history residual on the "
-                      f"config's operator at {n}^2 ({levels} levels), {len(times)} cycle(s) timed, "
+                      f"config's operator family at {n}^2 ({levels} levels), {len(times)} cycle(s) timed, "
                       f"setup {setup:.1f}s excluded; cpu {cpu_model()}",
             "per_cycle_s": per_cycle}
 
@@ -205,18 +233,26 @@ def cpu_model():
     return f"{os.cpu_count()} cpus"
 
 
+def workload_desc(cfg_name):
+    c = CONFIGS[cfg_name]
+    b = f"{c['batch']} x " if c["batch"] > 1 else ""
+    return (f"{cfg_name}: {c['desc']}, {b}{c['n']}^2, {c['levels']} levels, V({c['nu']},{c['nu']}) x "
+            f"{c['cycles']} cycles + history, learned conv smoother")
+
+
 def run_reference(args):
-    world, rank, local = dist_init()
+    from paper_2102_12071_b200 import dist as D
+    world, rank, local = D.env()
     if rank != 0:
         return 0
-    n, theta, eps, levels, nu, cycles, seed = CONFIGS[args.config]
+    cfg = CONFIGS[args.config]
     s = cpu_sample(args.config, steps=max(1, args.steps), warmup=min(args.warmup, 1))
     line = {"metric": "unknowns/sec per V-cycle (fp64)", "value": s["value"], "unit": "unknowns/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": s["per_cycle_s"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": s["per_cycle_s"] * 1e3, "higher_is_better": True,
+            "scaling": "strong" if cfg["batch"] > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators)", "impl": "reference",
-            "config": {"workload": f"{args.config}: rotated FD eps={eps} theta={theta:.4f} {n}^2 V({nu},{nu}) "
-                                   f"learned conv smoother", "sample_n": min(n, CPU_SAMPLE_N)},
+            "config": {"workload": workload_desc(args.config), "sample_n": min(cfg["n"], CPU_SAMPLE_N)},
             "cpu_baseline": {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": s["value"], "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -224,20 +260,23 @@ def run_reference(args):
 
 
 def run_ours(args):
+    import ctypes as C
     import torch
     import torch.distributed as dist
-    import paper_2102_12071_b200 as mg
-    from paper_2102_12071_b200 import _lib
-    world, rank, local = dist_init()
+    from paper_2102_12071_b200 import _lib, device as dv, dist as D
+    world, rank, local = D.env()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    h, f_host, info = build_problem(args.config, local)
-    n, levels, nu, cycles = info["n"], info["levels"], info["nu"], info["cycles"]
-    f = torch.from_numpy(f_host).to(dev)
+    D.init("nccl", device=dev)
+    cfg = CONFIGS[args.config]
+    batched = cfg["batch"] > 1
+    lo, hi = D.shard(cfg["batch"], rank, world) if batched else (0, 1)
+    h, f_host, info = build_problem(args.config, local, lo, hi)
+    n, levels, nu, cycles = cfg["n"], cfg["levels"], cfg["nu"], cfg["cycles"]
+    nb = info["local_batch"]
+    f = torch.from_numpy(np.ascontiguousarray(f_host if batched else f_host[0])).to(dev)
     u = torch.zeros_like(f)
-    hist = torch.empty((1, cycles + 1), dtype=torch.float64, device=dev)
+    hist = torch.empty((nb, cycles + 1), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -245,7 +284,8 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(max(3, args.warmup)):
+    warm = max(3, args.warmup)
+    for _ in range(warm):
         h.run_cycles(f, u, cycles, nu, nu, history=hist, u_zero=True)
     launches_per_step = h.last_launches
     barrier()
@@ -257,45 +297,40 @@ def run_ours(args):
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    final_hist = hist.cpu().numpy()[0]
-    value = world * n * n * cycles / (ms_max * 1e-3)
+    ms_max = D.max_over_ranks(ms, dev)
+    total_problems = cfg["batch"] if batched else world
+    value = total_problems * n * n * cycles / (ms_max * 1e-3)
+    hist_all = D.gather_rows(hist.cpu().numpy(), cfg["batch"], dev) if batched else hist.cpu().numpy()
 
-    # dominant kernels: the level-0 PRE / POST phases (row-streaming passes), timed
-    # live with CUDA events on the launching stream through mgb_time_pass
-    import ctypes as C
-    from paper_2102_12071_b200 import device as dv
+    # dominant kernels: level-0 PRE / POST phases, timed live (CUDA events on the
+    # launching stream) through mgb_time_pass
     compact = all(h.storage_info(0))
     w = h.acquire_work()
     try:
         ms_pre, ms_post = C.c_double(), C.c_double()
         ut = torch.zeros_like(f)
-        _lib.call("mgb_time_pass", h.handle, w, 0, 0, nu, dv.ptr(f), dv.ptr(ut), 20, C.byref(ms_pre), dv.stream(f))
-        _lib.call("mgb_time_pass", h.handle, w, 0, 1, nu, dv.ptr(f), dv.ptr(ut), 20, C.byref(ms_post), dv.stream(f))
+        _lib.call("mgb_time_pass", h.handle, w, 0, 0, nu, dv.ptr(f), dv.ptr(ut), 10, C.byref(ms_pre), dv.stream(f))
+        _lib.call("mgb_time_pass", h.handle, w, 0, 1, nu, dv.ptr(f), dv.ptr(ut), 10, C.byref(ms_post), dv.stream(f))
         torch.cuda.synchronize(dev)
     finally:
         h.release_work(w)
     peak, peak_kind = measured_peak()
-    # algorithmic bytes per fine point: u in, f, u out (8 B each) + restricted residual
-    # (PRE) or coarse correction (POST) at 8 B per coarse point; + 72 B each for A and
-    # M when they are per-point planes (the reference data model)
+    # algorithmic bytes per fine point of one phase: u in, f, u out (8 B each) plus
+    # the restricted residual (PRE) or coarse correction (POST) at 8 B per coarse
+    # point; + 72 B each for A and M when they are per-point planes
     per_pt = 26 + (0 if compact else 144)
-    pass_bytes = per_pt * n * n
+    pass_bytes = per_pt * n * n * nb
     achieved = pass_bytes / (ms_pre.value * 1e-3) / 1e9
     achieved_post = pass_bytes / (ms_post.value * 1e-3) / 1e9
-    traffic, _ = ncu_traffic()
+    traffic, _ = ncu_traffic(args.config)
 
     # e2e through the host-buffer C-ABI call (pinned host f in, u + history out)
-    f_pin = torch.from_numpy(f_host).pin_memory()
+    f_pin = torch.from_numpy(np.ascontiguousarray(f_host if batched else f_host[0])).pin_memory()
     u_pin = torch.zeros_like(f_pin).pin_memory()
-    hist_host = np.empty((1, cycles + 1))
+    hist_host = np.empty((nb, cycles + 1))
     fh, uh = f_pin.numpy(), u_pin.numpy()
     for _ in range(2):
-        h.run_cycles_host(fh, uh, cycles, nu, nu, history_host=hist_host, u_zero=True,
-                          stream=dv.stream(f))
+        h.run_cycles_host(fh, uh, cycles, nu, nu, history_host=hist_host, u_zero=True, stream=dv.stream(f))
     barrier()
     e_steps = max(1, min(args.steps, 5))
     e0 = torch.cuda.Event(enable_timing=True)
@@ -305,43 +340,42 @@ def run_ours(args):
         h.run_cycles_host(fh, uh, cycles, nu, nu, history_host=hist_host, u_zero=True, stream=dv.stream(f))
     e1.record(stream)
     barrier()
-    e_ms = e0.elapsed_time(e1) / e_steps
-    t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_value = world * n * n * cycles / (float(t.item()) * 1e-3)
+    e_ms = D.max_over_ranks(e0.elapsed_time(e1) / e_steps, dev)
+    e2e_value = total_problems * n * n * cycles / (e_ms * 1e-3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample(args.config, steps=1)
     if rank == 0:
         bpu = cycle_bytes_per_fine_unknown(n, levels, nu, nu)
+        hl = hist_all[:, -1]
         line = {
             "metric": "unknowns/sec per V-cycle (fp64)", "value": value, "unit": "unknowns/s",
-            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generators; trained seeded conv net fixture)",
-            "config": {"workload": f"{args.config}: rotated FD Laplacian eps={info['eps']} theta=pi/4 "
-                                   f"{n}^2, {levels} levels, V({nu},{nu}) x {cycles} cycles + history, "
-                                   f"learned conv smoother (per-point fp64 A and M)",
-                       "unknowns": n * n, "cycles_per_step": cycles,
-                       "l2": "inputs larger than L2 (level-0 A+M = 2.4 GB)", "parallelism": f"replicas x{world}"},
+            "n_gpus": world, "steps": args.steps, "warmup": warm, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong" if batched else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded generators; reference-trained seeded conv net fixture)",
+            "config": {"workload": workload_desc(args.config), "unknowns_per_problem": n * n,
+                       "problems": total_problems, "cycles_per_step": cycles,
+                       "l2": "inputs larger than L2 (level-0 u, f and tables exceed 126 MB)",
+                       "parallelism": (f"batch split x{world}" if batched else f"replicas x{world}")},
             "roofline": {"bound": "hbm",
-                         "kernel": "k_stream PRE, level 0 (2 sweeps + residual + full-weighting restriction, "
+                         "kernel": "k_stream PRE, level 0 (sweeps + residual + full-weighting restriction, "
                                    "one row-streaming pass)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": pass_bytes, "launch_ms": ms_pre.value,
                          "storage": "band-class tables (A, M exact, shared memory)" if compact else "per-point planes",
-                         "post": {"kernel": "k_stream POST, level 0 (prolongation + 2 sweeps)",
-                                  "achieved": achieved_post, "frac": achieved_post / peak, "launch_ms": ms_post.value}},
-            "cycle_model": {"survey_bytes_per_fine_unknown": bpu if not compact else 172.6,
-                            "survey_model": "per-point" if not compact else "compact (SURVEY 8(d))",
-                            "effective_GBps": value / world * (bpu if not compact else 172.6) / 1e9},
-            "e2e": {"value": e2e_value, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * n * n,
-                    "d2h_bytes_per_step": 8 * n * n + 8 * (cycles + 1)},
+                         "post": {"kernel": "k_stream POST, level 0 (prolongation + sweeps)",
+                                  "achieved": achieved_post, "frac": achieved_post / peak,
+                                  "launch_ms": ms_post.value}},
+            "cycle_model": {"survey_bytes_per_fine_unknown": 172.6 if compact else bpu,
+                            "survey_model": "compact (SURVEY 8(d))" if compact else "per-point (SURVEY 8(d))",
+                            "effective_GBps": value / world * (172.6 if compact else bpu) / 1e9},
+            "e2e": {"value": e2e_value, "unit": "unknowns/s", "h2d_bytes_per_step": 8 * n * n * nb,
+                    "d2h_bytes_per_step": 8 * n * n * nb + 8 * (cycles + 1) * nb},
             "gpu_launches": int(launches_per_step * args.steps),
-            "history_last": float(final_hist[-1]),
+            "history_last": float(np.median(hl)) if batched else float(hl[0]),
+            "history_last_stat": "median over problems" if batched else "single problem",
             "setup_s": {"galerkin_lu": info["setup_rap_lu_s"], "cnn_inference": info["setup_infer_s"]},
             "clocks": clk.summary(),
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},

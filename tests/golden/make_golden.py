@@ -65,6 +65,15 @@ def make_nets():
         net, _, _ = rtr.train_inference_net(A31c2, "conv", 4, cfg, k=1, seed_net=0)
         rs.save_model(path, net, {"fixture": "SURVEY G4 recipe at config-2 parameters"})
     out["conv_c2"] = rs.load_model(path)
+    # config 3 (GRF diffusion, 5-point): the recipe on a seeded 31^2 GRF (corr. length 1/4)
+    path = os.path.join(HERE, "net_conv_c3.json")
+    if not os.path.exists(path):
+        Ag = gen.grf_diffusion_5pt(31, corr_len=0.25, seed=2)
+        S = rg.StencilField(rg.GridSpec(31, 31, 1 / 31, np.ones((31, 31), bool)), Ag)
+        cfg = rtr.TrainConfig(samples=10, max_steps=2, batch_size=5, epochs=20, seed=0)
+        net, _, _ = rtr.train_inference_net(S, "conv", 4, cfg, k=1, seed_net=0)
+        rs.save_model(path, net, {"fixture": "SURVEY G4 recipe on a config-3 GRF 31^2", "corr_len": 0.25})
+    out["conv_c3"] = rs.load_model(path)
     path = os.path.join(HERE, "net_conv_k2.json")
     if not os.path.exists(path):
         net = rs.inference_net("conv", k=2, seed=5)
