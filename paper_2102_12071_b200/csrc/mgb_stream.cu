@@ -25,6 +25,7 @@
 // Reference: v_cycle hierarchy.py:96-111 (with RepeatedSmoother cli.py:365-377),
 // apply_stencil grid.py:216-226, inferred_apply smoothers.py:325-343, restrict
 // transfer.py:108-121, prolong transfer.py:124-147, history hierarchy.py:129-141.
+#include <cstdlib>
 #include <utility>
 #include <vector>
 #include <algorithm>
@@ -70,17 +71,19 @@ struct SP {
 __host__ __device__ constexpr int m3(int x) { return ((x % 3) + 3) % 3; }
 
 // 3x3 dot product with three independent accumulation chains
-__device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][3], int s0, int s1, int s2) {
-  double a0 = wt[0] * x[s0][0];
-  double a1 = wt[3] * x[s1][0];
-  double a2 = wt[6] * x[s2][0];
-  a0 = fma(wt[1], x[s0][1], a0);
-  a1 = fma(wt[4], x[s1][1], a1);
-  a2 = fma(wt[7], x[s2][1], a2);
-  a0 = fma(wt[2], x[s0][2], a0);
-  a1 = fma(wt[5], x[s1][2], a1);
-  a2 = fma(wt[8], x[s2][2], a2);
-  return (a0 + a1) + a2;
+// init +/- sum_o w[o] x[o] as one fused-multiply-add chain seeded with init
+// (f for a residual, the previous u for an update): 9 FP64 instructions
+template <bool NEG>
+__device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][3], int s0, int s1, int s2,
+                                       double init) {
+  double a = init;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) a = fma(NEG ? -wt[c] : wt[c], x[s0][c], a);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) a = fma(NEG ? -wt[3 + c] : wt[3 + c], x[s1][c], a);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) a = fma(NEG ? -wt[6 + c] : wt[6 + c], x[s2][c], a);
+  return a;
 }
 
 // Per-CTA constants of a streaming pass.
@@ -151,22 +154,22 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
     double val = 0.0;
     if (FAST || (unsigned)row < (unsigned)g.rows) {
       const Op& op = (k & 1) ? a.A : a.K;
-      double sdot;
+      const bool res_stage = k & 1;
+      const double init = res_stage ? c.ring_f[(row & (PDF - 1)) * SWT + c.tid] : hold[k / 2 - 1];
       if (!CL) {
         const double* base = op.planes + (int64_t)c.b * 9 * op.n + ((int64_t)row * g.cols + (c.cin ? c.col : 0));
         double wt[9];
 #pragma unroll
         for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
-        sdot = dot9(wt, w[k - 1], s0, s1, s2);
+        val = res_stage ? dot9<true>(wt, w[k - 1], s0, s1, s2, init) : dot9<false>(wt, w[k - 1], s0, s1, s2, init);
       } else if (FAST) {
         const double* reg = CM == 2 ? ((k & 1) ? a.ci : a.ci + 9) : (((k & 1) ? c.tA : c.tK) + CINT * 9);
-        sdot = dot9(reg, w[k - 1], s0, s1, s2);
+        val = res_stage ? dot9<true>(reg, w[k - 1], s0, s1, s2, init) : dot9<false>(reg, w[k - 1], s0, s1, s2, init);
       } else {
         const double* tab = (k & 1) ? c.tA : c.tK;
-        sdot = dot9(tab + (bandc(row, g.rows) * 5 + c.ccls) * 9, w[k - 1], s0, s1, s2);
+        const double* wt = tab + (bandc(row, g.rows) * 5 + c.ccls) * 9;
+        val = res_stage ? dot9<true>(wt, w[k - 1], s0, s1, s2, init) : dot9<false>(wt, w[k - 1], s0, s1, s2, init);
       }
-      if (k & 1) val = c.ring_f[(row & (PDF - 1)) * SWT + c.tid] - sdot;
-      else val = hold[k / 2 - 1] + sdot;
       if (MSK && c.cin && !c.mk[(int64_t)row * g.cols + c.col]) val = 0.0;
       if (!FAST) val = c.cin ? val : 0.0;
       if (NORM && k == 1 && c.owned_c && row >= c.R0 && row < c.R1) acc = fma(val, val, acc);
@@ -398,7 +401,8 @@ static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks)
     if (e != cudaSuccess) return e;
     occ_cache.push_back({(const void*)kern, occ});
   }
-  a.seg = choose_seg(a.g, nsw, res, occ);
+  static const int force_seg = getenv("MGB_SEG") ? atoi(getenv("MGB_SEG")) : 0;  // experiments only
+  a.seg = force_seg > 0 ? force_seg : choose_seg(a.g, nsw, res, occ);
   const int H = 2 * nsw + 2, wout = SWT - 2 * H;
   const dim3 grid((a.g.cols + wout - 1) / wout, (a.g.rows + a.seg - 1) / a.seg, a.g.batch);
   if (nblocks) *nblocks = (int)(grid.x * grid.y);
