@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmgb.so")
-SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_cnn.cu", "mgb_api.cu"]
+SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_coarse.cu", "mgb_cnn.cu", "mgb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -38,7 +38,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "mgb_internal.h"), os.path.join(CSRC, "mgb_cycle.h"), os.path.join(CSRC, "mgb_stream.h"),
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "mgb_internal.h"), os.path.join(CSRC, "mgb_cycle.h"), os.path.join(CSRC, "mgb_stream.h"), os.path.join(CSRC, "mgb_coarse.h"),
                                                         os.path.join(ROOT, "include", "mgb.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 

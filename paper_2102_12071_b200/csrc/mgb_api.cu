@@ -14,6 +14,7 @@
 
 #include "mgb_cycle.h"
 #include "mgb_stream.h"
+#include "mgb_coarse.h"
 #include "mgb_internal.h"
 
 namespace mgb {
@@ -92,7 +93,9 @@ struct mgb_hier {
   double slope = 0.01;
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
-  int64_t stream_min = 1500000;  // streaming passes on levels with at least this many points
+  int64_t stream_min = 1500000;
+  int64_t coarse_max = 256 * 256;  // levels up to this many points run in the single-launch cluster cycle
+                                   // (0 disables it)  // streaming passes on levels with at least this many points
                                    // (smaller levels are latency-bound: separate tile kernels win)
   int fused = 2;            // 2: one streaming pass per smoothing phase; 1: single-sweep streaming
                             // passes; 0: separate sweep / restriction / prolongation kernels
@@ -525,6 +528,7 @@ extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double 
   if (const char* e = getenv("MGB_STORAGE")) h->compact = std::string(e) != "planes";
   if (const char* e = getenv("MGB_FUSED")) h->fused = atoi(e);
   if (const char* e = getenv("MGB_STREAM_MIN")) h->stream_min = atoll(e);
+  if (const char* e = getenv("MGB_COARSE_MAX")) h->coarse_max = atoll(e);
   if (int st = classify_all(h.get(), s)) return st;
   *out = h.release();
   return MGB_OK;
@@ -850,6 +854,49 @@ static int enqueue_fnorm(mgb_work* w, const double* f, cudaStream_t s) {
   return MGB_OK;
 }
 
+// ---- single-launch coarse cycle (mgb_coarse.cu) ------------------------------
+
+// first level handled by the cluster kernel (levels lc..L-1), or -1
+static int coarse_first_level(const mgb_hier* h) {
+  if (h->coarse_max <= 0) return -1;
+  const int L = h->depth();
+  if (L - 1 > COARSE_MAX_LEVELS - 1) return -1;
+  int lc = L - 1;
+  while (lc > 0 && h->lv[lc - 1].n <= h->coarse_max) --lc;
+  if (lc >= L - 1) return -1;  // only the coarsest: nothing to gain
+  for (int l = lc; l + 1 < L; ++l)
+    if (h->lv[l].ks != 1 || !h->lv[l].K) return -1;
+  if (h->nc > 4096) return -1;
+  return lc;
+}
+
+static int enqueue_coarse(mgb_work* w, int lc, bool zero, int nu1, int nu2, cudaStream_t s) {
+  const mgb_hier* h = w->h;
+  CoarseArgs a{};
+  a.nlev = h->depth() - lc;
+  a.nu1 = nu1;
+  a.nu2 = nu2;
+  a.zero_top = zero ? 1 : 0;
+  a.nc = h->nc;
+  a.lu = h->lu;
+  a.perm = h->perm;
+  a.actp = h->actp;
+  for (int q = 0; q < a.nlev; ++q) {
+    const LevelD& lv = h->lv[lc + q];
+    CLevel& c = a.lv[q];
+    c.rows = lv.rows;
+    c.cols = lv.cols;
+    c.A = lv.opA();
+    c.K = q + 1 < a.nlev ? lv.opK() : Op{nullptr, nullptr, lv.n, 1};
+    c.mask = lv.mask;
+    c.u = w->u[lc + q];
+    c.f = w->f[lc + q];
+    c.r = w->r[lc + q];
+  }
+  MGB_CUDA_TRY(launch_coarse_cluster(a, h->batch, s));
+  return MGB_OK;
+}
+
 // ---- row-streaming passes (mgb_stream.cu) -----------------------------------
 
 static bool use_stream(const mgb_hier* h, int l, int nu1, int nu2) {
@@ -943,6 +990,11 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   }
   const LevelD& lv = h->lv[l];
   if (!lv.K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+  if (!hist && l > 0 && l == coarse_first_level(h) && u == w->u[l] && f == w->f[l]) {
+    if (int st = enqueue_coarse(w, l, zero, nu1, nu2, s)) return st;
+    *result = u;
+    return MGB_OK;
+  }
   double* cur = u;
   double* oth = w->t[l];
   const Grid g = h->grid(l);
@@ -1034,10 +1086,16 @@ extern "C" int mgb_smooth(const mgb_hier* h, mgb_work* w, int level, const doubl
 // Capture (once per key) and launch a graph.  mode 0: run_cycles; mode 1: one
 // solve iteration (cycle + residual norm into scratch).
 // allocations are not allowed while capturing: size the workspace first
+static int coarse_first_level(const mgb_hier* h);
+
 static int prepare_work(mgb_work* w) {
   for (int l = 0; l + 1 < w->h->depth(); ++l)
     if (w->h->lv[l].ks > 1)
       if (int st = ensure_generic(w, l)) return st;
+  const int lc = coarse_first_level(w->h);
+  if (lc >= 0)
+    for (int l = lc; l < w->h->depth(); ++l)
+      if (!w->r[l]) MGB_CUDA_TRY(dalloc(&w->r[l], (size_t)w->h->batch * w->h->lv[l].n));
   return MGB_OK;
 }
 
