@@ -94,8 +94,8 @@ struct mgb_hier {
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
   int64_t stream_min = 1500000;
-  int64_t coarse_max = 256 * 256;  // levels up to this many points run in the single-launch cluster cycle
-                                   // (0 disables it)  // streaming passes on levels with at least this many points
+  int64_t coarse_max = 64 * 64;    // levels up to this many points run in the single-launch
+                                   // shared-memory coarse cycle (0 disables it)  // streaming passes on levels with at least this many points
                                    // (smaller levels are latency-bound: separate tile kernels win)
   int fused = 2;            // 2: one streaming pass per smoothing phase; 1: single-sweep streaming
                             // passes; 0: separate sweep / restriction / prolongation kernels
@@ -867,6 +867,15 @@ static int coarse_first_level(const mgb_hier* h) {
   for (int l = lc; l + 1 < L; ++l)
     if (h->lv[l].ks != 1 || !h->lv[l].K) return -1;
   if (h->nc > 4096) return -1;
+  // shared-memory budget of the block kernel: drop the finest levels until it fits
+  while (lc < L - 1) {
+    size_t d = 0;
+    for (int l = lc; l < L; ++l) d += 3 * (size_t)h->lv[l].n + 2 * 25 * 9;
+    d += h->nc;
+    if (d * sizeof(double) <= 200 * 1024) break;
+    ++lc;
+  }
+  if (lc >= L - 1) return -1;
   return lc;
 }
 
@@ -893,7 +902,7 @@ static int enqueue_coarse(mgb_work* w, int lc, bool zero, int nu1, int nu2, cuda
     c.f = w->f[lc + q];
     c.r = w->r[lc + q];
   }
-  MGB_CUDA_TRY(launch_coarse_cluster(a, h->batch, s));
+  MGB_CUDA_TRY(launch_coarse_block(a, h->batch, s));
   return MGB_OK;
 }
 
@@ -990,7 +999,7 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
   }
   const LevelD& lv = h->lv[l];
   if (!lv.K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
-  if (!hist && l > 0 && l == coarse_first_level(h) && u == w->u[l] && f == w->f[l]) {
+  if (!hist && l > 0 && l == coarse_first_level(h) && u == w->u[l] && f == w->f[l] && w->r[l]) {
     if (int st = enqueue_coarse(w, l, zero, nu1, nu2, s)) return st;
     *result = u;
     return MGB_OK;
@@ -1058,6 +1067,7 @@ extern "C" int mgb_vcycle(const mgb_hier* h, mgb_work* w, int level, const doubl
   DeviceGuard dg(h->device);
   for (int l = level; l + 1 < h->depth(); ++l)
     if (!h->lv[l].K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+  if (int st = prepare_work(w)) return st;
   const int64_t l0 = g_launches;
   int st = enqueue_vcycle(w, level, f_dev, u_dev, nu1, nu2, S(stream));
   w->last_launches = g_launches - l0;

@@ -1,18 +1,15 @@
-// The coarse end of the V-cycle in ONE launch: a thread-block cluster per problem
-// runs every level below a size threshold (sweeps, residual, restriction, the
-// coarsest LU solve, prolongation) with cluster barriers between dependent
-// phases instead of kernel boundaries.  Coarse levels are latency-bound (a few
-// thousand points each); as separate kernels each pass costs a launch and a
-// memory round trip, here a phase costs a cluster barrier.
+// The coarse end of the V-cycle in ONE launch: one CTA per problem runs every
+// level below a size threshold (sweeps, residual, restriction, the coarsest LU
+// solve, prolongation) with all of those levels' u, f, r and class tables
+// resident in shared memory and __syncthreads between dependent phases.
+// Coarse levels are latency-bound (a few thousand points each): as separate
+// kernels each pass costs a launch and an HBM/L2 round trip, here a phase costs
+// a block barrier and shared-memory accesses.
 //
 // Reference: v_cycle hierarchy.py:96-111 (V(nu1, nu2) as RepeatedSmoother,
 // cli.py:365-377), coarse_solve hierarchy.py:91-93 / lu_solve dense.py:50-63,
 // restrict transfer.py:108-121, prolong transfer.py:124-147.
-#include <cooperative_groups.h>
-
 #include "mgb_coarse.h"
-
-namespace cg = cooperative_groups;
 
 namespace mgb {
 namespace {
@@ -46,62 +43,117 @@ __device__ __forceinline__ double apply9(const Op& t, int b, const double* v, in
   return s;
 }
 
-__global__ void __cluster_dims__(COARSE_CLUSTER, 1, 1) __launch_bounds__(CT)
-    k_coarse_cluster(CoarseArgs a) {
-  extern __shared__ double xs[];
-  cg::cluster_group cl = cg::this_cluster();
-  const int b = blockIdx.y;
-  const int rank = (int)cl.block_rank();
-  const int gt = rank * CT + threadIdx.x;
-  constexpr int GT = COARSE_CLUSTER * CT;
+// smem-resident variant of apply9: v in shared memory, weights from the level's
+// class table (shared) or per-point planes (global)
+struct SLevel {
+  int rows, cols;
+  const double* tA;      // shared class tables (null: planes)
+  const double* tK;
+};
 
-  // one smoothing sweep on level l: r = f - A u (u = 0 if zero), then u = u + M r
-  auto sweep = [&](const CLevel& L, bool zero) {
-    const int64_t n = (int64_t)L.rows * L.cols;
-    double* u = L.u + b * n;
-    const double* f = L.f + b * n;
-    double* r = L.r + b * n;
-    for (int64_t p = gt; p < n; p += GT) {
-      const int i = (int)(p / L.cols), j = (int)(p % L.cols);
-      double v = 0.0;
-      if (!L.mask || L.mask[p]) v = zero ? f[p] : f[p] - apply9(L.A, b, u, i, j, L.rows, L.cols);
-      r[p] = v;
+__device__ __forceinline__ double apply9s(const Op& t, const double* tab, int b, const double* v, int i, int j,
+                                          int rows, int cols) {
+  const int64_t p = (int64_t)i * cols + j;
+  const double* w = tab ? tab + (bandk(i, rows) * 5 + bandk(j, cols)) * 9 : nullptr;
+  double s = 0.0;
+#pragma unroll
+  for (int di = -1; di <= 1; ++di) {
+    const int ii = i + di;
+    if (ii < 0 || ii >= rows) continue;
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj) {
+      const int jj = j + dj;
+      if (jj < 0 || jj >= cols) continue;
+      const int o = (di + 1) * 3 + dj + 1;
+      const double wo = w ? w[o] : __ldg(t.planes + (int64_t)b * 9 * t.n + (int64_t)o * t.n + p);
+      s = fma(wo, v[ii * cols + jj], s);
     }
-    cl.sync();
-    for (int64_t p = gt; p < n; p += GT) {
-      const int i = (int)(p / L.cols), j = (int)(p % L.cols);
-      double v = 0.0;
-      if (!L.mask || L.mask[p]) v = (zero ? 0.0 : u[p]) + apply9(L.K, b, r, i, j, L.rows, L.cols);
-      u[p] = v;
+  }
+  return s;
+}
+
+// One CTA per problem runs levels lv[0..nlev-1] with every level's u, f, r (and
+// the class tables) resident in shared memory; phases are separated by
+// __syncthreads only.
+__global__ void __launch_bounds__(CT) k_coarse_block(CoarseArgs a) {
+  extern __shared__ double sm[];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  // carve shared memory: per level u, f, r (rows*cols each), then class tables
+  double* su[COARSE_MAX_LEVELS];
+  double* sf[COARSE_MAX_LEVELS];
+  double* sr[COARSE_MAX_LEVELS];
+  const double* stA[COARSE_MAX_LEVELS];
+  const double* stK[COARSE_MAX_LEVELS];
+  double* cur = sm;
+  for (int l = 0; l < a.nlev; ++l) {
+    const int n = a.lv[l].rows * a.lv[l].cols;
+    su[l] = cur; cur += n;
+    sf[l] = cur; cur += n;
+    sr[l] = cur; cur += n;
+  }
+  for (int l = 0; l < a.nlev; ++l) {
+    stA[l] = nullptr;
+    stK[l] = nullptr;
+    if (a.lv[l].A.cls) {
+      for (int q = tid; q < NCLS * 9; q += CT) cur[q] = a.lv[l].A.cls[(int64_t)b * NCLS * 9 + q];
+      stA[l] = cur;
+      cur += NCLS * 9;
     }
-    cl.sync();
+    if (l + 1 < a.nlev && a.lv[l].K.cls) {
+      for (int q = tid; q < NCLS * 9; q += CT) cur[q] = a.lv[l].K.cls[(int64_t)b * NCLS * 9 + q];
+      stK[l] = cur;
+      cur += NCLS * 9;
+    }
+  }
+  double* xs = cur;  // coarsest LU work vector
+  {
+    const CLevel& L = a.lv[0];
+    const int n = L.rows * L.cols;
+    for (int p = tid; p < n; p += CT) sf[0][p] = L.f[(int64_t)b * n + p];
+    if (!a.zero_top)
+      for (int p = tid; p < n; p += CT) su[0][p] = L.u[(int64_t)b * n + p];
+  }
+  __syncthreads();
+
+  auto act = [&](int l, int p) { return !a.lv[l].mask || a.lv[l].mask[p]; };
+  auto sweep = [&](int l, bool zero) {
+    const CLevel& L = a.lv[l];
+    const int n = L.rows * L.cols;
+    for (int p = tid; p < n; p += CT) {
+      const int i = p / L.cols, j = p - (p / L.cols) * L.cols;
+      double v = 0.0;
+      if (act(l, p)) v = zero ? sf[l][p] : sf[l][p] - apply9s(L.A, stA[l], b, su[l], i, j, L.rows, L.cols);
+      sr[l][p] = v;
+    }
+    __syncthreads();
+    for (int p = tid; p < n; p += CT) {
+      const int i = p / L.cols, j = p - (p / L.cols) * L.cols;
+      double v = 0.0;
+      if (act(l, p)) v = (zero ? 0.0 : su[l][p]) + apply9s(L.K, stK[l], b, sr[l], i, j, L.rows, L.cols);
+      su[l][p] = v;
+    }
+    __syncthreads();
   };
 
-  // descend
   for (int l = 0; l + 1 < a.nlev; ++l) {
     const CLevel& L = a.lv[l];
     const CLevel& Cc = a.lv[l + 1];
     const bool zero0 = l > 0 || a.zero_top;
-    for (int q = 0; q < a.nu1; ++q) sweep(L, zero0 && q == 0);
-    const int64_t n = (int64_t)L.rows * L.cols;
-    double* u = L.u + b * n;
-    const double* f = L.f + b * n;
-    double* r = L.r + b * n;
+    const int n = L.rows * L.cols;
+    for (int q = 0; q < a.nu1; ++q) sweep(l, zero0 && q == 0);
     if (a.nu1 == 0 && zero0) {
-      for (int64_t p = gt; p < n; p += GT) u[p] = 0.0;
-      cl.sync();
+      for (int p = tid; p < n; p += CT) su[l][p] = 0.0;
+      __syncthreads();
     }
-    for (int64_t p = gt; p < n; p += GT) {
-      const int i = (int)(p / L.cols), j = (int)(p % L.cols);
-      double v = 0.0;
-      if (!L.mask || L.mask[p]) v = f[p] - apply9(L.A, b, u, i, j, L.rows, L.cols);
-      r[p] = v;
+    for (int p = tid; p < n; p += CT) {
+      const int i = p / L.cols, j = p - (p / L.cols) * L.cols;
+      sr[l][p] = act(l, p) ? sf[l][p] - apply9s(L.A, stA[l], b, su[l], i, j, L.rows, L.cols) : 0.0;
     }
-    cl.sync();
-    const int64_t nc = (int64_t)Cc.rows * Cc.cols;
-    double* fc = Cc.f + b * nc;
-    for (int64_t pc = gt; pc < nc; pc += GT) {
-      const int ci = (int)(pc / Cc.cols), cj = (int)(pc % Cc.cols);
+    __syncthreads();
+    const int nc = Cc.rows * Cc.cols;
+    for (int pc = tid; pc < nc; pc += CT) {
+      const int ci = pc / Cc.cols, cj = pc - (pc / Cc.cols) * Cc.cols;
       double s = 0.0;
 #pragma unroll
       for (int di = 0; di < 3; ++di)
@@ -109,51 +161,43 @@ __global__ void __cluster_dims__(COARSE_CLUSTER, 1, 1) __launch_bounds__(CT)
         for (int dj = 0; dj < 3; ++dj) {
           const int fi = 2 * ci + di, fj = 2 * cj + dj;
           const double wv = (di == 1 ? 2.0 : 1.0) * (dj == 1 ? 2.0 : 1.0) * 0.0625;
-          if (fi < L.rows && fj < L.cols) s = fma(wv, r[(int64_t)fi * L.cols + fj], s);
+          if (fi < L.rows && fj < L.cols) s = fma(wv, sr[l][fi * L.cols + fj], s);
         }
-      fc[pc] = (!Cc.mask || Cc.mask[pc]) ? s : 0.0;
+      sf[l + 1][pc] = act(l + 1, pc) ? s : 0.0;
     }
-    cl.sync();
+    __syncthreads();
   }
-  // coarsest: dense LU solve (dense.py:50-63) in CTA 0
   {
-    const CLevel& L = a.lv[a.nlev - 1];
-    const int64_t n = (int64_t)L.rows * L.cols;
-    if (rank == 0) {
-      const int nn = a.nc;
-      const double* lu = a.lu + (int64_t)b * nn * nn;
-      const int32_t* pm = a.perm + (int64_t)b * nn;
-      const double* f = L.f + b * n;
-      double* x = L.u + b * n;
-      for (int q = threadIdx.x; q < nn; q += CT) xs[q] = f[a.actp[pm[q]]];
-      for (int64_t q = threadIdx.x; q < n; q += CT) x[q] = 0.0;
+    const int lc = a.nlev - 1;
+    const CLevel& L = a.lv[lc];
+    const int n = L.rows * L.cols;
+    const int nn = a.nc;
+    const double* lu = a.lu + (int64_t)b * nn * nn;
+    const int32_t* pm = a.perm + (int64_t)b * nn;
+    for (int q = tid; q < nn; q += CT) xs[q] = sf[lc][a.actp[pm[q]]];
+    for (int q = tid; q < n; q += CT) su[lc][q] = 0.0;
+    __syncthreads();
+    for (int k = 0; k < nn; ++k) {
+      const double xk = xs[k];
+      for (int i = k + 1 + tid; i < nn; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
       __syncthreads();
-      for (int k = 0; k < nn; ++k) {
-        const double xk = xs[k];
-        for (int i = k + 1 + threadIdx.x; i < nn; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
-        __syncthreads();
-      }
-      for (int k = nn - 1; k >= 0; --k) {
-        if (threadIdx.x == 0) xs[k] = xs[k] / lu[(int64_t)k * nn + k];
-        __syncthreads();
-        const double xk = xs[k];
-        for (int i = threadIdx.x; i < k; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
-        __syncthreads();
-      }
-      for (int q = threadIdx.x; q < nn; q += CT) x[a.actp[q]] = xs[q];
     }
-    cl.sync();
+    for (int k = nn - 1; k >= 0; --k) {
+      if (tid == 0) xs[k] = xs[k] / lu[(int64_t)k * nn + k];
+      __syncthreads();
+      const double xk = xs[k];
+      for (int i = tid; i < k; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
+      __syncthreads();
+    }
+    for (int q = tid; q < nn; q += CT) su[lc][a.actp[q]] = xs[q];
+    __syncthreads();
   }
-  // ascend: u_l += P u_{l+1}, then nu2 sweeps
   for (int l = a.nlev - 2; l >= 0; --l) {
     const CLevel& L = a.lv[l];
     const CLevel& Cc = a.lv[l + 1];
-    const int64_t n = (int64_t)L.rows * L.cols;
-    const int64_t ncc = (int64_t)Cc.rows * Cc.cols;
-    double* u = L.u + b * n;
-    const double* ec = Cc.u + b * ncc;
-    for (int64_t p = gt; p < n; p += GT) {
-      const int i = (int)(p / L.cols), j = (int)(p % L.cols);
+    const int n = L.rows * L.cols;
+    for (int p = tid; p < n; p += CT) {
+      const int i = p / L.cols, j = p - (p / L.cols) * L.cols;
       double s = 0.0;
 #pragma unroll
       for (int di = -1; di <= 1; ++di) {
@@ -164,29 +208,40 @@ __global__ void __cluster_dims__(COARSE_CLUSTER, 1, 1) __launch_bounds__(CT)
           const int tt = j - 1 - dj;
           if (tt < 0 || (tt & 1) || (tt >> 1) >= Cc.cols) continue;
           const double wv = (di == 0 ? 2.0 : 1.0) * (dj == 0 ? 2.0 : 1.0) * 0.125;
-          s = fma(wv, ec[(int64_t)(t >> 1) * Cc.cols + (tt >> 1)], s);
+          s = fma(wv, su[l + 1][(t >> 1) * Cc.cols + (tt >> 1)], s);
         }
       }
-      u[p] = (!L.mask || L.mask[p]) ? u[p] + s : 0.0;
+      su[l][p] = act(l, p) ? su[l][p] + s : 0.0;
     }
-    cl.sync();
-    for (int q = 0; q < a.nu2; ++q) sweep(L, false);
+    __syncthreads();
+    for (int q = 0; q < a.nu2; ++q) sweep(l, false);
+  }
+  {
+    const CLevel& L = a.lv[0];
+    const int n = L.rows * L.cols;
+    for (int p = tid; p < n; p += CT) L.u[(int64_t)b * n + p] = su[0][p];
   }
 }
 
 }  // namespace
 
-cudaError_t launch_coarse_cluster(const CoarseArgs& a, int batch, cudaStream_t s) {
-  static bool attr = false;
-  const size_t smem = sizeof(double) * (size_t)std::max(a.nc, 1);
-  if (!attr || smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_coarse_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)std::max<size_t>(smem, 48 * 1024));
-    if (e != cudaSuccess) return e;
-    attr = true;
+size_t coarse_block_smem(const CoarseArgs& a) {
+  size_t d = 0;
+  for (int l = 0; l < a.nlev; ++l) {
+    d += 3 * (size_t)a.lv[l].rows * a.lv[l].cols;
+    if (a.lv[l].A.cls) d += NCLS * 9;
+    if (l + 1 < a.nlev && a.lv[l].K.cls) d += NCLS * 9;
   }
+  d += std::max(a.nc, 1);
+  return d * sizeof(double);
+}
+
+cudaError_t launch_coarse_block(const CoarseArgs& a, int batch, cudaStream_t s) {
+  const size_t smem = coarse_block_smem(a);
+  cudaError_t e = cudaFuncSetAttribute(k_coarse_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   ++g_launches;
-  k_coarse_cluster<<<dim3(COARSE_CLUSTER, batch), CT, smem, s>>>(a);
+  k_coarse_block<<<batch, CT, smem, s>>>(a);
   return MGB_DBG(__func__);
 }
 

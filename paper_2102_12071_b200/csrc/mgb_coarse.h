@@ -5,7 +5,6 @@
 
 #include "mgb_cycle.h"
 
-#define COARSE_CLUSTER 8   // CTAs per cluster (portable maximum)
 
 namespace mgb {
 
@@ -31,6 +30,8 @@ struct CoarseArgs {
   CLevel lv[COARSE_MAX_LEVELS];
 };
 
-cudaError_t launch_coarse_cluster(const CoarseArgs& a, int batch, cudaStream_t s);
+// shared-memory bytes the block kernel needs for these levels (<= 227 KB to run)
+size_t coarse_block_smem(const CoarseArgs& a);
+cudaError_t launch_coarse_block(const CoarseArgs& a, int batch, cudaStream_t s);
 
 }  // namespace mgb
