@@ -162,6 +162,7 @@ struct mgb_work {
 };
 
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+int prepare_work(mgb_work* w);  // sizes per-solve scratch before any capture
 
 // ---------------------------------------------------------------------------
 // library / errors
@@ -1098,7 +1099,7 @@ extern "C" int mgb_smooth(const mgb_hier* h, mgb_work* w, int level, const doubl
 // allocations are not allowed while capturing: size the workspace first
 static int coarse_first_level(const mgb_hier* h);
 
-static int prepare_work(mgb_work* w) {
+int prepare_work(mgb_work* w) {
   for (int l = 0; l + 1 < w->h->depth(); ++l)
     if (w->h->lv[l].ks > 1)
       if (int st = ensure_generic(w, l)) return st;
