@@ -94,7 +94,7 @@ struct mgb_hier {
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
   int64_t stream_min = 1500000;
-  int64_t coarse_max = 64 * 64;    // levels up to this many points run in the single-launch
+  int64_t coarse_max = 32 * 32;    // levels up to this many points run in the single-launch
                                    // shared-memory coarse cycle (0 disables it)  // streaming passes on levels with at least this many points
                                    // (smaller levels are latency-bound: separate tile kernels win)
   int fused = 2;            // 2: one streaming pass per smoothing phase; 1: single-sweep streaming
