@@ -115,6 +115,15 @@ int mgb_lu_solve(int n, const double* lu_dev, const int32_t* perm_dev, const dou
 int mgb_hier_build(int device, int batch, int rows, int cols, double spacing,
                    const double* A0, int a0_on_device, const uint8_t* mask_host,
                    int levels, void* stream, mgb_hier** out);
+/* Constant-coefficient hierarchy from band-class tables, with no per-point planes
+   anywhere (memory = grid functions only; config 5's 32767^2 fits one GPU).
+   cls_host: (batch, 25, 3, 3) tables of A0 for the band classes band(i)*5 + band(j),
+   band = 0, 1 (first two rows/cols), 2 (interior), 3, 4 (last two).  A constant
+   stencil (grid.py:209 constant_stencil) is 25 copies of its table.  All points
+   active.  Galerkin products, the coarsest LU, CNN inference and Jacobi run on one
+   representative point per class; results equal the per-point build. */
+int mgb_hier_build_classed(int device, int batch, int rows, int cols, double spacing, const double* cls_host,
+                           int levels, void* stream, mgb_hier** out);
 void mgb_hier_destroy(mgb_hier* h);
 int mgb_hier_depth(const mgb_hier* h, int* depth, int* batch);
 /* level geometry; k = trimmed operator size; ks = installed smoother stages (0 = none) */

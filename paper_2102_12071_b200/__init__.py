@@ -16,7 +16,7 @@ from .transfer import TransferPair, coarsen_full, galerkin_product, prolong, res
 from .smoothers import (InferredSmoother, JacobiSmoother, KernelInferenceNet, infer_kernels, inference_net,
                         jacobi, load_model, save_model)
 from .hierarchy import (Level, MultigridHierarchy, RepeatedSmoother, SolveReport, build_hierarchy,
-                        build_hierarchy_batch, coarse_solve, cycle_correction, equip_classical,
+                        build_hierarchy_batch, build_hierarchy_classed, coarse_solve, cycle_correction, equip_classical,
                         equip_inferred, solve, v_cycle)
 
 __version__ = "0.1.0"

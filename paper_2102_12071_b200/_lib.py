@@ -40,6 +40,7 @@ SIGNATURES = {
     "mgb_lu_factor": (I, [I, P, P, P]),
     "mgb_lu_solve": (I, [I, P, P, P, P, P]),
     "mgb_hier_build": (I, [I, I, I, I, D, P, I, P, I, P, C.POINTER(P)]),
+    "mgb_hier_build_classed": (I, [I, I, I, I, D, P, I, P, C.POINTER(P)]),
     "mgb_hier_destroy": (None, [P]),
     "mgb_hier_depth": (I, [P, PI, PI]),
     "mgb_hier_level_info": (I, [P, I, PI, PI, PI, PI, PD]),

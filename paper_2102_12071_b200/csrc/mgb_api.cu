@@ -80,7 +80,7 @@ struct LevelD {
   std::vector<uint8_t> hmask;
   int64_t nact = 0;
   Op opA() const { return Op{A, Acls, n, 1}; }
-  Op opK() const { return Op{K, Kcls, n, ks}; }
+  Op opK() const { return Op{K == Kcls ? nullptr : K, Kcls, n, ks}; }
 };
 
 struct mgb_hier {
@@ -93,6 +93,7 @@ struct mgb_hier {
   double slope = 0.01;
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
+  int classed_only = 0;     // built from band-class tables: no per-point planes exist
   int64_t stream_min = 1500000;
   int64_t coarse_max = 32 * 32;    // levels up to this many points run in the single-launch
                                    // shared-memory coarse cycle (0 disables it)  // streaming passes on levels with at least this many points
@@ -103,6 +104,7 @@ struct mgb_hier {
     DeviceGuard dg(device);
     for (auto& l : lv) {
       dfree(l.A);
+      if (l.K == l.Kcls) l.K = nullptr;
       dfree(l.K);
       dfree(l.mask);
       dfree(l.Acls);
@@ -163,6 +165,15 @@ struct mgb_work {
 
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 int prepare_work(mgb_work* w);  // sizes per-solve scratch before any capture
+
+static Tab tabA(const mgb_hier* h, const LevelD& l) {
+  return h->classed_only ? tab_cls(l.Acls, l.rows, l.cols, 1) : tab_soa(l.A, l.n, 1);
+}
+static Tab tabK(const mgb_hier* h, const LevelD& l) {
+  return h->classed_only ? tab_cls(l.Kcls, l.rows, l.cols, l.ks) : tab_soa(l.K, l.n, l.ks);
+}
+
+
 
 // ---------------------------------------------------------------------------
 // library / errors
@@ -339,10 +350,23 @@ static int64_t count_active(const std::vector<uint8_t>& m) {
   return c;
 }
 
+// flat index of the first point of each band class (-1 if the class is empty)
+static void class_reps(int rows, int cols, int64_t rep[25]) {
+  for (int c = 0; c < 25; ++c) rep[c] = -1;
+  int ri[5], rj[5];
+  for (int c = 0; c < 5; ++c) ri[c] = rj[c] = -1;
+  for (int i = rows - 1; i >= 0; --i) ri[host_band(i, rows)] = i;
+  for (int j = cols - 1; j >= 0; --j) rj[host_band(j, cols)] = j;
+  for (int a = 0; a < 5; ++a)
+    for (int b = 0; b < 5; ++b)
+      if (ri[a] >= 0 && rj[b] >= 0) rep[a * 5 + b] = (int64_t)ri[a] * cols + rj[b];
+}
+
 // Band-class compaction (mgb_cycle.cu): if every point of the table equals its
 // class representative, keep the 25 class tables (exact) for the hot loop.
 static int classify_table(mgb_hier* h, int l, const double* planes, int ks, double** cls_out, cudaStream_t s,
                           double* interior_host = nullptr) {
+  if (h->classed_only) return MGB_OK;
   dfree(*cls_out);
   LevelD& lv = h->lv[l];
   if (!h->compact || lv.mask || !planes) return MGB_OK;
@@ -538,6 +562,10 @@ extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double 
 extern "C" int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream) {
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   if (mode != 0 && mode != 1) return fail(MGB_CONFIG, "storage mode must be 0 (auto) or 1 (per-point planes)");
+  if (h->classed_only) {
+    if (mode == 1) return fail(MGB_CONFIG, "a band-class hierarchy has no per-point planes");
+    return MGB_OK;
+  }
   DeviceGuard dg(h->device);
   h->compact = mode == 0;
   return classify_all(h, S(stream));
@@ -555,6 +583,111 @@ extern "C" int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classe
   if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
   if (a_classed) *a_classed = h->lv[level].Acls != nullptr;
   if (k_classed) *k_classed = h->lv[level].Kcls != nullptr;
+  return MGB_OK;
+}
+
+// Constant-coefficient hierarchy held entirely as band-class tables (no per-point
+// planes): the Galerkin product and the coarsest materialisation read the fine
+// tables through the class accessor and evaluate one representative point per
+// coarse class.  Memory is O(grid functions) only, so 32767^2 (config 5) fits one GPU.
+extern "C" int mgb_hier_build_classed(int device, int batch, int rows, int cols, double spacing,
+                                      const double* cls_host, int levels, void* stream, mgb_hier** out) {
+  if (!out) return fail(MGB_CONTRACT, "null output handle");
+  *out = nullptr;
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (!(spacing > 0.0)) return fail(MGB_CONTRACT, "grid spacing must be positive");
+  if (levels < 2) return fail(MGB_CONFIG, "a hierarchy needs at least two levels");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess || cnt == 0) return fail(MGB_CUDA, "no CUDA device available");
+  if (device < 0 || device >= cnt) return fail(MGB_CONFIG, "device index out of range");
+  for (int64_t q = 0; q < (int64_t)batch * 225; ++q)
+    if (!std::isfinite(cls_host[q])) return fail(MGB_NUMERIC, "non-finite stencil weights");
+  DeviceGuard dg(device);
+  cudaStream_t s = S(stream);
+  std::unique_ptr<mgb_hier> h(new mgb_hier());
+  h->device = device;
+  h->batch = batch;
+  h->classed_only = 1;
+  int r = rows, c = cols;
+  double sp = spacing;
+  for (int l = 0; l < levels; ++l) {
+    if (r < 1 || c < 1)
+      return fail(MGB_CONFIG, "level " + std::to_string(l - 1) + ": grid cannot be coarsened further");
+    LevelD lv;
+    lv.rows = r;
+    lv.cols = c;
+    lv.h = sp;
+    lv.n = (int64_t)r * c;
+    lv.k = 3;
+    lv.nact = lv.n;
+    h->lv.push_back(std::move(lv));
+    r /= 2;
+    c /= 2;
+    sp *= 2.0;
+  }
+  const int L = h->depth();
+  if (h->lv[L - 1].n > 4096) return fail(MGB_CONFIG, "coarsest level too large for the dense direct solve (add levels)");
+  for (auto& lv : h->lv) MGB_CUDA_TRY(dalloc(&lv.Acls, (size_t)batch * 225));
+  MGB_CUDA_TRY(cudaMemcpyAsync(h->lv[0].Acls, cls_host, sizeof(double) * batch * 225, cudaMemcpyHostToDevice, s));
+  int* ring = nullptr;
+  int64_t* drep = nullptr;
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ring), sizeof(int) * L, s));
+  MGB_CUDA_TRY(cudaMemsetAsync(ring, 0, sizeof(int) * L, s));
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&drep), sizeof(int64_t) * 25 * L, s));
+  for (int l = 0; l + 1 < L; ++l) {
+    LevelD& f = h->lv[l];
+    LevelD& cl = h->lv[l + 1];
+    int64_t rep[25];
+    class_reps(cl.rows, cl.cols, rep);
+    MGB_CUDA_TRY(cudaMemcpyAsync(drep + 25 * l, rep, sizeof(rep), cudaMemcpyHostToDevice, s));
+    MGB_CUDA_TRY(cudaMemsetAsync(cl.Acls, 0, sizeof(double) * batch * 225, s));
+    MGB_CUDA_TRY(launch_galerkin(h->grid(l), tab_cls(f.Acls, f.rows, f.cols, 1), nullptr, nullptr,
+                                 tabw_cls(cl.Acls, cl.rows, cl.cols, 1), ring + l + 1, s, drep + 25 * l, 25));
+  }
+  std::vector<int> hring(L, 1);
+  MGB_CUDA_TRY(cudaMemcpyAsync(hring.data(), ring, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
+  for (auto& lv : h->lv) MGB_CUDA_TRY(cudaMemcpyAsync(lv.hAint, lv.Acls + 12 * 9, 9 * sizeof(double),
+                                                      cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaFreeAsync(ring, s));
+  MGB_CUDA_TRY(cudaFreeAsync(drep, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int l = 1; l < L; ++l) h->lv[l].k = hring[l] ? 3 : 1;
+  // coarsest LU (all points active)
+  {
+    LevelD& cl = h->lv[L - 1];
+    const int nc = (int)cl.n;
+    h->nc = nc;
+    std::vector<int32_t> idx(cl.n), actp(nc);
+    for (int q = 0; q < nc; ++q) idx[q] = actp[q] = q;
+    int32_t* didx = nullptr;
+    int* dst = nullptr;
+    MGB_CUDA_TRY(dalloc(&h->actp, nc));
+    MGB_CUDA_TRY(dalloc(&h->lu, (size_t)batch * nc * nc));
+    MGB_CUDA_TRY(dalloc(&h->perm, (size_t)batch * nc));
+    MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&didx), sizeof(int32_t) * cl.n, s));
+    MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dst), sizeof(int) * batch, s));
+    MGB_CUDA_TRY(cudaMemcpyAsync(didx, idx.data(), sizeof(int32_t) * cl.n, cudaMemcpyHostToDevice, s));
+    MGB_CUDA_TRY(cudaMemcpyAsync(h->actp, actp.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, s));
+    MGB_CUDA_TRY(cudaMemsetAsync(h->lu, 0, sizeof(double) * batch * nc * nc, s));
+    MGB_CUDA_TRY(launch_materialize(h->grid(L - 1), tab_cls(cl.Acls, cl.rows, cl.cols, 1), didx, nc, h->actp,
+                                    h->lu, s));
+    MGB_CUDA_TRY(launch_lu_factor(batch, nc, h->lu, h->perm, dst, s));
+    std::vector<int> hs(batch);
+    MGB_CUDA_TRY(cudaMemcpyAsync(hs.data(), dst, sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
+    MGB_CUDA_TRY(cudaFreeAsync(didx, s));
+    MGB_CUDA_TRY(cudaFreeAsync(dst, s));
+    MGB_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int b = 0; b < batch; ++b)
+      if (hs[b] >= 0) {
+        set_error(MGB_SINGULAR, "coarsest operator singular to working precision at pivot " + std::to_string(hs[b]),
+                  hs[b]);
+        return MGB_SINGULAR;
+      }
+  }
+  if (const char* e = getenv("MGB_FUSED")) h->fused = atoi(e);
+  if (const char* e = getenv("MGB_STREAM_MIN")) h->stream_min = atoll(e);
+  if (const char* e = getenv("MGB_COARSE_MAX")) h->coarse_max = atoll(e);
+  *out = h.release();
   return MGB_OK;
 }
 
@@ -587,7 +720,8 @@ static int download_table(const mgb_hier* h, const LevelD& l, const double* plan
   const size_t cnt = (size_t)h->batch * kst * 9 * l.n;
   MGB_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&tmp), cnt * sizeof(double)));
   Grid g{h->batch, l.rows, l.cols};
-  cudaError_t e = launch_convert(g, kst, tab_soa(planes, l.n, kst), tabw_aos(tmp, l.n, kst), nullptr);
+  const Tab src = h->classed_only ? tab_cls(planes, l.rows, l.cols, kst) : tab_soa(planes, l.n, kst);
+  cudaError_t e = launch_convert(g, kst, src, tabw_aos(tmp, l.n, kst), nullptr);
   if (e == cudaSuccess) e = cudaMemcpy(out_host, tmp, cnt * sizeof(double), cudaMemcpyDeviceToHost);
   cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(e, "download_table");
@@ -598,9 +732,10 @@ extern "C" int mgb_hier_get_operator(const mgb_hier* h, int level, double* out_h
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
   const LevelD& l = h->lv[level];
-  if (l.k == 3) return download_table(h, l, l.A, 1, out_host);
+  const double* tabp = h->classed_only ? l.Acls : l.A;
+  if (l.k == 3) return download_table(h, l, tabp, 1, out_host);
   std::vector<double> full((size_t)h->batch * 9 * l.n);
-  if (int st = download_table(h, l, l.A, 1, full.data())) return st;
+  if (int st = download_table(h, l, tabp, 1, full.data())) return st;
   for (size_t q = 0; q < (size_t)h->batch * l.n; ++q) out_host[q] = full[q * 9 + 4];
   return MGB_OK;
 }
@@ -610,7 +745,7 @@ extern "C" int mgb_hier_get_kernels(const mgb_hier* h, int level, double* out_ho
   if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
   const LevelD& l = h->lv[level];
   if (!l.K) return fail(MGB_CONFIG, "level " + std::to_string(level) + " has no smoother installed");
-  return download_table(h, l, l.K, l.ks, out_host);
+  return download_table(h, l, h->classed_only ? l.Kcls : l.K, l.ks, out_host);
 }
 
 extern "C" int mgb_hier_get_mask(const mgb_hier* h, int level, uint8_t* out_host) {
@@ -629,6 +764,16 @@ extern "C" int mgb_hier_operator_planes(const mgb_hier* h, int level, const doub
 
 static int alloc_kernels(mgb_hier* h, LevelD& l, int kst) {
   ++h->version;
+  if (h->classed_only) {
+    if (l.Kcls && l.ks == kst) return MGB_OK;
+    dfree(l.Kcls);
+    l.ks = 0;
+    MGB_CUDA_TRY(dalloc(&l.Kcls, (size_t)h->batch * 25 * kst * 9));
+    MGB_CUDA_TRY(cudaMemset(l.Kcls, 0, sizeof(double) * h->batch * 25 * kst * 9));
+    l.K = l.Kcls;  // marks the level as equipped; the hot path reads Kcls
+    l.ks = kst;
+    return MGB_OK;
+  }
   if (l.K && l.ks == kst) return MGB_OK;
   dfree(l.K);
   l.ks = 0;
@@ -650,8 +795,23 @@ extern "C" int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const 
   for (int l = 0; l + 1 < h->depth(); ++l) {
     LevelD& lv = h->lv[l];
     if (int st = alloc_kernels(h, lv, kst)) return st;
-    cudaError_t e = launch_infer(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, variant, kst, w, slope,
-                                 precision, tabw_soa(lv.K, lv.n, kst), s);
+    cudaError_t e;
+    if (h->classed_only) {
+      // one evaluation per band class at its representative point
+      int64_t rep[25];
+      class_reps(lv.rows, lv.cols, rep);
+      int64_t* drep = nullptr;
+      MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&drep), sizeof(rep), s));
+      MGB_CUDA_TRY(cudaMemcpyAsync(drep, rep, sizeof(rep), cudaMemcpyHostToDevice, s));
+      e = launch_infer(h->grid(l), tabA(h, lv), nullptr, variant, kst, w, slope, precision,
+                       tabw_cls(lv.Kcls, lv.rows, lv.cols, kst), s, drep, 25);
+      cudaFreeAsync(drep, s);
+      if (e == cudaSuccess && kst == 1)
+        e = cudaMemcpyAsync(lv.hKint, lv.Kcls + 12 * 9, 9 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    } else {
+      e = launch_infer(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, variant, kst, w, slope,
+                       precision, tabw_soa(lv.K, lv.n, kst), s);
+    }
     if (e != cudaSuccess) {
       cudaFreeAsync(w, s);
       return cuda_fail(e, "launch_infer");
@@ -675,8 +835,20 @@ extern "C" int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream) {
   for (int l = 0; l + 1 < L; ++l) {
     LevelD& lv = h->lv[l];
     if (int st = alloc_kernels(h, lv, 1)) return st;
-    MGB_CUDA_TRY(launch_jacobi(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, omega,
-                               tabw_soa(lv.K, lv.n, 1), flag + l, s));
+    if (h->classed_only) {
+      int64_t rep[25];
+      class_reps(lv.rows, lv.cols, rep);
+      int64_t* drep = nullptr;
+      MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&drep), sizeof(rep), s));
+      MGB_CUDA_TRY(cudaMemcpyAsync(drep, rep, sizeof(rep), cudaMemcpyHostToDevice, s));
+      MGB_CUDA_TRY(launch_jacobi(h->grid(l), tabA(h, lv), nullptr, omega, tabw_cls(lv.Kcls, lv.rows, lv.cols, 1),
+                                 flag + l, s, drep, 25));
+      MGB_CUDA_TRY(cudaFreeAsync(drep, s));
+      MGB_CUDA_TRY(cudaMemcpyAsync(lv.hKint, lv.Kcls + 12 * 9, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    } else {
+      MGB_CUDA_TRY(launch_jacobi(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, omega,
+                                 tabw_soa(lv.K, lv.n, 1), flag + l, s));
+    }
   }
   std::vector<int> hf(L);
   MGB_CUDA_TRY(cudaMemcpyAsync(hf.data(), flag, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
@@ -692,6 +864,7 @@ extern "C" int mgb_hier_set_kernels(mgb_hier* h, int level, int kst, const doubl
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   if (level < 0 || level + 1 >= h->depth()) return fail(MGB_CONFIG, "no smoother on this level");
   if (kst < 1) return fail(MGB_CONTRACT, "smoother needs at least one stage");
+  if (h->classed_only) return fail(MGB_CONFIG, "per-point kernels cannot be installed in a band-class hierarchy");
   DeviceGuard dg(h->device);
   cudaStream_t s = S(stream);
   LevelD& lv = h->lv[level];
@@ -741,7 +914,7 @@ extern "C" int mgb_residual(const mgb_hier* h, int level, const double* f_dev, c
   double* part = nullptr;
   int nblk = residual_blocks(g);
   if (norm2_dev) MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * nblk * g.batch, s));
-  MGB_CUDA_TRY(launch_residual(g, tab_soa(l.A, l.n, 1), l.mask, f_dev, u_dev, r_dev, part, &nblk, s));
+  MGB_CUDA_TRY(launch_residual(g, tabA(h, l), l.mask, f_dev, u_dev, r_dev, part, &nblk, s));
   if (norm2_dev) {
     MGB_CUDA_TRY(launch_finalize(g.batch, nblk, part, norm2_dev, nullptr, nullptr, 0, s));
     MGB_CUDA_TRY(cudaFreeAsync(part, s));
@@ -825,10 +998,10 @@ static int sweep(mgb_work* w, int l, const double* f, const double* in, double* 
   if (int st = ensure_generic(w, l)) return st;
   const double* r = f;
   if (in) {
-    MGB_CUDA_TRY(launch_residual(g, tab_soa(lv.A, lv.n, 1), lv.mask, f, in, w->r[l], nullptr, nullptr, s));
+    MGB_CUDA_TRY(launch_residual(g, tabA(h, lv), lv.mask, f, in, w->r[l], nullptr, nullptr, s));
     r = w->r[l];
   }
-  return smoother_apply_tab(g, lv.ks, tab_soa(lv.K, lv.n, lv.ks), lv.mask, h->slope, r, out, w->v[l],
+  return smoother_apply_tab(g, lv.ks, tabK(h, lv), lv.mask, h->slope, r, out, w->v[l],
                             w->r[l], in, s);
 }
 

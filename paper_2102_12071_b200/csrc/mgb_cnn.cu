@@ -18,12 +18,8 @@ constexpr int MAXK = 4;  // smoother stages supported by the inference kernels
 template <typename T>
 __device__ __forceinline__ T lk(T x, T s) { return x > T(0) ? x : s * x; }
 
-__device__ __forceinline__ double tabv(const Tab& t, int b, int s, int o, int64_t p) {
-  return __ldg(t.base + b * t.bstride + s * t.sstride + o * t.ostride + p * t.pstride);
-}
-__device__ __forceinline__ void tabwv(const TabW& t, int b, int s, int o, int64_t p, double v) {
-  t.base[b * t.bstride + s * t.sstride + o * t.ostride + p * t.pstride] = v;
-}
+__device__ __forceinline__ double tabv(const Tab& t, int b, int s, int o, int64_t p) { return tab_get(t, b, s, o, p); }
+__device__ __forceinline__ void tabwv(const TabW& t, int b, int s, int o, int64_t p, double v) { tab_put(t, b, s, o, p, v); }
 
 // one 3x3 "same" correlation of a single-channel 3x3 image, reference order
 template <typename T>
@@ -48,7 +44,8 @@ __device__ __forceinline__ void conv_same(const T* w, const T* x, T* out) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_infer_conv(Grid g, Tab A, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(128) k_infer_conv(const int64_t* __restrict__ pts, int npts, Grid g, Tab A,
+                                                    const uint8_t* __restrict__ mask,
                                                     int kst, const double* __restrict__ Wd,
                                                     double slope_d, TabW K) {
   // weights: W0 (7,3,3) W1 (5,3,3) W2 (3,3,3) W3 (27, 9k)
@@ -64,7 +61,11 @@ __global__ void __launch_bounds__(128) k_infer_conv(Grid g, Tab A, const uint8_t
   const T slope = T(slope_d);
   const int64_t n = g.n();
   const int b = blockIdx.y;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pts) {
+    if (p >= npts || pts[p] < 0) return;
+    p = pts[p];
+  }
   if (p >= n) return;
   const int nout = 9 * kst;
   if (mask && !mask[p]) {
@@ -110,7 +111,8 @@ __global__ void __launch_bounds__(128) k_infer_conv(Grid g, Tab A, const uint8_t
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_infer_fc(Grid g, Tab A, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(128) k_infer_fc(const int64_t* __restrict__ pts, int npts, Grid g, Tab A,
+                                                    const uint8_t* __restrict__ mask,
                                                   int kst, const double* __restrict__ Wd,
                                                   double slope_d, TabW K) {
   // weights: W0 (81,40) W1 (40,40) W2 (40,40) W3 (40, 9k)
@@ -127,7 +129,11 @@ __global__ void __launch_bounds__(128) k_infer_fc(Grid g, Tab A, const uint8_t* 
   const T slope = T(slope_d);
   const int64_t n = g.n();
   const int b = blockIdx.y;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pts) {
+    if (p >= npts || pts[p] < 0) return;
+    p = pts[p];
+  }
   if (p >= n) return;
   if (mask && !mask[p]) {
     for (int m = 0; m < nout; ++m) tabwv(K, b, m / 9, m % 9, p, 0.0);
@@ -180,14 +186,14 @@ __global__ void __launch_bounds__(128) k_infer_fc(Grid g, Tab A, const uint8_t* 
 
 template <typename KF>
 cudaError_t launch_k(KF kern, const Grid& g, size_t smem, Tab A, const uint8_t* mask, int kst,
-                     const double* W, double slope, TabW K, cudaStream_t s) {
+                     const double* W, double slope, TabW K, cudaStream_t s, const int64_t* pts, int npts) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   ++g_launches;
-  dim3 grid((unsigned)((g.n() + 127) / 128), g.batch);
-  kern<<<grid, 128, smem, s>>>(g, A, mask, kst, W, slope, K);
+  dim3 grid((unsigned)(((pts ? npts : g.n()) + 127) / 128), g.batch);
+  kern<<<grid, 128, smem, s>>>(pts, npts, g, A, mask, kst, W, slope, K);
   return MGB_DBG(__func__);
 }
 
@@ -200,17 +206,17 @@ int64_t net_weight_count(int variant, int kst) {
 
 cudaError_t launch_infer(const Grid& g, Tab A, const uint8_t* mask, int variant, int kst,
                          const double* W_dev, double slope, int precision, TabW K,
-                         cudaStream_t s) {
+                         cudaStream_t s, const int64_t* pts, int npts) {
   if (kst < 1 || kst > MAXK) return cudaErrorInvalidValue;
   const size_t nw = (size_t)net_weight_count(variant, kst);
   if (variant == MGB_NET_CONV) {
     if (precision == 32)
-      return launch_k(k_infer_conv<float>, g, nw * sizeof(float), A, mask, kst, W_dev, slope, K, s);
-    return launch_k(k_infer_conv<double>, g, nw * sizeof(double), A, mask, kst, W_dev, slope, K, s);
+      return launch_k(k_infer_conv<float>, g, nw * sizeof(float), A, mask, kst, W_dev, slope, K, s, pts, npts);
+    return launch_k(k_infer_conv<double>, g, nw * sizeof(double), A, mask, kst, W_dev, slope, K, s, pts, npts);
   }
   if (precision == 32)
-    return launch_k(k_infer_fc<float>, g, nw * sizeof(float), A, mask, kst, W_dev, slope, K, s);
-  return launch_k(k_infer_fc<double>, g, nw * sizeof(double), A, mask, kst, W_dev, slope, K, s);
+    return launch_k(k_infer_fc<float>, g, nw * sizeof(float), A, mask, kst, W_dev, slope, K, s, pts, npts);
+  return launch_k(k_infer_fc<double>, g, nw * sizeof(double), A, mask, kst, W_dev, slope, K, s, pts, npts);
 }
 
 }  // namespace mgb

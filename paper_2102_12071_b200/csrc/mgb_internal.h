@@ -40,11 +40,48 @@ cudaError_t debug_sync(const char* what);
 struct Tab {
   const double* base;
   int64_t bstride, sstride, ostride, pstride;
+  // band-class mode (base unused): table [b][class][s][o], class of p = (i, j) from
+  // band(i, crow) * 5 + band(j, ccol), band = 0, 1 first rows, 3, 4 last rows, 2 inside
+  const double* cls = nullptr;
+  int crow = 0, ccol = 0, cks = 1;
 };
 struct TabW {
   double* base;
   int64_t bstride, sstride, ostride, pstride;
+  double* cls = nullptr;
+  int crow = 0, ccol = 0, cks = 1;
 };
+
+inline Tab tab_cls(const double* cls, int rows, int cols, int kst) {
+  Tab t{nullptr, 0, 0, 0, 0};
+  t.cls = cls; t.crow = rows; t.ccol = cols; t.cks = kst;
+  return t;
+}
+inline TabW tabw_cls(double* cls, int rows, int cols, int kst) {
+  TabW t{nullptr, 0, 0, 0, 0};
+  t.cls = cls; t.crow = rows; t.ccol = cols; t.cks = kst;
+  return t;
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ int band_of(int i, int n) { return i < 2 ? i : (i >= n - 2 ? 4 - (n - 1 - i) : 2); }
+__device__ __forceinline__ int64_t tab_index(int64_t bstride, int64_t sstride, int64_t ostride, int64_t pstride,
+                                             int b, int s, int o, int64_t p) {
+  return b * bstride + s * sstride + o * ostride + p * pstride;
+}
+__device__ __forceinline__ int64_t cls_index(int crow, int ccol, int cks, int b, int s, int o, int64_t p) {
+  const int i = (int)(p / ccol), j = (int)(p - (int64_t)(p / ccol) * ccol);
+  return ((int64_t)(b * 25 + band_of(i, crow) * 5 + band_of(j, ccol)) * cks + s) * 9 + o;
+}
+__device__ __forceinline__ double tab_get(const Tab& t, int b, int s, int o, int64_t p) {
+  if (t.cls) return __ldg(t.cls + cls_index(t.crow, t.ccol, t.cks, b, s, o, p));
+  return __ldg(t.base + tab_index(t.bstride, t.sstride, t.ostride, t.pstride, b, s, o, p));
+}
+__device__ __forceinline__ void tab_put(const TabW& t, int b, int s, int o, int64_t p, double v) {
+  if (t.cls) t.cls[cls_index(t.crow, t.ccol, t.cks, b, s, o, p)] = v;
+  else t.base[tab_index(t.bstride, t.sstride, t.ostride, t.pstride, b, s, o, p)] = v;
+}
+#endif
 
 inline Tab tab_aos(const double* p, int64_t n, int kst) {
   return Tab{p, n * kst * 9, 9, 1, (int64_t)kst * 9};
@@ -95,9 +132,12 @@ cudaError_t launch_restrict(const Grid& g, const uint8_t* mask_c, const double* 
 // fine = P coarse (add == false) or fine += P coarse (add == true); masked by mask_f
 cudaError_t launch_prolong(const Grid& g, const uint8_t* mask_f, const double* coarse,
                            double* fine, bool add, cudaStream_t s);
-// Ac = R A P; ring_flag (int, device) |= 1 where the outer ring is non-zero
+// Ac = R A P; ring_flag (int, device) |= 1 where the outer ring is non-zero.
+// pts (optional, npts entries, -1 = skip): evaluate only these coarse points
+// (band-class representatives when Ac is a class table).
 cudaError_t launch_galerkin(const Grid& g, Tab A, const uint8_t* mask_f, const uint8_t* mask_c,
-                            TabW Ac, int* ring_flag, cudaStream_t s);
+                            TabW Ac, int* ring_flag, cudaStream_t s, const int64_t* pts = nullptr,
+                            int npts = 0);
 // dense materialisation of the (coarsest) operator over active points
 cudaError_t launch_materialize(const Grid& g, Tab A, const int32_t* index_map, int nact,
                                const int32_t* act, double* M, cudaStream_t s);
@@ -111,14 +151,14 @@ cudaError_t launch_lu_solve_vec(int n, const double* lu, const int32_t* perm, co
                                 double* x, cudaStream_t s);
 // jacobi kernels: K (SoA, kst = 1) = omega / diag at the centre, 0 elsewhere / inactive
 cudaError_t launch_jacobi(const Grid& g, Tab A, const uint8_t* mask, double omega, TabW K,
-                          int* zero_diag_flag, cudaStream_t s);
+                          int* zero_diag_flag, cudaStream_t s, const int64_t* pts = nullptr, int npts = 0);
 // layout conversion between reference AoS and internal SoA tables
 cudaError_t launch_convert(const Grid& g, int kst, Tab src, TabW dst, cudaStream_t s);
 
 // ---- CNN inference (mgb_cnn.cu) -------------------------------------------------
 cudaError_t launch_infer(const Grid& g, Tab A, const uint8_t* mask, int variant, int kst,
                          const double* W_dev, double slope, int precision, TabW K,
-                         cudaStream_t s);
+                         cudaStream_t s, const int64_t* pts = nullptr, int npts = 0);
 int64_t net_weight_count(int variant, int kst);
 
 }  // namespace mgb

@@ -36,12 +36,8 @@ namespace {
 
 constexpr int BX = 32, BY = 8, NT = BX * BY;
 
-__device__ __forceinline__ double tab(const Tab& t, int b, int s, int o, int64_t p) {
-  return __ldg(t.base + b * t.bstride + s * t.sstride + o * t.ostride + p * t.pstride);
-}
-__device__ __forceinline__ void tabw(const TabW& t, int b, int s, int o, int64_t p, double v) {
-  t.base[b * t.bstride + s * t.sstride + o * t.ostride + p * t.pstride] = v;
-}
+__device__ __forceinline__ double tab(const Tab& t, int b, int s, int o, int64_t p) { return tab_get(t, b, s, o, p); }
+__device__ __forceinline__ void tabw(const TabW& t, int b, int s, int o, int64_t p, double v) { tab_put(t, b, s, o, p, v); }
 __device__ __forceinline__ bool act(const uint8_t* m, int64_t p) { return m == nullptr || m[p] != 0; }
 
 // out(p) = sum over (di, dj) in row-major order of A(p)[o] * u(p + o), 0 outside.
@@ -335,9 +331,17 @@ __global__ void __launch_bounds__(NT) k_prolong(Grid g, const uint8_t* __restric
 // exactly as transfer.py:166-198.
 __global__ void __launch_bounds__(NT) k_galerkin(Grid g, Tab A, const uint8_t* __restrict__ mf,
                                                  const uint8_t* __restrict__ mc, TabW Ac,
-                                                 int* __restrict__ ring) {
+                                                 int* __restrict__ ring, const int64_t* __restrict__ pts,
+                                                 int npts) {
   const int rows_c = g.rows / 2, cols_c = g.cols / 2;
-  const int cj = blockIdx.x * BX + threadIdx.x, ci = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+  int cj = blockIdx.x * BX + threadIdx.x, ci = blockIdx.y * BY + threadIdx.y;
+  const int b = blockIdx.z;
+  if (pts) {
+    const int q = blockIdx.x * NT + threadIdx.y * BX + threadIdx.x;
+    if (q >= npts || pts[q] < 0) return;
+    ci = (int)(pts[q] / cols_c);
+    cj = (int)(pts[q] % cols_c);
+  }
   if (ci >= rows_c || cj >= cols_c) return;
   auto fmask = [&](int i, int j) -> double {
     if (i < 0 || i >= g.rows || j < 0 || j >= g.cols) return 0.0;
@@ -526,8 +530,16 @@ __global__ void __launch_bounds__(256) k_lu_solve(int n, const double* __restric
 }
 
 __global__ void __launch_bounds__(NT) k_jacobi(Grid g, Tab A, const uint8_t* __restrict__ mask,
-                                               double omega, TabW K, int* __restrict__ flag) {
-  const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y, b = blockIdx.z;
+                                               double omega, TabW K, int* __restrict__ flag,
+                                               const int64_t* __restrict__ pts, int npts) {
+  int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y;
+  const int b = blockIdx.z;
+  if (pts) {
+    const int q = blockIdx.x * NT + threadIdx.y * BX + threadIdx.x;
+    if (q >= npts || pts[q] < 0) return;
+    i = (int)(pts[q] / g.cols);
+    j = (int)(pts[q] % g.cols);
+  }
   if (i >= g.rows || j >= g.cols) return;
   const int64_t p = (int64_t)i * g.cols + j;
   const double d = tab(A, b, 0, 4, p);
@@ -638,11 +650,12 @@ cudaError_t launch_prolong(const Grid& g, const uint8_t* mask_f, const double* c
 }
 
 cudaError_t launch_galerkin(const Grid& g, Tab A, const uint8_t* mask_f, const uint8_t* mask_c,
-                            TabW Ac, int* ring_flag, cudaStream_t s) {
+                            TabW Ac, int* ring_flag, cudaStream_t s, const int64_t* pts, int npts) {
   ++g_launches;
   const int rows_c = g.rows / 2, cols_c = g.cols / 2;
-  dim3 grid((cols_c + BX - 1) / BX, (rows_c + BY - 1) / BY, g.batch);
-  k_galerkin<<<grid, dim3(BX, BY), 0, s>>>(g, A, mask_f, mask_c, Ac, ring_flag);
+  dim3 grid = pts ? dim3((npts + NT - 1) / NT, 1, g.batch)
+                  : dim3((cols_c + BX - 1) / BX, (rows_c + BY - 1) / BY, g.batch);
+  k_galerkin<<<grid, dim3(BX, BY), 0, s>>>(g, A, mask_f, mask_c, Ac, ring_flag, pts, npts);
   return MGB_DBG(__func__);
 }
 
@@ -693,9 +706,10 @@ cudaError_t launch_lu_solve_vec(int n, const double* lu, const int32_t* perm, co
 }
 
 cudaError_t launch_jacobi(const Grid& g, Tab A, const uint8_t* mask, double omega, TabW K,
-                          int* zero_diag_flag, cudaStream_t s) {
+                          int* zero_diag_flag, cudaStream_t s, const int64_t* pts, int npts) {
   ++g_launches;
-  k_jacobi<<<pgrid(g), dim3(BX, BY), 0, s>>>(g, A, mask, omega, K, zero_diag_flag);
+  const dim3 grid = pts ? dim3((npts + NT - 1) / NT, 1, g.batch) : pgrid(g);
+  k_jacobi<<<grid, dim3(BX, BY), 0, s>>>(g, A, mask, omega, K, zero_diag_flag, pts, npts);
   return MGB_DBG(__func__);
 }
 

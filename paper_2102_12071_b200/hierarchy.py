@@ -351,6 +351,35 @@ def build_hierarchy_batch(A_batch: np.ndarray, levels: int, spec: GridSpec | Non
     return _build(A_batch, spec, levels, specs, transfers, None, device)
 
 
+def build_hierarchy_classed(rows: int, cols: int, tables, levels: int, spacing: float | None = None,
+                            device: int | None = None) -> MultigridHierarchy:
+    """Constant-coefficient hierarchy held entirely as band-class tables (no
+    per-point planes on any level): memory is O(grid functions), so config 5's
+    32767^2 fits one GPU.  `tables` is one 3x3 stencil (a constant_stencil,
+    grid.py:209), or (25, 3, 3) band-class tables, or (batch, 25, 3, 3); band
+    classes are band(i) * 5 + band(j) with band = 0, 1 for the first two
+    rows/cols, 2 inside, 3, 4 for the last two.  Results equal build_hierarchy
+    on the expanded per-point operator."""
+    t = np.asarray(tables, dtype=float)
+    if t.shape == (3, 3):
+        t = np.broadcast_to(t, (1, 25, 3, 3))
+    elif t.shape == (25, 3, 3):
+        t = t[None]
+    if t.ndim != 4 or t.shape[1:] != (25, 3, 3):
+        raise ContractError("band-class tables must be (3, 3), (25, 3, 3) or (batch, 25, 3, 3)")
+    t = np.ascontiguousarray(t)
+    if levels < 2:
+        raise ConfigError("a hierarchy needs at least two levels")
+    spec = GridSpec(rows, cols, 1.0 / (rows + 1) if spacing is None else spacing, np.ones((rows, cols), bool))
+    specs, transfers = _level_specs(spec, levels)
+    dev = dv.current_device() if device is None else device
+    dv.require_cuda(dev)
+    h = C.c_void_p()
+    _lib.call("mgb_hier_build_classed", dev, t.shape[0], rows, cols, float(spec.spacing), t.ctypes.data_as(_lib.P),
+              int(levels), None, C.byref(h))
+    return MultigridHierarchy(h, dev, t.shape[0], specs, transfers, None)
+
+
 def _build(A_host, spec, levels, specs, transfers, A0, device):
     dev = dv.current_device() if device is None else device
     dv.require_cuda(dev)

@@ -375,3 +375,28 @@ def test_fused_and_separate_passes_agree(name):
         h2 = dv.host(h.run_cycles(f, u2, c["cycles"], c["nu"], c["nu"], u_zero=True))[0]
         assert_hist(h1, h2)
         assert rel_err(dv.host(u1), dv.host(u2)) <= 1e-12
+
+
+@pytest.mark.parametrize("n,cols,variant,nu", [(255, 255, "conv", 2), (127, 127, "fc", 1), (20, 27, "conv", 1),
+                                               (64, 48, "jacobi", 2)])
+def test_classed_only_hierarchy_matches_per_point_build(n, cols, variant, nu):
+    """A hierarchy held only as band-class tables equals the per-point build:
+    operators and kernels on every level, and the cycle histories, bitwise."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    A = gen.rotated_fd(n, 0.9, 0.02, cols=cols)
+    levels = gen.levels_for(min(n, cols))
+    h1 = mg.build_hierarchy(mg.StencilField(mg.GridSpec(n, cols, 1.0 / (n + 1), np.ones((n, cols), bool)), A),
+                            levels)
+    h2 = mg.build_hierarchy_classed(n, cols, A[0, 0], levels)
+    for l in range(h1.depth):
+        assert np.array_equal(h1.operator_batch(l), h2.operator_batch(l)), l
+    _equip(h1, variant)
+    _equip(h2, variant)
+    for l in range(h1.depth - 1):
+        assert np.array_equal(h1.kernels_batch(l), h2.kernels_batch(l)), l
+    f = dv.to_dev(gen.uniform_rhs(n, 7, cols=cols))
+    u1, u2 = dv.zeros(f.shape), dv.zeros(f.shape)
+    a = h1.run_cycles(f, u1, 5, nu, nu, u_zero=True).clone()
+    b = h2.run_cycles(f, u2, 5, nu, nu, u_zero=True).clone()
+    assert t.equal(u1, u2) and t.equal(a, b)
