@@ -48,6 +48,9 @@ CONFIGS = {
                desc="-div(exp(GRF) grad u), 5-point cell-centred, corr. length 1/32, per-point tables"),
     "c4": dict(n=511, op="batch", levels=8, nu=1, cycles=10, seed=3, batch=256, net="net_conv.json",
                desc="256 rotated FD problems, log-uniform eps in [1e-3,1], theta ~ U[0,pi)"),
+    "c5": dict(n=32767, op="rot_classed", theta=math.pi / 3, eps=0.01, levels=14, nu=2, cycles=10, seed=5, batch=1,
+               net="net_conv_c5.json",
+               desc="rotated FD eps=0.01 theta=pi/3, band-class hierarchy (no per-point tables)"),
 }
 CPU_SAMPLE_N = 1023                  # bounded CPU sample: same operator family at <= 1023^2
 
@@ -145,6 +148,8 @@ def operators(cfg, lo=0, hi=None):
     """Host inputs of a config: (A (batch, n, n, 3, 3), f (batch, n, n)) for problems [lo, hi)."""
     from paper_2102_12071_b200 import problems as gen
     n = cfg["n"]
+    if cfg["op"] == "rot_classed":
+        return gen.rotated_fd(1, cfg["theta"], cfg["eps"], h=1.0 / (n + 1))[0, 0], gen.uniform_rhs(n, cfg["seed"])[None]
     if cfg["op"] == "rot":
         return gen.rotated_fd(n, cfg["theta"], cfg["eps"])[None], gen.uniform_rhs(n, cfg["seed"])[None]
     if cfg["op"] == "grf":
@@ -168,7 +173,9 @@ def build_problem(cfg_name, device, lo=0, hi=None):
     net = mg.load_model(os.path.join(ROOT, "paper_2102_12071_b200", "data", cfg["net"]))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    if cfg["batch"] == 1:
+    if cfg["op"] == "rot_classed":
+        h = mg.build_hierarchy_classed(n, n, A, cfg["levels"], device=device)
+    elif cfg["batch"] == 1:
         spec = mg.GridSpec(n, n, 1.0 / n if cfg["op"] == "grf" else 1.0 / (n + 1), np.ones((n, n), bool))
         h = mg.build_hierarchy(mg.StencilField(spec, A[0]), cfg["levels"], device=device)
     else:
@@ -194,7 +201,7 @@ def cpu_sample(cfg_name, steps=1, warmup=0):
     n = min(cfg["n"], CPU_SAMPLE_N)
     levels = gen.levels_for(n)
     nu = cfg["nu"]
-    if cfg["op"] == "rot":
+    if cfg["op"] in ("rot", "rot_classed"):
         A, f = gen.rotated_fd(n, cfg["theta"], cfg["eps"]), gen.uniform_rhs(n, cfg["seed"])
     elif cfg["op"] == "grf":
         A, f = gen.grf_diffusion_5pt(n, seed=cfg["seed"]), gen.uniform_rhs(n, cfg["seed"])

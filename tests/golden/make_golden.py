@@ -65,6 +65,14 @@ def make_nets():
         net, _, _ = rtr.train_inference_net(A31c2, "conv", 4, cfg, k=1, seed_net=0)
         rs.save_model(path, net, {"fixture": "SURVEY G4 recipe at config-2 parameters"})
     out["conv_c2"] = rs.load_model(path)
+    # config 5 parameters (theta = pi/3, anisotropy = 0.01)
+    path = os.path.join(HERE, "net_conv_c5.json")
+    if not os.path.exists(path):
+        A31c5 = rp.assemble_rotated_laplacian(rg.full_spec(31), math.pi / 3, 0.01)
+        cfg = rtr.TrainConfig(samples=10, max_steps=2, batch_size=5, epochs=20, seed=0)
+        net, _, _ = rtr.train_inference_net(A31c5, "conv", 4, cfg, k=1, seed_net=0)
+        rs.save_model(path, net, {"fixture": "SURVEY G4 recipe at config-5 parameters"})
+    out["conv_c5"] = rs.load_model(path)
     # config 3 (GRF diffusion, 5-point): the recipe on a seeded 31^2 GRF (corr. length 1/4)
     path = os.path.join(HERE, "net_conv_c3.json")
     if not os.path.exists(path):
