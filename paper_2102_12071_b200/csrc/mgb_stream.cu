@@ -375,22 +375,14 @@ static int choose_seg(const Grid& g, int nsw, bool res, int occ) {
     if (sms <= 0) sms = 148;
   }
   const int64_t slots = (int64_t)sms * std::max(occ, 1);
-  const int fill = 3 * S + 3;
-  int best = g.rows + (g.rows & 1);
+  int best = 256;
   double best_t = 1e300;
-  // k segments per strip: every CTA costs (segment + pipeline fill) row steps and a
-  // partial last wave costs a full CTA time
-  for (int k = 1; k <= 1024; ++k) {
-    int seg = (g.rows + k - 1) / k;
-    seg += seg & 1;  // even: coarse anchors 2c+1 never straddle segments
-    if (seg < 16 && k > 1) break;
+  for (int seg = 512; seg >= 16; seg /= 2) {
     const int64_t ctas = strips * ((g.rows + seg - 1) / seg) * g.batch;
     const int64_t waves = (ctas + slots - 1) / slots;
-    const double t = (double)waves * (seg + fill) + 1e-6 * seg;
-    if (t < best_t) {
-      best_t = t;
-      best = seg;
-    }
+    // a partial last wave still costs a full CTA time; fill = 3S + 3 steps
+    const double t = (double)waves * (seg + 3 * S + 3) + 1e-3 * seg;
+    if (t < best_t) { best_t = t; best = seg; }
   }
   return best;
 }
