@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   c.owned_c = c.tid >= H && c.tid < H + WOUT && c.cin;
   c.ccls = c.cin ? bandc(c.col, g.cols) : 2;     // out-of-grid columns are zeroed anyway
   c.cjb = ((c.j0 - H) >> 1) - 1;
-  c.R0 = blockIdx.y * a.seg;
-  c.R1 = min(g.rows, c.R0 + a.seg);
+  c.R0 = a.own0 + blockIdx.y * a.seg;
+  c.R1 = min(a.own1 > 0 ? a.own1 : g.rows, c.R0 + a.seg);
   c.fb = a.f + c.b * n;
   c.ub = ZU ? nullptr : a.u + c.b * n;
   c.uob = a.uo + c.b * n;
@@ -291,8 +291,12 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   const double* pf = c.fb + (int64_t)prow * cstride + c.col;
   const int rows_c = g.rows / 2, cols_c = g.cols / 2;
   const double* ecb = PRO ? a.ec + c.b * (int64_t)rows_c * cols_c : nullptr;
+  // rows the owned outputs depend on (a ghost band of S + 1 rows each side); rows
+  // outside are never read, so domain-decomposed blocks need only S + 1 ghost rows
+  const int lo_row = max(0, c.R0 - S - 1), hi_row = min(g.rows - 1, c.R1 + S);
+  const int lo_c = (lo_row - 2) >> 1, hi_c = (hi_row >> 1) + 1;
   auto issue = [&]() {
-    const bool rv = (unsigned)prow < (unsigned)g.rows && c.cin;
+    const bool rv = prow >= lo_row && prow <= hi_row && c.cin;
     if (!ZU) cp_async8(&c.ring_u[(prow & (PD - 1)) * SWT + c.tid], rv ? pu : c.ub, rv);
     cp_async8(&c.ring_f[(prow & (PDF - 1)) * SWT + c.tid], rv ? pf : c.fb, rv);
     if (PRO && !(prow & 1) && c.tid < EW) {
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
       // group of fine row 2ci - 2 so every thread's copy is complete and published by
       // the barrier of step 2ci - 2.  Out-of-range coarse points read as zero.
       const int ci = (prow >> 1) + 1, cj = c.cjb + c.tid;
-      const bool ev = ci >= 0 && ci < rows_c && cj >= 0 && cj < cols_c;
+      const bool ev = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c && cj >= 0 && cj < cols_c;
       cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + c.tid], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
     }
     cp_commit();
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
     for (int ci = (t0 >> 1) - 1; ci <= (t0 >> 1) + 1; ++ci) {
       const int cj = c.cjb + c.tid;
       if (c.tid < EW) {
-        const bool ev = ci >= 0 && ci < rows_c && cj >= 0 && cj < cols_c;
+        const bool ev = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c && cj >= 0 && cj < cols_c;
         cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + c.tid], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
       }
     }
@@ -402,9 +406,15 @@ static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks)
     occ_cache.push_back({(const void*)kern, occ});
   }
   static const int force_seg = getenv("MGB_SEG") ? atoi(getenv("MGB_SEG")) : 0;  // experiments only
-  a.seg = force_seg > 0 ? force_seg : choose_seg(a.g, nsw, res, occ);
+  if (a.own1 <= 0) {
+    a.own0 = 0;
+    a.own1 = a.g.rows;
+  }
+  Grid go = a.g;
+  go.rows = a.own1 - a.own0;
+  a.seg = force_seg > 0 ? force_seg : choose_seg(go, nsw, res, occ);
   const int H = 2 * nsw + 2, wout = SWT - 2 * H;
-  const dim3 grid((a.g.cols + wout - 1) / wout, (a.g.rows + a.seg - 1) / a.seg, a.g.batch);
+  const dim3 grid((a.g.cols + wout - 1) / wout, (go.rows + a.seg - 1) / a.seg, a.g.batch);
   if (nblocks) *nblocks = (int)(grid.x * grid.y);
   kern<<<grid, SWT, smem, a.stream>>>(a);
   return MGB_DBG(__func__);

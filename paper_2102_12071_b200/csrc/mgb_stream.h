@@ -17,6 +17,10 @@ struct StreamArgs {
   double* rc;              // restricted residual (PRE)
   double* partials;        // per-CTA sums of the input residual squared (history)
   int seg;                 // rows per CTA segment (set by the launcher)
+  int own0, own1;          // owned global rows [own0, own1) (own1 == 0: the whole grid).  Rows
+                           // own0 - 6 .. own1 + 5 of u, f (and the matching coarse rows of ec)
+                           // must be addressable: with domain decomposition the arrays are
+                           // ghosted row blocks passed as pointers pre-offset to global rows.
   int ci_valid;            // 1: ci holds the interior-class weights (batch == 1, classed A and M)
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
   cudaStream_t stream;
