@@ -218,6 +218,31 @@ int mgb_solve(const mgb_hier* h, mgb_work* w, const double* f_dev, double* u_dev
 int mgb_time_pass(const mgb_hier* h, mgb_work* w, int level, int pass, int nu, const double* f_dev,
                   double* u_dev, int reps, double* ms, void* stream);
 
+/* ---- domain decomposition ------------------------------------------
+   The fine levels of a band-class hierarchy (mgb_hier_build_classed) split into
+   `nparts` row blocks; every streaming pass runs on a block with 6 ghost rows per
+   edge, refreshed by a halo exchange before each pass; levels with at most
+   `agglomerate_rows` rows are solved redundantly on every part after an
+   all-gather of the restricted residual.  Two layouts:
+     virtual: nlocal == nparts, first_part = 0 — all parts on this GPU, halos by
+              device copies (single-GPU test of the decomposition);
+     NCCL:    nlocal == 1, first_part = rank — one part per process, halos by grouped
+              ncclSend/ncclRecv, agglomeration by ncclAllGather, history norms by an
+              8-byte ncclAllReduce; nccl_id from mgb_dd_nccl_unique_id on rank 0.
+   The hierarchy must be built identically on every rank. */
+typedef struct mgb_dd mgb_dd;
+int  mgb_dd_nccl_unique_id(void* id_out /* 128 bytes */);
+int  mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int nlocal, const void* nccl_id,
+                   int agglomerate_rows, mgb_dd** out);
+void mgb_dd_destroy(mgb_dd* d);
+/* level-0 rows [r0, r1) owned by `part`; number of distributed levels */
+int  mgb_dd_info(const mgb_dd* d, int part, int* r0, int* r1, int* dist_levels);
+int  mgb_dd_set_rhs(mgb_dd* d, int part, const double* f_owned_dev, void* stream);
+int  mgb_dd_get_solution(const mgb_dd* d, int part, double* u_owned_dev, void* stream);
+/* fixed-count V(nu1, nu2) cycles of the decomposed solve (graph-replayed); history_dev
+   (cycles + 1) as mgb_run_cycles, identical on every rank. */
+int  mgb_dd_run_cycles(mgb_dd* d, int nu1, int nu2, int cycles, int u_zero, double* history_dev, void* stream);
+
 /* instrumentation for bench.py: number of kernel launches issued by the last
    mgb_run_cycles / mgb_vcycle call (graph replays count their nodes). */
 int64_t mgb_last_launch_count(const mgb_work* w);

@@ -65,6 +65,13 @@ SIGNATURES = {
     "mgb_run_cycles": (I, [P, P, P, P, I, I, I, I, P, P]),
     "mgb_run_cycles_host": (I, [P, P, P, P, I, I, I, I, P, P]),
     "mgb_solve": (I, [P, P, P, P, I, I, D, I, PD, PI, PI, PI, PD, P]),
+    "mgb_dd_nccl_unique_id": (I, [P]),
+    "mgb_dd_create": (I, [P, I, I, I, P, I, C.POINTER(P)]),
+    "mgb_dd_destroy": (None, [P]),
+    "mgb_dd_info": (I, [P, I, PI, PI, PI]),
+    "mgb_dd_set_rhs": (I, [P, I, P, P]),
+    "mgb_dd_get_solution": (I, [P, I, P, P]),
+    "mgb_dd_run_cycles": (I, [P, I, I, I, I, P, P]),
     "mgb_time_pass": (I, [P, P, I, I, I, P, P, I, PD, P]),
     "mgb_last_launch_count": (I64, [P]),
 }

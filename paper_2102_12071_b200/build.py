@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmgb.so")
-SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_coarse.cu", "mgb_cnn.cu", "mgb_api.cu"]
+SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_coarse.cu", "mgb_dd.cu", "mgb_cnn.cu", "mgb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -38,7 +38,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "mgb_internal.h"), os.path.join(CSRC, "mgb_cycle.h"), os.path.join(CSRC, "mgb_stream.h"), os.path.join(CSRC, "mgb_coarse.h"),
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "mgb_internal.h"), os.path.join(CSRC, "mgb_cycle.h"), os.path.join(CSRC, "mgb_stream.h"), os.path.join(CSRC, "mgb_coarse.h"), os.path.join(CSRC, "mgb_dd.h"),
                                                         os.path.join(ROOT, "include", "mgb.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

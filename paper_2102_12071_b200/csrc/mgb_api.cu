@@ -15,6 +15,7 @@
 #include "mgb_cycle.h"
 #include "mgb_stream.h"
 #include "mgb_coarse.h"
+#include "mgb_dd.h"
 #include "mgb_internal.h"
 
 namespace mgb {
@@ -34,30 +35,6 @@ int fail(int status, const std::string& msg) {
 int cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " + what;
   return MGB_CUDA;
-}
-
-struct DeviceGuard {
-  int prev = -1;
-  bool ok = true;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-template <typename T>
-static cudaError_t dalloc(T** p, size_t count) {
-  *p = nullptr;
-  if (count == 0) return cudaSuccess;
-  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
-}
-template <typename T>
-static void dfree(T*& p) {
-  if (p) cudaFree(p);
-  p = nullptr;
 }
 
 }  // namespace mgb
@@ -943,7 +920,8 @@ extern "C" int mgb_prolong_correct(const mgb_hier* h, int level, const double* e
 // ---------------------------------------------------------------------------
 // workspace + cycle driver
 
-extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
+// workspace for cycles starting at level `first` (levels below it get no buffers)
+int mgb::work_create_from(const mgb_hier* h, int first, mgb_work** out) {
   if (!h || !out) return fail(MGB_CONTRACT, "null argument");
   *out = nullptr;
   DeviceGuard dg(h->device);
@@ -955,7 +933,7 @@ extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
   w->f.assign(L, nullptr);
   w->r.assign(L, nullptr);
   w->v.assign(L, nullptr);
-  for (int l = 0; l < L; ++l) {
+  for (int l = first; l < L; ++l) {
     const size_t cnt = (size_t)h->batch * h->lv[l].n;
     if (l > 0) {
       MGB_CUDA_TRY(dalloc(&w->u[l], cnt));
@@ -963,8 +941,9 @@ extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
     }
     if (l + 1 < L) MGB_CUDA_TRY(dalloc(&w->t[l], cnt));
   }
-  w->max_nblk = std::max(std::max(residual_blocks(h->grid(0)), resnorm_blocks(h->grid(0))),
-                         std::max(sweep_blocks(h->grid(0)), stream_max_blocks(h->grid(0))));
+  const Grid g0 = h->grid(first);
+  w->max_nblk = std::max(std::max(residual_blocks(g0), resnorm_blocks(g0)),
+                         std::max(sweep_blocks(g0), stream_max_blocks(g0)));
   MGB_CUDA_TRY(dalloc(&w->partials, (size_t)w->max_nblk * h->batch));
   MGB_CUDA_TRY(dalloc(&w->fnorm2, (size_t)h->batch));
   MGB_CUDA_TRY(dalloc(&w->scratch, (size_t)h->batch * 4));
@@ -972,6 +951,8 @@ extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) {
   *out = w.release();
   return MGB_OK;
 }
+
+extern "C" int mgb_work_create(const mgb_hier* h, mgb_work** out) { return work_create_from(h, 0, out); }
 
 extern "C" void mgb_work_destroy(mgb_work* w) { delete w; }
 
@@ -1517,3 +1498,32 @@ extern "C" int mgb_time_pass(const mgb_hier* h, mgb_work* w, int level, int pass
   if (ms) *ms = (double)t / reps;
   return st;
 }
+
+// ---- accessors used by the domain-decomposition driver (mgb_dd.cu) ------------
+namespace mgb {
+int hier_rows(const mgb_hier* h, int l) { return h->lv[l].rows; }
+int hier_cols(const mgb_hier* h, int l) { return h->lv[l].cols; }
+int hier_batch(const mgb_hier* h) { return h->batch; }
+int hier_depth(const mgb_hier* h) { return h->depth(); }
+int hier_device(const mgb_hier* h) { return h->device; }
+int hier_level_ks(const mgb_hier* h, int l) { return h->lv[l].ks; }
+bool hier_level_classed(const mgb_hier* h, int l) { return h->lv[l].Acls && h->lv[l].Kcls && !h->lv[l].mask; }
+Grid hier_grid(const mgb_hier* h, int l) { return h->grid(l); }
+Op hier_opA(const mgb_hier* h, int l) { return h->lv[l].opA(); }
+Op hier_opK(const mgb_hier* h, int l) { return h->lv[l].opK(); }
+void hier_interior(const mgb_hier* h, int l, int* valid, double* ci) {
+  const LevelD& lv = h->lv[l];
+  *valid = h->batch == 1 && lv.Acls && lv.Kcls;
+  for (int o = 0; o < 9; ++o) {
+    ci[o] = lv.hAint[o];
+    ci[9 + o] = lv.hKint[o];
+  }
+}
+double* work_level_u(mgb_work* w, int l) { return w->u[l]; }
+double* work_level_f(mgb_work* w, int l) { return w->f[l]; }
+int work_prepare(mgb_work* w) { return prepare_work(w); }
+int work_vcycle_level(mgb_work* w, int l, const double* f, double* u, bool zero, int nu1, int nu2, cudaStream_t s,
+                      double** result) {
+  return vcycle_rec(w, l, f, u, zero, nu1, nu2, s, result);
+}
+}  // namespace mgb

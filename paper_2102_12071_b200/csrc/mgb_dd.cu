@@ -1,0 +1,503 @@
+// Domain-decomposed V-cycle: the fine levels are split into row
+// blocks ("parts"), one per GPU; every pass is the same row-streaming kernel run
+// on a ghosted block (pointers pre-offset to global rows, owned range
+// [R0, R1)), preceded by a halo exchange of the S + 1 = 6 rows it reads across
+// each block edge.  Below the agglomeration level the restricted residual is
+// all-gathered and every rank runs the coarse cycle redundantly (no idle ranks,
+// no scatter), then prolongs from its rows of the replicated correction.
+//
+// Exchange backends:
+//  * NCCL (one part per process): grouped ncclSend/ncclRecv of contiguous ghost
+//    row blocks on the solve stream, ncclAllGather for agglomeration,
+//    ncclAllReduce of the 8-byte history partial sums — all graph-capturable;
+//  * virtual (all parts in one process on one GPU): the same schedule with
+//    device-to-device copies; used to test the decomposition on a single B200.
+// Per-point results are independent of the partition (every point runs the
+// same operation sequence), so u matches the single-domain solve bitwise; only
+// the history norms are summed in a different order.
+//
+// NCCL is loaded at run time (dlopen of the libnccl.so.2 the process already has,
+// e.g. PyTorch's), so the library has no link-time NCCL dependency.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mgb_dd.h"
+
+namespace mgb {
+
+// ---- minimal NCCL binding (types from the public ABI of nccl.h) -------------
+namespace nccl {
+typedef struct ncclComm* Comm;
+struct UniqueId { char internal[128]; };
+enum Result { Success = 0 };
+enum DataType { Float64 = 8 };
+enum RedOp { Sum = 0 };
+typedef Result (*CommInitRank_t)(Comm*, int, UniqueId, int);
+typedef Result (*CommDestroy_t)(Comm);
+typedef Result (*Send_t)(const void*, size_t, DataType, int, Comm, cudaStream_t);
+typedef Result (*Recv_t)(void*, size_t, DataType, int, Comm, cudaStream_t);
+typedef Result (*AllReduce_t)(const void*, void*, size_t, DataType, RedOp, Comm, cudaStream_t);
+typedef Result (*AllGather_t)(const void*, void*, size_t, DataType, Comm, cudaStream_t);
+typedef Result (*Group_t)();
+typedef Result (*GetUniqueId_t)(UniqueId*);
+typedef const char* (*GetErrorString_t)(Result);
+struct Api {
+  CommInitRank_t CommInitRank = nullptr;
+  CommDestroy_t CommDestroy = nullptr;
+  Send_t Send = nullptr;
+  Recv_t Recv = nullptr;
+  AllReduce_t AllReduce = nullptr;
+  AllGather_t AllGather = nullptr;
+  Group_t GroupStart = nullptr, GroupEnd = nullptr;
+  GetUniqueId_t GetUniqueId = nullptr;
+  GetErrorString_t GetErrorString = nullptr;
+  bool ok = false;
+};
+static Api& api() {
+  static Api a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  void* hdl = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!hdl) hdl = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!hdl) hdl = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!hdl) return a;
+  a.CommInitRank = (CommInitRank_t)dlsym(hdl, "ncclCommInitRank");
+  a.CommDestroy = (CommDestroy_t)dlsym(hdl, "ncclCommDestroy");
+  a.Send = (Send_t)dlsym(hdl, "ncclSend");
+  a.Recv = (Recv_t)dlsym(hdl, "ncclRecv");
+  a.AllReduce = (AllReduce_t)dlsym(hdl, "ncclAllReduce");
+  a.AllGather = (AllGather_t)dlsym(hdl, "ncclAllGather");
+  a.GroupStart = (Group_t)dlsym(hdl, "ncclGroupStart");
+  a.GroupEnd = (Group_t)dlsym(hdl, "ncclGroupEnd");
+  a.GetUniqueId = (GetUniqueId_t)dlsym(hdl, "ncclGetUniqueId");
+  a.GetErrorString = (GetErrorString_t)dlsym(hdl, "ncclGetErrorString");
+  a.ok = a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.AllReduce && a.AllGather && a.GroupStart &&
+         a.GroupEnd && a.GetUniqueId;
+  return a;
+}
+}  // namespace nccl
+
+#define MGB_NCCL_TRY(expr)                                                                   \
+  do {                                                                                      \
+    nccl::Result _r = (expr);                                                               \
+    if (_r != nccl::Success) {                                                              \
+      const char* m = nccl::api().GetErrorString ? nccl::api().GetErrorString(_r) : "?";   \
+      return fail(MGB_NCCL, std::string("NCCL error in " #expr ": ") + m);                 \
+    }                                                                                       \
+  } while (0)
+
+namespace {
+
+__global__ void k_sum_norm(const double* __restrict__ parts, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < n; ++q) s += parts[q];
+    *out = s;
+  }
+}
+
+__global__ void k_hist_entry(const double* __restrict__ r2, const double* __restrict__ f2,
+                             double* __restrict__ hist) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double nr = sqrt(*r2), fn = sqrt(*f2);
+    const double den = fn > 0.0 ? fn : 1.0;      // hierarchy.py:126-127
+    *hist = nr == 0.0 ? 0.0 : nr / den;           // hierarchy.py:129-131
+  }
+}
+
+}  // namespace
+}  // namespace mgb
+
+using namespace mgb;
+
+struct DDPart {
+  int part = 0;
+  std::vector<int> R0, R1;       // owned rows per distributed level
+  std::vector<double*> u, t, f;  // ghosted blocks: rows [R0 - G, R1 + G) x cols
+  double* partials = nullptr;
+  double* norm2 = nullptr;       // per-part sum of squares (device scalar)
+};
+
+struct mgb_dd {
+  const mgb_hier* h = nullptr;
+  int device = 0, nparts = 1, first = 0, nlocal = 1, Ld = 0, La = 0, cols0 = 0;
+  std::vector<DDPart> parts;
+  mgb_work* cw = nullptr;        // replicated coarse levels (>= La)
+  double* gather = nullptr;      // padded all-gather target for the agglomerated residual
+  int Bc = 0;                    // coarse rows per part in the gather layout
+  double* norm_parts = nullptr;  // nlocal doubles
+  double* r2 = nullptr;          // total residual^2 (device scalar)
+  double* f2 = nullptr;          // total ||f||^2
+  double* hist_scratch = nullptr;
+  nccl::Comm comm = nullptr;
+  cudaStream_t cap = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int gkey[4] = {-1, -1, -1, -1};
+  double* ghist = nullptr;
+  int max_blocks = 0;
+  ~mgb_dd() {
+    DeviceGuard dg(device);
+    if (graph) cudaGraphExecDestroy(graph);
+    for (auto& p : parts) {
+      for (auto* v : {&p.u, &p.t, &p.f})
+        for (auto*& q : *v) dfree(q);
+      dfree(p.partials);
+      dfree(p.norm2);
+    }
+    dfree(gather);
+    dfree(norm_parts);
+    dfree(r2);
+    dfree(f2);
+    dfree(hist_scratch);
+    if (cw) mgb_work_destroy(cw);
+    if (comm && nccl::api().ok) nccl::api().CommDestroy(comm);
+    if (cap) cudaStreamDestroy(cap);
+  }
+  int rows(int l) const { return hier_rows(h, l); }
+  int cols(int l) const { return hier_cols(h, l); }
+  // pointer to global row 0 of a ghosted block whose first stored row is R0 - G
+  static double* gview(double* blk, int R0, int cols) { return blk - (int64_t)(R0 - DD_GHOST) * cols; }
+};
+
+static constexpr int G = DD_GHOST;
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" int mgb_dd_nccl_unique_id(void* id_out) {
+  if (!nccl::api().ok) return fail(MGB_NCCL, "libnccl.so.2 not available");
+  nccl::UniqueId id;
+  MGB_NCCL_TRY(nccl::api().GetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof(id));
+  return MGB_OK;
+}
+
+extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int nlocal, const void* nccl_id,
+                             int agglomerate_rows, mgb_dd** out) {
+  if (!h || !out) return fail(MGB_CONTRACT, "null argument");
+  *out = nullptr;
+  if (nparts < 1 || nlocal < 1 || first_part < 0 || first_part + nlocal > nparts)
+    return fail(MGB_CONFIG, "invalid part layout");
+  if (nlocal != nparts && nlocal != 1) return fail(MGB_CONFIG, "either all parts local (virtual) or one per rank");
+  if (nlocal == 1 && nparts > 1 && !nccl_id) return fail(MGB_CONFIG, "multi-rank decomposition needs an NCCL id");
+  if (hier_batch(h) != 1) return fail(MGB_CONFIG, "domain decomposition takes a single problem");
+  const int L = hier_depth(h);
+  for (int l = 0; l + 1 < L; ++l)
+    if (hier_level_ks(h, l) != 1 || !hier_level_classed(h, l))
+      return fail(MGB_CONFIG, "domain decomposition needs band-class (constant-coefficient) levels with 1-stage smoothers");
+  DeviceGuard dg(hier_device(h));
+  std::unique_ptr<mgb_dd> d(new mgb_dd());
+  d->h = h;
+  d->device = hier_device(h);
+  d->nparts = nparts;
+  d->first = first_part;
+  d->nlocal = nlocal;
+  d->cols0 = d->cols(0);
+  // distributed levels: rows > agglomerate_rows, at least one, coarse cycle needs >= 2 levels below
+  int Ld = 0;
+  while (Ld + 2 < L && d->rows(Ld) > agglomerate_rows) ++Ld;
+  if (Ld == 0) Ld = 1;
+  d->Ld = Ld;
+  d->La = Ld;
+  // level-0 blocks: multiples of 2^Ld so every distributed level's block start is even
+  const int align = 1 << Ld;
+  const int rows0 = d->rows(0);
+  int blk = (rows0 + nparts - 1) / nparts;
+  blk = (blk + align - 1) / align * align;
+  for (int p = 0; p < nparts; ++p) {
+    const int r0 = std::min(p * blk, rows0), r1 = std::min((p + 1) * blk, rows0);
+    if (r1 - r0 < 2 * G * align) return fail(MGB_CONFIG, "too many parts for this grid (blocks smaller than the halo)");
+  }
+  d->Bc = blk >> Ld;
+  for (int q = 0; q < nlocal; ++q) {
+    DDPart P;
+    P.part = first_part + q;
+    for (int l = 0; l < Ld; ++l) {
+      const int r0 = std::min(P.part * blk, rows0) >> l;
+      const int r1 = P.part == nparts - 1 ? d->rows(l) : (std::min((P.part + 1) * blk, rows0) >> l);
+      P.R0.push_back(r0);
+      P.R1.push_back(r1);
+      const size_t cnt = (size_t)(r1 - r0 + 2 * G) * d->cols(l);
+      double *a = nullptr, *b = nullptr, *c = nullptr;
+      MGB_CUDA_TRY(dalloc(&a, cnt));
+      MGB_CUDA_TRY(dalloc(&b, cnt));
+      MGB_CUDA_TRY(dalloc(&c, cnt));
+      MGB_CUDA_TRY(cudaMemset(a, 0, cnt * sizeof(double)));
+      MGB_CUDA_TRY(cudaMemset(b, 0, cnt * sizeof(double)));
+      MGB_CUDA_TRY(cudaMemset(c, 0, cnt * sizeof(double)));
+      P.u.push_back(a);
+      P.t.push_back(b);
+      P.f.push_back(c);
+    }
+    d->parts.push_back(std::move(P));
+  }
+  d->max_blocks = stream_max_blocks(hier_grid(h, 0));
+  for (auto& P : d->parts) {
+    MGB_CUDA_TRY(dalloc(&P.partials, (size_t)d->max_blocks));
+    MGB_CUDA_TRY(dalloc(&P.norm2, 1));
+  }
+  MGB_CUDA_TRY(dalloc(&d->norm_parts, (size_t)nlocal));
+  MGB_CUDA_TRY(dalloc(&d->r2, 1));
+  MGB_CUDA_TRY(dalloc(&d->f2, 1));
+  MGB_CUDA_TRY(dalloc(&d->hist_scratch, 1));
+  // replicated coarse workspace from the agglomeration level + padded gather buffer
+  if (int st = work_create_from(h, d->La, &d->cw)) return st;
+  MGB_CUDA_TRY(dalloc(&d->gather, (size_t)nparts * d->Bc * d->cols(d->La)));
+  MGB_CUDA_TRY(cudaMemset(d->gather, 0, sizeof(double) * nparts * d->Bc * d->cols(d->La)));
+  MGB_CUDA_TRY(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
+  if (nlocal == 1 && nparts > 1) {
+    if (!nccl::api().ok) return fail(MGB_NCCL, "libnccl.so.2 not available");
+    nccl::UniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    MGB_NCCL_TRY(nccl::api().CommInitRank(&d->comm, nparts, id, first_part));
+  }
+  *out = d.release();
+  return MGB_OK;
+}
+
+extern "C" void mgb_dd_destroy(mgb_dd* d) { delete d; }
+
+extern "C" int mgb_dd_info(const mgb_dd* d, int part, int* r0, int* r1, int* dist_levels) {
+  if (!d) return fail(MGB_CONTRACT, "null decomposition");
+  const int q = part - d->first;
+  if (q < 0 || q >= d->nlocal) return fail(MGB_CONFIG, "part not held by this process");
+  if (r0) *r0 = d->parts[q].R0[0];
+  if (r1) *r1 = d->parts[q].R1[0];
+  if (dist_levels) *dist_levels = d->Ld;
+  return MGB_OK;
+}
+
+// ---- halo exchange of one level's field (ghost rows [R0-G, R0) and [R1, R1+G)) ----
+// which: 0 = u, 1 = t, 2 = f
+static int exchange(mgb_dd* d, int l, int which, cudaStream_t s) {
+  const int cols = d->cols(l), rows = d->rows(l);
+  auto buf = [&](DDPart& P) -> double* { return which == 0 ? P.u[l] : which == 1 ? P.t[l] : P.f[l]; };
+  const size_t gcount = (size_t)G * cols;
+  if (d->comm == nullptr) {
+    // virtual: all parts local
+    for (int q = 0; q < d->nlocal; ++q) {
+      DDPart& P = d->parts[q];
+      double* v = mgb_dd::gview(buf(P), P.R0[l], cols);
+      if (q > 0) {
+        DDPart& A = d->parts[q - 1];
+        const double* va = mgb_dd::gview(buf(A), A.R0[l], cols);
+        MGB_CUDA_TRY(cudaMemcpyAsync(v + (int64_t)(P.R0[l] - G) * cols, va + (int64_t)(P.R0[l] - G) * cols,
+                                     gcount * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      }
+      if (q + 1 < d->nlocal) {
+        DDPart& B = d->parts[q + 1];
+        const double* vb = mgb_dd::gview(buf(B), B.R0[l], cols);
+        const int n = std::min(G, rows - P.R1[l]);
+        MGB_CUDA_TRY(cudaMemcpyAsync(v + (int64_t)P.R1[l] * cols, vb + (int64_t)P.R1[l] * cols,
+                                     (size_t)n * cols * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    return MGB_OK;
+  }
+  auto& A = nccl::api();
+  DDPart& P = d->parts[0];
+  double* v = mgb_dd::gview(buf(P), P.R0[l], cols);
+  const int me = P.part;
+  MGB_NCCL_TRY(A.GroupStart());
+  if (me > 0) {
+    MGB_NCCL_TRY(A.Send(v + (int64_t)P.R0[l] * cols, gcount, nccl::Float64, me - 1, d->comm, s));
+    MGB_NCCL_TRY(A.Recv(v + (int64_t)(P.R0[l] - G) * cols, gcount, nccl::Float64, me - 1, d->comm, s));
+  }
+  if (me + 1 < d->nparts) {
+    const int nb = std::min(G, rows - P.R1[l]);
+    MGB_NCCL_TRY(A.Send(v + (int64_t)(P.R1[l] - nb) * cols, (size_t)nb * cols, nccl::Float64, me + 1, d->comm, s));
+    MGB_NCCL_TRY(A.Recv(v + (int64_t)P.R1[l] * cols, (size_t)nb * cols, nccl::Float64, me + 1, d->comm, s));
+  }
+  MGB_NCCL_TRY(A.GroupEnd());
+  return MGB_OK;
+}
+
+// sum the per-part sums of squares into *dst (all ranks)
+static int reduce_norm(mgb_dd* d, double* dst, cudaStream_t s) {
+  for (int q = 0; q < d->nlocal; ++q)
+    MGB_CUDA_TRY(cudaMemcpyAsync(d->norm_parts + q, d->parts[q].norm2, sizeof(double), cudaMemcpyDeviceToDevice, s));
+  k_sum_norm<<<1, 32, 0, s>>>(d->norm_parts, d->nlocal, dst);
+  MGB_CUDA_TRY(cudaGetLastError());
+  if (d->comm) MGB_NCCL_TRY(nccl::api().AllReduce(dst, dst, 1, nccl::Float64, nccl::Sum, d->comm, s));
+  return MGB_OK;
+}
+
+static StreamArgs dd_args(const mgb_dd* d, int l, cudaStream_t s) {
+  StreamArgs a{};
+  a.g = hier_grid(d->h, l);
+  a.A = hier_opA(d->h, l);
+  a.K = hier_opK(d->h, l);
+  a.stream = s;
+  hier_interior(d->h, l, &a.ci_valid, a.ci);
+  return a;
+}
+
+// residual norm^2 of the current level-0 u (or of f when u == null) per part, via a
+// streaming plain-sweep pass whose output goes to scratch
+static int norm_pass(mgb_dd* d, bool of_f, double* dst, cudaStream_t s) {
+  const int cols = d->cols(0);
+  if (!of_f)
+    if (int st = exchange(d, 0, 0, s)) return st;
+  for (auto& P : d->parts) {
+    StreamArgs a = dd_args(d, 0, s);
+    a.f = mgb_dd::gview(P.f[0], P.R0[0], cols);
+    a.u = of_f ? nullptr : mgb_dd::gview(P.u[0], P.R0[0], cols);
+    a.uo = mgb_dd::gview(P.t[0], P.R0[0], cols);
+    a.partials = P.partials;
+    a.own0 = P.R0[0];
+    a.own1 = P.R1[0];
+    int nb = 0;
+    MGB_CUDA_TRY(launch_stream(a, 1, false, false, true, &nb));
+    MGB_CUDA_TRY(launch_finalize(1, nb, P.partials, P.norm2, nullptr, nullptr, 0, s));
+  }
+  return reduce_norm(d, dst, s);
+}
+
+// one V(nu1, nu2) cycle; hist != null: the relative residual of the input u
+static int dd_cycle(mgb_dd* d, int nu1, int nu2, bool zero, double* hist, cudaStream_t s) {
+  const int Ld = d->Ld, La = d->La;
+  // descend over the distributed levels
+  for (int l = 0; l < Ld; ++l) {
+    const int cols = d->cols(l);
+    const bool z = zero || l > 0;
+    if (!z)
+      if (int st = exchange(d, l, 0, s)) return st;
+    if (l > 0)
+      if (int st = exchange(d, l, 2, s)) return st;
+    const bool last = l + 1 == Ld;
+    for (auto& P : d->parts) {
+      StreamArgs a = dd_args(d, l, s);
+      a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
+      a.u = z ? nullptr : mgb_dd::gview(P.u[l], P.R0[l], cols);
+      a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
+      a.own0 = P.R0[l];
+      a.own1 = P.R1[l];
+      if (last) {
+        // restricted residual straight into this part's slot of the gather layout
+        const int cc = d->cols(La);
+        a.rc = d->gather + (int64_t)P.part * d->Bc * cc - (int64_t)(P.R0[l] / 2) * cc;
+      } else {
+        const int cc = d->cols(l + 1);
+        a.rc = mgb_dd::gview(P.f[l + 1], P.R0[l] / 2, cc);
+      }
+      const bool nrm = hist && l == 0;
+      a.partials = nrm ? P.partials : nullptr;
+      int nb = 0;
+      MGB_CUDA_TRY(launch_stream(a, nu1, true, false, nrm, &nb));
+      if (nrm) MGB_CUDA_TRY(launch_finalize(1, nb, P.partials, P.norm2, nullptr, nullptr, 0, s));
+      std::swap(P.u[l], P.t[l]);
+    }
+    if (hist && l == 0) {
+      if (int st = reduce_norm(d, d->r2, s)) return st;
+      k_hist_entry<<<1, 32, 0, s>>>(d->r2, d->f2, hist);
+      MGB_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  // agglomerate: every rank gets the whole restricted residual, solves the coarse part
+  const int cc = d->cols(La);
+  const size_t blkc = (size_t)d->Bc * cc;
+  if (d->comm) {
+    MGB_NCCL_TRY(nccl::api().AllGather(d->gather + (int64_t)d->first * blkc, d->gather, blkc, nccl::Float64,
+                                       d->comm, s));
+  }
+  double* cf = work_level_f(d->cw, La);
+  double* cu = work_level_u(d->cw, La);
+  MGB_CUDA_TRY(cudaMemcpyAsync(cf, d->gather, sizeof(double) * d->rows(La) * cc, cudaMemcpyDeviceToDevice, s));
+  double* ec_full = nullptr;
+  if (int st = work_vcycle_level(d->cw, La, cf, cu, true, nu1, nu2, s, &ec_full)) return st;
+  // ascend
+  for (int l = Ld - 1; l >= 0; --l) {
+    const int cols = d->cols(l);
+    if (int st = exchange(d, l, 0, s)) return st;
+    if (l + 1 < Ld)
+      if (int st = exchange(d, l + 1, 0, s)) return st;
+    for (auto& P : d->parts) {
+      StreamArgs a = dd_args(d, l, s);
+      a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
+      a.u = mgb_dd::gview(P.u[l], P.R0[l], cols);
+      a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
+      a.own0 = P.R0[l];
+      a.own1 = P.R1[l];
+      if (l + 1 < Ld) a.ec = mgb_dd::gview(P.u[l + 1], P.R0[l + 1], d->cols(l + 1));
+      else a.ec = ec_full;
+      int nb = 0;
+      MGB_CUDA_TRY(launch_stream(a, nu2, false, true, false, &nb));
+      std::swap(P.u[l], P.t[l]);
+    }
+  }
+  return MGB_OK;
+}
+
+extern "C" int mgb_dd_set_rhs(mgb_dd* d, int part, const double* f_owned_dev, void* stream) {
+  if (!d) return fail(MGB_CONTRACT, "null decomposition");
+  const int q = part - d->first;
+  if (q < 0 || q >= d->nlocal) return fail(MGB_CONFIG, "part not held by this process");
+  DeviceGuard dg(d->device);
+  DDPart& P = d->parts[q];
+  const int cols = d->cols(0);
+  MGB_CUDA_TRY(cudaMemcpyAsync(P.f[0] + (int64_t)G * cols, f_owned_dev,
+                               sizeof(double) * (size_t)(P.R1[0] - P.R0[0]) * cols, cudaMemcpyDeviceToDevice,
+                               S(stream)));
+  return MGB_OK;
+}
+
+extern "C" int mgb_dd_get_solution(const mgb_dd* d, int part, double* u_owned_dev, void* stream) {
+  if (!d) return fail(MGB_CONTRACT, "null decomposition");
+  const int q = part - d->first;
+  if (q < 0 || q >= d->nlocal) return fail(MGB_CONFIG, "part not held by this process");
+  DeviceGuard dg(d->device);
+  const DDPart& P = d->parts[q];
+  const int cols = d->cols(0);
+  MGB_CUDA_TRY(cudaMemcpyAsync(u_owned_dev, P.u[0] + (int64_t)G * cols,
+                               sizeof(double) * (size_t)(P.R1[0] - P.R0[0]) * cols, cudaMemcpyDeviceToDevice,
+                               S(stream)));
+  return MGB_OK;
+}
+
+static int dd_enqueue(mgb_dd* d, int nu1, int nu2, int cycles, int u_zero, double* hist, cudaStream_t s) {
+  if (int st = exchange(d, 0, 2, s)) return st;  // f ghosts of level 0
+  if (int st = norm_pass(d, true, d->f2, s)) return st;
+  for (int c = 0; c < cycles; ++c)
+    if (int st = dd_cycle(d, nu1, nu2, u_zero && c == 0, hist + c, s)) return st;
+  if (int st = norm_pass(d, false, d->r2, s)) return st;
+  k_hist_entry<<<1, 32, 0, s>>>(d->r2, d->f2, hist + cycles);
+  MGB_CUDA_TRY(cudaGetLastError());
+  return MGB_OK;
+}
+
+extern "C" int mgb_dd_run_cycles(mgb_dd* d, int nu1, int nu2, int cycles, int u_zero, double* history_dev,
+                                 void* stream) {
+  if (!d) return fail(MGB_CONTRACT, "null decomposition");
+  if ((nu1 != 1 && nu1 != 2) || (nu2 != 1 && nu2 != 2)) return fail(MGB_CONFIG, "decomposed cycles support V(1|2, 1|2)");
+  if (cycles < 0 || !history_dev) return fail(MGB_CONFIG, "bad cycle count or history buffer");
+  DeviceGuard dg(d->device);
+  cudaStream_t s = S(stream);
+  if (int st = work_prepare(d->cw)) return st;
+  // one CUDA graph per (nu1, nu2, cycles, u_zero, history) (halo copies / NCCL ops are captured too)
+  const int key[4] = {nu1, nu2, cycles, u_zero};
+  if (!d->graph || std::memcmp(key, d->gkey, sizeof(key)) != 0 || d->ghist != history_dev) {
+    if (d->graph) cudaGraphExecDestroy(d->graph);
+    d->graph = nullptr;
+    cudaGraph_t g = nullptr;
+    MGB_CUDA_TRY(cudaStreamBeginCapture(d->cap, cudaStreamCaptureModeThreadLocal));
+    int st = dd_enqueue(d, nu1, nu2, cycles, u_zero, history_dev, d->cap);
+    cudaError_t e = cudaStreamEndCapture(d->cap, &g);
+    if (st) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&d->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    std::memcpy(d->gkey, key, sizeof(key));
+    d->ghist = history_dev;
+  }
+  MGB_CUDA_TRY(cudaGraphLaunch(d->graph, s));
+  return MGB_OK;
+}

@@ -30,6 +30,32 @@ extern thread_local int64_t g_launches;
 cudaError_t debug_sync(const char* what);
 #define MGB_DBG(name) ::mgb::debug_sync(name)
 
+// ---- small RAII / allocation helpers ----------------------------------------
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+inline cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return cudaSuccess;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+template <typename T>
+inline void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+
 // ---- stencil storage descriptors --------------------------------------------
 // Operators and smoother kernels are addressed per problem b of a batch as
 //   value(p, s, o) = base[b * bstride + s * sstride + o * ostride + p * pstride]

@@ -400,3 +400,30 @@ def test_classed_only_hierarchy_matches_per_point_build(n, cols, variant, nu):
     a = h1.run_cycles(f, u1, 5, nu, nu, u_zero=True).clone()
     b = h2.run_cycles(f, u2, 5, nu, nu, u_zero=True).clone()
     assert t.equal(u1, u2) and t.equal(a, b)
+
+
+@pytest.mark.parametrize("n,nparts,nu", [(511, 2, 2), (511, 3, 1), (1023, 4, 2), (255, 2, 2)])
+def test_virtual_domain_decomposition_matches_single_domain(n, nparts, nu, monkeypatch):
+    """Row-block decomposition on one GPU (halos by device copies, agglomerated
+    coarse levels): u is bitwise the single-domain result, histories agree to
+    rounding (only the norm summation order differs)."""
+    from paper_2102_12071_b200 import dd, device as dv
+    monkeypatch.setenv("MGB_STREAM_MIN", "0")       # streaming passes on every level, as the decomposition
+    t = dv.torch()
+    table = gen.rotated_fd(1, math.pi / 3, 0.01, h=1.0 / (n + 1))[0, 0]
+    levels = gen.levels_for(n)
+    h = mg.equip_inferred(mg.build_hierarchy_classed(n, n, table, levels), net_of("conv"))
+    f_full = dv.to_dev(gen.uniform_rhs(n, 11))
+    u_ref = dv.zeros(f_full.shape)
+    hist_ref = dv.host(h.run_cycles(f_full, u_ref, 4, nu, nu, u_zero=True))[0]
+    agg = n // 4
+    s = dd.DecomposedSolver(h, nparts, local=True, agglomerate_rows=agg)
+    assert s.distributed_levels >= 1
+    blocks = [s.rows(p) for p in range(nparts)]
+    assert blocks == dd.partition_rows(n, nparts, s.distributed_levels)
+    for p, (r0, r1) in enumerate(blocks):
+        s.set_rhs(p, f_full[r0:r1].contiguous())
+    hist = dv.host(s.run_cycles(4, nu, nu))
+    u = t.cat([s.solution(p) for p in range(nparts)])
+    assert t.equal(u, u_ref), float((u - u_ref).abs().max())
+    assert np.allclose(hist, hist_ref, rtol=1e-13, atol=0)
