@@ -250,7 +250,7 @@ extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int 
   MGB_CUDA_TRY(dalloc(&d->gather, (size_t)nparts * d->Bc * d->cols(d->La)));
   MGB_CUDA_TRY(cudaMemset(d->gather, 0, sizeof(double) * nparts * d->Bc * d->cols(d->La)));
   MGB_CUDA_TRY(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
-  if (nlocal == 1 && nparts > 1) {
+  if (nlocal == 1 && nccl_id) {  // (a 1-rank communicator also takes the NCCL path: tested on one GPU)
     if (!nccl::api().ok) return fail(MGB_NCCL, "libnccl.so.2 not available");
     nccl::UniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));

@@ -427,3 +427,24 @@ def test_virtual_domain_decomposition_matches_single_domain(n, nparts, nu, monke
     u = t.cat([s.solution(p) for p in range(nparts)])
     assert t.equal(u, u_ref), float((u - u_ref).abs().max())
     assert np.allclose(hist, hist_ref, rtol=1e-13, atol=0)
+
+
+def test_nccl_decomposition_single_rank(monkeypatch):
+    """The NCCL backend of the decomposition (dlopen'd NCCL, communicator init,
+    graph-captured all-gather / all-reduce) on a 1-rank communicator: identical to
+    the single-domain solve.  Multi-rank halos need several GPUs."""
+    import torch.distributed as dist
+    from paper_2102_12071_b200 import dd, device as dv
+    monkeypatch.setenv("MGB_STREAM_MIN", "0")
+    t = dv.torch()
+    n = 511
+    table = gen.rotated_fd(1, math.pi / 3, 0.01, h=1.0 / (n + 1))[0, 0]
+    h = mg.equip_inferred(mg.build_hierarchy_classed(n, n, table, gen.levels_for(n)), net_of("conv"))
+    f = dv.to_dev(gen.uniform_rhs(n, 3))
+    u_ref = dv.zeros(f.shape)
+    hist_ref = dv.host(h.run_cycles(f, u_ref, 3, 2, 2, u_zero=True))[0]
+    s = dd.DecomposedSolver(h, 1, 0, local=False, nccl_id=dd.nccl_unique_id(), agglomerate_rows=127)
+    s.set_rhs(0, f)
+    hist = dv.host(s.run_cycles(3, 2, 2))
+    assert t.equal(s.solution(0), u_ref)
+    assert np.allclose(hist, hist_ref, rtol=1e-13, atol=0)
