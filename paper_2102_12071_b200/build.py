@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmgb.so")
-SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_coarse.cu", "mgb_dd.cu", "mgb_cnn.cu", "mgb_api.cu"]
+SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_tile.cu", "mgb_coarse.cu", "mgb_dd.cu", "mgb_cnn.cu", "mgb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -38,35 +38,46 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "mgb_internal.h"), os.path.join(CSRC, "mgb_cycle.h"), os.path.join(CSRC, "mgb_stream.h"), os.path.join(CSRC, "mgb_coarse.h"), os.path.join(CSRC, "mgb_dd.h"),
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".h")] + [
                                                         os.path.join(ROOT, "include", "mgb.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """defines / out: experiment builds (e.g. -DMGB_MINB=4 into experiments/)."""
+    if out == LIB and not defines and not force and not needs_build():
         return LIB
     nvcc = nvcc_path()
-    objs = []
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc, *flags(), "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        obj = obj if out == LIB else obj.replace(".o", f".{os.getpid()}.o")
+        cmd = [nvcc, *flags(), *defines, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = []
+    for src, obj, r in results:
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, out)
     for o in objs:
         os.remove(o)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else LIB
+    print(build(force="--force" in args, verbose="-v" in args, out=os.path.abspath(out),
+                defines=[a for a in args if a.startswith("-D")]))

@@ -14,6 +14,7 @@
 
 #include "mgb_cycle.h"
 #include "mgb_stream.h"
+#include "mgb_tile.h"
 #include "mgb_coarse.h"
 #include "mgb_dd.h"
 #include "mgb_internal.h"
@@ -71,12 +72,13 @@ struct mgb_hier {
   int version = 0;          // bumped whenever smoother kernels are (re)installed
   int compact = 1;          // use band-class tables where they represent a table exactly
   int classed_only = 0;     // built from band-class tables: no per-point planes exist
-  int64_t stream_min = 1500000;
-  int64_t coarse_max = 32 * 32;    // levels up to this many points run in the single-launch
-                                   // shared-memory coarse cycle (0 disables it)  // streaming passes on levels with at least this many points
-                                   // (smaller levels are latency-bound: separate tile kernels win)
-  int fused = 2;            // 2: one streaming pass per smoothing phase; 1: single-sweep streaming
-                            // passes; 0: separate sweep / restriction / prolongation kernels
+  int64_t stream_min = 1000000;   // row-streaming passes on levels with at least this many points
+                                  // (batch x rows x cols); smaller levels use tile passes
+  int tile = 1;                   // 1: tile-local fused passes below stream_min; 0: separate kernels
+  int64_t coarse_max = 32 * 32;   // levels up to this many points run in the single-launch
+                                  // shared-memory coarse cycle (0 disables it)
+  int fused = 2;            // 2: one fused pass per smoothing phase; 1: one fused pass per sweep;
+                            // 0: separate sweep / restriction / prolongation kernels
   ~mgb_hier() {
     DeviceGuard dg(device);
     for (auto& l : lv) {
@@ -530,6 +532,7 @@ extern "C" int mgb_hier_build(int device, int batch, int rows, int cols, double 
   if (const char* e = getenv("MGB_STORAGE")) h->compact = std::string(e) != "planes";
   if (const char* e = getenv("MGB_FUSED")) h->fused = atoi(e);
   if (const char* e = getenv("MGB_STREAM_MIN")) h->stream_min = atoll(e);
+  if (const char* e = getenv("MGB_TILE")) h->tile = atoi(e);
   if (const char* e = getenv("MGB_COARSE_MAX")) h->coarse_max = atoll(e);
   if (int st = classify_all(h.get(), s)) return st;
   *out = h.release();
@@ -551,6 +554,14 @@ extern "C" int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream) {
 extern "C" int mgb_hier_set_fused(mgb_hier* h, int enable) {
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   h->fused = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
+  ++h->version;
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_set_passes(mgb_hier* h, int64_t stream_min, int tile) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (stream_min >= 0) h->stream_min = stream_min;
+  if (tile >= 0) h->tile = tile ? 1 : 0;
   ++h->version;
   return MGB_OK;
 }
@@ -663,6 +674,7 @@ extern "C" int mgb_hier_build_classed(int device, int batch, int rows, int cols,
   }
   if (const char* e = getenv("MGB_FUSED")) h->fused = atoi(e);
   if (const char* e = getenv("MGB_STREAM_MIN")) h->stream_min = atoll(e);
+  if (const char* e = getenv("MGB_TILE")) h->tile = atoi(e);
   if (const char* e = getenv("MGB_COARSE_MAX")) h->coarse_max = atoll(e);
   *out = h.release();
   return MGB_OK;
@@ -943,7 +955,7 @@ int mgb::work_create_from(const mgb_hier* h, int first, mgb_work** out) {
   }
   const Grid g0 = h->grid(first);
   w->max_nblk = std::max(std::max(residual_blocks(g0), resnorm_blocks(g0)),
-                         std::max(sweep_blocks(g0), stream_max_blocks(g0)));
+                         std::max(std::max(sweep_blocks(g0), stream_max_blocks(g0)), tile_max_blocks(g0)));
   MGB_CUDA_TRY(dalloc(&w->partials, (size_t)w->max_nblk * h->batch));
   MGB_CUDA_TRY(dalloc(&w->fnorm2, (size_t)h->batch));
   MGB_CUDA_TRY(dalloc(&w->scratch, (size_t)h->batch * 4));
@@ -1063,10 +1075,19 @@ static int enqueue_coarse(mgb_work* w, int lc, bool zero, int nu1, int nu2, cuda
 
 // ---- row-streaming passes (mgb_stream.cu) -----------------------------------
 
-static bool use_stream(const mgb_hier* h, int l, int nu1, int nu2) {
+// fused pass kind for level l: 0 separate kernels, 1 row streaming, 2 tile-local
+static int pass_kind(const mgb_hier* h, int l, int nu1, int nu2) {
   const LevelD& lv = h->lv[l];
-  return h->fused && lv.ks == 1 && (nu1 == 1 || nu1 == 2) && (nu2 == 1 || nu2 == 2) &&
-         (int64_t)lv.n * h->batch >= h->stream_min;
+  if (!h->fused || lv.ks != 1 || !(nu1 == 1 || nu1 == 2) || !(nu2 == 1 || nu2 == 2)) return 0;
+  if ((int64_t)lv.n * h->batch >= h->stream_min) return 1;
+  return h->tile ? 2 : 0;
+}
+static bool use_stream(const mgb_hier* h, int l, int nu1, int nu2) { return pass_kind(h, l, nu1, nu2) != 0; }
+
+static cudaError_t launch_pass(const mgb_hier* h, int l, const StreamArgs& a, int nsw, bool res, bool pro,
+                               bool norm, int* nb) {
+  if ((int64_t)h->lv[l].n * h->batch >= h->stream_min) return launch_stream(a, nsw, res, pro, norm, nb);
+  return launch_tile(a, nsw, res, pro, norm, nb);
 }
 
 static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStream_t s) {
@@ -1101,7 +1122,7 @@ static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, do
     a.u = in;
     a.uo = *oth;
     a.partials = hist ? w->partials : nullptr;
-    MGB_CUDA_TRY(launch_stream(a, 1, false, false, hist != nullptr, &nb));
+    MGB_CUDA_TRY(launch_pass(h, l, a, 1, false, false, hist != nullptr, &nb));
     if (hist) MGB_CUDA_TRY(launch_finalize(h->batch, nb, w->partials, nullptr, w->fnorm2, hist, hstride, s));
     std::swap(*cur, *oth);
     in = *cur;
@@ -1111,7 +1132,7 @@ static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, do
   a.uo = *oth;
   a.rc = w->f[l + 1];
   a.partials = hist ? w->partials : nullptr;
-  MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu1, true, false, hist != nullptr, &nb));
+  MGB_CUDA_TRY(launch_pass(h, l, a, split ? 1 : nu1, true, false, hist != nullptr, &nb));
   if (hist) MGB_CUDA_TRY(launch_finalize(h->batch, nb, w->partials, nullptr, w->fnorm2, hist, hstride, s));
   std::swap(*cur, *oth);
   return MGB_OK;
@@ -1127,13 +1148,13 @@ static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, d
   a.u = *cur;
   a.uo = *oth;
   a.ec = ec;
-  MGB_CUDA_TRY(launch_stream(a, split ? 1 : nu2, false, true, false, &nb));
+  MGB_CUDA_TRY(launch_pass(h, l, a, split ? 1 : nu2, false, true, false, &nb));
   std::swap(*cur, *oth);
   if (split && nu2 == 2) {
     a.u = *cur;
     a.uo = *oth;
     a.ec = nullptr;
-    MGB_CUDA_TRY(launch_stream(a, 1, false, false, false, &nb));
+    MGB_CUDA_TRY(launch_pass(h, l, a, 1, false, false, false, &nb));
     std::swap(*cur, *oth);
   }
   return MGB_OK;

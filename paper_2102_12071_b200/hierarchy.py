@@ -197,6 +197,11 @@ class MultigridHierarchy:
         streaming pass per sweep, 0 / False separate sweep, restriction, prolongation."""
         _lib.call("mgb_hier_set_fused", self._h, int(mode))
 
+    def set_passes(self, stream_min: int = -1, tile: int = -1):
+        """Levels with batch*rows*cols >= stream_min run row-streaming passes, smaller
+        ones tile-local passes (tile=1) or separate kernels (tile=0); -1 keeps a setting."""
+        _lib.call("mgb_hier_set_passes", self._h, int(stream_min), int(tile))
+
     def storage_info(self, l: int):
         """(A class-compact, M class-compact) for level l."""
         a, k = C.c_int(), C.c_int()

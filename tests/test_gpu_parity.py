@@ -448,3 +448,46 @@ def test_nccl_decomposition_single_rank(monkeypatch):
     hist = dv.host(s.run_cycles(3, 2, 2))
     assert t.equal(s.solution(0), u_ref)
     assert np.allclose(hist, hist_ref, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("name", ["c1_fd_conv", "c1_q1_conv", "case_var31_conv_v22", "case_lshape31_conv_v11",
+                                  "case_rot31_fc_v22", "c4_p0", "case_rect20x27_conv_v11"])
+def test_tile_and_stream_passes_bit_identical(name):
+    """Tile-local fused passes (mid-size levels) vs row-streaming passes on every
+    level: the same arithmetic, so u is bitwise equal; histories differ only in
+    the order of the norm's partial sums."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    c = load(name)
+    g = c["golden"]
+    spec = spec_of(c["mask"], float(g["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), c["smoother"])
+    f = dv.to_dev(np.where(c["mask"], c["f"], 0.0))
+    runs = []
+    for stream_min, tile in ((0, 1), (1 << 62, 1), (1 << 62, 0)):
+        h.set_passes(stream_min, tile)
+        u = dv.zeros(f.shape)
+        hist = h.run_cycles(f, u, c["cycles"], c["nu"], c["nu"], u_zero=True).clone()
+        runs.append((u, dv.host(hist)[0]))
+    assert t.equal(runs[0][0], runs[1][0])
+    assert np.allclose(runs[0][1], runs[1][1], rtol=1e-13, atol=1e-300)
+    assert_hist(runs[1][1], runs[2][1])                       # vs separate kernels: rounding only
+    assert rel_err(dv.host(runs[1][0]), dv.host(runs[2][0])) <= 1e-12
+    assert_hist(runs[1][1], g["history"])                     # and the reference
+
+
+@pytest.mark.parametrize("n,nu", [(1023, 2), (1023, 1), (600, 2)])
+def test_tile_passes_large_tiles(n, nu):
+    """The 32-point tile (levels of ~550^2 and more) against row streaming, bitwise."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    table = gen.rotated_fd(1, math.pi / 4, 1e-3, h=1.0 / (n + 1))[0, 0]
+    h = mg.equip_inferred(mg.build_hierarchy_classed(n, n, table, gen.levels_for(n)), net_of("conv_c2"))
+    f = dv.to_dev(gen.uniform_rhs(n, 2))
+    out = []
+    for stream_min in (0, 1 << 62):
+        h.set_passes(stream_min, 1)
+        u = dv.zeros(f.shape)
+        out.append((u, dv.host(h.run_cycles(f, u, 3, nu, nu, u_zero=True))[0]))
+    assert t.equal(out[0][0], out[1][0])
+    assert np.allclose(out[0][1], out[1][1], rtol=1e-13, atol=0)
