@@ -153,8 +153,10 @@ int mgb_hier_set_fused(mgb_hier* h, int enable);
 /* Which fused pass runs where: levels with batch*rows*cols >= stream_min use the
    row-streaming passes (large, HBM-bound levels), smaller ones the tile-local passes
    when tile = 1 (latency-bound levels: one launch per phase) or separate kernels when
-   tile = 0.  Negative arguments keep the current setting.  Bit-identical results. */
-int mgb_hier_set_passes(mgb_hier* h, int64_t stream_min, int tile);
+   tile = 0 (streaming and tile passes are bit-identical).  coarse_max > 0 runs every
+   level with at most that many points in one single-CTA shared-memory kernel (default
+   0: off, the tile passes measured faster).  Negative arguments keep a setting. */
+int mgb_hier_set_passes(mgb_hier* h, int64_t stream_min, int tile, int64_t coarse_max);
 
 /* equip_inferred (hierarchy.py:207-214): per-level CNN inference on levels 0..L-2. */
 int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const double* weights_host,

@@ -51,7 +51,7 @@ SIGNATURES = {
     "mgb_hier_set_storage": (I, [P, I, P]),
     "mgb_hier_storage_info": (I, [P, I, PI, PI]),
     "mgb_hier_set_fused": (I, [P, I]),
-    "mgb_hier_set_passes": (I, [P, I64, I]),
+    "mgb_hier_set_passes": (I, [P, I64, I, I64]),
     "mgb_hier_equip_inferred": (I, [P, I, I, P, I64, D, I, P]),
     "mgb_hier_equip_jacobi": (I, [P, D, P]),
     "mgb_hier_set_kernels": (I, [P, I, I, P, I, D, P]),

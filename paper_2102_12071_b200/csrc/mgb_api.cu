@@ -75,7 +75,7 @@ struct mgb_hier {
   int64_t stream_min = 1000000;   // row-streaming passes on levels with at least this many points
                                   // (batch x rows x cols); smaller levels use tile passes
   int tile = 1;                   // 1: tile-local fused passes below stream_min; 0: separate kernels
-  int64_t coarse_max = 32 * 32;   // levels up to this many points run in the single-launch
+  int64_t coarse_max = 0;         // levels up to this many points run in the single-launch
                                   // shared-memory coarse cycle (0 disables it)
   int fused = 2;            // 2: one fused pass per smoothing phase; 1: one fused pass per sweep;
                             // 0: separate sweep / restriction / prolongation kernels
@@ -558,10 +558,11 @@ extern "C" int mgb_hier_set_fused(mgb_hier* h, int enable) {
   return MGB_OK;
 }
 
-extern "C" int mgb_hier_set_passes(mgb_hier* h, int64_t stream_min, int tile) {
+extern "C" int mgb_hier_set_passes(mgb_hier* h, int64_t stream_min, int tile, int64_t coarse_max) {
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   if (stream_min >= 0) h->stream_min = stream_min;
   if (tile >= 0) h->tile = tile ? 1 : 0;
+  if (coarse_max >= 0) h->coarse_max = coarse_max;
   ++h->version;
   return MGB_OK;
 }
@@ -1038,7 +1039,7 @@ static int coarse_first_level(const mgb_hier* h) {
   while (lc < L - 1) {
     size_t d = 0;
     for (int l = lc; l < L; ++l) d += 3 * (size_t)h->lv[l].n + 2 * 25 * 9;
-    d += h->nc;
+    d += std::max(h->nc, 32);
     if (d * sizeof(double) <= 200 * 1024) break;
     ++lc;
   }

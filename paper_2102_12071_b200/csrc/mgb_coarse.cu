@@ -174,21 +174,41 @@ __global__ void __launch_bounds__(CT) k_coarse_block(CoarseArgs a) {
     const int nn = a.nc;
     const double* lu = a.lu + (int64_t)b * nn * nn;
     const int32_t* pm = a.perm + (int64_t)b * nn;
-    for (int q = tid; q < nn; q += CT) xs[q] = sf[lc][a.actp[pm[q]]];
     for (int q = tid; q < n; q += CT) su[lc][q] = 0.0;
+    if (nn <= 32) {
+      // one warp: forward (unit lower) and back substitution with the unknowns
+      // distributed over the lanes (dense.py:50-63 order of operations)
+      if (tid < 32) {
+        const int i = tid;
+        double x = i < nn ? sf[lc][a.actp[pm[i]]] : 0.0;
+        for (int k = 0; k < nn; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, x, k);
+          if (i > k && i < nn) x = x - __ldg(lu + (int64_t)i * nn + k) * xk;
+        }
+        for (int k = nn - 1; k >= 0; --k) {
+          if (i == k) x = x / __ldg(lu + (int64_t)k * nn + k);
+          const double xk = __shfl_sync(0xffffffffu, x, k);
+          if (i < k) x = x - __ldg(lu + (int64_t)i * nn + k) * xk;
+        }
+        xs[i] = x;
+      }
+    } else {
+      for (int q = tid; q < nn; q += CT) xs[q] = sf[lc][a.actp[pm[q]]];
+      __syncthreads();
+      for (int k = 0; k < nn; ++k) {
+        const double xk = xs[k];
+        for (int i = k + 1 + tid; i < nn; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
+        __syncthreads();
+      }
+      for (int k = nn - 1; k >= 0; --k) {
+        if (tid == 0) xs[k] = xs[k] / lu[(int64_t)k * nn + k];
+        __syncthreads();
+        const double xk = xs[k];
+        for (int i = tid; i < k; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
+        __syncthreads();
+      }
+    }
     __syncthreads();
-    for (int k = 0; k < nn; ++k) {
-      const double xk = xs[k];
-      for (int i = k + 1 + tid; i < nn; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
-      __syncthreads();
-    }
-    for (int k = nn - 1; k >= 0; --k) {
-      if (tid == 0) xs[k] = xs[k] / lu[(int64_t)k * nn + k];
-      __syncthreads();
-      const double xk = xs[k];
-      for (int i = tid; i < k; i += CT) xs[i] = xs[i] - lu[(int64_t)i * nn + k] * xk;
-      __syncthreads();
-    }
     for (int q = tid; q < nn; q += CT) su[lc][a.actp[q]] = xs[q];
     __syncthreads();
   }
@@ -232,7 +252,7 @@ size_t coarse_block_smem(const CoarseArgs& a) {
     if (a.lv[l].A.cls) d += NCLS * 9;
     if (l + 1 < a.nlev && a.lv[l].K.cls) d += NCLS * 9;
   }
-  d += std::max(a.nc, 1);
+  d += std::max(a.nc, 32);
   return d * sizeof(double);
 }
 

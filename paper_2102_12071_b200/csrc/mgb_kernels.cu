@@ -505,6 +505,26 @@ __global__ void __launch_bounds__(256) k_lu_solve(int n, const double* __restric
   const int32_t* pm = perm + (int64_t)b * n;
   const double* fb = f + b * fstride;
   double* xb = x + b * xstride;
+  if (n <= 32) {
+    // one warp, unknowns over the lanes: no block barriers on the latency path
+    if (t < 32) {
+      double v = t < n ? (actp ? fb[actp[pm[t]]] : fb[pm[t]]) : 0.0;
+      for (int k = 0; k < n; ++k) {
+        const double xk = __shfl_sync(0xffffffffu, v, k);
+        if (t > k && t < n) v = v - a[(int64_t)t * n + k] * xk;
+      }
+      for (int k = n - 1; k >= 0; --k) {
+        if (t == k) v = v / a[(int64_t)k * n + k];
+        const double xk = __shfl_sync(0xffffffffu, v, k);
+        if (t < k) v = v - a[(int64_t)t * n + k] * xk;
+      }
+      if (t < n) {
+        if (actp) xb[actp[t]] = v;
+        else xb[t] = v;
+      }
+    }
+    return;
+  }
   for (int q = t; q < n; q += nt) {
     const int src = pm[q];
     xs[q] = actp ? fb[actp[src]] : fb[src];

@@ -71,7 +71,8 @@ struct SP {
 // compile-time positive modulo 3
 __host__ __device__ constexpr int m3(int x) { return ((x % 3) + 3) % 3; }
 
-// 3x3 dot product over the register window (slots s0, s1, s2 = rows di = -1, 0, 1)
+// 3x3 dot product over the register window (slots s0, s1, s2 = rows di = -1, 0, 1);
+// the same function as the tile passes (mgb_tile.cu), so both round identically
 template <bool NEG>
 __device__ __forceinline__ double dot9(const double* wt, const double (&x)[3][3], int s0, int s1, int s2,
                                        double init) {
@@ -319,38 +320,20 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
   }
   for (int q = 0; q < DIST; ++q) issue();
 
-#define MGB_STEP(FAST_, PH_)                                                                           \
+#define MGB_STEP(PH_)                                                                                  \
   {                                                                                                    \
     const int t = tb + PH_;                                                                            \
     issue();                                                                                           \
     cp_wait<DIST>();                                                                                   \
-    stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, FAST_, PH_>(a, c, t, w, hold, acc);                  \
+    if (cta_fast && t - 2 * S >= 2 && t <= g.rows - 3)                                                 \
+      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, true, PH_>(a, c, t, w, hold, acc);                 \
+    else                                                                                               \
+      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, false, PH_>(a, c, t, w, hold, acc);                \
   }
-  // Steps run in chunks of 3 (window slots are row mod 3).  The chunks whose steps
-  // are all interior ("fast": no bounds, band-class or column tests) form one
-  // contiguous range [tf0, tf1) run by its own loop, so neither loop branches per
-  // step and the register windows stay in place across iterations.
-  int tf0 = t0, tf1 = t0;
-  if (cta_fast) {
-    const int lo = max(t0, 2 * S + 2), hi = min(g.rows - 3, t1);  // fast steps: lo <= t <= hi
-    tf0 = t0 + ((lo - t0 + 2) / 3) * 3;
-    tf1 = tf0 + max(0, (hi - tf0 + 1) / 3) * 3;
-  }
-  int tb = t0;
-  for (; tb < tf0; tb += 3) {
-    MGB_STEP(false, 0)
-    MGB_STEP(false, 1)
-    MGB_STEP(false, 2)
-  }
-  for (; tb < tf1; tb += 3) {
-    MGB_STEP(true, 0)
-    MGB_STEP(true, 1)
-    MGB_STEP(true, 2)
-  }
-  for (; tb <= t1; tb += 3) {
-    MGB_STEP(false, 0)
-    MGB_STEP(false, 1)
-    MGB_STEP(false, 2)
+  for (int tb = t0; tb <= t1; tb += 3) {
+    MGB_STEP(0)
+    MGB_STEP(1)
+    MGB_STEP(2)
   }
 #undef MGB_STEP
   cp_wait<0>();

@@ -197,10 +197,12 @@ class MultigridHierarchy:
         streaming pass per sweep, 0 / False separate sweep, restriction, prolongation."""
         _lib.call("mgb_hier_set_fused", self._h, int(mode))
 
-    def set_passes(self, stream_min: int = -1, tile: int = -1):
+    def set_passes(self, stream_min: int = -1, tile: int = -1, coarse_max: int = -1):
         """Levels with batch*rows*cols >= stream_min run row-streaming passes, smaller
-        ones tile-local passes (tile=1) or separate kernels (tile=0); -1 keeps a setting."""
-        _lib.call("mgb_hier_set_passes", self._h, int(stream_min), int(tile))
+        ones tile-local passes (tile=1) or separate kernels (tile=0); levels of at most
+        coarse_max points run in the single-launch coarse kernel (0 = off); -1 keeps a
+        setting."""
+        _lib.call("mgb_hier_set_passes", self._h, int(stream_min), int(tile), int(coarse_max))
 
     def storage_info(self, l: int):
         """(A class-compact, M class-compact) for level l."""

@@ -491,3 +491,24 @@ def test_tile_passes_large_tiles(n, nu):
         out.append((u, dv.host(h.run_cycles(f, u, 3, nu, nu, u_zero=True))[0]))
     assert t.equal(out[0][0], out[1][0])
     assert np.allclose(out[0][1], out[1][1], rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("name", ["c1_fd_conv", "case_lshape31_conv_v11", "c4_p0", "case_var31_conv_v22"])
+def test_single_launch_coarse_cycle_agrees(name):
+    """The single-CTA shared-memory coarse cycle (levels <= 32^2 in one launch)
+    against the per-level tile passes: rounding-level agreement and the reference."""
+    from paper_2102_12071_b200 import device as dv
+    c = load(name)
+    g = c["golden"]
+    spec = spec_of(c["mask"], float(g["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), c["smoother"])
+    f = dv.to_dev(np.where(c["mask"], c["f"], 0.0))
+    out = []
+    for coarse_max in (0, 32 * 32):
+        h.set_passes(coarse_max=coarse_max)
+        u = dv.zeros(f.shape)
+        hist = dv.host(h.run_cycles(f, u, c["cycles"], c["nu"], c["nu"], u_zero=True))[0]
+        out.append((dv.host(u), hist))
+    assert_hist(out[0][1], out[1][1])
+    assert rel_err(out[0][0], out[1][0]) <= 1e-12
+    assert_hist(out[1][1], g["history"])
