@@ -361,6 +361,9 @@ static size_t stream_smem(int nsw, bool res) {
 
 // Rows per CTA segment: minimise waves x (segment + pipeline fill) for the
 // kernel's measured occupancy (the whole grid runs ~one row step per CTA at a time).
+// Any segment length is allowed, so the grid can be sized to fill whole waves
+// (e.g. 4095 rows x 36 strips: 12 segments of 342 rows = 432 CTAs, one wave on
+// 148 SMs x 3, instead of 2.6 waves of 128-row segments).
 static int choose_seg(const Grid& g, int nsw, bool res, int occ) {
   const int H = 2 * nsw + 2, wout = SWT - 2 * H, S = 2 * nsw + (res ? 1 : 0);
   const int64_t strips = (g.cols + wout - 1) / wout;
@@ -372,13 +375,23 @@ static int choose_seg(const Grid& g, int nsw, bool res, int occ) {
     if (sms <= 0) sms = 148;
   }
   const int64_t slots = (int64_t)sms * std::max(occ, 1);
-  int best = 256;
+  int best = g.rows;
   double best_t = 1e300;
-  for (int seg = 512; seg >= 16; seg /= 2) {
-    const int64_t ctas = strips * ((g.rows + seg - 1) / seg) * g.batch;
+  // measured: per-step cost rises with the segment length beyond ~128 rows (4095^2:
+  // 64 -> 481 us, 128 -> 485, 171 -> 544, 256 -> 660 per V(2,2) level), so segments
+  // are capped and the count is chosen to fill whole waves below the cap
+  // (very large grids, many waves even at 512-row segments, keep long segments:
+  // 32767^2 measured 6% faster at 512 than at 96)
+  static const int seg_max_env = getenv("MGB_SEG_MAX") ? atoi(getenv("MGB_SEG_MAX")) : 0;
+  const int64_t ctas512 = strips * (int64_t)((g.rows + 511) / 512) * g.batch;
+  const int seg_max = seg_max_env > 0 ? seg_max_env : (ctas512 >= 8 * slots ? 512 : 96);
+  for (int nseg = 1; nseg <= std::max(1, g.rows / 16); ++nseg) {
+    const int seg = (g.rows + nseg - 1) / nseg;
+    if (seg > seg_max && nseg < g.rows / 16) continue;
+    const int64_t ctas = strips * (int64_t)((g.rows + seg - 1) / seg) * g.batch;
     const int64_t waves = (ctas + slots - 1) / slots;
     // a partial last wave still costs a full CTA time; fill = 3S + 3 steps
-    const double t = (double)waves * (seg + 3 * S + 3) + 1e-3 * seg;
+    const double t = (double)waves * (seg + 3 * S + 3);
     if (t < best_t) { best_t = t; best = seg; }
   }
   return best;
