@@ -254,6 +254,20 @@ int  mgb_dd_run_cycles(mgb_dd* d, int nu1, int nu2, int cycles, int u_zero, doub
    mgb_run_cycles / mgb_vcycle call (graph replays count their nodes). */
 int64_t mgb_last_launch_count(const mgb_work* w);
 
+/* Flexible GMRES (method 0; krylov.py:60-164 fgmres/_fgmres_cycle) and plain GMRES
+   (method 1; krylov.py:167-236) on the flat grid vector.  Operator: apply_stencil
+   with the per-point table A_dev (rows*cols*9, reference AoS layout; grid_action,
+   krylov.py:249-258) and mask_dev (NULL = all active).  Right preconditioner: one
+   V(nu1, nu2)-cycle from zero of the hierarchy behind workspace `pc` on the masked
+   vector (cycle_preconditioner, krylov.py:261-270), or none (pc == NULL; required
+   for gmres).  restart <= 0: no restart.  u_dev receives the solution (initial
+   guess 0); history_host (max_iter + 1 entries) the absolute residual estimates,
+   *n_hist their count, *iterations the Arnoldi steps, *converged the stopping
+   test.  MGB_NUMERIC on an Arnoldi breakdown (krylov.py:119-122). */
+int mgb_krylov(int method, int rows, int cols, const double* A_dev, const uint8_t* mask_dev, mgb_work* pc,
+               int nu1, int nu2, const double* f_dev, double* u_dev, double tol, int max_iter, int restart,
+               double* history_host, int* n_hist, int* iterations, int* converged, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

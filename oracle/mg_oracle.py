@@ -469,3 +469,131 @@ def run_cycles(h: Hierarchy, f: np.ndarray, cycles: int, nu1: int, nu2: int,
         u = v_cycle(h, 0, f, u, nu1, nu2)
         hist.append(float(np.linalg.norm(masked(f - apply_stencil(A, u, m), m))) / denom)
     return u, np.array(hist)
+
+
+# ---------------------------------------------------------------------------
+# Krylov (krylov.py:60-270): flexible GMRES with the V-cycle as right
+# preconditioner and plain GMRES, restated on flat vectors.
+
+REORTH_TOL = 1e-8       # krylov.py:19
+BREAKDOWN_TOL = 1e-14   # krylov.py:20
+
+
+def _givens(a: float, b: float):
+    """krylov.py:54-58."""
+    r = math.hypot(a, b)
+    if r == 0.0:
+        return 1.0, 0.0
+    return a / r, b / r
+
+
+def _arnoldi(apply_a, f, precond, u0, steps, tol_abs, history, record_beta, early_exit):
+    """One (F)GMRES cycle from u0: krylov.py:60-135 (fgmres: record_beta on the
+    first cycle, early_exit) and the body of krylov.py:189-230 (gmres)."""
+    r = f - apply_a(u0)
+    beta = float(np.linalg.norm(r))
+    if record_beta:
+        history.append(beta)
+    if early_exit and beta <= tol_abs:
+        return u0, True, 0
+    steps = min(steps, r.size)
+    V, Z = [r / beta], []
+    H = np.zeros((steps + 1, steps))
+    cs, sn, g = np.zeros(steps), np.zeros(steps), np.zeros(steps + 1)
+    g[0] = beta
+    j = 0
+    while j < steps:
+        z = V[j] if precond is None else precond(V[j])
+        w = apply_a(z)
+        Z.append(z)
+        wnorm0 = float(np.linalg.norm(w))
+        for i in range(j + 1):
+            H[i, j] = float(V[i] @ w)
+            w = w - H[i, j] * V[i]
+        wnorm = float(np.linalg.norm(w))
+        if wnorm < REORTH_TOL * wnorm0 or any(abs(float(V[i] @ w)) > REORTH_TOL * max(wnorm, 1e-300)
+                                              for i in range(j + 1)):
+            for i in range(j + 1):
+                c = float(V[i] @ w)
+                H[i, j] += c
+                w = w - c * V[i]
+        hsub = float(np.linalg.norm(w))
+        H[j + 1, j] = hsub
+        for i in range(j):
+            t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+            H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+            H[i, j] = t
+        cs[j], sn[j] = _givens(H[j, j], H[j + 1, j])
+        H[j, j] = cs[j] * H[j, j] + sn[j] * H[j + 1, j]
+        H[j + 1, j] = 0.0
+        g[j + 1] = -sn[j] * g[j]
+        g[j] = cs[j] * g[j]
+        res = abs(g[j + 1])
+        history.append(res)
+        j += 1
+        if res <= tol_abs:
+            break
+        if hsub <= BREAKDOWN_TOL * max(wnorm0, 1.0):
+            raise OracleError("NumericError", f"Arnoldi breakdown at step {j}")
+        V.append(w / hsub)
+    y = np.zeros(j)
+    for i in range(j - 1, -1, -1):
+        y[i] = (g[i] - H[i, i + 1:j] @ y[i + 1:j]) / H[i, i]
+    u = u0.copy()
+    for i in range(j):
+        u = u + y[i] * Z[i]
+    return u, abs(g[j]) <= tol_abs, j
+
+
+def fgmres(apply_a, f, precond=None, tol=1e-6, max_iter=200, restart=None):
+    """krylov.py:138-164.  Returns (u, iterations, history, converged)."""
+    f = np.asarray(f, dtype=float)
+    beta0 = float(np.linalg.norm(f))
+    if beta0 == 0.0:
+        return np.zeros_like(f), 0, [0.0], True
+    tol_abs = tol * beta0
+    history: list = []
+    u = np.zeros_like(f)
+    done, total = False, 0
+    while total < max_iter and not done:
+        steps = max_iter - total
+        if restart is not None:
+            steps = min(steps, restart)
+        u, done, took = _arnoldi(apply_a, f, precond, u, steps, tol_abs, history, not history, True)
+        total += took
+        if took == 0:
+            break
+    return u, total, history, done
+
+
+def gmres(apply_a, f, tol=1e-6, max_iter=200, restart=None):
+    """krylov.py:167-236.  Returns (u, iterations, history, converged)."""
+    f = np.asarray(f, dtype=float)
+    beta0 = float(np.linalg.norm(f))
+    if beta0 == 0.0:
+        return np.zeros_like(f), 0, [0.0], True
+    tol_abs = tol * beta0
+    history = [beta0]
+    u = np.zeros_like(f)
+    if beta0 <= tol_abs:
+        return u, 0, history, True
+    budget = max_iter
+    while budget > 0:
+        steps = budget if restart is None else min(budget, restart)
+        u, done, j = _arnoldi(apply_a, f, None, u, steps, tol_abs, history, False, False)
+        budget -= j
+        if done or j == 0:
+            return u, max_iter - budget, history, done
+    return u, max_iter, history, False
+
+
+def grid_action(A: np.ndarray, mask: np.ndarray | None = None):
+    """krylov.py:249-258."""
+    shape = A.shape[:2]
+    return lambda x: apply_stencil(A, x.reshape(shape), mask).ravel()
+
+
+def cycle_preconditioner(h: Hierarchy, nu1: int = 1, nu2: int = 1):
+    """krylov.py:261-270: one V(nu1, nu2)-cycle from zero on the masked vector."""
+    m = h.masks[0]
+    return lambda r: v_cycle(h, 0, r.reshape(m.shape) * m, np.zeros(m.shape), nu1, nu2).ravel()

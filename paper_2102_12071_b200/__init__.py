@@ -18,5 +18,7 @@ from .smoothers import (InferredSmoother, JacobiSmoother, KernelInferenceNet, in
 from .hierarchy import (Level, MultigridHierarchy, RepeatedSmoother, SolveReport, build_hierarchy,
                         build_hierarchy_batch, build_hierarchy_classed, coarse_solve, cycle_correction, equip_classical,
                         equip_inferred, solve, v_cycle)
+from .krylov import (CyclePreconditioner, FgmresConfig, GridAction, KrylovReport, cycle_preconditioner, fgmres,
+                     gmres, grid_action)
 
 __version__ = "0.1.0"

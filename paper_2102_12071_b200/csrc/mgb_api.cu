@@ -1544,6 +1544,7 @@ void hier_interior(const mgb_hier* h, int l, int* valid, double* ci) {
 double* work_level_u(mgb_work* w, int l) { return w->u[l]; }
 double* work_level_f(mgb_work* w, int l) { return w->f[l]; }
 int work_prepare(mgb_work* w) { return prepare_work(w); }
+const mgb_hier* work_hier(const mgb_work* w) { return w->h; }
 int work_vcycle_level(mgb_work* w, int l, const double* f, double* u, bool zero, int nu1, int nu2, cudaStream_t s,
                       double** result) {
   return vcycle_rec(w, l, f, u, zero, nu1, nu2, s, result);

@@ -24,6 +24,7 @@ int work_create_from(const mgb_hier* h, int first, mgb_work** out);
 double* work_level_u(mgb_work* w, int l);
 double* work_level_f(mgb_work* w, int l);
 int work_prepare(mgb_work* w);
+const mgb_hier* work_hier(const mgb_work* w);
 int work_vcycle_level(mgb_work* w, int l, const double* f, double* u, bool zero, int nu1, int nu2, cudaStream_t s,
                       double** result);
 }  // namespace mgb

@@ -16,6 +16,8 @@ Outputs (committed, small):
     case_<name>.npz              full hierarchies: per-level A, per-level K
         (small cases), f, residual history, u after N cycles.
     c1.npz                       config 1 (255^2, V(2,2), 20 cycles) history + u.
+    krylov.npz                   fgmres / gmres (krylov.py) with grid_action and
+        cycle_preconditioner: histories, iteration counts, solutions.
 """
 
 from __future__ import annotations
@@ -189,7 +191,64 @@ def make_problem_pins():
     np.savez_compressed(os.path.join(HERE, "problems.npz"), **d)
 
 
+def make_krylov(nets):
+    """krylov.npz: the reference's fgmres / gmres (krylov.py) with grid_action and
+    cycle_preconditioner on small stencil problems."""
+    from mgsmooth import krylov as rk
+    d = {}
+    n = 31
+    A = gen.rotated_fd(n, math.pi / 6, 0.01)     # the conv net's training operator family
+    full = np.ones((n, n), bool)
+    lsh = gen.geometry_mask("lshape", n)
+    Av = rp.assemble_variable_diffusion(rg.full_spec(n), 10.0).data
+    cases = [
+        # name, A, mask, smoother/net, nu (None = no preconditioner), method, tol, max_iter, restart
+        ("fg_conv_v11", A, full, nets["conv"], 1, "fgmres", 1e-10, 30, None),
+        ("fg_conv_v22", A, full, nets["conv"], 2, "fgmres", 1e-10, 30, None),
+        ("fg_lshape_v11", A, lsh, nets["conv"], 1, "fgmres", 1e-10, 30, None),
+        ("fg_var_v22", Av, full, nets["conv"], 2, "fgmres", 1e-10, 30, 6),
+        ("fg_jacobi_v11", A, full, "jacobi", 1, "fgmres", 1e-9, 40, None),
+        ("fg_none_restart", A, full, None, None, "fgmres", 1e-8, 60, 8),
+        ("fg_maxiter", A, full, nets["conv"], 1, "fgmres", 1e-14, 3, None),
+        ("gm_restart", A, full, None, None, "gmres", 1e-9, 80, 10),
+        ("gm_lshape", A, lsh, None, None, "gmres", 1e-8, 50, None),
+    ]
+    for name, Ac, mask, sm, nu, method, tol, max_iter, restart in cases:
+        spec = spec_of(mask, 1 / (n + 1))
+        S = rg.StencilField(spec, Ac)
+        f = np.where(mask, gen.uniform_rhs(n, 9), 0.0).ravel()
+        cfg = rk.FgmresConfig(tol=tol, max_iter=max_iter, restart=restart)
+        pc = None
+        if nu is not None:
+            hier = rh.build_hierarchy(S, 4)
+            if sm == "jacobi":
+                rh.equip_classical(hier, "jacobi")
+            else:
+                rh.equip_inferred(hier, sm)
+            if nu > 1:
+                for lev in hier.levels[:-1]:
+                    lev.smoother = RepeatedSmoother(lev.smoother, lev.operator, nu)
+            pc = rk.cycle_preconditioner(hier)
+        if method == "fgmres":
+            u, rep = rk.fgmres(rk.grid_action(S), f, precond=pc, cfg=cfg)
+        else:
+            u, rep = rk.gmres(rk.grid_action(S), f, cfg=cfg)
+        d[f"{name}/A"] = Ac
+        d[f"{name}/mask"] = mask
+        d[f"{name}/f"] = f
+        d[f"{name}/u"] = u
+        d[f"{name}/history"] = np.array(rep.history)
+        d[f"{name}/meta"] = np.array([-1 if nu is None else nu, 0 if method == "fgmres" else 1, tol, max_iter,
+                                      0 if restart is None else restart, rep.iterations, int(rep.converged)])
+        d[f"{name}/smoother"] = np.array("none" if sm is None else ("jacobi" if sm == "jacobi" else "conv"))
+        print(f"krylov {name}: iters={rep.iterations} conv={rep.converged} hist[-1]={rep.history[-1]:.3e}")
+    np.savez_compressed(os.path.join(HERE, "krylov.npz"), **d)
+
+
 def main():
+    if "--only-krylov" in sys.argv:
+        make_krylov(make_nets())
+        return
     make_problem_pins()
     nets = make_nets()
     make_ops()
@@ -232,6 +291,7 @@ def main():
     for i in range(2):
         run_case(f"c4_p{i}", gen.rotated_fd(n, theta[i], eps[i]), np.ones((n, n), bool), 8, nets["conv"], 1, 10,
                  gen.uniform_rhs(n, [4, i]), 1 / (n + 1), store_levels=False)
+    make_krylov(nets)
 
 
 if __name__ == "__main__":

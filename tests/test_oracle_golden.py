@@ -109,3 +109,39 @@ def test_config1_history(name, nets):
     u, hist = mo.run_cycles(h, c["f"], c["cycles"], c["nu"], c["nu"])
     assert np.all(np.abs(hist - g["history"]) <= 1e-10 * np.abs(g["history"]))
     assert rel_err(u, g["u"]) < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# Krylov (krylov.py): the oracle's fgmres / gmres against the reference's runs
+
+from krylov_cases import krylov_case, krylov_names  # noqa: E402
+
+
+@pytest.mark.parametrize("name", krylov_names())
+def test_krylov_oracle_matches_reference(name, nets):
+    c = krylov_case(name)
+    mask = c["mask"]
+    act = mo.grid_action(c["A"], mask)
+    pc = None
+    if c["nu"] > 0:
+        h = mo.build_hierarchy(c["A"], 4, mask)
+        h = mo.equip_jacobi(h) if c["smoother"] == "jacobi" else mo.equip_inferred(h, nets["conv"])
+        pc = mo.cycle_preconditioner(h, c["nu"], c["nu"])
+    if c["method"] == "fgmres":
+        u, it, hist, conv = mo.fgmres(act, c["f"], pc, c["tol"], c["max_iter"], c["restart"])
+    else:
+        u, it, hist, conv = mo.gmres(act, c["f"], c["tol"], c["max_iter"], c["restart"])
+    assert it == c["iterations"] and conv == c["converged"]
+    assert len(hist) == len(c["history"])
+    assert np.allclose(hist, c["history"], rtol=1e-12, atol=0), np.max(np.abs(np.array(hist) / c["history"] - 1))
+    assert rel_err(u, c["u"]) <= 1e-11
+
+
+def test_fgmres_config_validation():
+    import paper_2102_12071_b200 as mg
+    with pytest.raises(mg.ConfigError):
+        mg.FgmresConfig(tol=0.0)
+    with pytest.raises(mg.ConfigError):
+        mg.FgmresConfig(restart=0)
+    with pytest.raises(mg.ConfigError):
+        mg.FgmresConfig(max_iter=0)
