@@ -208,6 +208,13 @@ int mgb_run_cycles(const mgb_hier* h, mgb_work* w, const double* f_dev, double* 
 int mgb_run_cycles_host(const mgb_hier* h, mgb_work* w, const double* f_host, double* u_host,
                         int nu1, int nu2, int cycles, int u_zero, double* history_host,
                         void* stream);
+/* A stream of `count` independent host-buffer solves (each as mgb_run_cycles_host),
+   pipelined: the host->device copy of solve k+1 and the device->host copy of solve
+   k overlap the cycles of solve k (two staging sets, two copy streams).  Returns
+   after every copy has landed. */
+int mgb_run_cycles_host_many(const mgb_hier* h, mgb_work* w, int count, const double* const* f_hosts,
+                             double* const* u_hosts, int nu1, int nu2, int cycles, int u_zero,
+                             double* const* history_hosts, void* stream);
 
 /* solve (hierarchy.py:119-146) for batch == 1: loop until history < tol or max_iter,
    NonConvergedError (MGB_NONCONVERGED) when rr is non-finite or > 1e6 max(r0, tol).

@@ -65,6 +65,7 @@ SIGNATURES = {
     "mgb_vcycle": (I, [P, P, I, P, P, I, I, P]),
     "mgb_run_cycles": (I, [P, P, P, P, I, I, I, I, P, P]),
     "mgb_run_cycles_host": (I, [P, P, P, P, I, I, I, I, P, P]),
+    "mgb_run_cycles_host_many": (I, [P, P, I, P, P, I, I, I, I, P, P]),
     "mgb_solve": (I, [P, P, P, P, I, I, D, I, PD, PI, PI, PI, PD, P]),
     "mgb_krylov": (I, [I, I, I, P, P, P, I, I, P, P, D, I, I, PD, PI, PI, PI, P]),
     "mgb_dd_nccl_unique_id": (I, [P]),

@@ -123,6 +123,12 @@ struct mgb_work {
   double* scratch = nullptr;  // batch x 4 (solve history slots)
   double *hf = nullptr, *hu = nullptr, *hh = nullptr;  // host-call staging (level 0 f, u, history)
   int64_t hh_cap = 0;
+  // second staging set + copy streams / events of the pipelined host call
+  double *hf2 = nullptr, *hu2 = nullptr, *hh2 = nullptr;
+  double* hist_pinned = nullptr;  // pinned host staging of the histories (pageable copies would block)
+  int64_t hist_pinned_cap = 0;
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   std::vector<GraphEntry> graphs;
   int graph_version = -1;   // hierarchy version the cached graphs were captured against
   int64_t last_launches = 0;
@@ -138,6 +144,15 @@ struct mgb_work {
     dfree(hf);
     dfree(hu);
     dfree(hh);
+    dfree(hf2);
+    dfree(hu2);
+    dfree(hh2);
+    if (hist_pinned) cudaFreeHost(hist_pinned);
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t e : {ev_in[b], ev_done[b], ev_out[b]})
+        if (e) cudaEventDestroy(e);
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
     if (cap) cudaStreamDestroy(cap);
   }
 };
@@ -1414,6 +1429,84 @@ extern "C" int mgb_run_cycles_host(const mgb_hier* h, mgb_work* w, const double*
   MGB_CUDA_TRY(cudaMemcpyAsync(u_host, w->hu, cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
   MGB_CUDA_TRY(cudaMemcpyAsync(history_host, w->hh, nh * sizeof(double), cudaMemcpyDeviceToHost, s));
   MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  return MGB_OK;
+}
+
+// A stream of `count` independent solves with host buffers, pipelined: the
+// host->device copy of solve k+1 (copy stream cin) and the device->host copy of
+// solve k (copy stream cout) overlap the cycles of solve k (stream `stream`);
+// two staging sets alternate.  Same per-solve semantics as mgb_run_cycles_host.
+extern "C" int mgb_run_cycles_host_many(const mgb_hier* h, mgb_work* w, int count, const double* const* f_hosts,
+                                        double* const* u_hosts, int nu1, int nu2, int cycles, int u_zero,
+                                        double* const* history_hosts, void* stream) {
+  if (!h || !w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
+  if (count < 0 || !f_hosts || !u_hosts || !history_hosts) return fail(MGB_CONTRACT, "null host buffer list");
+  if (cycles < 0 || nu1 < 0 || nu2 < 0) return fail(MGB_CONFIG, "counts must be non-negative");
+  for (int k = 0; k < count; ++k)
+    if (!f_hosts[k] || !u_hosts[k] || !history_hosts[k]) return fail(MGB_CONTRACT, "null host buffer");
+  if (int st = check_equipped(h)) return st;
+  DeviceGuard dg(h->device);
+  cudaStream_t s = S(stream);
+  const size_t cnt = (size_t)h->batch * h->lv[0].n;
+  const int64_t nh = (int64_t)h->batch * (cycles + 1);
+  if (!w->hf) MGB_CUDA_TRY(dalloc(&w->hf, cnt));
+  if (!w->hu) MGB_CUDA_TRY(dalloc(&w->hu, cnt));
+  if (!w->hf2) MGB_CUDA_TRY(dalloc(&w->hf2, cnt));
+  if (!w->hu2) MGB_CUDA_TRY(dalloc(&w->hu2, cnt));
+  if (nh > w->hh_cap) {
+    dfree(w->hh);
+    dfree(w->hh2);
+    MGB_CUDA_TRY(dalloc(&w->hh, (size_t)nh));
+    w->hh_cap = nh;
+  }
+  if (!w->hh2) MGB_CUDA_TRY(dalloc(&w->hh2, (size_t)w->hh_cap));
+  if (!w->cin) MGB_CUDA_TRY(cudaStreamCreateWithFlags(&w->cin, cudaStreamNonBlocking));
+  if (!w->cout) MGB_CUDA_TRY(cudaStreamCreateWithFlags(&w->cout, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b)
+    for (cudaEvent_t* e : {&w->ev_in[b], &w->ev_done[b], &w->ev_out[b]})
+      if (!*e) MGB_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  if ((int64_t)count * nh > w->hist_pinned_cap) {
+    if (w->hist_pinned) cudaFreeHost(w->hist_pinned);
+    w->hist_pinned = nullptr;
+    MGB_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&w->hist_pinned), sizeof(double) * count * nh));
+    w->hist_pinned_cap = (int64_t)count * nh;
+  }
+  double* hf[2] = {w->hf, w->hf2};
+  double* hu[2] = {w->hu, w->hu2};
+  double* hh[2] = {w->hh, w->hh2};
+  // the copy streams start after everything already queued on `stream`
+  MGB_CUDA_TRY(cudaEventRecord(w->ev_done[0], s));
+  MGB_CUDA_TRY(cudaEventRecord(w->ev_done[1], s));
+  MGB_CUDA_TRY(cudaEventRecord(w->ev_out[0], s));
+  MGB_CUDA_TRY(cudaEventRecord(w->ev_out[1], s));
+  for (int k = 0; k < count; ++k) {
+    const int b = k & 1;
+    // inputs of solve k once solve k-2 no longer reads this staging set
+    MGB_CUDA_TRY(cudaStreamWaitEvent(w->cin, w->ev_done[b], 0));
+    MGB_CUDA_TRY(cudaMemcpyAsync(hf[b], f_hosts[k], cnt * sizeof(double), cudaMemcpyHostToDevice, w->cin));
+    if (!u_zero) {
+      MGB_CUDA_TRY(cudaStreamWaitEvent(w->cin, w->ev_out[b], 0));
+      MGB_CUDA_TRY(cudaMemcpyAsync(hu[b], u_hosts[k], cnt * sizeof(double), cudaMemcpyHostToDevice, w->cin));
+    }
+    MGB_CUDA_TRY(cudaEventRecord(w->ev_in[b], w->cin));
+    // cycles of solve k after its inputs arrived and solve k-2's results left
+    MGB_CUDA_TRY(cudaStreamWaitEvent(s, w->ev_in[b], 0));
+    MGB_CUDA_TRY(cudaStreamWaitEvent(s, w->ev_out[b], 0));
+    GraphKey key{hf[b], hu[b], nu1, nu2, cycles, u_zero ? 1 : 0, 0, hh[b]};
+    if (int st = launch_graph(w, key, s)) return st;
+    MGB_CUDA_TRY(cudaEventRecord(w->ev_done[b], s));
+    // results of solve k
+    MGB_CUDA_TRY(cudaStreamWaitEvent(w->cout, w->ev_done[b], 0));
+    MGB_CUDA_TRY(cudaMemcpyAsync(u_hosts[k], hu[b], cnt * sizeof(double), cudaMemcpyDeviceToHost, w->cout));
+    MGB_CUDA_TRY(cudaMemcpyAsync(w->hist_pinned + (int64_t)k * nh, hh[b], nh * sizeof(double),
+                                 cudaMemcpyDeviceToHost, w->cout));
+    MGB_CUDA_TRY(cudaEventRecord(w->ev_out[b], w->cout));
+  }
+  MGB_CUDA_TRY(cudaStreamSynchronize(w->cin));
+  MGB_CUDA_TRY(cudaStreamSynchronize(w->cout));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int k = 0; k < count; ++k)
+    std::memcpy(history_hosts[k], w->hist_pinned + (int64_t)k * nh, sizeof(double) * nh);
   return MGB_OK;
 }
 

@@ -36,7 +36,10 @@
 namespace mgb {
 namespace {
 
-constexpr int SWT = 128;   // threads (= columns incl. halo) per CTA
+#ifndef MGB_SWT
+#define MGB_SWT 128
+#endif
+constexpr int SWT = MGB_SWT;  // threads (= columns incl. halo) per CTA
 constexpr int PD = 8;      // prefetch ring depth (rows) for u (power of two)
 constexpr int PDF = 16;    // ring depth for f (also read by the later residual stages): rows t-10 .. t+DIST
 constexpr int DIST = 5;    // prefetch distance (rows ahead)

@@ -293,6 +293,32 @@ class MultigridHierarchy:
             self.release_work(w)
         return history_host
 
+    def run_cycles_host_many(self, f_hosts, u_hosts, cycles: int, nu1: int | None = None, nu2: int | None = None,
+                             history_hosts=None, u_zero: bool = False, stream=None):
+        """A stream of independent host-buffer solves (mgb_run_cycles_host_many):
+        copies of neighbouring solves overlap each solve's cycles.  Lists of
+        C-contiguous fp64 arrays (pinned for full-speed copies); u_hosts updated
+        in place; returns the list of (batch, cycles + 1) histories."""
+        nu1, nu2 = self._sweeps(nu1, nu2)
+        count = len(f_hosts)
+        if len(u_hosts) != count:
+            raise ContractError("f_hosts and u_hosts differ in length")
+        if history_hosts is None:
+            history_hosts = [np.empty((self.batch, cycles + 1)) for _ in range(count)]
+        for a in list(f_hosts) + list(u_hosts) + list(history_hosts):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ContractError("host buffers must be C-contiguous float64")
+        arr = lambda xs: (C.c_void_p * max(count, 1))(*[x.ctypes.data for x in xs])  # noqa: E731
+        fp, up, hp = arr(f_hosts), arr(u_hosts), arr(history_hosts)
+        w = self.acquire_work()
+        try:
+            _lib.call("mgb_run_cycles_host_many", self._h, w, count, C.cast(fp, C.c_void_p), C.cast(up, C.c_void_p),
+                      nu1, nu2, int(cycles), 1 if u_zero else 0, C.cast(hp, C.c_void_p), stream)
+            self.last_launches = int(_lib.lib().mgb_last_launch_count(w))
+        finally:
+            self.release_work(w)
+        return history_hosts
+
     def solve_device(self, f, u, tol: float = 1e-6, max_iter: int = 100, nu1=None, nu2=None) -> SolveReport:
         nu1, nu2 = self._sweeps(nu1, nu2)
         hist = np.zeros(max_iter + 1)
