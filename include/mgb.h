@@ -163,6 +163,22 @@ int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const double* wei
                             int64_t n_weights, double slope, int precision, void* stream);
 /* equip_classical(kind="jacobi") (hierarchy.py:152-161, smoothers.py:29-50). */
 int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream);
+/* Shared-kernel convolutional smoother on level `level` (ConvSmoother,
+   smoothers.py:105-145; equip_conv_init / retarget / equip_trained,
+   hierarchy.py:164-204): M(r) = gain * (L_{nl-1} * act(... act(L_0 * r)) + S * r)
+   with nl 3x3 layer kernels (layers_host: nl x 9, [di+1][dj+1]), skip kernel S
+   (skip_host: 9, NULL = none), leaky(slope) between chained layers when leaky != 0.
+   Replaces any per-point smoother on that level. */
+int mgb_hier_set_conv_smoother(mgb_hier* h, int level, int nl, const double* layers_host,
+                               const double* skip_host, int leaky, double slope, double gain);
+/* convolve (grid.py:229-239): out = mask ? sum over non-zero w of w * u(p + o) : 0,
+   zero padding; w_host: 9 weights.  Bit-identical to the reference. */
+int mgb_convolve(int batch, int rows, int cols, const double* w_host, const uint8_t* mask_dev,
+                 const double* u_dev, double* out_dev, void* stream);
+/* ConvSmoother.apply (smoothers.py:133-145): out = M(r).  Bit-identical. */
+int mgb_conv_smoother_apply(int batch, int rows, int cols, int nl, const double* layers_host,
+                            const double* skip_host, int leaky, double slope, double gain,
+                            const uint8_t* mask_dev, const double* r_dev, double* out_dev, void* stream);
 /* install explicit kernels on one level: (batch, rows, cols, kst, 3, 3) host or device. */
 int mgb_hier_set_kernels(mgb_hier* h, int level, int kst, const double* K, int on_device,
                          double slope, void* stream);

@@ -409,12 +409,97 @@ def coarse_solve(h: Hierarchy, f: np.ndarray) -> np.ndarray:
 
 def _smooth(h: Hierarchy, l: int, r: np.ndarray, nu: int) -> np.ndarray:
     """RepeatedSmoother(M, A, nu).apply(r) (cli.py:373-377): c = M r, then
-    nu - 1 times c <- c + M(r - A c)."""
+    nu - 1 times c <- c + M(r - A c).  M: per-point kernels or a ConvSm."""
     K, m = h.kernels[l], h.masks[l]
-    c = smoother_apply(K, r, m, h.slope)
+    M = (lambda x: conv_apply(K, x, m)) if isinstance(K, ConvSm) else (lambda x: smoother_apply(K, x, m, h.slope))
+    c = M(r)
     for _ in range(nu - 1):
-        c = masked(c + smoother_apply(K, masked(r - apply_stencil(h.ops[l], c, m), m), m, h.slope), m)
+        c = masked(c + M(masked(r - apply_stencil(h.ops[l], c, m), m)), m)
     return c
+
+
+# --------------------------------------------------------------------------
+# shared-kernel convolutional smoother (grid.py:229-266, smoothers.py:99-178)
+
+def convolve(w: np.ndarray, u: np.ndarray, mask: np.ndarray | None = None) -> np.ndarray:
+    """grid.py:229-239: out += w[o] * u(p + o) over the non-zero weights,
+    di-major, zero padding, output re-masked."""
+    r = w.shape[0] // 2
+    out = np.zeros(u.shape)
+    for di in range(-r, r + 1):
+        for dj in range(-r, r + 1):
+            wo = w[di + r, dj + r]
+            if wo != 0.0:
+                out += wo * neighbor(u, di, dj)
+    if mask is not None:
+        out[~mask] = 0.0
+    return out
+
+
+@dataclass
+class ConvSm:
+    """ConvSmoother (smoothers.py:105-130) parameters."""
+    layers: list
+    skip: np.ndarray | None
+    activation: str = "linear"
+    slope: float = LEAKY_SLOPE
+    gain: float = 1.0
+
+
+def conv_apply(s: ConvSm, r: np.ndarray, mask: np.ndarray) -> np.ndarray:
+    """ConvSmoother.apply (smoothers.py:133-145)."""
+    v = convolve(s.layers[0], r, mask)
+    for w in s.layers[1:]:
+        if s.activation == "leaky":
+            v = leaky(v, s.slope)
+        v = convolve(w, v, mask)
+    out = v
+    if s.skip is not None:
+        out = out + convolve(s.skip, r, mask)
+    return s.gain * out
+
+
+def representative_diagonal(A: np.ndarray, mask: np.ndarray) -> float:
+    """smoothers.py:99-102."""
+    return float(np.median(A[:, :, 1, 1][mask]))
+
+
+def conv_init(A: np.ndarray, mask: np.ndarray, form: str = "full", omega: float = 2.0 / 3.0,
+              activation: str = "linear") -> ConvSm:
+    """conv_smoother (smoothers.py:148-164): Jacobi-equivalent initialisation."""
+    jk = np.zeros((3, 3))
+    jk[1, 1] = omega
+    gain = 1.0 / representative_diagonal(A, mask)
+    if form == "full":
+        return ConvSm([np.zeros((3, 3)) for _ in range(5)], jk, activation, gain=gain)
+    delta = np.zeros((3, 3))
+    delta[1, 1] = 1.0
+    return ConvSm([delta, jk], None, activation, gain=gain)
+
+
+def compose(outer: np.ndarray, inner: np.ndarray) -> np.ndarray:
+    """compose_kernels (grid.py:242-256)."""
+    k1, k2 = outer.shape[0], inner.shape[0]
+    out = np.zeros((k1 + k2 - 1, k1 + k2 - 1))
+    for i in range(k1):
+        for j in range(k1):
+            if outer[i, j] != 0.0:
+                out[i:i + k2, j:j + k2] += outer[i, j] * inner
+    return out
+
+
+def effective_kernel(s: ConvSm) -> np.ndarray:
+    """smoothers.py:167-178 with pad_kernel (grid.py:259-266)."""
+    acc = s.layers[0]
+    for w in s.layers[1:]:
+        acc = compose(w, acc)
+    out = acc.copy()
+    if s.skip is not None:
+        off = (acc.shape[0] - s.skip.shape[0]) // 2
+        pad = np.zeros(acc.shape)
+        pad[off:off + s.skip.shape[0], off:off + s.skip.shape[0]] = s.skip
+        out = out + pad
+    return s.gain * out
 
 
 def v_cycle(h: Hierarchy, l: int, f: np.ndarray, u: np.ndarray, nu1: int = 1, nu2: int = 1) -> np.ndarray:

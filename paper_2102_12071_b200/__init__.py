@@ -10,14 +10,15 @@ in hand-written sm_100a CUDA kernels behind the C-ABI in include/mgb.h
 
 from .errors import (ConfigError, ContractError, MgError, NonConvergedError, NumericError,
                      SingularMatrixError, TrainingError, UnsupportedOperationError)
-from .grid import (GridFunction, GridSpec, StencilField, apply_stencil, constant_stencil, from_active,
-                   full_spec, to_active, zeros)
+from .grid import (ConvKernel, GridFunction, GridSpec, StencilField, apply_stencil, compose_kernels,
+                   constant_stencil, convolve, delta_kernel, from_active, full_spec, pad_kernel, to_active, zeros)
 from .transfer import TransferPair, coarsen_full, galerkin_product, prolong, restrict
-from .smoothers import (InferredSmoother, JacobiSmoother, KernelInferenceNet, infer_kernels, inference_net,
-                        jacobi, load_model, save_model)
+from .smoothers import (ConvSmoother, InferredSmoother, JacobiSmoother, KernelInferenceNet, conv_smoother,
+                        effective_kernel, infer_kernels, inference_net, jacobi, load_model, model_from_dict,
+                        model_to_dict, representative_diagonal, save_model)
 from .hierarchy import (Level, MultigridHierarchy, RepeatedSmoother, SolveReport, build_hierarchy,
                         build_hierarchy_batch, build_hierarchy_classed, coarse_solve, cycle_correction, equip_classical,
-                        equip_inferred, solve, v_cycle)
+                        equip_conv_init, equip_inferred, equip_trained, retarget, solve, v_cycle)
 from .krylov import (CyclePreconditioner, FgmresConfig, GridAction, KrylovReport, cycle_preconditioner, fgmres,
                      gmres, grid_action)
 

@@ -16,6 +16,7 @@
 #include "mgb_stream.h"
 #include "mgb_tile.h"
 #include "mgb_coarse.h"
+#include "mgb_conv.h"
 #include "mgb_dd.h"
 #include "mgb_internal.h"
 
@@ -57,6 +58,8 @@ struct LevelD {
   double hAint[9] = {0}, hKint[9] = {0};  // interior-class weights (host copy, batch 0)
   std::vector<uint8_t> hmask;
   int64_t nact = 0;
+  ConvSm conv;             // shared-kernel convolutional smoother (conv.nl > 0 replaces K)
+  bool has_smoother() const { return K != nullptr || conv.nl > 0; }
   Op opA() const { return Op{A, Acls, n, 1}; }
   Op opK() const { return Op{K == Kcls ? nullptr : K, Kcls, n, ks}; }
 };
@@ -582,6 +585,73 @@ extern "C" int mgb_hier_set_passes(mgb_hier* h, int64_t stream_min, int tile, in
   return MGB_OK;
 }
 
+extern "C" int mgb_hier_set_conv_smoother(mgb_hier* h, int level, int nl, const double* layers_host,
+                                          const double* skip_host, int leaky, double slope, double gain) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (level < 0 || level + 1 >= h->depth()) return fail(MGB_CONFIG, "level has no smoother slot");
+  if (nl < 1 || nl > CONV_MAX_LAYERS) return fail(MGB_CONFIG, "conv smoother needs 1..8 layers");
+  if (!layers_host) return fail(MGB_CONTRACT, "null layer weights");
+  DeviceGuard dg(h->device);
+  LevelD& l = h->lv[level];
+  ConvSm cs;
+  cs.nl = nl;
+  for (int q = 0; q < nl; ++q)
+    for (int o = 0; o < 9; ++o) cs.layer[q].w[o] = layers_host[q * 9 + o];
+  cs.has_skip = skip_host != nullptr;
+  if (skip_host)
+    for (int o = 0; o < 9; ++o) cs.skip.w[o] = skip_host[o];
+  cs.leaky = leaky != 0;
+  cs.slope = slope;
+  cs.gain = gain;
+  for (int q = 0; q < nl * 9; ++q)
+    if (!std::isfinite(layers_host[q])) return fail(MGB_NUMERIC, "non-finite kernel weights");
+  if (!std::isfinite(gain)) return fail(MGB_NUMERIC, "non-finite gain");
+  if (l.K == l.Kcls) l.K = nullptr;
+  dfree(l.K);
+  dfree(l.Kcls);
+  l.ks = 0;
+  l.conv = cs;
+  ++h->version;
+  return MGB_OK;
+}
+
+extern "C" int mgb_convolve(int batch, int rows, int cols, const double* w_host, const uint8_t* mask_dev,
+                            const double* u_dev, double* out_dev, void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (!w_host) return fail(MGB_CONTRACT, "null kernel");
+  ConvW w;
+  for (int o = 0; o < 9; ++o) w.w[o] = w_host[o];
+  MGB_CUDA_TRY(launch_convolve(Grid{batch, rows, cols}, w, mask_dev, u_dev, out_dev, false, 0.0, S(stream)));
+  return MGB_OK;
+}
+
+extern "C" int mgb_conv_smoother_apply(int batch, int rows, int cols, int nl, const double* layers_host,
+                                       const double* skip_host, int leaky, double slope, double gain,
+                                       const uint8_t* mask_dev, const double* r_dev, double* out_dev, void* stream) {
+  if (int st = check_dims(batch, rows, cols)) return st;
+  if (nl < 1 || nl > CONV_MAX_LAYERS || !layers_host) return fail(MGB_CONFIG, "conv smoother needs 1..8 layers");
+  ConvSm cs;
+  cs.nl = nl;
+  for (int q = 0; q < nl; ++q)
+    for (int o = 0; o < 9; ++o) cs.layer[q].w[o] = layers_host[q * 9 + o];
+  cs.has_skip = skip_host != nullptr;
+  if (skip_host)
+    for (int o = 0; o < 9; ++o) cs.skip.w[o] = skip_host[o];
+  cs.leaky = leaky != 0;
+  cs.slope = slope;
+  cs.gain = gain;
+  const Grid g{batch, rows, cols};
+  double *t1 = nullptr, *t2 = nullptr;
+  const size_t bytes = sizeof(double) * g.n() * batch;
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t1), bytes, S(stream)));
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t2), bytes, S(stream)));
+  cudaError_t e = conv_smoother_apply(g, cs, mask_dev, r_dev, nullptr, out_dev, t1, t2, S(stream));
+  cudaFreeAsync(t1, S(stream));
+  cudaFreeAsync(t2, S(stream));
+  MGB_CUDA_TRY(e);
+  return MGB_OK;
+}
+
 extern "C" int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_classed) {
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
@@ -749,6 +819,7 @@ extern "C" int mgb_hier_get_kernels(const mgb_hier* h, int level, double* out_ho
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
   const LevelD& l = h->lv[level];
+  if (l.conv.nl > 0) return fail(MGB_CONFIG, "level " + std::to_string(level) + " has a convolutional smoother (no per-point kernels)");
   if (!l.K) return fail(MGB_CONFIG, "level " + std::to_string(level) + " has no smoother installed");
   return download_table(h, l, h->classed_only ? l.Kcls : l.K, l.ks, out_host);
 }
@@ -769,6 +840,7 @@ extern "C" int mgb_hier_operator_planes(const mgb_hier* h, int level, const doub
 
 static int alloc_kernels(mgb_hier* h, LevelD& l, int kst) {
   ++h->version;
+  l.conv.nl = 0;
   if (h->classed_only) {
     if (l.Kcls && l.ks == kst) return MGB_OK;
     dfree(l.Kcls);
@@ -999,6 +1071,17 @@ static int sweep(mgb_work* w, int l, const double* f, const double* in, double* 
   const mgb_hier* h = w->h;
   const LevelD& lv = h->lv[l];
   const Grid g = h->grid(l);
+  if (lv.conv.nl > 0) {
+    // u_out = u_in + M(f - A u_in) with the layer chain in v[l] / out
+    if (int st = ensure_generic(w, l)) return st;
+    const double* r = f;
+    if (in) {
+      MGB_CUDA_TRY(launch_residual(g, tabA(h, lv), lv.mask, f, in, w->r[l], nullptr, nullptr, s));
+      r = w->r[l];
+    }
+    MGB_CUDA_TRY(conv_smoother_apply(g, lv.conv, lv.mask, r, in, out, w->v[l], out, s));
+    return MGB_OK;
+  }
   if (lv.ks == 1) {
     MGB_CUDA_TRY(launch_sweep2(g, lv.opA(), lv.opK(), lv.mask, f, in, out, nullptr, s));
     return MGB_OK;
@@ -1190,7 +1273,7 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
     return MGB_OK;
   }
   const LevelD& lv = h->lv[l];
-  if (!lv.K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+  if (!lv.has_smoother()) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
   if (!hist && l > 0 && l == coarse_first_level(h) && u == w->u[l] && f == w->f[l] && w->r[l]) {
     if (int st = enqueue_coarse(w, l, zero, nu1, nu2, s)) return st;
     *result = u;
@@ -1247,7 +1330,7 @@ static int enqueue_vcycle(mgb_work* w, int l, const double* f, double* u, int nu
 
 static int check_equipped(const mgb_hier* h) {
   for (int l = 0; l + 1 < h->depth(); ++l)
-    if (!h->lv[l].K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+    if (!h->lv[l].has_smoother()) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
   return MGB_OK;
 }
 
@@ -1258,7 +1341,7 @@ extern "C" int mgb_vcycle(const mgb_hier* h, mgb_work* w, int level, const doubl
   if (nu1 < 0 || nu2 < 0) return fail(MGB_CONFIG, "sweep counts must be non-negative");
   DeviceGuard dg(h->device);
   for (int l = level; l + 1 < h->depth(); ++l)
-    if (!h->lv[l].K) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
+    if (!h->lv[l].has_smoother()) return fail(MGB_CONFIG, "level " + std::to_string(l) + " has no smoother installed");
   if (int st = prepare_work(w)) return st;
   const int64_t l0 = g_launches;
   int st = enqueue_vcycle(w, level, f_dev, u_dev, nu1, nu2, S(stream));
@@ -1270,7 +1353,7 @@ extern "C" int mgb_smooth(const mgb_hier* h, mgb_work* w, int level, const doubl
                           int sweeps, void* stream) {
   if (int st = check_level(h, level, true)) return st;
   if (!w || w->h != h) return fail(MGB_CONTRACT, "workspace does not belong to this hierarchy");
-  if (!h->lv[level].K) return fail(MGB_CONFIG, "level " + std::to_string(level) + " has no smoother installed");
+  if (!h->lv[level].has_smoother()) return fail(MGB_CONFIG, "level " + std::to_string(level) + " has no smoother installed");
   DeviceGuard dg(h->device);
   cudaStream_t s = S(stream);
   double* cur = u_dev;
@@ -1292,7 +1375,7 @@ static int coarse_first_level(const mgb_hier* h);
 
 int prepare_work(mgb_work* w) {
   for (int l = 0; l + 1 < w->h->depth(); ++l)
-    if (w->h->lv[l].ks > 1)
+    if (w->h->lv[l].ks > 1 || w->h->lv[l].conv.nl > 0)
       if (int st = ensure_generic(w, l)) return st;
   const int lc = coarse_first_level(w->h);
   if (lc >= 0)

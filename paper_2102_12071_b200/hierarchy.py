@@ -23,7 +23,8 @@ import numpy as np
 from . import _lib, device as dv
 from .errors import ConfigError, ContractError, UnsupportedOperationError
 from .grid import GridFunction, GridSpec, StencilField, apply_stencil, zeros
-from .smoothers import (LEAKY_SLOPE, VARIANT_ID, InferredSmoother, JacobiSmoother, KernelInferenceNet)
+from .smoothers import (LEAKY_SLOPE, VARIANT_ID, ConvSmoother, InferredSmoother, JacobiSmoother, KernelInferenceNet,
+                        conv_smoother, representative_diagonal)
 from .transfer import TransferPair, coarsen_full
 
 
@@ -237,6 +238,15 @@ class MultigridHierarchy:
     def _install(self, l: int, sm):
         """Upload an arbitrary per-point smoother (InferredSmoother / JacobiSmoother)."""
         if isinstance(sm, DeviceSmoother) and sm._hier is self:
+            self._installed[l] = sm
+            return
+        if isinstance(sm, ConvSmoother):
+            if sm.spec != self.levels[l].spec:
+                raise ContractError(f"smoother on level {l} is bound to a different grid")
+            layers, skip = sm.device_args()
+            _lib.call("mgb_hier_set_conv_smoother", self._h, l, len(sm.layers), layers.ctypes.data_as(_lib.P),
+                      None if skip is None else skip.ctypes.data_as(_lib.P), 1 if sm.activation == "leaky" else 0,
+                      float(sm.slope), float(sm.gain))
             self._installed[l] = sm
             return
         if isinstance(sm, JacobiSmoother):
@@ -488,6 +498,37 @@ def equip_classical(hier: MultigridHierarchy, kind: str = "jacobi", omega: float
     return hier
 
 
+def equip_conv_init(hier: MultigridHierarchy, omega: float = 2.0 / 3.0, activation: str = "linear") -> MultigridHierarchy:
+    """hierarchy.py:164-172: Jacobi-equivalent five-layer conv smoothers (full
+    coarsening) on every smoothed level, run on the GPU."""
+    for lev in hier.levels[:-1]:
+        lev.smoother = conv_smoother(lev.operator, "full", omega, activation)
+        hier._install(lev.index, lev.smoother)
+    return hier
+
+
+def retarget(sm: ConvSmoother, source: StencilField, target: StencilField) -> ConvSmoother:
+    """hierarchy.py:175-182: rebind a trained conv smoother to an operator of
+    another scale (ratio of representative diagonals in the gain)."""
+    gain = sm.gain * representative_diagonal(source) / representative_diagonal(target)
+    return ConvSmoother(target.spec, sm.form, list(sm.layers), sm.skip, sm.activation, sm.slope, gain)
+
+
+def equip_trained(target: MultigridHierarchy, source: MultigridHierarchy) -> MultigridHierarchy:
+    """hierarchy.py:185-204: install another hierarchy's conv smoothers level by
+    level (deeper targets reuse the deepest), re-scaled to the target operators."""
+    for l, lev in enumerate(target.levels[:-1]):
+        ls = min(l, source.depth - 2)
+        src = source.levels[ls].smoother
+        if src is None:
+            raise ConfigError(f"source level {ls} has no trained smoother")
+        if not isinstance(src, ConvSmoother):
+            raise ConfigError("only convolutional smoothers can be transported")
+        lev.smoother = retarget(src, source.levels[ls].operator, lev.operator)
+        target._install(l, lev.smoother)
+    return target
+
+
 def equip_inferred(hier: MultigridHierarchy, net: KernelInferenceNet, precision: int = 64) -> MultigridHierarchy:
     """hierarchy.py:207-214: CNN inference of every smoothed level on the device."""
     for lev in hier.levels[:-1]:
@@ -501,10 +542,3 @@ def equip_inferred(hier: MultigridHierarchy, net: KernelInferenceNet, precision:
         lev.smoother = sm
         hier._installed[lev.index] = sm
     return hier
-
-
-def equip_conv_init(*a, **k):
-    raise UnsupportedOperationError("shared-kernel ConvSmoother training is not on the B200 path")
-
-
-retarget = equip_trained = equip_conv_init

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _lib, device as dv
 from .errors import ConfigError, ContractError, UnsupportedOperationError
-from .grid import GridFunction, GridSpec, StencilField
+from .grid import (ConvKernel, GridFunction, GridSpec, StencilField, compose_kernels, delta_kernel, pad_kernel)
 
 LEAKY_SLOPE = 0.01
 _FC_SIZES = (81, 40, 40, 40)
@@ -155,12 +155,103 @@ def infer_kernels(net: KernelInferenceNet, A: StencilField, precision: int = 64)
 
 
 # ---------------------------------------------------------------------------
+# shared-kernel convolutional smoother (smoothers.py:99-178)
+
+def representative_diagonal(A: StencilField) -> float:
+    """smoothers.py:99-102: median active centre entry."""
+    return float(np.median(A.center()[A.spec.mask]))
+
+
+@dataclass
+class ConvSmoother:
+    """smoothers.py:105-145: form "full" = five chained 3x3 kernels plus a
+    parallel skip kernel, "rb" = two chained kernels and no skip; optional leaky
+    activation between chained layers; gain rescales the output.  ``apply`` and
+    the V-cycle run it on the GPU (mgb_conv.cu), bit-identical to the reference."""
+    spec: GridSpec
+    form: str
+    layers: list
+    skip: ConvKernel | None
+    activation: str = "linear"
+    slope: float = LEAKY_SLOPE
+    gain: float = 1.0
+
+    def __post_init__(self):
+        if self.form not in ("full", "rb"):
+            raise ConfigError(f"unknown smoother form {self.form!r}")
+        if self.form == "full" and (len(self.layers) != 5 or self.skip is None):
+            raise ConfigError("full form takes five layers and a skip kernel")
+        if self.form == "rb" and (len(self.layers) != 2 or self.skip is not None):
+            raise ConfigError("rb form takes two layers and no skip")
+        if self.activation not in ("linear", "leaky"):
+            raise ConfigError(f"unknown activation {self.activation!r}")
+
+    def device_args(self):
+        if any(k.size != 3 for k in self.layers) or (self.skip is not None and self.skip.size != 3):
+            raise UnsupportedOperationError("the device conv smoother takes 3x3 kernels")
+        layers = np.ascontiguousarray(np.stack([k.weights for k in self.layers]))
+        skip = None if self.skip is None else np.ascontiguousarray(self.skip.weights)
+        return layers, skip
+
+    def apply(self, r: GridFunction) -> GridFunction:
+        if r.spec != self.spec:
+            raise ContractError("conv smoother: residual on a different spec")
+        layers, skip = self.device_args()
+        x = dv.to_dev(r.values)
+        m = dv.mask_dev(r.spec.mask)
+        out = dv.empty(x.shape)
+        _lib.call("mgb_conv_smoother_apply", 1, r.spec.rows, r.spec.cols, len(self.layers),
+                  layers.ctypes.data_as(_lib.P), None if skip is None else skip.ctypes.data_as(_lib.P),
+                  1 if self.activation == "leaky" else 0, float(self.slope), float(self.gain), dv.ptr(m),
+                  dv.ptr(x), dv.ptr(out), dv.stream(out))
+        return GridFunction(self.spec, dv.host(out))
+
+    def is_linear(self) -> bool:
+        return self.activation == "linear"
+
+
+def conv_smoother(A: StencilField, form: str, omega: float = 2.0 / 3.0, activation: str = "linear") -> ConvSmoother:
+    """smoothers.py:148-164: initialisation reproducing weighted Jacobi exactly
+    (inverse representative diagonal in the gain)."""
+    jk = delta_kernel(3, omega)
+    gain = 1.0 / representative_diagonal(A)
+    if form == "full":
+        return ConvSmoother(A.spec, form, [ConvKernel(np.zeros((3, 3))) for _ in range(5)], jk, activation, gain=gain)
+    if form == "rb":
+        return ConvSmoother(A.spec, form, [delta_kernel(3), jk], None, activation, gain=gain)
+    raise ConfigError(f"unknown smoother form {form!r}")
+
+
+def effective_kernel(s: ConvSmoother) -> ConvKernel:
+    """smoothers.py:167-178: the single kernel a linear smoother equals."""
+    if s.activation != "linear":
+        raise UnsupportedOperationError("effective kernel undefined for nonlinear activation")
+    acc = s.layers[0]
+    for kern in s.layers[1:]:
+        acc = compose_kernels(kern, acc)
+    w = acc.weights
+    if s.skip is not None:
+        w = w + pad_kernel(s.skip, acc.size).weights
+    return ConvKernel(s.gain * w)
+
+
+# ---------------------------------------------------------------------------
 # model files (smoothers.py:349-414)
 
 FORMAT_VERSION = 1
 
 
+def _arrays_to_lists(ws):
+    return [{"shape": list(np.asarray(w).shape), "data": np.asarray(w).ravel().tolist()} for w in ws]
+
+
 def model_to_dict(model, metadata: dict | None = None) -> dict:
+    if isinstance(model, ConvSmoother):
+        return {"format_version": FORMAT_VERSION, "metadata": metadata or {}, "kind": "conv_smoother",
+                "form": model.form, "activation": model.activation, "slope": model.slope, "gain": model.gain,
+                "layers": _arrays_to_lists([k.weights for k in model.layers]),
+                "skip": _arrays_to_lists([model.skip.weights]) if model.skip is not None else None,
+                "spec": {"rows": model.spec.rows, "cols": model.spec.cols, "spacing": model.spec.spacing}}
     if not isinstance(model, KernelInferenceNet):
         raise ConfigError(f"cannot serialize {type(model).__name__}")
     return {"format_version": FORMAT_VERSION, "metadata": metadata or {}, "kind": "inference_net",
@@ -177,7 +268,13 @@ def model_from_dict(doc: dict, spec: GridSpec | None = None):
         ws = [np.array(it["data"], dtype=float).reshape(it["shape"]) for it in doc["weights"]]
         return KernelInferenceNet(doc["variant"], ws, int(doc["k"]), float(doc["slope"]))
     if kind == "conv_smoother":
-        raise UnsupportedOperationError("shared-kernel ConvSmoother is not on the B200 path yet")
+        if spec is None:
+            meta = doc["spec"]
+            spec = GridSpec(meta["rows"], meta["cols"], meta["spacing"], np.ones((meta["rows"], meta["cols"]), bool))
+        lists = lambda items: [np.array(it["data"], dtype=float).reshape(it["shape"]) for it in items]  # noqa: E731
+        layers = [ConvKernel(w) for w in lists(doc["layers"])]
+        skip = ConvKernel(lists(doc["skip"])[0]) if doc["skip"] is not None else None
+        return ConvSmoother(spec, doc["form"], layers, skip, doc["activation"], doc["slope"], doc["gain"])
     raise ConfigError(f"unknown model kind {kind!r}")
 
 

@@ -18,6 +18,8 @@ Outputs (committed, small):
     c1.npz                       config 1 (255^2, V(2,2), 20 cycles) history + u.
     krylov.npz                   fgmres / gmres (krylov.py) with grid_action and
         cycle_preconditioner: histories, iteration counts, solutions.
+    conv.npz                     shared-kernel ConvSmoother (smoothers.py:105-178,
+        hierarchy.py:164-204): convolve / apply / effective_kernel pins, V-cycles.
 """
 
 from __future__ import annotations
@@ -245,7 +247,112 @@ def make_krylov(nets):
     np.savez_compressed(os.path.join(HERE, "krylov.npz"), **d)
 
 
+def _conv_params(sm):
+    return {"form": np.array(sm.form), "activation": np.array(sm.activation), "slope": sm.slope, "gain": sm.gain,
+            "layers": np.stack([k.weights for k in sm.layers]),
+            "skip": sm.skip.weights if sm.skip is not None else np.zeros((0, 3, 3))}
+
+
+def _random_conv(spec, A, form, activation, seed, scale=0.05, omega=2.0 / 3.0):
+    """A 'trained-looking' conv smoother: the Jacobi-equivalent initialisation
+    (smoothers.py:148-164) plus seeded perturbations of every kernel."""
+    rng = np.random.default_rng(seed)
+    base = rs.conv_smoother(rg.StencilField(spec, A.data) if isinstance(A, rg.StencilField) else A, form, omega,
+                            activation)
+    layers = [rg.ConvKernel(k.weights + scale * rng.standard_normal((3, 3))) for k in base.layers]
+    skip = None if base.skip is None else rg.ConvKernel(base.skip.weights + scale * rng.standard_normal((3, 3)))
+    return rs.ConvSmoother(base.spec, form, layers, skip, activation, base.slope, base.gain)
+
+
+def make_conv():
+    """conv.npz: convolve / ConvSmoother.apply / effective_kernel pins and V-cycles
+    with shared-kernel conv smoothers (equip_conv_init, perturbed full / rb forms,
+    leaky activation, masked domain, equip_trained transport)."""
+    d = {}
+    rng = np.random.default_rng(77)
+    n = 23
+    for gname in ("square", "lshape"):
+        mask = gen.geometry_mask(gname, n) if gname != "square" else np.ones((n, n), bool)
+        spec = spec_of(mask, 1 / (n + 1))
+        u = rg.GridFunction(spec, np.where(mask, rng.standard_normal((n, n)), 0.0))
+        w = rng.standard_normal((3, 3))
+        w[0, 2] = 0.0
+        w[1, 0] = 0.0
+        d[f"convolve/{gname}/w"] = w
+        d[f"convolve/{gname}/mask"] = mask
+        d[f"convolve/{gname}/u"] = u.values
+        d[f"convolve/{gname}/out"] = rg.convolve(rg.ConvKernel(w), u).values
+        A = rg.StencilField(spec, gen.rotated_fd(n, 0.4, 0.05))
+        for form, act in (("full", "linear"), ("full", "leaky"), ("rb", "linear"), ("rb", "leaky")):
+            sm = _random_conv(spec, A, form, act, seed=len(d), scale=0.3)
+            key = f"apply/{gname}/{form}_{act}"
+            for k2, v in _conv_params(sm).items():
+                d[f"{key}/{k2}"] = v
+            d[f"{key}/r"] = u.values
+            d[f"{key}/out"] = sm.apply(u).values
+            if act == "linear":
+                d[f"{key}/effective"] = rs.effective_kernel(sm).weights
+    # V-cycles: rotated FD 31^2, 4 levels
+    n = 31
+    A = gen.rotated_fd(n, math.pi / 6, 0.01)
+    f = gen.uniform_rhs(n, 12)
+    cases = [("init_v11", None, "init", "linear", 1), ("full_lin_v22", None, "full", "linear", 2),
+             ("full_leaky_v11", None, "full", "leaky", 1), ("rb_lin_v22", None, "rb", "linear", 2),
+             ("lshape_full_v11", "lshape", "full", "linear", 1)]
+    for name, geom, form, act, nu in cases:
+        mask = np.ones((n, n), bool) if geom is None else gen.geometry_mask(geom, n)
+        spec = spec_of(mask, 1 / (n + 1))
+        S = rg.StencilField(spec, A)
+        hier = rh.build_hierarchy(S, 4)
+        if form == "init":
+            rh.equip_conv_init(hier)
+        else:
+            for l, lev in enumerate(hier.levels[:-1]):
+                lev.smoother = _random_conv(lev.spec, lev.operator, form, act, seed=100 + l)
+        for l, lev in enumerate(hier.levels[:-1]):
+            for k2, v in _conv_params(lev.smoother).items():
+                d[f"cycle/{name}/L{l}/{k2}"] = v
+            if nu > 1:
+                lev.smoother = RepeatedSmoother(lev.smoother, lev.operator, nu)
+        F = rg.GridFunction(spec, np.where(mask, f, 0.0))
+        u = rg.zeros(spec)
+        hist = [(F - rg.apply_stencil(S, u)).norm() / F.norm()]
+        for _ in range(8):
+            u = rh.v_cycle(hier, 0, F, u)
+            hist.append((F - rg.apply_stencil(S, u)).norm() / F.norm())
+        d[f"cycle/{name}/A0"] = A
+        d[f"cycle/{name}/mask"] = mask
+        d[f"cycle/{name}/f"] = F.values
+        d[f"cycle/{name}/nu"] = nu
+        d[f"cycle/{name}/history"] = np.array(hist)
+        d[f"cycle/{name}/u"] = u.values
+        print(f"conv {name}: hist[-1]={hist[-1]:.3e}")
+    # transport: smoothers of a 15^2 source hierarchy into a 31^2 target (equip_trained)
+    src = rh.build_hierarchy(rg.StencilField(rg.full_spec(15), gen.rotated_fd(15, math.pi / 6, 0.01)), 3)
+    for l, lev in enumerate(src.levels[:-1]):
+        lev.smoother = _random_conv(lev.spec, lev.operator, "full", "linear", seed=200 + l)
+    tgt = rh.build_hierarchy(rg.StencilField(rg.full_spec(n), A), 4)
+    rh.equip_trained(tgt, src)
+    for l, lev in enumerate(src.levels[:-1]):
+        for k2, v in _conv_params(lev.smoother).items():
+            d[f"transport/src/L{l}/{k2}"] = v
+    for l, lev in enumerate(tgt.levels[:-1]):
+        d[f"transport/tgt/L{l}/gain"] = lev.smoother.gain
+    F = rg.GridFunction(rg.full_spec(n), f)
+    u = rg.zeros(F.spec)
+    hist = [F.norm() / F.norm()]
+    for _ in range(6):
+        u = rh.v_cycle(tgt, 0, F, u)
+        hist.append((F - rg.apply_stencil(rg.StencilField(F.spec, A), u)).norm() / F.norm())
+    d["transport/history"] = np.array(hist)
+    d["transport/u"] = u.values
+    np.savez_compressed(os.path.join(HERE, "conv.npz"), **d)
+
+
 def main():
+    if "--only-conv" in sys.argv:
+        make_conv()
+        return
     if "--only-krylov" in sys.argv:
         make_krylov(make_nets())
         return
@@ -292,6 +399,7 @@ def main():
         run_case(f"c4_p{i}", gen.rotated_fd(n, theta[i], eps[i]), np.ones((n, n), bool), 8, nets["conv"], 1, 10,
                  gen.uniform_rhs(n, [4, i]), 1 / (n + 1), store_levels=False)
     make_krylov(nets)
+    make_conv()
 
 
 if __name__ == "__main__":

@@ -145,3 +145,55 @@ def test_fgmres_config_validation():
         mg.FgmresConfig(restart=0)
     with pytest.raises(mg.ConfigError):
         mg.FgmresConfig(max_iter=0)
+
+
+# ---------------------------------------------------------------------------
+# shared-kernel conv smoother (smoothers.py:105-178): oracle vs reference
+
+import conv_cases as cc  # noqa: E402
+
+
+def _osm(prefix):
+    form, layers, skip, act, slope, gain = cc.params(prefix)
+    return mo.ConvSm(list(layers), skip, act, slope, gain)
+
+
+@pytest.mark.parametrize("g", ["square", "lshape"])
+def test_convolve_and_conv_apply_bit_exact(g):
+    z = cc.conv_golden()
+    mask = z[f"convolve/{g}/mask"]
+    assert np.array_equal(mo.convolve(z[f"convolve/{g}/w"], z[f"convolve/{g}/u"], mask), z[f"convolve/{g}/out"])
+    for key in [k for k in cc.names("apply") if k.startswith(g)]:
+        pre = f"apply/{key}"
+        assert np.array_equal(mo.conv_apply(_osm(pre), z[f"{pre}/r"], mask), z[f"{pre}/out"]), key
+        if f"{pre}/effective" in z.files:
+            assert np.allclose(mo.effective_kernel(_osm(pre)), z[f"{pre}/effective"], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", cc.names("cycle"))
+def test_conv_smoother_cycles_oracle(name):
+    z = cc.conv_golden()
+    pre = f"cycle/{name}"
+    A, mask, f, nu = z[f"{pre}/A0"], z[f"{pre}/mask"], z[f"{pre}/f"], int(z[f"{pre}/nu"])
+    h = mo.build_hierarchy(A, 4, mask)
+    h.kernels = [_osm(f"{pre}/L{l}") for l in range(3)]
+    if name.startswith("init"):
+        for l in range(3):   # equip_conv_init restated
+            ref, mine = h.kernels[l], mo.conv_init(h.ops[l], h.masks[l])
+            assert ref.gain == mine.gain and all(np.array_equal(a, b) for a, b in zip(ref.layers, mine.layers))
+    u, hist = mo.run_cycles(h, f, 8, nu, nu)
+    assert np.allclose(hist, z[f"{pre}/history"], rtol=1e-13, atol=0)
+    assert rel_err(u, z[f"{pre}/u"]) <= 1e-12
+
+
+def test_conv_smoother_model_json_round_trip(tmp_path):
+    import paper_2102_12071_b200 as mg
+    form, layers, skip, act, slope, gain = cc.params("apply/square/full_leaky")
+    spec = mg.full_spec(23)
+    sm = mg.ConvSmoother(spec, form, [mg.ConvKernel(w) for w in layers], mg.ConvKernel(skip), act, slope, gain)
+    mg.save_model(tmp_path / "c.json", sm, {"note": "round trip"})
+    back = mg.load_model(tmp_path / "c.json")
+    assert back.form == "full" and back.activation == "leaky" and back.gain == gain
+    assert all(np.array_equal(a.weights, b.weights) for a, b in zip(back.layers, sm.layers))
+    with pytest.raises(mg.ConfigError):
+        mg.ConvSmoother(spec, "full", sm.layers[:2], None)
