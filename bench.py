@@ -479,8 +479,8 @@ def run_ours(args):
     u_list = [uh[k % 2] for k in range(e_steps)]
     for _ in range(2):
         h.run_cycles_host(fh[0], uh[0], cycles, nu, nu, history_host=hist_hosts[0], u_zero=True, stream=dv.stream(f))
-    h.run_cycles_host_many(f_list[:2], u_list[:2], cycles, nu, nu, history_hosts=hist_hosts[:2], u_zero=True,
-                           stream=dv.stream(f))
+    h.run_cycles_host_many(f_list, u_list, cycles, nu, nu, history_hosts=hist_hosts, u_zero=True,
+                           stream=dv.stream(f))   # warm: graphs of both staging sets, pinned history staging
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)

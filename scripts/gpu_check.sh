@@ -6,6 +6,6 @@ timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; ec
 python scripts/profile_step.py > gpurun_out/prof_plain.log 2>&1 && \
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv python scripts/profile_step.py > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
-ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_stream -s 19 -c 2 \
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_stream -s 6 -c 6 \
     -o gpurun_out/sweep python scripts/profile_step.py > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
 tail -5 gpurun_out/pytest_gpu.log; tail -3 gpurun_out/bench.log; tail -3 gpurun_out/smoke.log
