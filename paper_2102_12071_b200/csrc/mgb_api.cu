@@ -55,7 +55,15 @@ struct LevelD {
   uint8_t* mask = nullptr; // null = all active
   double* Acls = nullptr;  // band-class tables (batch x 25 x 9) when A is class-constant
   double* Kcls = nullptr;  // band-class tables (batch x 25 x ks x 9) when M is class-constant
-  double hAint[9] = {0}, hKint[9] = {0};  // interior-class weights (host copy, batch 0)
+  double hAcls[225] = {0}, hKcls[225] = {0};  // band-class tables, host copy of problem 0 (class 12 = interior)
+  const double* hAint() const { return hAcls + 12 * 9; }
+  const double* hKint() const { return hKcls + 12 * 9; }
+  // every class equals the interior one (A and M): boundary strips need no class lookups
+  bool uniform() const {
+    for (int q = 0; q < 225; ++q)
+      if (hAcls[q] != hAcls[108 + q % 9] || hKcls[q] != hKcls[108 + q % 9]) return false;
+    return true;
+  }
   std::vector<uint8_t> hmask;
   int64_t nact = 0;
   ConvSm conv;             // shared-kernel convolutional smoother (conv.nl > 0 replaces K)
@@ -390,7 +398,7 @@ static int classify_table(mgb_hier* h, int l, const double* planes, int ks, doub
     MGB_CUDA_TRY(dalloc(cls_out, (size_t)h->batch * 25 * ks * 9));
     MGB_CUDA_TRY(launch_gather_cls(h->grid(l), T, drep, *cls_out, s));
     if (interior_host && ks == 1)
-      MGB_CUDA_TRY(cudaMemcpyAsync(interior_host, *cls_out + 12 * 9, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      MGB_CUDA_TRY(cudaMemcpyAsync(interior_host, *cls_out, 225 * sizeof(double), cudaMemcpyDeviceToHost, s));
   }
   MGB_CUDA_TRY(cudaFreeAsync(drep, s));
   MGB_CUDA_TRY(cudaFreeAsync(flag, s));
@@ -401,9 +409,9 @@ static int classify_table(mgb_hier* h, int l, const double* planes, int ks, doub
 static int classify_all(mgb_hier* h, cudaStream_t s) {
   for (int l = 0; l < h->depth(); ++l) {
     LevelD& lv = h->lv[l];
-    if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s, lv.hAint)) return st;
+    if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s, lv.hAcls)) return st;
     if (lv.K) {
-      if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s, lv.hKint)) return st;
+      if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s, lv.hKcls)) return st;
     } else {
       dfree(lv.Kcls);
     }
@@ -720,7 +728,7 @@ extern "C" int mgb_hier_build_classed(int device, int batch, int rows, int cols,
   }
   std::vector<int> hring(L, 1);
   MGB_CUDA_TRY(cudaMemcpyAsync(hring.data(), ring, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
-  for (auto& lv : h->lv) MGB_CUDA_TRY(cudaMemcpyAsync(lv.hAint, lv.Acls + 12 * 9, 9 * sizeof(double),
+  for (auto& lv : h->lv) MGB_CUDA_TRY(cudaMemcpyAsync(lv.hAcls, lv.Acls, 225 * sizeof(double),
                                                       cudaMemcpyDeviceToHost, s));
   MGB_CUDA_TRY(cudaFreeAsync(ring, s));
   MGB_CUDA_TRY(cudaFreeAsync(drep, s));
@@ -884,7 +892,7 @@ extern "C" int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const 
                        tabw_cls(lv.Kcls, lv.rows, lv.cols, kst), s, drep, 25);
       cudaFreeAsync(drep, s);
       if (e == cudaSuccess && kst == 1)
-        e = cudaMemcpyAsync(lv.hKint, lv.Kcls + 12 * 9, 9 * sizeof(double), cudaMemcpyDeviceToHost, s);
+        e = cudaMemcpyAsync(lv.hKcls, lv.Kcls, 225 * sizeof(double), cudaMemcpyDeviceToHost, s);
     } else {
       e = launch_infer(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, variant, kst, w, slope,
                        precision, tabw_soa(lv.K, lv.n, kst), s);
@@ -921,7 +929,7 @@ extern "C" int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream) {
       MGB_CUDA_TRY(launch_jacobi(h->grid(l), tabA(h, lv), nullptr, omega, tabw_cls(lv.Kcls, lv.rows, lv.cols, 1),
                                  flag + l, s, drep, 25));
       MGB_CUDA_TRY(cudaFreeAsync(drep, s));
-      MGB_CUDA_TRY(cudaMemcpyAsync(lv.hKint, lv.Kcls + 12 * 9, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      MGB_CUDA_TRY(cudaMemcpyAsync(lv.hKcls, lv.Kcls, 225 * sizeof(double), cudaMemcpyDeviceToHost, s));
     } else {
       MGB_CUDA_TRY(launch_jacobi(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, omega,
                                  tabw_soa(lv.K, lv.n, 1), flag + l, s));
@@ -1201,9 +1209,10 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   a.f = f;
   a.stream = s;
   a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
+  a.uniform = a.ci_valid && lv.uniform();
   for (int o = 0; o < 9; ++o) {
-    a.ci[o] = lv.hAint[o];
-    a.ci[9 + o] = lv.hKint[o];
+    a.ci[o] = lv.hAint()[o];
+    a.ci[9 + o] = lv.hKint()[o];
   }
   return a;
 }
@@ -1709,12 +1718,13 @@ bool hier_level_classed(const mgb_hier* h, int l) { return h->lv[l].Acls && h->l
 Grid hier_grid(const mgb_hier* h, int l) { return h->grid(l); }
 Op hier_opA(const mgb_hier* h, int l) { return h->lv[l].opA(); }
 Op hier_opK(const mgb_hier* h, int l) { return h->lv[l].opK(); }
-void hier_interior(const mgb_hier* h, int l, int* valid, double* ci) {
+void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform) {
   const LevelD& lv = h->lv[l];
   *valid = h->batch == 1 && lv.Acls && lv.Kcls;
+  if (uniform) *uniform = *valid && lv.uniform();
   for (int o = 0; o < 9; ++o) {
-    ci[o] = lv.hAint[o];
-    ci[9 + o] = lv.hKint[o];
+    ci[o] = lv.hAint()[o];
+    ci[9 + o] = lv.hKint()[o];
   }
 }
 double* work_level_u(mgb_work* w, int l) { return w->u[l]; }

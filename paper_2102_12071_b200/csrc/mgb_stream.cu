@@ -433,7 +433,12 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   const bool zu = a.u == nullptr;
   const bool msk = a.mask != nullptr;
   const int cm = (a.A.cls != nullptr && a.K.cls != nullptr && !msk) ? (a.ci_valid ? 2 : 1) : 0;
+  static const bool one_col = getenv("MGB_STREAM1") && atoi(getenv("MGB_STREAM1")) != 0;
   ++g_launches;
+  // two-column kernel: single-problem band-class levels (interior weights from the
+  // constant bank); batched levels keep the one-column kernel (measured faster: the
+  // pair kernel would read every interior weight from shared memory)
+  if (cm == 2 && !one_col) return launch_stream2(a, nsw, res, pro, norm, nblocks);
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
     if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, true>, nsw, res, a, nblocks);     \

@@ -22,6 +22,10 @@ struct StreamArgs {
                            // must be addressable: with domain decomposition the arrays are
                            // ghosted row blocks passed as pointers pre-offset to global rows.
   int ci_valid;            // 1: ci holds the interior-class weights (batch == 1, classed A and M)
+  int uniform;             // 1: every band class equals the interior one (ci valid everywhere)
+  // two-column kernel CTA map (set by its launcher): edge strips (first / last) get
+  // shorter segments (their steps take the boundary-class path), listed first
+  int nstrips, nedge, seg_edge, nseg_edge;
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
   cudaStream_t stream;
 };
@@ -32,5 +36,8 @@ struct StreamArgs {
 // (the number of history partials written when norm is set).
 cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 int stream_max_blocks(const Grid& g);
+// Two-columns-per-thread variant for band-class levels without masks (mgb_stream2.cu);
+// launch_stream dispatches to it (MGB_STREAM1=1 keeps the one-column kernel).
+cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 
 }  // namespace mgb

@@ -1,0 +1,551 @@
+// Row-streaming V-cycle passes, two columns per thread (band-class levels).
+//
+// The same PRE / sweep / POST passes and the same pipeline as k_stream
+// (mgb_stream.cu): a CTA owns a strip of columns and a segment of rows, marches
+// down the rows, and stage k (odd = residual, even = smoother update) produces
+// row t - 2k at step t, each stage keeping the 3x3 window of its input field in
+// registers.  The difference is the work per thread: every thread owns a column
+// PAIR (2c, 2c+1), so the per-row fixed cost of a step (prefetch issue, the
+// barrier, loop control, neighbour exchange, row tests) is paid once per two
+// points and the two columns' fused-multiply-add chains interleave (ILP 2 x S).
+// The strip is 256 columns (128 threads), so the column halo costs 12/256 instead
+// of 12/128.  With one column per thread the level-0 pass issued ~240
+// instructions per fine point for ~50 FP64 FMAs (issue-bound, ncu r01); the pair
+// form halves the non-FMA part.
+//
+// Only band-class levels run here (A and M constant per band class: every
+// constant-coefficient operator, its Galerkin chain and its CNN kernels), without
+// masks; per-point planes and masked levels stay on k_stream.  The FMA chains are
+// the shared stencil_dot (mgb_dot.h) in the same order, so results are
+// bit-identical to k_stream and to the tile passes (tested).
+//
+// Reference: v_cycle hierarchy.py:96-111 (with RepeatedSmoother cli.py:365-377),
+// apply_stencil grid.py:216-226, inferred_apply smoothers.py:325-343, restrict
+// transfer.py:108-121, prolong transfer.py:124-147, history hierarchy.py:129-141.
+#include <cstdlib>
+#include <utility>
+#include <vector>
+#include <algorithm>
+
+#include "mgb_stream.h"
+#include "mgb_dot.h"
+
+#ifdef MGB_CTA_PROF
+// experiment builds only: per-CTA (smid, start, end) of the last streaming launch
+__device__ unsigned long long g_cta_prof[3 * 8192];
+#endif
+
+namespace mgb {
+namespace {
+
+#ifndef MGB_S2T
+#define MGB_S2T 128
+#endif
+constexpr int T2 = MGB_S2T;       // threads per CTA (column pairs)
+constexpr int SW = 2 * T2;        // strip columns incl. halo
+constexpr int PD = 8;             // prefetch ring depth (rows) for u (power of two)
+constexpr int PDF = 16;           // ring depth for f: rows t-10 .. t+DIST
+constexpr int DIST = 5;           // prefetch distance (rows ahead)
+#ifndef MGB_S2MINB
+#define MGB_S2MINB 2
+#endif
+constexpr int MINB = MGB_S2MINB;  // CTAs per SM the register budget is sized for
+constexpr int PE = 8;             // ring of coarse rows (POST prolongation), power of two
+constexpr int EW = T2 + 2;        // coarse columns staged per CTA
+constexpr int NCLS = 25;
+constexpr int CINT = 12;          // interior band class (2 * 5 + 2)
+
+__device__ __forceinline__ int bandc(int i, int n) { return i < 2 ? i : (i >= n - 2 ? 4 - (n - 1 - i) : 2); }
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int NSW, bool RES>
+struct SP2 {
+  static constexpr int S = 2 * NSW + (RES ? 1 : 0);  // stencil stages after the input field
+  static constexpr int H = 2 * NSW + 2;              // column halo per side (even)
+  static constexpr int WOUT = SW - 2 * H;            // owned columns per strip (even)
+  static constexpr int NF = S;                       // fields with a window (F_0 .. F_{S-1})
+};
+
+__host__ __device__ constexpr int m3(int x) { return ((x % 3) + 3) % 3; }
+
+struct Ctx2 {
+  Grid g;
+  int b, tid, j0, c0, R0, R1;
+  bool cin0, cin1, own;
+  bool colmask;     // FAST steps of a uniform level's edge strip: zero out-of-grid columns
+  int cc0, cc1;     // band classes of columns c0, c0 + 1
+  double* ring_u;
+  double* ring_f;
+  double* ring_e;
+  double* xch;
+  double* rlast;
+  const double* tA;
+  const double* tK;
+  double* uob;
+};
+
+// One pipeline step (row t) for the thread's column pair.  FAST: every row the
+// step touches and every column of the CTA is interior (band class 2).
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool FAST, int PH>
+__device__ __forceinline__ void step2(const StreamArgs& a, const Ctx2& c, const int t,
+                                      double (&w)[SP2<NSW, RES>::NF][3][4], double (&hold)[NSW][2],
+                                      double& acc) {
+  using P = SP2<NSW, RES>;
+  constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
+  const Grid& g = c.g;
+  double nv[NF + 1][2];
+  // ---- F_0 = u (+ P ec) at row t
+  {
+    double u0 = 0.0, u1 = 0.0;
+    const bool rvr = FAST || (unsigned)t < (unsigned)g.rows;
+    if (!ZU) {
+      const double2 v = *reinterpret_cast<const double2*>(&c.ring_u[(t & (PD - 1)) * SW + 2 * c.tid]);
+      u0 = v.x;
+      u1 = v.y;
+    }
+    if (PRO && rvr) {
+      // u += P ec, coarse rows staged in ring_e (entry q = coarse column cjb + q);
+      // the k_stream loop order: di = -1, 0, 1 (row parity), dj = -1, 0, 1 (column parity)
+      double s0 = 0.0, s1 = 0.0;
+      if (t & 1) {
+        const double* er = c.ring_e + (((t - 1) >> 1) & (PE - 1)) * EW;
+        s0 = fma(0.25, er[c.tid + 1], s0);   // (di 0, dj -1): coarse m
+        s0 = fma(0.25, er[c.tid], s0);       // (di 0, dj +1): coarse m - 1
+        s1 = fma(0.5, er[c.tid + 1], s1);    // (di 0, dj 0)
+      } else {
+        const double* ea = c.ring_e + ((t >> 1) & (PE - 1)) * EW;        // di = -1: coarse row t/2
+        const double* eb = c.ring_e + (((t - 2) >> 1) & (PE - 1)) * EW;  // di = +1: coarse row t/2 - 1
+        s0 = fma(0.125, ea[c.tid + 1], s0);
+        s0 = fma(0.125, ea[c.tid], s0);
+        s1 = fma(0.25, ea[c.tid + 1], s1);
+        s0 = fma(0.125, eb[c.tid + 1], s0);
+        s0 = fma(0.125, eb[c.tid], s0);
+        s1 = fma(0.25, eb[c.tid + 1], s1);
+      }
+      u0 += s0;
+      u1 += s1;
+    }
+    // (the prolongation can reach one column past the grid: zero it there too)
+    const bool m0 = FAST ? (!c.colmask || c.cin0) : (rvr && c.cin0);
+    const bool m1 = FAST ? (!c.colmask || c.cin1) : (rvr && c.cin1);
+    nv[0][0] = m0 ? u0 : 0.0;
+    nv[0][1] = m1 ? u1 : 0.0;
+  }
+  // ---- stages k = 1..S at row t - 2k (rows are CTA-uniform).  All 2S chains
+  // advance in lockstep, one window entry o at a time, so 2S independent FMAs are
+  // in flight per thread (each chain keeps stencil_dot's order: bitwise equal).
+  double v[S][2];
+  const double* wts[S][2];
+#pragma unroll
+  for (int k = 1; k <= S; ++k) {
+    const int row = t - 2 * k;
+    if (k & 1) {
+      const double2 fv = *reinterpret_cast<const double2*>(&c.ring_f[(row & (PDF - 1)) * SW + 2 * c.tid]);
+      v[k - 1][0] = fv.x;
+      v[k - 1][1] = fv.y;
+    } else {
+      v[k - 1][0] = hold[k / 2 - 1][0];
+      v[k - 1][1] = hold[k / 2 - 1][1];
+    }
+    if (FAST) {
+      wts[k - 1][0] = wts[k - 1][1] = CM == 2 ? ((k & 1) ? a.ci : a.ci + 9) : (((k & 1) ? c.tA : c.tK) + CINT * 9);
+    } else {
+      const double* tab = (k & 1) ? c.tA : c.tK;
+      const int rb = ((unsigned)row < (unsigned)g.rows ? bandc(row, g.rows) : 2) * 5;
+      wts[k - 1][0] = tab + (rb + c.cc0) * 9;
+      wts[k - 1][1] = tab + (rb + c.cc1) * 9;
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < 9; ++o) {
+#pragma unroll
+    for (int k = 1; k <= S; ++k) {
+      const int sl = m3(PH - 2 * k - 1 + o / 3);
+      const double wa = (k & 1) ? -wts[k - 1][0][o] : wts[k - 1][0][o];
+      const double wb = (k & 1) ? -wts[k - 1][1][o] : wts[k - 1][1][o];
+      v[k - 1][0] = fma(wa, w[k - 1][sl][o % 3], v[k - 1][0]);
+      v[k - 1][1] = fma(wb, w[k - 1][sl][o % 3 + 1], v[k - 1][1]);
+    }
+  }
+#pragma unroll
+  for (int k = 1; k <= S; ++k) {
+    const int row = t - 2 * k;
+    double v0 = v[k - 1][0], v1 = v[k - 1][1];
+    if (!FAST) {
+      const bool rv = (unsigned)row < (unsigned)g.rows;
+      v0 = rv && c.cin0 ? v0 : 0.0;
+      v1 = rv && c.cin1 ? v1 : 0.0;
+    } else if (c.colmask) {
+      // uniform level, edge strip: interior weights, Dirichlet zeros outside the grid
+      v0 = c.cin0 ? v0 : 0.0;
+      v1 = c.cin1 ? v1 : 0.0;
+    }
+    const bool orow = c.own && row >= c.R0 && row < c.R1;
+    if (NORM && k == 1 && orow) {
+      acc = fma(v0, v0, acc);   // out-of-grid columns hold 0
+      acc = fma(v1, v1, acc);
+    }
+    if (k == 2 * NSW && orow) {
+      double* dst = c.uob + (int64_t)row * g.cols + c.c0;
+      dst[0] = v0;                                   // owned pairs start in the grid
+      if ((FAST && !c.colmask) || c.cin1) dst[1] = v1;
+    }
+    nv[k][0] = v0;
+    nv[k][1] = v1;
+  }
+  // ---- publish, then slide the windows (slot of the evicted row)
+  const int sl = t & 1;
+  // exchange rows are split into even- and odd-column planes (conflict-free
+  // neighbour loads: left = odd plane [tid - 1], right = even plane [tid + 1])
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    c.xch[(k * 2 + sl) * SW + c.tid] = nv[k][0];
+    c.xch[(k * 2 + sl) * SW + T2 + c.tid] = nv[k][1];
+  }
+  if (RES) {
+    c.rlast[((t - 2 * S) & 3) * SW + c.tid] = nv[S][0];
+    c.rlast[((t - 2 * S) & 3) * SW + T2 + c.tid] = nv[S][1];
+  }
+  __syncthreads();
+  if (RES) {
+    const int top = t - 2 * S;
+    if (top >= 2 && !(top & 1)) {
+      // coarse point (ci, m), m = c0 / 2: fine rows top-2..top, fine columns c0..c0+2
+      const int ci = (top - 2) >> 1;
+      const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+      const int cj = c.c0 >> 1;
+      if (c.own && ci >= (c.R0 >> 1) && 2 * ci + 1 < c.R1 && ci < rows_c && cj < cols_c) {
+        // even plane [tid], odd plane [tid], even plane [tid + 1] = columns c0, c0+1, c0+2
+        const double* r0p = &c.rlast[((top - 2) & 3) * SW + c.tid];
+        const double* r1p = &c.rlast[((top - 1) & 3) * SW + c.tid];
+        const double* r2p = &c.rlast[(top & 3) * SW + c.tid];
+        double s = 0.0625 * r0p[0];
+        s = fma(0.125, r0p[T2], s);
+        s = fma(0.0625, r0p[1], s);
+        s = fma(0.125, r1p[0], s);
+        s = fma(0.25, r1p[T2], s);
+        s = fma(0.125, r1p[1], s);
+        s = fma(0.0625, r2p[0], s);
+        s = fma(0.125, r2p[T2], s);
+        s = fma(0.0625, r2p[1], s);
+        const int64_t pc = (int64_t)ci * cols_c + cj;
+        const bool actc = a.mask_c == nullptr || a.mask_c[pc];
+        a.rc[c.b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
+      }
+    }
+  }
+  const int iL = T2 + max(c.tid - 1, 0), iR = min(c.tid + 1, T2 - 1);
+#pragma unroll
+  for (int k = 0; k < NF; ++k) {
+    const int sn = m3(PH - 2 * k);  // slot of the new row t - 2k (evicts row t - 2k - 3)
+    if (!(k & 1) && k / 2 < NSW) {
+      hold[k / 2][0] = w[k][sn][1];
+      hold[k / 2][1] = w[k][sn][2];
+    }
+    const double* xr = &c.xch[(k * 2 + sl) * SW];
+    w[k][sn][0] = xr[iL];
+    w[k][sn][1] = nv[k][0];
+    w[k][sn][2] = nv[k][1];
+    w[k][sn][3] = xr[iR];
+  }
+}
+
+// CM: 1 = band-class tables in shared memory; 2 = band-class tables with the
+// interior class read from the kernel parameters (constant-bank operands).
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM>
+__global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
+  using P = SP2<NSW, RES>;
+  constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
+  extern __shared__ __align__(16) double smem2[];
+  Ctx2 c;
+  c.g = a.g;
+  const Grid& g = c.g;
+  c.ring_u = smem2;                               // PD x SW (unused when ZU)
+  c.ring_f = c.ring_u + PD * SW;                  // PDF x SW
+  c.xch = c.ring_f + PDF * SW;                    // NF x 2 x SW neighbour exchange rows
+  c.rlast = c.xch + NF * 2 * SW;                  // 4 x SW last-residual ring (RES)
+  c.ring_e = c.rlast + 4 * SW;                    // PE x EW (POST)
+  double* tA = c.ring_e + PE * EW;                // 25 x 9
+  double* tK = tA + NCLS * 9;                     // 25 x 9
+  double* red = tK + NCLS * 9;                    // 32
+  c.tA = tA;
+  c.tK = tK;
+  c.tid = threadIdx.x;
+  c.b = blockIdx.z;
+  const int64_t n = g.n();
+  // CTA -> (strip, row segment): the edge strips' CTAs first, then the interior ones
+  int strip, seg, sy;
+  {
+    const int id = blockIdx.x;
+    const int ne = a.nedge;
+    if (id < ne * a.nseg_edge) {
+      strip = (id % ne == 0) ? 0 : a.nstrips - 1;
+      sy = id / ne;
+      seg = a.seg_edge;
+    } else {
+      const int q = id - ne * a.nseg_edge, ni = a.nstrips - ne;
+      strip = 1 + q % ni;
+      sy = q / ni;
+      seg = a.seg;
+    }
+  }
+  c.j0 = strip * WOUT;                            // first owned column (even)
+  c.c0 = c.j0 - H + 2 * c.tid;                    // the thread's pair (even column)
+  c.cin0 = c.c0 >= 0 && c.c0 < g.cols;
+  c.cin1 = c.c0 + 1 >= 0 && c.c0 + 1 < g.cols;
+  c.own = 2 * c.tid >= H && 2 * c.tid < H + WOUT && c.cin0;
+  c.cc0 = c.cin0 ? bandc(c.c0, g.cols) : 2;       // out-of-grid columns are zeroed anyway
+  c.cc1 = c.cin1 ? bandc(c.c0 + 1, g.cols) : 2;
+  c.R0 = a.own0 + sy * seg;
+  c.R1 = min(a.own1 > 0 ? a.own1 : g.rows, c.R0 + seg);
+  const double* fb = a.f + c.b * n;
+  const double* ub = ZU ? nullptr : a.u + c.b * n;
+  c.uob = a.uo + c.b * n;
+  // fast steps: every CTA column interior (band class 2) and in the grid, or a level
+  // whose band classes are all equal (then only out-of-grid columns need zeroing)
+  const bool cta_int = c.j0 - H >= 2 && c.j0 - H + SW - 1 <= g.cols - 3;
+  const bool cta_fast = cta_int || a.uniform;
+  c.colmask = !cta_int;
+#ifdef MGB_CTA_PROF
+  unsigned long long prof_t0 = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
+#endif
+
+  for (int q = c.tid; q < NCLS * 9; q += T2) {
+    tA[q] = a.A.cls[(int64_t)c.b * NCLS * 9 + q];
+    tK[q] = a.K.cls[(int64_t)c.b * NCLS * 9 + q];
+  }
+  __syncthreads();
+
+  double w[NF][3][4];
+#pragma unroll
+  for (int k = 0; k < NF; ++k)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[k][r][q] = 0.0;
+  double hold[NSW][2];
+#pragma unroll
+  for (int m = 0; m < NSW; ++m) hold[m][0] = hold[m][1] = 0.0;
+  double acc = 0.0;
+
+  int t0 = c.R0 - S - 1;
+  t0 -= m3(t0);
+  const int t1 = c.R1 + 2 * S;
+  int prow = t0;
+  const int64_t cstride = g.cols;
+  // prefetch: thread copies strip columns tid and tid + T2 (coalesced rows)
+  const int ca = c.j0 - H + c.tid, cb = ca + T2;
+  const bool ina = ca >= 0 && ca < g.cols, inb = cb >= 0 && cb < g.cols;
+  const double* pu = ZU ? nullptr : ub + (int64_t)prow * cstride + ca;
+  const double* pf = fb + (int64_t)prow * cstride + ca;
+  const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+  const double* ecb = PRO ? a.ec + c.b * (int64_t)rows_c * cols_c : nullptr;
+  const int cjb = ((c.j0 - H) >> 1) - 1;          // coarse column of ring_e entry 0
+  const int lo_row = max(0, c.R0 - S - 1), hi_row = min(g.rows - 1, c.R1 + S);
+  const int lo_c = (lo_row - 2) >> 1, hi_c = (hi_row >> 1) + 1;
+  auto stage_e = [&](int ci) {
+    for (int q = c.tid; q < EW; q += T2) {
+      const int cj = cjb + q;
+      const bool ev = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c && cj >= 0 && cj < cols_c;
+      cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + q], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
+    }
+  };
+  auto issue = [&]() {
+    const bool rv = prow >= lo_row && prow <= hi_row;
+    double* du = &c.ring_u[(prow & (PD - 1)) * SW + c.tid];
+    double* df = &c.ring_f[(prow & (PDF - 1)) * SW + c.tid];
+    if (!ZU) {
+      cp_async8(du, rv && ina ? pu : ub, rv && ina);
+      cp_async8(du + T2, rv && inb ? pu + T2 : ub, rv && inb);
+    }
+    cp_async8(df, rv && ina ? pf : fb, rv && ina);
+    cp_async8(df + T2, rv && inb ? pf + T2 : fb, rv && inb);
+    // coarse row ci is first needed by fine row 2ci (as di = -1); staged with the
+    // group of fine row 2ci - 2 so it is complete and published by that step's barrier
+    if (PRO && !(prow & 1)) stage_e((prow >> 1) + 1);
+    cp_commit();
+    ++prow;
+    if (!ZU) pu += cstride;
+    pf += cstride;
+  };
+  if (PRO) {
+    for (int ci = (t0 >> 1) - 1; ci <= (t0 >> 1) + 1; ++ci) stage_e(ci);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+  }
+  for (int q = 0; q < DIST; ++q) issue();
+  // ring rows are copied by other threads than the ones reading the pair: row t
+  // must be complete before the barrier of step t - 1 (row t0: this one)
+  cp_wait<DIST - 1>();
+  __syncthreads();
+
+#define MGB_STEP2(PH_)                                                                     \
+  {                                                                                        \
+    const int t = tb + PH_;                                                                \
+    issue();                                                                               \
+    cp_wait<DIST - 1>(); /* row t + 1 lands before this step's barrier publishes it */     \
+    if (cta_fast && t - 2 * S >= 2 && t <= g.rows - 3)                                     \
+      step2<NSW, RES, PRO, NORM, ZU, CM, true, PH_>(a, c, t, w, hold, acc);                \
+    else                                                                                   \
+      step2<NSW, RES, PRO, NORM, ZU, CM, false, PH_>(a, c, t, w, hold, acc);               \
+  }
+  for (int tb = t0; tb <= t1; tb += 3) {
+    MGB_STEP2(0)
+    MGB_STEP2(1)
+    MGB_STEP2(2)
+  }
+#undef MGB_STEP2
+  cp_wait<0>();
+#ifdef MGB_CTA_PROF
+  if (c.tid == 0 && blockIdx.x < 8192) {
+    unsigned long long t1, sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    sm = smid;
+    g_cta_prof[3 * blockIdx.x] = sm;
+    g_cta_prof[3 * blockIdx.x + 1] = prof_t0;
+    g_cta_prof[3 * blockIdx.x + 2] = t1;
+  }
+#endif
+  if (NORM) {
+    double v = acc;
+    const int lane = c.tid & 31, wid = c.tid >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (c.tid == 0) {
+      double s = 0.0;
+      for (int q = 0; q < T2 / 32; ++q) s += red[q];
+      a.partials[(int64_t)c.b * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+}  // namespace
+
+static size_t stream2_smem(int nsw, bool res) {
+  const int nf = 2 * nsw + (res ? 1 : 0);
+  return sizeof(double) * ((size_t)(PD + PDF + 2 * nf + 4) * SW + PE * EW + 2 * NCLS * 9 + 32);
+}
+
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// Rows per CTA segment.  Interior strips get segments of seg rows, the edge strips
+// (boundary band classes: every step takes the class-lookup path, r times the cost
+// of an interior step) segments of about seg / r rows, so all CTAs finish together;
+// the segment counts fill whole waves of the measured occupancy with the fewest
+// pipeline fills (3S + 3 steps per segment).
+static void choose_seg2(const Grid& g, int nsw, bool res, int occ, bool uniform, StreamArgs& a) {
+  const int H = 2 * nsw + 2, wout = SW - 2 * H, S = 2 * nsw + (res ? 1 : 0);
+  const int strips = (g.cols + wout - 1) / wout;
+  const int ne = std::min(strips, 2), ni = strips - ne;
+  const int64_t slots = (int64_t)sm_count() * std::max(occ, 1);
+  static const double r_env = getenv("MGB_EDGE_RATIO") ? atof(getenv("MGB_EDGE_RATIO")) : 0.0;
+  // measured (k_stream2, 4095^2, per-CTA timers): class-lookup steps ~2.2x interior steps
+  const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : (uniform ? 1.05 : 2.2));
+  const int F = 3 * S + 3;
+  double best_t = 1e300;
+  a.nstrips = strips;
+  a.nedge = ne;
+  a.seg = a.seg_edge = g.rows;
+  a.nseg_edge = 1;
+  for (int nseg = 1; nseg <= std::max(1, g.rows / 16); ++nseg) {
+    const int seg = (g.rows + nseg - 1) / nseg;
+    const int nsi = (g.rows + seg - 1) / seg;
+    int seg_e = std::max(16, (int)((seg + F) / r) - F);
+    seg_e = std::min(seg_e, g.rows);
+    const int nse = (g.rows + seg_e - 1) / seg_e;
+    const int64_t ctas = ((int64_t)ni * nsi + (int64_t)ne * nse) * g.batch;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    const double t = (double)waves * std::max((double)(seg + F), r * (seg_e + F));
+    if (t < best_t) {
+      best_t = t;
+      a.seg = seg;
+      a.seg_edge = seg_e;
+      a.nseg_edge = nse;
+    }
+  }
+  static const int force_seg = getenv("MGB_SEG") ? atoi(getenv("MGB_SEG")) : 0;  // experiments only
+  if (force_seg > 0) {
+    a.seg = a.seg_edge = force_seg;
+    a.nseg_edge = (g.rows + force_seg - 1) / force_seg;
+  }
+}
+
+template <typename KF>
+static cudaError_t run_k2(KF kern, int nsw, bool res, StreamArgs a, int* nblocks) {
+  static thread_local std::vector<std::pair<const void*, int>> occ_cache;
+  const size_t smem = stream2_smem(nsw, res);
+  int occ = -1;
+  for (auto& e : occ_cache)
+    if (e.first == (const void*)kern) occ = e.second;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T2, smem);
+    if (e != cudaSuccess) return e;
+    occ_cache.push_back({(const void*)kern, occ});
+  }
+  if (a.own1 <= 0) {
+    a.own0 = 0;
+    a.own1 = a.g.rows;
+  }
+  Grid go = a.g;
+  go.rows = a.own1 - a.own0;
+  choose_seg2(go, nsw, res, occ, a.uniform != 0, a);
+  const int ni = a.nstrips - a.nedge;
+  const int nsi = (go.rows + a.seg - 1) / a.seg;
+  const int nctas = a.nedge * a.nseg_edge + ni * nsi;
+  const dim3 grid(nctas, 1, a.g.batch);
+  if (nblocks) *nblocks = nctas;
+  kern<<<grid, T2, smem, a.stream>>>(a);
+  return MGB_DBG(__func__);
+}
+
+cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks) {
+  const bool zu = a.u == nullptr;
+  const int cm = a.ci_valid ? 2 : 1;
+#define MGB_ST2(NSW_, RES_, PRO_, NORM_, ZU_)                                                     \
+  if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                \
+    if (cm == 2) return run_k2(k_stream2<NSW_, RES_, PRO_, NORM_, ZU_, 2>, nsw, res, a, nblocks); \
+    return run_k2(k_stream2<NSW_, RES_, PRO_, NORM_, ZU_, 1>, nsw, res, a, nblocks);             \
+  }
+  MGB_ST2(1, true, false, false, false) MGB_ST2(1, true, false, true, false)
+  MGB_ST2(1, true, false, false, true)  MGB_ST2(1, true, false, true, true)
+  MGB_ST2(2, true, false, false, false) MGB_ST2(2, true, false, true, false)
+  MGB_ST2(2, true, false, false, true)  MGB_ST2(2, true, false, true, true)
+  MGB_ST2(1, false, false, false, false) MGB_ST2(1, false, false, true, false)
+  MGB_ST2(1, false, false, false, true)  MGB_ST2(1, false, false, true, true)
+  MGB_ST2(1, false, true, false, false) MGB_ST2(2, false, true, false, false)
+#undef MGB_ST2
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mgb
+
+#ifdef MGB_CTA_PROF
+extern "C" __attribute__((visibility("default"))) int mgb_debug_cta_prof(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_cta_prof, sizeof(unsigned long long) * 3 * n);
+}
+#endif
