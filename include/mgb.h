@@ -157,6 +157,10 @@ int mgb_hier_set_fused(mgb_hier* h, int enable);
    level with at most that many points in one single-CTA shared-memory kernel (default
    0: off, the tile passes measured faster).  Negative arguments keep a setting. */
 int mgb_hier_set_passes(mgb_hier* h, int64_t stream_min, int tile, int64_t coarse_max);
+/* Row-streaming kernel for single-problem band-class levels: 0 auto (column pairs
+   per thread on levels of >= 2M points, one column per thread below), 1 always one
+   column, 2 always column pairs.  Both produce bit-identical results (tests, tuning). */
+int mgb_hier_set_stream_kernel(mgb_hier* h, int kind);
 
 /* equip_inferred (hierarchy.py:207-214): per-level CNN inference on levels 0..L-2. */
 int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const double* weights_host,

@@ -52,6 +52,7 @@ SIGNATURES = {
     "mgb_hier_storage_info": (I, [P, I, PI, PI]),
     "mgb_hier_set_fused": (I, [P, I]),
     "mgb_hier_set_passes": (I, [P, I64, I, I64]),
+    "mgb_hier_set_stream_kernel": (I, [P, I]),
     "mgb_hier_set_conv_smoother": (I, [P, I, I, P, P, I, D, D]),
     "mgb_convolve": (I, [I, I, I, P, P, P, P, P]),
     "mgb_conv_smoother_apply": (I, [I, I, I, I, P, P, I, D, D, P, P, P, P]),

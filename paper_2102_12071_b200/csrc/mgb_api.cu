@@ -86,6 +86,7 @@ struct mgb_hier {
   int64_t stream_min = 1000000;   // row-streaming passes on levels with at least this many points
                                   // (batch x rows x cols); smaller levels use tile passes
   int tile = 1;                   // 1: tile-local fused passes below stream_min; 0: separate kernels
+  int stream_kernel = 0;          // 0 auto, 1 one-column streaming kernel, 2 column-pair kernel
   int64_t coarse_max = 0;         // levels up to this many points run in the single-launch
                                   // shared-memory coarse cycle (0 disables it)
   int fused = 2;            // 2: one fused pass per smoothing phase; 1: one fused pass per sweep;
@@ -580,6 +581,14 @@ extern "C" int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream) {
 extern "C" int mgb_hier_set_fused(mgb_hier* h, int enable) {
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
   h->fused = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
+  ++h->version;
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_set_stream_kernel(mgb_hier* h, int kind) {
+  if (!h) return fail(MGB_CONTRACT, "null hierarchy");
+  if (kind < 0 || kind > 2) return fail(MGB_CONFIG, "stream kernel must be 0 (auto), 1 or 2");
+  h->stream_kernel = kind;
   ++h->version;
   return MGB_OK;
 }
@@ -1210,6 +1219,7 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   a.stream = s;
   a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
   a.uniform = a.ci_valid && lv.uniform();
+  a.kernel = h->stream_kernel;
   for (int o = 0; o < 9; ++o) {
     a.ci[o] = lv.hAint()[o];
     a.ci[9 + o] = lv.hKint()[o];
@@ -1718,10 +1728,11 @@ bool hier_level_classed(const mgb_hier* h, int l) { return h->lv[l].Acls && h->l
 Grid hier_grid(const mgb_hier* h, int l) { return h->grid(l); }
 Op hier_opA(const mgb_hier* h, int l) { return h->lv[l].opA(); }
 Op hier_opK(const mgb_hier* h, int l) { return h->lv[l].opK(); }
-void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform) {
+void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform, int* kernel) {
   const LevelD& lv = h->lv[l];
   *valid = h->batch == 1 && lv.Acls && lv.Kcls;
   if (uniform) *uniform = *valid && lv.uniform();
+  if (kernel) *kernel = h->stream_kernel;
   for (int o = 0; o < 9; ++o) {
     ci[o] = lv.hAint()[o];
     ci[9 + o] = lv.hKint()[o];

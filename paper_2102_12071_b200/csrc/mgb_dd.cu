@@ -333,7 +333,7 @@ static StreamArgs dd_args(const mgb_dd* d, int l, cudaStream_t s) {
   a.A = hier_opA(d->h, l);
   a.K = hier_opK(d->h, l);
   a.stream = s;
-  hier_interior(d->h, l, &a.ci_valid, a.ci, &a.uniform);
+  hier_interior(d->h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel);
   return a;
 }
 

@@ -19,7 +19,7 @@ bool hier_level_classed(const mgb_hier* h, int l);
 Grid hier_grid(const mgb_hier* h, int l);
 Op hier_opA(const mgb_hier* h, int l);
 Op hier_opK(const mgb_hier* h, int l);
-void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform = nullptr);
+void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform = nullptr, int* kernel = nullptr);
 int work_create_from(const mgb_hier* h, int first, mgb_work** out);
 double* work_level_u(mgb_work* w, int l);
 double* work_level_f(mgb_work* w, int l);

@@ -438,7 +438,10 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   // two-column kernel: single-problem band-class levels (interior weights from the
   // constant bank); batched levels keep the one-column kernel (measured faster: the
   // pair kernel would read every interior weight from shared memory)
-  if (cm == 2 && !one_col) return launch_stream2(a, nsw, res, pro, norm, nblocks);
+  // (levels below ~2M points, e.g. 1023^2 with five strips, measured faster on the
+  // one-column kernel: more, shorter CTAs)
+  const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() >= (2 << 20));
+  if (cm == 2 && pairs) return launch_stream2(a, nsw, res, pro, norm, nblocks);
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
     if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, true>, nsw, res, a, nblocks);     \

@@ -23,6 +23,7 @@ struct StreamArgs {
                            // ghosted row blocks passed as pointers pre-offset to global rows.
   int ci_valid;            // 1: ci holds the interior-class weights (batch == 1, classed A and M)
   int uniform;             // 1: every band class equals the interior one (ci valid everywhere)
+  int kernel;              // streaming kernel: 0 auto, 1 one column per thread, 2 column pairs
   // two-column kernel CTA map (set by its launcher): edge strips (first / last) get
   // shorter segments (their steps take the boundary-class path), listed first
   int nstrips, nedge, seg_edge, nseg_edge;

@@ -92,16 +92,155 @@ struct Ctx2 {
   double* uob;
 };
 
+// Per-thread pipeline state (push form).  Stage k's output rows are accumulated
+// as their input rows arrive: input row x of field k-1 adds the top weights to
+// output row x+1 (a fresh chain seeded with f or the old u), the middle weights
+// to row x and the bottom weights to row x-1, which completes.  So each output
+// chain sees its nine terms in stencil_dot's order (bit-identical results) while a
+// step carries 6 S independent three-term chains instead of 2 S nine-term ones,
+// and only two open rows per stage (acc, ring of 3 by row mod 3) plus the newest
+// own values of each field (cur) stay in registers instead of 3 x 4 windows.
+template <int NSW, bool RES>
+struct St3 {
+  static constexpr int S = 2 * NSW + (RES ? 1 : 0);
+  static constexpr int NX = RES ? S + 1 : S;   // exchanged fields (F_S feeds the restriction)
+  double acc[S][3][2];    // open output rows of stage k (slot = row mod 3), two columns
+  double cur[NX][2];      // own values of field j published at the previous step
+  double prev[NSW][2];    // own values of fields 0, 2, .. published two steps back
+  double racc;            // open restriction sum (coarse row being accumulated)
+  double norm;            // history: sum of squares of the input residual
+};
+
+
 // One pipeline step (row t) for the thread's column pair.  FAST: every row the
-// step touches and every column of the CTA is interior (band class 2).
+// step touches is interior and the CTA's columns are interior (or the level is
+// uniform: then only out-of-grid columns need zeroing, colmask).  PH = t mod 3.
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool FAST, int PH>
-__device__ __forceinline__ void step2(const StreamArgs& a, const Ctx2& c, const int t,
-                                      double (&w)[SP2<NSW, RES>::NF][3][4], double (&hold)[NSW][2],
-                                      double& acc) {
+__device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const int t, St3<NSW, RES>& st) {
   using P = SP2<NSW, RES>;
-  constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
+  constexpr int S = P::S, NX = St3<NSW, RES>::NX;
   const Grid& g = c.g;
-  double nv[NF + 1][2];
+  const int slp = (t - 1) & 1;  // exchange slot published by step t - 1
+  // ---- neighbours of the rows published by step t - 1 (even / odd column planes)
+  double L[NX], R[NX];
+  {
+    const int iL = max(c.tid - 1, 0), iR = min(c.tid + 1, T2 - 1);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      const double* xr = &c.xch[(j * 2 + slp) * SW];
+      L[j] = xr[T2 + iL];
+      R[j] = xr[iR];
+    }
+  }
+  double out[S + 1][2];
+  // ---- stages k = 1..S: push field k-1 row x = t - 2k + 1; completes row t - 2k
+#pragma unroll
+  for (int k = 1; k <= S; ++k) {
+    const bool resid = k & 1;
+    const int x = t - 2 * k + 1;
+    const int sN = m3(PH - 2 * k + 2), sM = m3(PH - 2 * k + 1), sB = m3(PH - 2 * k);  // rows x+1, x, x-1
+    const double in0 = L[k - 1], in1 = st.cur[k - 1][0], in2 = st.cur[k - 1][1], in3 = R[k - 1];
+    // seed of the new chain (row x + 1): f, or the u the update adds to
+    double s0, s1;
+    if (resid) {
+      const double2 fv = *reinterpret_cast<const double2*>(&c.ring_f[((x + 1) & (PDF - 1)) * SW + 2 * c.tid]);
+      s0 = fv.x;
+      s1 = fv.y;
+    } else {
+      s0 = st.prev[k / 2 - 1][0];
+      s1 = st.prev[k / 2 - 1][1];
+    }
+    const double* wN0;  // weights of rows x+1, x, x-1 for the two columns
+    const double* wN1;
+    const double* wM0;
+    const double* wM1;
+    const double* wB0;
+    const double* wB1;
+    if (FAST) {
+      const double* wi = CM == 2 ? (resid ? a.ci : a.ci + 9) : ((resid ? c.tA : c.tK) + CINT * 9);
+      wN0 = wN1 = wM0 = wM1 = wB0 = wB1 = wi;
+    } else {
+      const double* tab = resid ? c.tA : c.tK;
+      const int bN = ((unsigned)(x + 1) < (unsigned)g.rows ? bandc(x + 1, g.rows) : 2) * 5;
+      const int bM = ((unsigned)x < (unsigned)g.rows ? bandc(x, g.rows) : 2) * 5;
+      const int bB = ((unsigned)(x - 1) < (unsigned)g.rows ? bandc(x - 1, g.rows) : 2) * 5;
+      wN0 = tab + (bN + c.cc0) * 9; wN1 = tab + (bN + c.cc1) * 9;
+      wM0 = tab + (bM + c.cc0) * 9; wM1 = tab + (bM + c.cc1) * 9;
+      wB0 = tab + (bB + c.cc0) * 9; wB1 = tab + (bB + c.cc1) * 9;
+    }
+    double (&A)[3][2] = st.acc[k - 1];
+#define FMS(w_, x_, a_) fma(resid ? -(w_) : (w_), (x_), (a_))
+    // bottom terms complete row x - 1
+    A[sB][0] = FMS(wB0[6], in0, A[sB][0]);
+    A[sB][1] = FMS(wB1[6], in1, A[sB][1]);
+    A[sM][0] = FMS(wM0[3], in0, A[sM][0]);
+    A[sM][1] = FMS(wM1[3], in1, A[sM][1]);
+    s0 = FMS(wN0[0], in0, s0);
+    s1 = FMS(wN1[0], in1, s1);
+    A[sB][0] = FMS(wB0[7], in1, A[sB][0]);
+    A[sB][1] = FMS(wB1[7], in2, A[sB][1]);
+    A[sM][0] = FMS(wM0[4], in1, A[sM][0]);
+    A[sM][1] = FMS(wM1[4], in2, A[sM][1]);
+    s0 = FMS(wN0[1], in1, s0);
+    s1 = FMS(wN1[1], in2, s1);
+    A[sB][0] = FMS(wB0[8], in2, A[sB][0]);
+    A[sB][1] = FMS(wB1[8], in3, A[sB][1]);
+    A[sM][0] = FMS(wM0[5], in2, A[sM][0]);
+    A[sM][1] = FMS(wM1[5], in3, A[sM][1]);
+    s0 = FMS(wN0[2], in2, s0);
+    s1 = FMS(wN1[2], in3, s1);
+#undef FMS
+    double v0 = A[sB][0], v1 = A[sB][1];
+    A[sN][0] = s0;   // slot of row x + 1 (was row x - 2, long complete)
+    A[sN][1] = s1;
+    const int row = x - 1;  // = t - 2k
+    if (!FAST) {
+      const bool rv = (unsigned)row < (unsigned)g.rows;
+      v0 = rv && c.cin0 ? v0 : 0.0;
+      v1 = rv && c.cin1 ? v1 : 0.0;
+    } else if (c.colmask) {
+      v0 = c.cin0 ? v0 : 0.0;
+      v1 = c.cin1 ? v1 : 0.0;
+    }
+    const bool orow = c.own && row >= c.R0 && row < c.R1;
+    if (NORM && k == 1 && orow) {
+      st.norm = fma(v0, v0, st.norm);   // out-of-grid columns hold 0
+      st.norm = fma(v1, v1, st.norm);
+    }
+    if (k == 2 * NSW && orow) {
+      double* dst = c.uob + (int64_t)row * g.cols + c.c0;
+      dst[0] = v0;                                   // owned pairs start in the grid
+      if ((FAST && !c.colmask) || c.cin1) dst[1] = v1;
+    }
+    out[k][0] = v0;
+    out[k][1] = v1;
+  }
+  // ---- restriction: push field S row y = t - 1 - 2S (columns c0, c0+1, c0+2)
+  if (RES) {
+    const int y = t - 1 - 2 * S;
+    const double x0 = st.cur[S][0], x1 = st.cur[S][1], x2 = R[S];
+    if (y & 1) {
+      st.racc = fma(0.125, x0, st.racc);
+      st.racc = fma(0.25, x1, st.racc);
+      st.racc = fma(0.125, x2, st.racc);
+    } else {
+      // bottom row of coarse row ci = y/2 - 1 (completes), top row of coarse row y/2
+      double s = fma(0.0625, x0, st.racc);
+      s = fma(0.125, x1, s);
+      s = fma(0.0625, x2, s);
+      const int ci = (y - 2) >> 1;
+      const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+      const int cj = c.c0 >> 1;
+      if (c.own && y >= 2 && ci >= (c.R0 >> 1) && 2 * ci + 1 < c.R1 && ci < rows_c && cj < cols_c) {
+        const int64_t pc = (int64_t)ci * cols_c + cj;
+        const bool actc = a.mask_c == nullptr || a.mask_c[pc];
+        a.rc[c.b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
+      }
+      double r = 0.0625 * x0;
+      r = fma(0.125, x1, r);
+      st.racc = fma(0.0625, x2, r);
+    }
+  }
   // ---- F_0 = u (+ P ec) at row t
   {
     double u0 = 0.0, u1 = 0.0;
@@ -114,148 +253,49 @@ __device__ __forceinline__ void step2(const StreamArgs& a, const Ctx2& c, const 
     if (PRO && rvr) {
       // u += P ec, coarse rows staged in ring_e (entry q = coarse column cjb + q);
       // the k_stream loop order: di = -1, 0, 1 (row parity), dj = -1, 0, 1 (column parity)
-      double s0 = 0.0, s1 = 0.0;
+      double p0 = 0.0, p1 = 0.0;
       if (t & 1) {
         const double* er = c.ring_e + (((t - 1) >> 1) & (PE - 1)) * EW;
-        s0 = fma(0.25, er[c.tid + 1], s0);   // (di 0, dj -1): coarse m
-        s0 = fma(0.25, er[c.tid], s0);       // (di 0, dj +1): coarse m - 1
-        s1 = fma(0.5, er[c.tid + 1], s1);    // (di 0, dj 0)
+        p0 = fma(0.25, er[c.tid + 1], p0);   // (di 0, dj -1): coarse m
+        p0 = fma(0.25, er[c.tid], p0);       // (di 0, dj +1): coarse m - 1
+        p1 = fma(0.5, er[c.tid + 1], p1);    // (di 0, dj 0)
       } else {
         const double* ea = c.ring_e + ((t >> 1) & (PE - 1)) * EW;        // di = -1: coarse row t/2
         const double* eb = c.ring_e + (((t - 2) >> 1) & (PE - 1)) * EW;  // di = +1: coarse row t/2 - 1
-        s0 = fma(0.125, ea[c.tid + 1], s0);
-        s0 = fma(0.125, ea[c.tid], s0);
-        s1 = fma(0.25, ea[c.tid + 1], s1);
-        s0 = fma(0.125, eb[c.tid + 1], s0);
-        s0 = fma(0.125, eb[c.tid], s0);
-        s1 = fma(0.25, eb[c.tid + 1], s1);
+        p0 = fma(0.125, ea[c.tid + 1], p0);
+        p0 = fma(0.125, ea[c.tid], p0);
+        p1 = fma(0.25, ea[c.tid + 1], p1);
+        p0 = fma(0.125, eb[c.tid + 1], p0);
+        p0 = fma(0.125, eb[c.tid], p0);
+        p1 = fma(0.25, eb[c.tid + 1], p1);
       }
-      u0 += s0;
-      u1 += s1;
+      u0 += p0;
+      u1 += p1;
     }
     // (the prolongation can reach one column past the grid: zero it there too)
     const bool m0 = FAST ? (!c.colmask || c.cin0) : (rvr && c.cin0);
     const bool m1 = FAST ? (!c.colmask || c.cin1) : (rvr && c.cin1);
-    nv[0][0] = m0 ? u0 : 0.0;
-    nv[0][1] = m1 ? u1 : 0.0;
+    out[0][0] = m0 ? u0 : 0.0;
+    out[0][1] = m1 ? u1 : 0.0;
   }
-  // ---- stages k = 1..S at row t - 2k (rows are CTA-uniform).  All 2S chains
-  // advance in lockstep, one window entry o at a time, so 2S independent FMAs are
-  // in flight per thread (each chain keeps stencil_dot's order: bitwise equal).
-  double v[S][2];
-  const double* wts[S][2];
-#pragma unroll
-  for (int k = 1; k <= S; ++k) {
-    const int row = t - 2 * k;
-    if (k & 1) {
-      const double2 fv = *reinterpret_cast<const double2*>(&c.ring_f[(row & (PDF - 1)) * SW + 2 * c.tid]);
-      v[k - 1][0] = fv.x;
-      v[k - 1][1] = fv.y;
-    } else {
-      v[k - 1][0] = hold[k / 2 - 1][0];
-      v[k - 1][1] = hold[k / 2 - 1][1];
-    }
-    if (FAST) {
-      wts[k - 1][0] = wts[k - 1][1] = CM == 2 ? ((k & 1) ? a.ci : a.ci + 9) : (((k & 1) ? c.tA : c.tK) + CINT * 9);
-    } else {
-      const double* tab = (k & 1) ? c.tA : c.tK;
-      const int rb = ((unsigned)row < (unsigned)g.rows ? bandc(row, g.rows) : 2) * 5;
-      wts[k - 1][0] = tab + (rb + c.cc0) * 9;
-      wts[k - 1][1] = tab + (rb + c.cc1) * 9;
-    }
-  }
-#pragma unroll
-  for (int o = 0; o < 9; ++o) {
-#pragma unroll
-    for (int k = 1; k <= S; ++k) {
-      const int sl = m3(PH - 2 * k - 1 + o / 3);
-      const double wa = (k & 1) ? -wts[k - 1][0][o] : wts[k - 1][0][o];
-      const double wb = (k & 1) ? -wts[k - 1][1][o] : wts[k - 1][1][o];
-      v[k - 1][0] = fma(wa, w[k - 1][sl][o % 3], v[k - 1][0]);
-      v[k - 1][1] = fma(wb, w[k - 1][sl][o % 3 + 1], v[k - 1][1]);
-    }
-  }
-#pragma unroll
-  for (int k = 1; k <= S; ++k) {
-    const int row = t - 2 * k;
-    double v0 = v[k - 1][0], v1 = v[k - 1][1];
-    if (!FAST) {
-      const bool rv = (unsigned)row < (unsigned)g.rows;
-      v0 = rv && c.cin0 ? v0 : 0.0;
-      v1 = rv && c.cin1 ? v1 : 0.0;
-    } else if (c.colmask) {
-      // uniform level, edge strip: interior weights, Dirichlet zeros outside the grid
-      v0 = c.cin0 ? v0 : 0.0;
-      v1 = c.cin1 ? v1 : 0.0;
-    }
-    const bool orow = c.own && row >= c.R0 && row < c.R1;
-    if (NORM && k == 1 && orow) {
-      acc = fma(v0, v0, acc);   // out-of-grid columns hold 0
-      acc = fma(v1, v1, acc);
-    }
-    if (k == 2 * NSW && orow) {
-      double* dst = c.uob + (int64_t)row * g.cols + c.c0;
-      dst[0] = v0;                                   // owned pairs start in the grid
-      if ((FAST && !c.colmask) || c.cin1) dst[1] = v1;
-    }
-    nv[k][0] = v0;
-    nv[k][1] = v1;
-  }
-  // ---- publish, then slide the windows (slot of the evicted row)
+  // ---- publish this step's rows (field j: row t - 2j), shift the own-value history
   const int sl = t & 1;
-  // exchange rows are split into even- and odd-column planes (conflict-free
-  // neighbour loads: left = odd plane [tid - 1], right = even plane [tid + 1])
 #pragma unroll
-  for (int k = 0; k < NF; ++k) {
-    c.xch[(k * 2 + sl) * SW + c.tid] = nv[k][0];
-    c.xch[(k * 2 + sl) * SW + T2 + c.tid] = nv[k][1];
+  for (int j = 0; j < NX; ++j) {
+    c.xch[(j * 2 + sl) * SW + c.tid] = out[j][0];
+    c.xch[(j * 2 + sl) * SW + T2 + c.tid] = out[j][1];
   }
-  if (RES) {
-    c.rlast[((t - 2 * S) & 3) * SW + c.tid] = nv[S][0];
-    c.rlast[((t - 2 * S) & 3) * SW + T2 + c.tid] = nv[S][1];
+#pragma unroll
+  for (int m = 0; m < NSW; ++m) {
+    st.prev[m][0] = st.cur[2 * m][0];
+    st.prev[m][1] = st.cur[2 * m][1];
+  }
+#pragma unroll
+  for (int j = 0; j < NX; ++j) {
+    st.cur[j][0] = out[j][0];
+    st.cur[j][1] = out[j][1];
   }
   __syncthreads();
-  if (RES) {
-    const int top = t - 2 * S;
-    if (top >= 2 && !(top & 1)) {
-      // coarse point (ci, m), m = c0 / 2: fine rows top-2..top, fine columns c0..c0+2
-      const int ci = (top - 2) >> 1;
-      const int rows_c = g.rows / 2, cols_c = g.cols / 2;
-      const int cj = c.c0 >> 1;
-      if (c.own && ci >= (c.R0 >> 1) && 2 * ci + 1 < c.R1 && ci < rows_c && cj < cols_c) {
-        // even plane [tid], odd plane [tid], even plane [tid + 1] = columns c0, c0+1, c0+2
-        const double* r0p = &c.rlast[((top - 2) & 3) * SW + c.tid];
-        const double* r1p = &c.rlast[((top - 1) & 3) * SW + c.tid];
-        const double* r2p = &c.rlast[(top & 3) * SW + c.tid];
-        double s = 0.0625 * r0p[0];
-        s = fma(0.125, r0p[T2], s);
-        s = fma(0.0625, r0p[1], s);
-        s = fma(0.125, r1p[0], s);
-        s = fma(0.25, r1p[T2], s);
-        s = fma(0.125, r1p[1], s);
-        s = fma(0.0625, r2p[0], s);
-        s = fma(0.125, r2p[T2], s);
-        s = fma(0.0625, r2p[1], s);
-        const int64_t pc = (int64_t)ci * cols_c + cj;
-        const bool actc = a.mask_c == nullptr || a.mask_c[pc];
-        a.rc[c.b * (int64_t)rows_c * cols_c + pc] = actc ? s : 0.0;
-      }
-    }
-  }
-  const int iL = T2 + max(c.tid - 1, 0), iR = min(c.tid + 1, T2 - 1);
-#pragma unroll
-  for (int k = 0; k < NF; ++k) {
-    const int sn = m3(PH - 2 * k);  // slot of the new row t - 2k (evicts row t - 2k - 3)
-    if (!(k & 1) && k / 2 < NSW) {
-      hold[k / 2][0] = w[k][sn][1];
-      hold[k / 2][1] = w[k][sn][2];
-    }
-    const double* xr = &c.xch[(k * 2 + sl) * SW];
-    w[k][sn][0] = xr[iL];
-    w[k][sn][1] = nv[k][0];
-    w[k][sn][2] = nv[k][1];
-    w[k][sn][3] = xr[iR];
-  }
 }
 
 // CM: 1 = band-class tables in shared memory; 2 = band-class tables with the
@@ -270,9 +310,8 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   const Grid& g = c.g;
   c.ring_u = smem2;                               // PD x SW (unused when ZU)
   c.ring_f = c.ring_u + PD * SW;                  // PDF x SW
-  c.xch = c.ring_f + PDF * SW;                    // NF x 2 x SW neighbour exchange rows
-  c.rlast = c.xch + NF * 2 * SW;                  // 4 x SW last-residual ring (RES)
-  c.ring_e = c.rlast + 4 * SW;                    // PE x EW (POST)
+  c.xch = c.ring_f + PDF * SW;                    // NX x 2 x SW exchange rows (even / odd planes)
+  c.ring_e = c.xch + St3<NSW, RES>::NX * 2 * SW;  // PE x EW (POST)
   double* tA = c.ring_e + PE * EW;                // 25 x 9
   double* tK = tA + NCLS * 9;                     // 25 x 9
   double* red = tK + NCLS * 9;                    // 32
@@ -325,21 +364,24 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   }
   __syncthreads();
 
-  double w[NF][3][4];
+  St3<NSW, RES> st;
 #pragma unroll
-  for (int k = 0; k < NF; ++k)
+  for (int k = 0; k < S; ++k)
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+    for (int r = 0; r < 3; ++r) st.acc[k][r][0] = st.acc[k][r][1] = 0.0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[k][r][q] = 0.0;
-  double hold[NSW][2];
+  for (int j = 0; j < St3<NSW, RES>::NX; ++j) st.cur[j][0] = st.cur[j][1] = 0.0;
 #pragma unroll
-  for (int m = 0; m < NSW; ++m) hold[m][0] = hold[m][1] = 0.0;
-  double acc = 0.0;
+  for (int m = 0; m < NSW; ++m) st.prev[m][0] = st.prev[m][1] = 0.0;
+  st.racc = 0.0;
+  st.norm = 0.0;
+  // the first step reads the exchange slot of step t0 - 1: start it at zero
+  for (int q = c.tid; q < 2 * St3<NSW, RES>::NX * SW; q += T2) c.xch[q] = 0.0;
 
   int t0 = c.R0 - S - 1;
   t0 -= m3(t0);
-  const int t1 = c.R1 + 2 * S;
+  // the restriction pushes field S row t - 1 - 2S: its last row R1 at step R1 + 2S + 1
+  const int t1 = c.R1 + 2 * S + (RES ? 1 : 0);
   int prow = t0;
   const int64_t cstride = g.cols;
   // prefetch: thread copies strip columns tid and tid + T2 (coalesced rows)
@@ -395,9 +437,9 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
     issue();                                                                               \
     cp_wait<DIST - 1>(); /* row t + 1 lands before this step's barrier publishes it */     \
     if (cta_fast && t - 2 * S >= 2 && t <= g.rows - 3)                                     \
-      step2<NSW, RES, PRO, NORM, ZU, CM, true, PH_>(a, c, t, w, hold, acc);                \
+      step3<NSW, RES, PRO, NORM, ZU, CM, true, PH_>(a, c, t, st);                          \
     else                                                                                   \
-      step2<NSW, RES, PRO, NORM, ZU, CM, false, PH_>(a, c, t, w, hold, acc);               \
+      step3<NSW, RES, PRO, NORM, ZU, CM, false, PH_>(a, c, t, st);                         \
   }
   for (int tb = t0; tb <= t1; tb += 3) {
     MGB_STEP2(0)
@@ -419,7 +461,7 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   }
 #endif
   if (NORM) {
-    double v = acc;
+    double v = st.norm;
     const int lane = c.tid & 31, wid = c.tid >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -436,8 +478,8 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
 }  // namespace
 
 static size_t stream2_smem(int nsw, bool res) {
-  const int nf = 2 * nsw + (res ? 1 : 0);
-  return sizeof(double) * ((size_t)(PD + PDF + 2 * nf + 4) * SW + PE * EW + 2 * NCLS * 9 + 32);
+  const int nx = 2 * nsw + (res ? 2 : 0);
+  return sizeof(double) * ((size_t)(PD + PDF + 2 * nx) * SW + PE * EW + 2 * NCLS * 9 + 32);
 }
 
 static int sm_count() {

@@ -536,3 +536,72 @@ def test_pipelined_host_solves_equal_single_calls():
     u1 = us[3].copy()
     h.run_cycles_host(np.ascontiguousarray(fs[3]), u1, 2, 1, 1, u_zero=False)
     assert np.array_equal(us2[3], u1)
+
+
+@pytest.mark.parametrize("rows,cols,theta,nu,net", [
+    (600, 600, math.pi / 4, 2, "conv_c2"),     # even sides
+    (511, 511, math.pi / 6, 2, "conv"),        # odd sides, two strips
+    (300, 777, math.pi / 3, 1, "conv"),        # rectangle, V(1,1)
+    (1023, 1023, math.pi / 4, 2, "fc"),        # fc net: boundary band classes differ
+    (97, 1201, math.pi / 4, 2, "conv_c2"),     # short and wide: many strips, few rows
+])
+def test_column_pair_stream_kernel_bit_identical(rows, cols, theta, nu, net):
+    """The column-pair row-streaming kernel (push-form stage chains) against the
+    one-column kernel, forced on every level of a band-class hierarchy: edge strips,
+    uniform and non-uniform levels, odd and even sides, segment boundaries.  u and
+    the histories are bitwise equal (the kernels share stencil_dot's FMA order)."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    table = gen.rotated_fd(1, theta, 1e-2, h=1.0 / (max(rows, cols) + 1))[0, 0]
+    levels = gen.levels_for(min(rows, cols))
+    h = mg.equip_inferred(mg.build_hierarchy_classed(rows, cols, table, levels), net_of(net))
+    h.set_passes(0, 1)                                    # streaming passes on every level
+    f = dv.to_dev(np.random.default_rng(7).uniform(-1, 1, (rows, cols)))
+    out = []
+    for kind in (1, 2):
+        h.set_stream_kernel(kind)
+        u = dv.zeros(f.shape)
+        out.append((u, dv.host(h.run_cycles(f, u, 3, nu, nu, u_zero=True))[0]))
+    h.set_stream_kernel(0)
+    assert t.equal(out[0][0], out[1][0]), float((out[0][0] - out[1][0]).abs().max())
+    assert np.allclose(out[0][1], out[1][1], rtol=1e-13, atol=0)
+
+
+def test_column_pair_stream_kernel_full_size_c2():
+    """Config-2 size (4095^2, where the automatic choice is the column-pair kernel
+    on levels 0-1): bitwise equal to the one-column kernel over 3 V(2,2) cycles."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    n = 4095
+    table = gen.rotated_fd(1, math.pi / 4, 1e-3, h=1.0 / (n + 1))[0, 0]
+    h = mg.equip_inferred(mg.build_hierarchy_classed(n, n, table, gen.levels_for(n)), net_of("conv_c2"))
+    f = dv.to_dev(gen.uniform_rhs(n, 1))
+    out = []
+    for kind in (1, 0):
+        h.set_stream_kernel(kind)
+        u = dv.zeros(f.shape)
+        out.append((u, dv.host(h.run_cycles(f, u, 3, 2, 2, u_zero=True))[0]))
+    assert t.equal(out[0][0], out[1][0]), float((out[0][0] - out[1][0]).abs().max())
+    assert np.allclose(out[0][1], out[1][1], rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("n,nparts", [(1023, 2), (1023, 3)])
+def test_virtual_decomposition_column_pair_kernel(n, nparts, monkeypatch):
+    """Row-block decomposition with the column-pair kernel on the distributed levels
+    (owned row ranges, ghost bands): bitwise the single-domain result."""
+    from paper_2102_12071_b200 import dd, device as dv
+    monkeypatch.setenv("MGB_STREAM_MIN", "0")
+    t = dv.torch()
+    table = gen.rotated_fd(1, math.pi / 3, 0.01, h=1.0 / (n + 1))[0, 0]
+    h = mg.equip_inferred(mg.build_hierarchy_classed(n, n, table, gen.levels_for(n)), net_of("conv"))
+    h.set_stream_kernel(2)
+    f_full = dv.to_dev(gen.uniform_rhs(n, 11))
+    u_ref = dv.zeros(f_full.shape)
+    hist_ref = dv.host(h.run_cycles(f_full, u_ref, 4, 2, 2, u_zero=True))[0]
+    s = dd.DecomposedSolver(h, nparts, local=True, agglomerate_rows=n // 4)
+    for p, (r0, r1) in enumerate(s.rows(p) for p in range(nparts)):
+        s.set_rhs(p, f_full[r0:r1].contiguous())
+    hist = dv.host(s.run_cycles(4, 2, 2))
+    u = t.cat([s.solution(p) for p in range(nparts)])
+    assert t.equal(u, u_ref), float((u - u_ref).abs().max())
+    assert np.allclose(hist, hist_ref, rtol=1e-13, atol=0)
