@@ -80,7 +80,6 @@ struct Ctx2 {
   Grid g;
   int b, tid, j0, c0, R0, R1;
   bool cin0, cin1, own;
-  bool colmask;     // FAST steps of a uniform level's edge strip: zero out-of-grid columns
   int cc0, cc1;     // band classes of columns c0, c0 + 1
   double* ring_u;
   double* ring_f;
@@ -113,9 +112,9 @@ struct St3 {
 
 
 // One pipeline step (row t) for the thread's column pair.  FAST: every row the
-// step touches is interior and the CTA's columns are interior (or the level is
-// uniform: then only out-of-grid columns need zeroing, colmask).  PH = t mod 3.
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool FAST, int PH>
+// step touches is interior and the CTA's columns are interior, or (CMASK) the level
+// is uniform and only out-of-grid columns need zeroing.  PH = t mod 3.
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool FAST, bool CMASK, int PH>
 __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const int t, St3<NSW, RES>& st) {
   using P = SP2<NSW, RES>;
   constexpr int S = P::S, NX = St3<NSW, RES>::NX;
@@ -198,7 +197,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
       const bool rv = (unsigned)row < (unsigned)g.rows;
       v0 = rv && c.cin0 ? v0 : 0.0;
       v1 = rv && c.cin1 ? v1 : 0.0;
-    } else if (c.colmask) {
+    } else if (CMASK) {
       v0 = c.cin0 ? v0 : 0.0;
       v1 = c.cin1 ? v1 : 0.0;
     }
@@ -210,7 +209,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     if (k == 2 * NSW && orow) {
       double* dst = c.uob + (int64_t)row * g.cols + c.c0;
       dst[0] = v0;                                   // owned pairs start in the grid
-      if ((FAST && !c.colmask) || c.cin1) dst[1] = v1;
+      if ((FAST && !CMASK) || c.cin1) dst[1] = v1;
     }
     out[k][0] = v0;
     out[k][1] = v1;
@@ -273,8 +272,8 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
       u1 += p1;
     }
     // (the prolongation can reach one column past the grid: zero it there too)
-    const bool m0 = FAST ? (!c.colmask || c.cin0) : (rvr && c.cin0);
-    const bool m1 = FAST ? (!c.colmask || c.cin1) : (rvr && c.cin1);
+    const bool m0 = FAST ? (!CMASK || c.cin0) : (rvr && c.cin0);
+    const bool m1 = FAST ? (!CMASK || c.cin1) : (rvr && c.cin1);
     out[0][0] = m0 ? u0 : 0.0;
     out[0][1] = m1 ? u1 : 0.0;
   }
@@ -352,7 +351,6 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   // whose band classes are all equal (then only out-of-grid columns need zeroing)
   const bool cta_int = c.j0 - H >= 2 && c.j0 - H + SW - 1 <= g.cols - 3;
   const bool cta_fast = cta_int || a.uniform;
-  c.colmask = !cta_int;
 #ifdef MGB_CTA_PROF
   unsigned long long prof_t0 = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
@@ -436,10 +434,12 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
     const int t = tb + PH_;                                                                \
     issue();                                                                               \
     cp_wait<DIST - 1>(); /* row t + 1 lands before this step's barrier publishes it */     \
-    if (cta_fast && t - 2 * S >= 2 && t <= g.rows - 3)                                     \
-      step3<NSW, RES, PRO, NORM, ZU, CM, true, PH_>(a, c, t, st);                          \
+    if (t - 2 * S >= 2 && t <= g.rows - 3 && cta_int)                                      \
+      step3<NSW, RES, PRO, NORM, ZU, CM, true, false, PH_>(a, c, t, st);                   \
+    else if (t - 2 * S >= 2 && t <= g.rows - 3 && cta_fast)                                \
+      step3<NSW, RES, PRO, NORM, ZU, CM, true, true, PH_>(a, c, t, st);                    \
     else                                                                                   \
-      step3<NSW, RES, PRO, NORM, ZU, CM, false, PH_>(a, c, t, st);                         \
+      step3<NSW, RES, PRO, NORM, ZU, CM, false, false, PH_>(a, c, t, st);                  \
   }
   for (int tb = t0; tb <= t1; tb += 3) {
     MGB_STEP2(0)
