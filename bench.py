@@ -503,6 +503,9 @@ def run_ours(args):
         cpu = cpu_sample_pool(args.config) if batched else cpu_sample(args.config, steps=1)
     if rank == 0:
         bpu = cycle_bytes_per_fine_unknown(n, levels, nu, nu)
+        # which streaming kernel runs level 0 (mgb_stream.cu launch_stream dispatch)
+        kname = ("k_stream2 (column pairs, push-form chains)" if compact and nb == 1 and n * n >= (2 << 20)
+                 else "k_stream (one column per thread)")
         hl = hist_all[:, -1]
         line = {
             "metric": "unknowns/sec per V-cycle (fp64)", "value": value, "unit": "unknowns/s",
@@ -514,13 +517,13 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (level-0 u, f and tables exceed 126 MB)",
                        "parallelism": (f"batch split x{world}" if batched else f"replicas x{world}")},
             "roofline": {"bound": "hbm",
-                         "kernel": "k_stream PRE, level 0 (sweeps + residual + full-weighting restriction, "
+                         "kernel": f"{kname} PRE, level 0 (sweeps + residual + full-weighting restriction, "
                                    "one row-streaming pass)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": pass_bytes, "launch_ms": ms_pre.value,
                          "storage": "band-class tables (A, M exact, shared memory)" if compact else "per-point planes",
-                         "post": {"kernel": "k_stream POST, level 0 (prolongation + sweeps)",
+                         "post": {"kernel": f"{kname} POST, level 0 (prolongation + sweeps)",
                                   "achieved": achieved_post, "frac": achieved_post / peak,
                                   "launch_ms": ms_post.value}},
             "cycle_model": {"survey_bytes_per_fine_unknown": 172.6 if compact else bpu,
