@@ -1120,11 +1120,24 @@ static int enqueue_finalize(mgb_work* w, int nblk, double* hist, int64_t hstride
   return MGB_OK;
 }
 
+static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStream_t s);
+
 // hist[b * hstride] = ||f - A u|| / ||f|| on level 0
 static int enqueue_resnorm(mgb_work* w, const double* f, const double* u, double* hist, int64_t hstride,
                            cudaStream_t s) {
   const mgb_hier* h = w->h;
   const LevelD& l0 = h->lv[0];
+  if (u && h->fused && l0.ks == 1 && l0.K && (int64_t)l0.n * h->batch >= h->stream_min) {
+    // row-streaming residual pass (the plain-sweep pass with its norm and no output):
+    // HBM-bound, where the per-point residual kernel is load-latency-bound at this size
+    StreamArgs a = stream_args(w, 0, f, s);
+    a.u = u;
+    a.uo = nullptr;
+    a.partials = w->partials;
+    int nb = 0;
+    MGB_CUDA_TRY(launch_stream(a, 1, false, false, true, &nb));
+    return enqueue_finalize(w, nb, hist, hstride, s);
+  }
   MGB_CUDA_TRY(launch_resnorm(h->grid(0), l0.opA(), l0.mask, f, u, w->partials, s));
   return enqueue_finalize(w, resnorm_blocks(h->grid(0)), hist, hstride, s);
 }
@@ -1227,6 +1240,20 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   return a;
 }
 
+// history entry from a fused pass's partial sums.  Zero start: the input residual is
+// f itself (f - A 0 = f exactly), so the same sums give ||f||^2: stored as the
+// denominator (history[0] = 1 exactly; no separate ||f|| pass, see get_graph).
+static cudaError_t finalize_pre(mgb_work* w, int nb, bool zero_start, double* hist, int64_t hstride,
+                                cudaStream_t s) {
+  if (zero_start) return launch_finalize(w->h->batch, nb, w->partials, w->fnorm2, nullptr, hist, hstride, s);
+  return launch_finalize(w->h->batch, nb, w->partials, nullptr, w->fnorm2, hist, hstride, s);
+}
+
+// the first fused PRE of a zero-start solve yields ||f|| (finalize_pre)
+static bool pre_gives_fnorm(const mgb_hier* h, int nu1, int nu2) {
+  return use_stream(h, 0, nu1, nu2) && nu1 > 0 && h->lv[0].ks == 1;
+}
+
 // PRE on level l: [history norm of the input] + nu1 sweeps + residual + restriction
 // into w->f[l+1].  in == null: zero initial guess.  *cur / *oth: ping-pong buffers
 // (the result ends in *cur).  hist != null: relative residual of the input.
@@ -1241,7 +1268,7 @@ static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, do
     a.uo = *oth;
     a.partials = hist ? w->partials : nullptr;
     MGB_CUDA_TRY(launch_pass(h, l, a, 1, false, false, hist != nullptr, &nb));
-    if (hist) MGB_CUDA_TRY(launch_finalize(h->batch, nb, w->partials, nullptr, w->fnorm2, hist, hstride, s));
+    if (hist) MGB_CUDA_TRY(finalize_pre(w, nb, in == nullptr, hist, hstride, s));
     std::swap(*cur, *oth);
     in = *cur;
     hist = nullptr;
@@ -1251,7 +1278,7 @@ static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, do
   a.rc = w->f[l + 1];
   a.partials = hist ? w->partials : nullptr;
   MGB_CUDA_TRY(launch_pass(h, l, a, split ? 1 : nu1, true, false, hist != nullptr, &nb));
-  if (hist) MGB_CUDA_TRY(launch_finalize(h->batch, nb, w->partials, nullptr, w->fnorm2, hist, hstride, s));
+  if (hist) MGB_CUDA_TRY(finalize_pre(w, nb, in == nullptr, hist, hstride, s));
   std::swap(*cur, *oth);
   return MGB_OK;
 }
@@ -1427,7 +1454,8 @@ static int get_graph(mgb_work* w, const GraphKey& key, GraphEntry** out) {
         cudaError_t e = cudaMemsetAsync(key.u, 0, sizeof(double) * nb, w->cap);
         if (e != cudaSuccess) st = cuda_fail(e, "memset");
       }
-      if (!st) st = enqueue_fnorm(w, key.f, w->cap);
+      if (!st && !(key.u_zero && key.cycles > 0 && pre_gives_fnorm(w->h, key.nu1, key.nu2)))
+        st = enqueue_fnorm(w, key.f, w->cap);
       for (int c = 0; c < key.cycles && !st; ++c)
         st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap, key.u_zero && c == 0,
                             key.hist + c, key.cycles + 1);
@@ -1467,7 +1495,8 @@ static int enqueue_key(mgb_work* w, const GraphKey& key, cudaStream_t cs) {
       cudaError_t e = cudaMemsetAsync(key.u, 0, sizeof(double) * nb, cs);
       if (e != cudaSuccess) st = cuda_fail(e, "memset");
     }
-    if (!st) st = enqueue_fnorm(w, key.f, cs);
+    if (!st && !(key.u_zero && key.cycles > 0 && pre_gives_fnorm(w->h, key.nu1, key.nu2)))
+      st = enqueue_fnorm(w, key.f, cs);
     for (int c = 0; c < key.cycles && !st; ++c)
       st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, cs, key.u_zero && c == 0, key.hist + c,
                           key.cycles + 1);

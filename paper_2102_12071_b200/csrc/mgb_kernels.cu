@@ -146,7 +146,9 @@ __global__ void __launch_bounds__(1024) k_finalize(int nblk, const double* __res
     if (out2) out2[b] = t;
     if (hist) {
       const double nr = sqrt(t);
-      const double fn = fnorm2 ? sqrt(fnorm2[b]) : 1.0;
+      // out2 without fnorm2: the sum is ||f||^2 itself (zero-start residual), stored as
+      // the denominator of this and later entries
+      const double fn = fnorm2 ? sqrt(fnorm2[b]) : (out2 ? nr : 1.0);
       const double den = fn > 0.0 ? fn : 1.0;          // hierarchy.py:126-127
       hist[b * hstride] = nr == 0.0 ? 0.0 : nr / den;    // hierarchy.py:129-131
     }

@@ -169,7 +169,7 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
       if (MSK && c.cin && !c.mk[(int64_t)row * g.cols + c.col]) val = 0.0;
       if (!FAST) val = c.cin ? val : 0.0;
       if (NORM && k == 1 && c.owned_c && row >= c.R0 && row < c.R1) acc = fma(val, val, acc);
-      if (k == 2 * NSW && c.owned_c && row >= c.R0 && row < c.R1) c.uob[(int64_t)row * g.cols + c.col] = val;
+      if (k == 2 * NSW && a.uo && c.owned_c && row >= c.R0 && row < c.R1) c.uob[(int64_t)row * g.cols + c.col] = val;
     }
     nv[k] = val;
   }

@@ -206,7 +206,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
       st.norm = fma(v0, v0, st.norm);   // out-of-grid columns hold 0
       st.norm = fma(v1, v1, st.norm);
     }
-    if (k == 2 * NSW && orow) {
+    if (k == 2 * NSW && orow && a.uo) {
       double* dst = c.uob + (int64_t)row * g.cols + c.c0;
       dst[0] = v0;                                   // owned pairs start in the grid
       if ((FAST && !CMASK) || c.cin1) dst[1] = v1;

@@ -454,8 +454,10 @@ def test_nccl_decomposition_single_rank(monkeypatch):
                                   "case_rot31_fc_v22", "c4_p0", "case_rect20x27_conv_v11"])
 def test_tile_and_stream_passes_bit_identical(name):
     """Tile-local fused passes (mid-size levels) vs row-streaming passes on every
-    level: the same arithmetic, so u is bitwise equal; histories differ only in
-    the order of the norm's partial sums."""
+    level: the same arithmetic, so u is bitwise equal; histories differ in the
+    order of the norm's partial sums and in how the final entry's residual is
+    evaluated (streamed FMA chain vs the reference-order residual kernel), so
+    they are held to the reference tolerance."""
     from paper_2102_12071_b200 import device as dv
     t = dv.torch()
     c = load(name)
@@ -470,7 +472,7 @@ def test_tile_and_stream_passes_bit_identical(name):
         hist = h.run_cycles(f, u, c["cycles"], c["nu"], c["nu"], u_zero=True).clone()
         runs.append((u, dv.host(hist)[0]))
     assert t.equal(runs[0][0], runs[1][0])
-    assert np.allclose(runs[0][1], runs[1][1], rtol=1e-13, atol=1e-300)
+    assert_hist(runs[0][1], runs[1][1])
     assert_hist(runs[1][1], runs[2][1])                       # vs separate kernels: rounding only
     assert rel_err(dv.host(runs[1][0]), dv.host(runs[2][0])) <= 1e-12
     assert_hist(runs[1][1], g["history"])                     # and the reference
