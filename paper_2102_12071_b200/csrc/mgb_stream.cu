@@ -440,7 +440,7 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   // pair kernel would read every interior weight from shared memory)
   // (levels below ~2M points, e.g. 1023^2 with five strips, measured faster on the
   // one-column kernel: more, shorter CTAs)
-  const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() >= (2 << 20));
+  const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() >= 1000000);
   if (cm == 2 && pairs) return launch_stream2(a, nsw, res, pro, norm, nblocks);
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \

@@ -26,7 +26,10 @@ struct StreamArgs {
   int kernel;              // streaming kernel: 0 auto, 1 one column per thread, 2 column pairs
   // two-column kernel CTA map (set by its launcher): edge strips (first / last) get
   // shorter segments (their steps take the boundary-class path), listed first
-  int nstrips, nedge, seg_edge, nseg_edge;
+  // segments of a strip: the first has seg_first rows, the others seg (the last: the
+  // rest); first / last segments on the grid's top / bottom are trimmed because their
+  // boundary rows take the slow step variant
+  int nstrips, nedge, seg_first, nseg, seg_edge, seg_edge_first, nseg_edge;
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
   cudaStream_t stream;
 };

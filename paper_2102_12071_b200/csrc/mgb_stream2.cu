@@ -111,11 +111,15 @@ struct St3 {
 };
 
 
-// One pipeline step (row t) for the thread's column pair.  FAST: every row the
-// step touches is interior and the CTA's columns are interior, or (CMASK) the level
-// is uniform and only out-of-grid columns need zeroing.  PH = t mod 3.
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool FAST, bool CMASK, int PH>
+// One pipeline step (row t) for the thread's column pair.  PH = t mod 3.
+// MODE 0: interior strip, interior rows (constant-bank weights, no tests);
+//      1: uniform level, edge strip, interior rows (constant weights, out-of-grid columns zeroed);
+//      2: edge strip, interior rows (each column's row-band-2 class weights, columns zeroed);
+//      3: anything else (per output row band and column class, rows and columns tested).
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, int MODE, int PH>
 __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const int t, St3<NSW, RES>& st) {
+  constexpr bool FAST = MODE < 3;                  // every row the step touches is interior
+  constexpr bool CMASK = MODE == 1 || MODE == 2;   // zero out-of-grid columns
   using P = SP2<NSW, RES>;
   constexpr int S = P::S, NX = St3<NSW, RES>::NX;
   const Grid& g = c.g;
@@ -155,9 +159,13 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     const double* wM1;
     const double* wB0;
     const double* wB1;
-    if (FAST) {
+    if (MODE <= 1) {
       const double* wi = CM == 2 ? (resid ? a.ci : a.ci + 9) : ((resid ? c.tA : c.tK) + CINT * 9);
       wN0 = wN1 = wM0 = wM1 = wB0 = wB1 = wi;
+    } else if (MODE == 2) {
+      const double* tab = resid ? c.tA : c.tK;
+      wN0 = wM0 = wB0 = tab + (10 + c.cc0) * 9;   // row band 2: nine weights per column
+      wN1 = wM1 = wB1 = tab + (10 + c.cc1) * 9;
     } else {
       const double* tab = resid ? c.tA : c.tK;
       const int bN = ((unsigned)(x + 1) < (unsigned)g.rows ? bandc(x + 1, g.rows) : 2) * 5;
@@ -320,7 +328,7 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   c.b = blockIdx.z;
   const int64_t n = g.n();
   // CTA -> (strip, row segment): the edge strips' CTAs first, then the interior ones
-  int strip, seg, sy;
+  int strip, seg, seg1, sy;
   {
     const int id = blockIdx.x;
     const int ne = a.nedge;
@@ -328,11 +336,13 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
       strip = (id % ne == 0) ? 0 : a.nstrips - 1;
       sy = id / ne;
       seg = a.seg_edge;
+      seg1 = a.seg_edge_first;
     } else {
       const int q = id - ne * a.nseg_edge, ni = a.nstrips - ne;
       strip = 1 + q % ni;
       sy = q / ni;
       seg = a.seg;
+      seg1 = a.seg_first;
     }
   }
   c.j0 = strip * WOUT;                            // first owned column (even)
@@ -342,8 +352,8 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   c.own = 2 * c.tid >= H && 2 * c.tid < H + WOUT && c.cin0;
   c.cc0 = c.cin0 ? bandc(c.c0, g.cols) : 2;       // out-of-grid columns are zeroed anyway
   c.cc1 = c.cin1 ? bandc(c.c0 + 1, g.cols) : 2;
-  c.R0 = a.own0 + sy * seg;
-  c.R1 = min(a.own1 > 0 ? a.own1 : g.rows, c.R0 + seg);
+  c.R0 = a.own0 + (sy == 0 ? 0 : seg1 + (sy - 1) * seg);
+  c.R1 = min(a.own1 > 0 ? a.own1 : g.rows, c.R0 + (sy == 0 ? seg1 : seg));
   const double* fb = a.f + c.b * n;
   const double* ub = ZU ? nullptr : a.u + c.b * n;
   c.uob = a.uo + c.b * n;
@@ -434,12 +444,15 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
     const int t = tb + PH_;                                                                \
     issue();                                                                               \
     cp_wait<DIST - 1>(); /* row t + 1 lands before this step's barrier publishes it */     \
-    if (t - 2 * S >= 2 && t <= g.rows - 3 && cta_int)                                      \
-      step3<NSW, RES, PRO, NORM, ZU, CM, true, false, PH_>(a, c, t, st);                   \
-    else if (t - 2 * S >= 2 && t <= g.rows - 3 && cta_fast)                                \
-      step3<NSW, RES, PRO, NORM, ZU, CM, true, true, PH_>(a, c, t, st);                    \
+    const bool rows_int = t - 2 * S >= 2 && t <= g.rows - 3;                               \
+    if (rows_int && cta_int)                                                               \
+      step3<NSW, RES, PRO, NORM, ZU, CM, 0, PH_>(a, c, t, st);                             \
+    else if (rows_int && cta_fast)                                                         \
+      step3<NSW, RES, PRO, NORM, ZU, CM, 1, PH_>(a, c, t, st);                             \
+    else if (rows_int)                                                                     \
+      step3<NSW, RES, PRO, NORM, ZU, CM, 2, PH_>(a, c, t, st);                             \
     else                                                                                   \
-      step3<NSW, RES, PRO, NORM, ZU, CM, false, false, PH_>(a, c, t, st);                  \
+      step3<NSW, RES, PRO, NORM, ZU, CM, 3, PH_>(a, c, t, st);                             \
   }
   for (int tb = t0; tb <= t1; tb += 3) {
     MGB_STEP2(0)
@@ -494,44 +507,66 @@ static int sm_count() {
 }
 
 // Rows per CTA segment.  Interior strips get segments of seg rows, the edge strips
-// (boundary band classes: every step takes the class-lookup path, r times the cost
-// of an interior step) segments of about seg / r rows, so all CTAs finish together;
-// the segment counts fill whole waves of the measured occupancy with the fewest
+// (boundary columns: every step takes a class-lookup variant, r times the cost of
+// an interior step) segments of about seg / r rows, and the first / last segment on
+// the grid's top / bottom edge is shorter by the extra cost of its boundary-row
+// steps, so that all CTAs finish together (per-CTA %globaltimer probes); the
+// segment counts fill whole waves of the measured occupancy with the fewest
 // pipeline fills (3S + 3 steps per segment).
-static void choose_seg2(const Grid& g, int nsw, bool res, int occ, bool uniform, StreamArgs& a) {
+struct SegPlan {
+  int seg, first, n;
+};
+// n segments over R rows: first = seg - dt, middle seg, last ~ seg - db
+static SegPlan seg_plan(int R, int n, int dt, int db) {
+  SegPlan p;
+  p.n = std::max(1, std::min(n, R));
+  p.seg = std::max(1, (R + dt + db + p.n - 1) / p.n);
+  p.first = std::max(1, std::min(R, p.seg - dt));
+  // the plan must cover R rows with exactly n non-empty segments
+  while (p.n > 1 && p.first + (int64_t)(p.n - 2) * p.seg >= R) --p.n;
+  while (p.first + (int64_t)(p.n - 1) * p.seg < R) ++p.seg;
+  return p;
+}
+
+static void choose_seg2(const Grid& g, int nsw, bool res, int occ, bool uniform, bool top, bool bot,
+                        StreamArgs& a) {
   const int H = 2 * nsw + 2, wout = SW - 2 * H, S = 2 * nsw + (res ? 1 : 0);
   const int strips = (g.cols + wout - 1) / wout;
   const int ne = std::min(strips, 2), ni = strips - ne;
   const int64_t slots = (int64_t)sm_count() * std::max(occ, 1);
   static const double r_env = getenv("MGB_EDGE_RATIO") ? atof(getenv("MGB_EDGE_RATIO")) : 0.0;
-  // measured (k_stream2, 4095^2, per-CTA timers): class-lookup steps ~2.2x interior steps
-  const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : (uniform ? 1.05 : 2.2));
+  // measured (k_stream2, 4095^2 / 2047^2, per-CTA timers): uniform edge strips ~1.05x,
+  // class-weight edge steps ~1.3x, boundary-row steps ~2.2x an interior step
+  const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : (uniform ? 1.05 : 1.3));
   const int F = 3 * S + 3;
+  const int dtrim = (int)(1.2 * (2 * S + 2));
+  const int dt = top ? dtrim : 0, db = bot ? dtrim : 0;
   double best_t = 1e300;
   a.nstrips = strips;
   a.nedge = ne;
-  a.seg = a.seg_edge = g.rows;
-  a.nseg_edge = 1;
   for (int nseg = 1; nseg <= std::max(1, g.rows / 16); ++nseg) {
-    const int seg = (g.rows + nseg - 1) / nseg;
-    const int nsi = (g.rows + seg - 1) / seg;
-    int seg_e = std::max(16, (int)((seg + F) / r) - F);
-    seg_e = std::min(seg_e, g.rows);
-    const int nse = (g.rows + seg_e - 1) / seg_e;
-    const int64_t ctas = ((int64_t)ni * nsi + (int64_t)ne * nse) * g.batch;
+    const SegPlan pi = seg_plan(g.rows, nseg, dt, db);
+    const int seg_e_target = std::max(16, (int)((pi.seg + F) / r) - F);
+    const SegPlan pe = seg_plan(g.rows, (g.rows + dt + db + seg_e_target - 1) / seg_e_target, dt, db);
+    const int64_t ctas = ((int64_t)(ni > 0 ? ni : 0) * pi.n + (int64_t)ne * pe.n) * g.batch;
     const int64_t waves = (ctas + slots - 1) / slots;
-    const double t = (double)waves * std::max((double)(seg + F), r * (seg_e + F));
+    const double t = (double)waves * std::max((double)(pi.seg + F), r * (pe.seg + F));
     if (t < best_t) {
       best_t = t;
-      a.seg = seg;
-      a.seg_edge = seg_e;
-      a.nseg_edge = nse;
+      a.seg = pi.seg;
+      a.seg_first = pi.first;
+      a.nseg = pi.n;
+      a.seg_edge = pe.seg;
+      a.seg_edge_first = pe.first;
+      a.nseg_edge = pe.n;
     }
   }
   static const int force_seg = getenv("MGB_SEG") ? atoi(getenv("MGB_SEG")) : 0;  // experiments only
   if (force_seg > 0) {
-    a.seg = a.seg_edge = force_seg;
-    a.nseg_edge = (g.rows + force_seg - 1) / force_seg;
+    const SegPlan p = seg_plan(g.rows, (g.rows + force_seg - 1) / force_seg, 0, 0);
+    a.seg = a.seg_edge = p.seg;
+    a.seg_first = a.seg_edge_first = p.first;
+    a.nseg = a.nseg_edge = p.n;
   }
 }
 
@@ -555,10 +590,9 @@ static cudaError_t run_k2(KF kern, int nsw, bool res, StreamArgs a, int* nblocks
   }
   Grid go = a.g;
   go.rows = a.own1 - a.own0;
-  choose_seg2(go, nsw, res, occ, a.uniform != 0, a);
+  choose_seg2(go, nsw, res, occ, a.uniform != 0, a.own0 == 0, a.own1 == a.g.rows, a);
   const int ni = a.nstrips - a.nedge;
-  const int nsi = (go.rows + a.seg - 1) / a.seg;
-  const int nctas = a.nedge * a.nseg_edge + ni * nsi;
+  const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
   const dim3 grid(nctas, 1, a.g.batch);
   if (nblocks) *nblocks = nctas;
   kern<<<grid, T2, smem, a.stream>>>(a);

@@ -7,6 +7,10 @@ import bench
 from paper_2102_12071_b200 import _lib, device as dv
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 h, f_host, info = bench.build_problem(cfg, 0)
+if len(sys.argv) > 2:  # streaming kernel: 0 auto, 1 one column, 2 column pairs
+    h.set_stream_kernel(int(sys.argv[2]))
+if len(sys.argv) > 3:  # stream_min (points): levels below run tile passes
+    h.set_passes(int(sys.argv[3]))
 nu = info["nu"]
 w = h.acquire_work()
 res = []
