@@ -49,7 +49,12 @@ constexpr int DIST = 5;           // prefetch distance (rows ahead)
 #ifndef MGB_S2MINB
 #define MGB_S2MINB 2
 #endif
-constexpr int MINB = MGB_S2MINB;  // CTAs per SM the register budget is sized for
+#ifndef MGB_S2MINB_PRE
+#define MGB_S2MINB_PRE 2
+#endif
+// CTAs per SM the register budget is sized for (3 PRE CTAs fit in shared memory with
+// the compact exchange layout, but measured 40 % slower at 168 registers)
+constexpr int MINB = MGB_S2MINB, MINB_PRE = MGB_S2MINB_PRE;
 constexpr int PE = 8;             // ring of coarse rows (POST prolongation), power of two
 constexpr int EW = T2 + 2;        // coarse columns staged per CTA
 constexpr int NCLS = 25;
@@ -103,6 +108,9 @@ template <int NSW, bool RES>
 struct St3 {
   static constexpr int S = 2 * NSW + (RES ? 1 : 0);
   static constexpr int NX = RES ? S + 1 : S;   // exchanged fields (F_S feeds the restriction)
+  // one exchange buffer: NX fields x (even, odd) column planes; the restriction field
+  // F_S (last) needs only its even plane (right neighbours)
+  static constexpr int XB = NX * SW - (RES ? T2 : 0);
   double acc[S][3][2];    // open output rows of stage k (slot = row mod 3), two columns
   double cur[NX][2];      // own values of field j published at the previous step
   double prev[NSW][2];    // own values of fields 0, 2, .. published two steps back
@@ -130,8 +138,8 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     const int iL = max(c.tid - 1, 0), iR = min(c.tid + 1, T2 - 1);
 #pragma unroll
     for (int j = 0; j < NX; ++j) {
-      const double* xr = &c.xch[(j * 2 + slp) * SW];
-      L[j] = xr[T2 + iL];
+      const double* xr = &c.xch[slp * St3<NSW, RES>::XB + j * SW];
+      L[j] = (RES && j == S) ? 0.0 : xr[T2 + iL];
       R[j] = xr[iR];
     }
   }
@@ -289,8 +297,8 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
   const int sl = t & 1;
 #pragma unroll
   for (int j = 0; j < NX; ++j) {
-    c.xch[(j * 2 + sl) * SW + c.tid] = out[j][0];
-    c.xch[(j * 2 + sl) * SW + T2 + c.tid] = out[j][1];
+    c.xch[sl * St3<NSW, RES>::XB + j * SW + c.tid] = out[j][0];
+    if (!(RES && j == S)) c.xch[sl * St3<NSW, RES>::XB + j * SW + T2 + c.tid] = out[j][1];
   }
 #pragma unroll
   for (int m = 0; m < NSW; ++m) {
@@ -308,7 +316,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
 // CM: 1 = band-class tables in shared memory; 2 = band-class tables with the
 // interior class read from the kernel parameters (constant-bank operands).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM>
-__global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
+__global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArgs a) {
   using P = SP2<NSW, RES>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
   extern __shared__ __align__(16) double smem2[];
@@ -318,8 +326,8 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   c.ring_u = smem2;                               // PD x SW (unused when ZU)
   c.ring_f = c.ring_u + PD * SW;                  // PDF x SW
   c.xch = c.ring_f + PDF * SW;                    // NX x 2 x SW exchange rows (even / odd planes)
-  c.ring_e = c.xch + St3<NSW, RES>::NX * 2 * SW;  // PE x EW (POST)
-  double* tA = c.ring_e + PE * EW;                // 25 x 9
+  c.ring_e = c.xch + 2 * St3<NSW, RES>::XB;       // PE x EW (POST)
+  double* tA = c.ring_e + (PRO ? PE * EW : 0);    // 25 x 9
   double* tK = tA + NCLS * 9;                     // 25 x 9
   double* red = tK + NCLS * 9;                    // 32
   c.tA = tA;
@@ -384,7 +392,7 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
   st.racc = 0.0;
   st.norm = 0.0;
   // the first step reads the exchange slot of step t0 - 1: start it at zero
-  for (int q = c.tid; q < 2 * St3<NSW, RES>::NX * SW; q += T2) c.xch[q] = 0.0;
+  for (int q = c.tid; q < 2 * St3<NSW, RES>::XB; q += T2) c.xch[q] = 0.0;
 
   int t0 = c.R0 - S - 1;
   t0 -= m3(t0);
@@ -490,9 +498,10 @@ __global__ void __launch_bounds__(T2, MINB) k_stream2(StreamArgs a) {
 
 }  // namespace
 
-static size_t stream2_smem(int nsw, bool res) {
+static size_t stream2_smem(int nsw, bool res, bool pro) {
   const int nx = 2 * nsw + (res ? 2 : 0);
-  return sizeof(double) * ((size_t)(PD + PDF + 2 * nx) * SW + PE * EW + 2 * NCLS * 9 + 32);
+  const int xb = nx * SW - (res ? T2 : 0);
+  return sizeof(double) * ((size_t)(PD + PDF) * SW + 2 * xb + (pro ? PE * EW : 0) + 2 * NCLS * 9 + 32);
 }
 
 static int sm_count() {
@@ -571,9 +580,9 @@ static void choose_seg2(const Grid& g, int nsw, bool res, int occ, bool uniform,
 }
 
 template <typename KF>
-static cudaError_t run_k2(KF kern, int nsw, bool res, StreamArgs a, int* nblocks) {
+static cudaError_t run_k2(KF kern, int nsw, bool res, bool pro, StreamArgs a, int* nblocks) {
   static thread_local std::vector<std::pair<const void*, int>> occ_cache;
-  const size_t smem = stream2_smem(nsw, res);
+  const size_t smem = stream2_smem(nsw, res, pro);
   int occ = -1;
   for (auto& e : occ_cache)
     if (e.first == (const void*)kern) occ = e.second;
@@ -604,8 +613,8 @@ cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, boo
   const int cm = a.ci_valid ? 2 : 1;
 #define MGB_ST2(NSW_, RES_, PRO_, NORM_, ZU_)                                                     \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                \
-    if (cm == 2) return run_k2(k_stream2<NSW_, RES_, PRO_, NORM_, ZU_, 2>, nsw, res, a, nblocks); \
-    return run_k2(k_stream2<NSW_, RES_, PRO_, NORM_, ZU_, 1>, nsw, res, a, nblocks);             \
+    if (cm == 2) return run_k2(k_stream2<NSW_, RES_, PRO_, NORM_, ZU_, 2>, nsw, res, pro, a, nblocks); \
+    return run_k2(k_stream2<NSW_, RES_, PRO_, NORM_, ZU_, 1>, nsw, res, pro, a, nblocks);             \
   }
   MGB_ST2(1, true, false, false, false) MGB_ST2(1, true, false, true, false)
   MGB_ST2(1, true, false, false, true)  MGB_ST2(1, true, false, true, true)
