@@ -508,17 +508,21 @@ __global__ void __launch_bounds__(256) k_lu_solve(int n, const double* __restric
   const double* fb = f + b * fstride;
   double* xb = x + b * xstride;
   if (n <= 32) {
-    // one warp, unknowns over the lanes: no block barriers on the latency path
+    // the factors are staged in shared memory by the whole block (one round of L2
+    // loads instead of 2n dependent ones), then one warp, unknowns over the lanes,
+    // substitutes with shuffles: no block barriers on the latency path
+    for (int q = t; q < n * n; q += nt) xs[q] = a[q];
+    __syncthreads();
     if (t < 32) {
       double v = t < n ? (actp ? fb[actp[pm[t]]] : fb[pm[t]]) : 0.0;
       for (int k = 0; k < n; ++k) {
         const double xk = __shfl_sync(0xffffffffu, v, k);
-        if (t > k && t < n) v = v - a[(int64_t)t * n + k] * xk;
+        if (t > k && t < n) v = v - xs[t * n + k] * xk;
       }
       for (int k = n - 1; k >= 0; --k) {
-        if (t == k) v = v / a[(int64_t)k * n + k];
+        if (t == k) v = v / xs[k * n + k];
         const double xk = __shfl_sync(0xffffffffu, v, k);
-        if (t < k) v = v - a[(int64_t)t * n + k] * xk;
+        if (t < k) v = v - xs[t * n + k] * xk;
       }
       if (t < n) {
         if (actp) xb[actp[t]] = v;
@@ -714,7 +718,7 @@ cudaError_t launch_lu_solve_grid(const Grid& g, int n, const double* lu, const i
     e = cudaMemsetAsync(x, 0, sizeof(double) * g.n() * g.batch, s);
     if (e != cudaSuccess) return e;
   }
-  k_lu_solve<<<g.batch, 256, sizeof(double) * n, s>>>(n, lu, perm, actp, f, g.n(), x, g.n());
+  k_lu_solve<<<g.batch, 256, sizeof(double) * (n <= 32 ? n * n : n), s>>>(n, lu, perm, actp, f, g.n(), x, g.n());
   return MGB_DBG(__func__);
 }
 
@@ -723,7 +727,7 @@ cudaError_t launch_lu_solve_vec(int n, const double* lu, const int32_t* perm, co
   cudaError_t e = lu_solve_smem(n);
   if (e != cudaSuccess) return e;
   ++g_launches;
-  k_lu_solve<<<1, 256, sizeof(double) * n, s>>>(n, lu, perm, nullptr, b, n, x, n);
+  k_lu_solve<<<1, 256, sizeof(double) * (n <= 32 ? n * n : n), s>>>(n, lu, perm, nullptr, b, n, x, n);
   return MGB_DBG(__func__);
 }
 
