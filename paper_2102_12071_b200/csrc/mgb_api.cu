@@ -55,13 +55,18 @@ struct LevelD {
   uint8_t* mask = nullptr; // null = all active
   double* Acls = nullptr;  // band-class tables (batch x 25 x 9) when A is class-constant
   double* Kcls = nullptr;  // band-class tables (batch x 25 x ks x 9) when M is class-constant
-  double hAcls[225] = {0}, hKcls[225] = {0};  // band-class tables, host copy of problem 0 (class 12 = interior)
-  const double* hAint() const { return hAcls + 12 * 9; }
-  const double* hKint() const { return hKcls + 12 * 9; }
-  // every class equals the interior one (A and M): boundary strips need no class lookups
+  // band-class tables, host copies (batch x 225; class 12 = interior)
+  std::vector<double> hAcls = std::vector<double>(225, 0.0), hKcls = std::vector<double>(225, 0.0);
+  const double* hAint() const { return hAcls.data() + 12 * 9; }
+  const double* hKint() const { return hKcls.data() + 12 * 9; }
+  // every class equals its problem's interior one (A and M): boundary strips need no
+  // class lookups
   bool uniform() const {
-    for (int q = 0; q < 225; ++q)
-      if (hAcls[q] != hAcls[108 + q % 9] || hKcls[q] != hKcls[108 + q % 9]) return false;
+    if (hAcls.size() != hKcls.size()) return false;
+    for (size_t q = 0; q < hAcls.size(); ++q) {
+      const size_t i = q - q % 225 + 108 + q % 9;
+      if (hAcls[q] != hAcls[i] || hKcls[q] != hKcls[i]) return false;
+    }
     return true;
   }
   std::vector<uint8_t> hmask;
@@ -371,7 +376,7 @@ static void class_reps(int rows, int cols, int64_t rep[25]) {
 // Band-class compaction (mgb_cycle.cu): if every point of the table equals its
 // class representative, keep the 25 class tables (exact) for the hot loop.
 static int classify_table(mgb_hier* h, int l, const double* planes, int ks, double** cls_out, cudaStream_t s,
-                          double* interior_host = nullptr) {
+                          std::vector<double>* host_copy = nullptr) {
   if (h->classed_only) return MGB_OK;
   dfree(*cls_out);
   LevelD& lv = h->lv[l];
@@ -398,8 +403,11 @@ static int classify_table(mgb_hier* h, int l, const double* planes, int ks, doub
   if (!hf) {
     MGB_CUDA_TRY(dalloc(cls_out, (size_t)h->batch * 25 * ks * 9));
     MGB_CUDA_TRY(launch_gather_cls(h->grid(l), T, drep, *cls_out, s));
-    if (interior_host && ks == 1)
-      MGB_CUDA_TRY(cudaMemcpyAsync(interior_host, *cls_out, 225 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (host_copy && ks == 1) {
+      host_copy->assign((size_t)h->batch * 225, 0.0);
+      MGB_CUDA_TRY(cudaMemcpyAsync(host_copy->data(), *cls_out, host_copy->size() * sizeof(double),
+                                   cudaMemcpyDeviceToHost, s));
+    }
   }
   MGB_CUDA_TRY(cudaFreeAsync(drep, s));
   MGB_CUDA_TRY(cudaFreeAsync(flag, s));
@@ -410,9 +418,9 @@ static int classify_table(mgb_hier* h, int l, const double* planes, int ks, doub
 static int classify_all(mgb_hier* h, cudaStream_t s) {
   for (int l = 0; l < h->depth(); ++l) {
     LevelD& lv = h->lv[l];
-    if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s, lv.hAcls)) return st;
+    if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s, &lv.hAcls)) return st;
     if (lv.K) {
-      if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s, lv.hKcls)) return st;
+      if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s, &lv.hKcls)) return st;
     } else {
       dfree(lv.Kcls);
     }
@@ -737,8 +745,11 @@ extern "C" int mgb_hier_build_classed(int device, int batch, int rows, int cols,
   }
   std::vector<int> hring(L, 1);
   MGB_CUDA_TRY(cudaMemcpyAsync(hring.data(), ring, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
-  for (auto& lv : h->lv) MGB_CUDA_TRY(cudaMemcpyAsync(lv.hAcls, lv.Acls, 225 * sizeof(double),
-                                                      cudaMemcpyDeviceToHost, s));
+  for (auto& lv : h->lv) {
+    lv.hAcls.assign((size_t)batch * 225, 0.0);
+    MGB_CUDA_TRY(cudaMemcpyAsync(lv.hAcls.data(), lv.Acls, lv.hAcls.size() * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+  }
   MGB_CUDA_TRY(cudaFreeAsync(ring, s));
   MGB_CUDA_TRY(cudaFreeAsync(drep, s));
   MGB_CUDA_TRY(cudaStreamSynchronize(s));
@@ -900,8 +911,10 @@ extern "C" int mgb_hier_equip_inferred(mgb_hier* h, int variant, int kst, const 
       e = launch_infer(h->grid(l), tabA(h, lv), nullptr, variant, kst, w, slope, precision,
                        tabw_cls(lv.Kcls, lv.rows, lv.cols, kst), s, drep, 25);
       cudaFreeAsync(drep, s);
-      if (e == cudaSuccess && kst == 1)
-        e = cudaMemcpyAsync(lv.hKcls, lv.Kcls, 225 * sizeof(double), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess && kst == 1) {
+        lv.hKcls.assign((size_t)h->batch * 225, 0.0);
+        e = cudaMemcpyAsync(lv.hKcls.data(), lv.Kcls, lv.hKcls.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
+      }
     } else {
       e = launch_infer(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, variant, kst, w, slope,
                        precision, tabw_soa(lv.K, lv.n, kst), s);
@@ -938,7 +951,9 @@ extern "C" int mgb_hier_equip_jacobi(mgb_hier* h, double omega, void* stream) {
       MGB_CUDA_TRY(launch_jacobi(h->grid(l), tabA(h, lv), nullptr, omega, tabw_cls(lv.Kcls, lv.rows, lv.cols, 1),
                                  flag + l, s, drep, 25));
       MGB_CUDA_TRY(cudaFreeAsync(drep, s));
-      MGB_CUDA_TRY(cudaMemcpyAsync(lv.hKcls, lv.Kcls, 225 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      lv.hKcls.assign((size_t)h->batch * 225, 0.0);
+      MGB_CUDA_TRY(cudaMemcpyAsync(lv.hKcls.data(), lv.Kcls, lv.hKcls.size() * sizeof(double),
+                                   cudaMemcpyDeviceToHost, s));
     } else {
       MGB_CUDA_TRY(launch_jacobi(h->grid(l), tab_soa(lv.A, lv.n, 1), lv.mask, omega,
                                  tabw_soa(lv.K, lv.n, 1), flag + l, s));
@@ -1231,7 +1246,7 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   a.f = f;
   a.stream = s;
   a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
-  a.uniform = a.ci_valid && lv.uniform();
+  a.uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
   a.kernel = h->stream_kernel;
   for (int o = 0; o < 9; ++o) {
     a.ci[o] = lv.hAint()[o];
@@ -1760,7 +1775,7 @@ Op hier_opK(const mgb_hier* h, int l) { return h->lv[l].opK(); }
 void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform, int* kernel) {
   const LevelD& lv = h->lv[l];
   *valid = h->batch == 1 && lv.Acls && lv.Kcls;
-  if (uniform) *uniform = *valid && lv.uniform();
+  if (uniform) *uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
   if (kernel) *kernel = h->stream_kernel;
   for (int o = 0; o < 9; ++o) {
     ci[o] = lv.hAint()[o];

@@ -435,13 +435,10 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   const int cm = (a.A.cls != nullptr && a.K.cls != nullptr && !msk) ? (a.ci_valid ? 2 : 1) : 0;
   static const bool one_col = getenv("MGB_STREAM1") && atoi(getenv("MGB_STREAM1")) != 0;
   ++g_launches;
-  // two-column kernel: single-problem band-class levels (interior weights from the
-  // constant bank); batched levels keep the one-column kernel (measured faster: the
-  // pair kernel would read every interior weight from shared memory)
-  // (levels below ~2M points, e.g. 1023^2 with five strips, measured faster on the
-  // one-column kernel: more, shorter CTAs)
-  const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() >= 1000000);
-  if (cm == 2 && pairs) return launch_stream2(a, nsw, res, pro, norm, nblocks);
+  // column-pair kernel: band-class levels of >= 1M points (batch included; interior
+  // weights from the constant bank or, batched, from registers)
+  const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() * a.g.batch >= 1000000);
+  if (cm != 0 && pairs) return launch_stream2(a, nsw, res, pro, norm, nblocks);
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
     if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, true>, nsw, res, a, nblocks);     \

@@ -26,6 +26,7 @@
 #include <utility>
 #include <vector>
 #include <algorithm>
+#include <cstdint>
 
 #include "mgb_stream.h"
 #include "mgb_dot.h"
@@ -41,8 +42,7 @@ namespace {
 #ifndef MGB_S2T
 #define MGB_S2T 128
 #endif
-constexpr int T2 = MGB_S2T;       // threads per CTA (column pairs)
-constexpr int SW = 2 * T2;        // strip columns incl. halo
+constexpr int T2 = MGB_S2T;       // widest strip: threads per CTA (column pairs)
 constexpr int PD = 8;             // prefetch ring depth (rows) for u (power of two)
 constexpr int PDF = 16;           // ring depth for f: rows t-10 .. t+DIST
 constexpr int DIST = 5;           // prefetch distance (rows ahead)
@@ -56,7 +56,6 @@ constexpr int DIST = 5;           // prefetch distance (rows ahead)
 // the compact exchange layout, but measured 40 % slower at 168 registers)
 constexpr int MINB = MGB_S2MINB, MINB_PRE = MGB_S2MINB_PRE;
 constexpr int PE = 8;             // ring of coarse rows (POST prolongation), power of two
-constexpr int EW = T2 + 2;        // coarse columns staged per CTA
 constexpr int NCLS = 25;
 constexpr int CINT = 12;          // interior band class (2 * 5 + 2)
 
@@ -75,8 +74,6 @@ template <int NSW, bool RES>
 struct SP2 {
   static constexpr int S = 2 * NSW + (RES ? 1 : 0);  // stencil stages after the input field
   static constexpr int H = 2 * NSW + 2;              // column halo per side (even)
-  static constexpr int WOUT = SW - 2 * H;            // owned columns per strip (even)
-  static constexpr int NF = S;                       // fields with a window (F_0 .. F_{S-1})
 };
 
 __host__ __device__ constexpr int m3(int x) { return ((x % 3) + 3) % 3; }
@@ -84,6 +81,10 @@ __host__ __device__ constexpr int m3(int x) { return ((x % 3) + 3) % 3; }
 struct Ctx2 {
   Grid g;
   int b, tid, j0, c0, R0, R1;
+  int tw, sw, ew, xb;  // threads (column pairs), strip columns, staged coarse columns, and one
+                       // exchange buffer: NX fields x (even, odd) column planes, the restriction
+                       // field F_S (last) with its even plane only (right neighbours)
+  double wI[18];       // CM 1: the problem's interior-class A and M weights (registers)
   bool cin0, cin1, own;
   int cc0, cc1;     // band classes of columns c0, c0 + 1
   double* ring_u;
@@ -108,9 +109,6 @@ template <int NSW, bool RES>
 struct St3 {
   static constexpr int S = 2 * NSW + (RES ? 1 : 0);
   static constexpr int NX = RES ? S + 1 : S;   // exchanged fields (F_S feeds the restriction)
-  // one exchange buffer: NX fields x (even, odd) column planes; the restriction field
-  // F_S (last) needs only its even plane (right neighbours)
-  static constexpr int XB = NX * SW - (RES ? T2 : 0);
   double acc[S][3][2];    // open output rows of stage k (slot = row mod 3), two columns
   double cur[NX][2];      // own values of field j published at the previous step
   double prev[NSW][2];    // own values of fields 0, 2, .. published two steps back
@@ -135,11 +133,11 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
   // ---- neighbours of the rows published by step t - 1 (even / odd column planes)
   double L[NX], R[NX];
   {
-    const int iL = max(c.tid - 1, 0), iR = min(c.tid + 1, T2 - 1);
+    const int iL = max(c.tid - 1, 0), iR = min(c.tid + 1, c.tw - 1);
 #pragma unroll
     for (int j = 0; j < NX; ++j) {
-      const double* xr = &c.xch[slp * St3<NSW, RES>::XB + j * SW];
-      L[j] = (RES && j == S) ? 0.0 : xr[T2 + iL];
+      const double* xr = &c.xch[slp * c.xb + j * c.sw];
+      L[j] = (RES && j == S) ? 0.0 : xr[c.tw + iL];
       R[j] = xr[iR];
     }
   }
@@ -154,7 +152,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     // seed of the new chain (row x + 1): f, or the u the update adds to
     double s0, s1;
     if (resid) {
-      const double2 fv = *reinterpret_cast<const double2*>(&c.ring_f[((x + 1) & (PDF - 1)) * SW + 2 * c.tid]);
+      const double2 fv = *reinterpret_cast<const double2*>(&c.ring_f[((x + 1) & (PDF - 1)) * c.sw + 2 * c.tid]);
       s0 = fv.x;
       s1 = fv.y;
     } else {
@@ -168,7 +166,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     const double* wB0;
     const double* wB1;
     if (MODE <= 1) {
-      const double* wi = CM == 2 ? (resid ? a.ci : a.ci + 9) : ((resid ? c.tA : c.tK) + CINT * 9);
+      const double* wi = CM == 2 ? (resid ? a.ci : a.ci + 9) : (resid ? c.wI : c.wI + 9);
       wN0 = wN1 = wM0 = wM1 = wB0 = wB1 = wi;
     } else if (MODE == 2) {
       const double* tab = resid ? c.tA : c.tK;
@@ -261,7 +259,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     double u0 = 0.0, u1 = 0.0;
     const bool rvr = FAST || (unsigned)t < (unsigned)g.rows;
     if (!ZU) {
-      const double2 v = *reinterpret_cast<const double2*>(&c.ring_u[(t & (PD - 1)) * SW + 2 * c.tid]);
+      const double2 v = *reinterpret_cast<const double2*>(&c.ring_u[(t & (PD - 1)) * c.sw + 2 * c.tid]);
       u0 = v.x;
       u1 = v.y;
     }
@@ -270,13 +268,13 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
       // the k_stream loop order: di = -1, 0, 1 (row parity), dj = -1, 0, 1 (column parity)
       double p0 = 0.0, p1 = 0.0;
       if (t & 1) {
-        const double* er = c.ring_e + (((t - 1) >> 1) & (PE - 1)) * EW;
+        const double* er = c.ring_e + (((t - 1) >> 1) & (PE - 1)) * c.ew;
         p0 = fma(0.25, er[c.tid + 1], p0);   // (di 0, dj -1): coarse m
         p0 = fma(0.25, er[c.tid], p0);       // (di 0, dj +1): coarse m - 1
         p1 = fma(0.5, er[c.tid + 1], p1);    // (di 0, dj 0)
       } else {
-        const double* ea = c.ring_e + ((t >> 1) & (PE - 1)) * EW;        // di = -1: coarse row t/2
-        const double* eb = c.ring_e + (((t - 2) >> 1) & (PE - 1)) * EW;  // di = +1: coarse row t/2 - 1
+        const double* ea = c.ring_e + ((t >> 1) & (PE - 1)) * c.ew;        // di = -1: coarse row t/2
+        const double* eb = c.ring_e + (((t - 2) >> 1) & (PE - 1)) * c.ew;  // di = +1: coarse row t/2 - 1
         p0 = fma(0.125, ea[c.tid + 1], p0);
         p0 = fma(0.125, ea[c.tid], p0);
         p1 = fma(0.25, ea[c.tid + 1], p1);
@@ -297,8 +295,8 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
   const int sl = t & 1;
 #pragma unroll
   for (int j = 0; j < NX; ++j) {
-    c.xch[sl * St3<NSW, RES>::XB + j * SW + c.tid] = out[j][0];
-    if (!(RES && j == S)) c.xch[sl * St3<NSW, RES>::XB + j * SW + T2 + c.tid] = out[j][1];
+    c.xch[sl * c.xb + j * c.sw + c.tid] = out[j][0];
+    if (!(RES && j == S)) c.xch[sl * c.xb + j * c.sw + c.tw + c.tid] = out[j][1];
   }
 #pragma unroll
   for (int m = 0; m < NSW; ++m) {
@@ -313,21 +311,29 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
   __syncthreads();
 }
 
-// CM: 1 = band-class tables in shared memory; 2 = band-class tables with the
-// interior class read from the kernel parameters (constant-bank operands).
+// CM: 1 = band-class tables in shared memory, the interior class copied to registers
+// (batched levels: one problem per CTA); 2 = the interior class read from the kernel
+// parameters (constant-bank operands; single problem).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM>
 __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArgs a) {
   using P = SP2<NSW, RES>;
-  constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
+  constexpr int S = P::S, H = P::H;
   extern __shared__ __align__(16) double smem2[];
   Ctx2 c;
   c.g = a.g;
   const Grid& g = c.g;
-  c.ring_u = smem2;                               // PD x SW (unused when ZU)
-  c.ring_f = c.ring_u + PD * SW;                  // PDF x SW
-  c.xch = c.ring_f + PDF * SW;                    // NX x 2 x SW exchange rows (even / odd planes)
-  c.ring_e = c.xch + 2 * St3<NSW, RES>::XB;       // PE x EW (POST)
-  double* tA = c.ring_e + (PRO ? PE * EW : 0);    // 25 x 9
+  // strip width: 128 column pairs for single problems (compile-time strides), batched
+  // levels blockDim.x (the launcher picks 64, 96 or 128 for the problems' width)
+  c.tw = CM == 2 ? T2 : (int)blockDim.x;
+  c.sw = 2 * c.tw;
+  c.ew = c.tw + 2;
+  c.xb = St3<NSW, RES>::NX * c.sw - (RES ? c.tw : 0);
+  const int WOUT = c.sw - 2 * H;                  // owned columns per strip (even)
+  c.ring_u = smem2;                               // PD x sw (unused when ZU)
+  c.ring_f = c.ring_u + PD * c.sw;                // PDF x sw
+  c.xch = c.ring_f + PDF * c.sw;                  // 2 buffers x NX fields x (even, odd) planes
+  c.ring_e = c.xch + 2 * c.xb;                    // PE x ew (POST)
+  double* tA = c.ring_e + (PRO ? PE * c.ew : 0);  // 25 x 9
   double* tK = tA + NCLS * 9;                     // 25 x 9
   double* red = tK + NCLS * 9;                    // 32
   c.tA = tA;
@@ -367,18 +373,26 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   c.uob = a.uo + c.b * n;
   // fast steps: every CTA column interior (band class 2) and in the grid, or a level
   // whose band classes are all equal (then only out-of-grid columns need zeroing)
-  const bool cta_int = c.j0 - H >= 2 && c.j0 - H + SW - 1 <= g.cols - 3;
+  const bool cta_int = c.j0 - H >= 2 && c.j0 - H + c.sw - 1 <= g.cols - 3;
   const bool cta_fast = cta_int || a.uniform;
 #ifdef MGB_CTA_PROF
   unsigned long long prof_t0 = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
 #endif
 
-  for (int q = c.tid; q < NCLS * 9; q += T2) {
+  for (int q = c.tid; q < NCLS * 9; q += c.tw) {
     tA[q] = a.A.cls[(int64_t)c.b * NCLS * 9 + q];
     tK[q] = a.K.cls[(int64_t)c.b * NCLS * 9 + q];
   }
   __syncthreads();
+  if (CM == 1) {
+    // batched levels: this problem's interior weights live in registers for the pass
+#pragma unroll
+    for (int o = 0; o < 9; ++o) {
+      c.wI[o] = tA[CINT * 9 + o];
+      c.wI[9 + o] = tK[CINT * 9 + o];
+    }
+  }
 
   St3<NSW, RES> st;
 #pragma unroll
@@ -392,7 +406,7 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   st.racc = 0.0;
   st.norm = 0.0;
   // the first step reads the exchange slot of step t0 - 1: start it at zero
-  for (int q = c.tid; q < 2 * St3<NSW, RES>::XB; q += T2) c.xch[q] = 0.0;
+  for (int q = c.tid; q < 2 * c.xb; q += c.tw) c.xch[q] = 0.0;
 
   int t0 = c.R0 - S - 1;
   t0 -= m3(t0);
@@ -400,8 +414,8 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   const int t1 = c.R1 + 2 * S + (RES ? 1 : 0);
   int prow = t0;
   const int64_t cstride = g.cols;
-  // prefetch: thread copies strip columns tid and tid + T2 (coalesced rows)
-  const int ca = c.j0 - H + c.tid, cb = ca + T2;
+  // prefetch: thread copies strip columns tid and tid + tw (coalesced rows)
+  const int ca = c.j0 - H + c.tid, cb = ca + c.tw;
   const bool ina = ca >= 0 && ca < g.cols, inb = cb >= 0 && cb < g.cols;
   const double* pu = ZU ? nullptr : ub + (int64_t)prow * cstride + ca;
   const double* pf = fb + (int64_t)prow * cstride + ca;
@@ -411,22 +425,22 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   const int lo_row = max(0, c.R0 - S - 1), hi_row = min(g.rows - 1, c.R1 + S);
   const int lo_c = (lo_row - 2) >> 1, hi_c = (hi_row >> 1) + 1;
   auto stage_e = [&](int ci) {
-    for (int q = c.tid; q < EW; q += T2) {
+    for (int q = c.tid; q < c.ew; q += c.tw) {
       const int cj = cjb + q;
       const bool ev = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c && cj >= 0 && cj < cols_c;
-      cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + q], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
+      cp_async8(&c.ring_e[(ci & (PE - 1)) * c.ew + q], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
     }
   };
   auto issue = [&]() {
     const bool rv = prow >= lo_row && prow <= hi_row;
-    double* du = &c.ring_u[(prow & (PD - 1)) * SW + c.tid];
-    double* df = &c.ring_f[(prow & (PDF - 1)) * SW + c.tid];
+    double* du = &c.ring_u[(prow & (PD - 1)) * c.sw + c.tid];
+    double* df = &c.ring_f[(prow & (PDF - 1)) * c.sw + c.tid];
     if (!ZU) {
       cp_async8(du, rv && ina ? pu : ub, rv && ina);
-      cp_async8(du + T2, rv && inb ? pu + T2 : ub, rv && inb);
+      cp_async8(du + c.tw, rv && inb ? pu + c.tw : ub, rv && inb);
     }
     cp_async8(df, rv && ina ? pf : fb, rv && ina);
-    cp_async8(df + T2, rv && inb ? pf + T2 : fb, rv && inb);
+    cp_async8(df + c.tw, rv && inb ? pf + c.tw : fb, rv && inb);
     // coarse row ci is first needed by fine row 2ci (as di = -1); staged with the
     // group of fine row 2ci - 2 so it is complete and published by that step's barrier
     if (PRO && !(prow & 1)) stage_e((prow >> 1) + 1);
@@ -490,7 +504,7 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
     __syncthreads();
     if (c.tid == 0) {
       double s = 0.0;
-      for (int q = 0; q < T2 / 32; ++q) s += red[q];
+      for (int q = 0; q < (c.tw + 31) / 32; ++q) s += red[q];
       a.partials[(int64_t)c.b * gridDim.x + blockIdx.x] = s;
     }
   }
@@ -498,10 +512,29 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
 
 }  // namespace
 
-static size_t stream2_smem(int nsw, bool res, bool pro) {
+static size_t stream2_smem(int nsw, bool res, bool pro, int tw) {
   const int nx = 2 * nsw + (res ? 2 : 0);
-  const int xb = nx * SW - (res ? T2 : 0);
-  return sizeof(double) * ((size_t)(PD + PDF) * SW + 2 * xb + (pro ? PE * EW : 0) + 2 * NCLS * 9 + 32);
+  const int sw = 2 * tw, xb = nx * sw - (res ? tw : 0);
+  return sizeof(double) * ((size_t)(PD + PDF) * sw + 2 * xb + (pro ? PE * (tw + 2) : 0) + 2 * NCLS * 9 + 32);
+}
+
+// Strip width (threads = column pairs per CTA, a multiple of 32 up to 128): the
+// fewest padded columns (strips x 2 tw) for the level's width, wider on ties.
+static int choose_tw(int cols, int nsw) {
+  static const int tw_env = getenv("MGB_S2TW") ? atoi(getenv("MGB_S2TW")) : 0;  // experiments only
+  if (tw_env > 0) return tw_env;
+  const int H = 2 * nsw + 2;
+  int best = T2;
+  int64_t best_w = INT64_MAX;
+  for (int tw = T2; tw >= 64; tw -= 32) {
+    const int wout = 2 * tw - 2 * H;
+    const int64_t padded = (int64_t)((cols + wout - 1) / wout) * 2 * tw;
+    if (padded < best_w) {
+      best_w = padded;
+      best = tw;
+    }
+  }
+  return best;
 }
 
 static int sm_count() {
@@ -537,9 +570,9 @@ static SegPlan seg_plan(int R, int n, int dt, int db) {
   return p;
 }
 
-static void choose_seg2(const Grid& g, int nsw, bool res, int occ, bool uniform, bool top, bool bot,
+static void choose_seg2(const Grid& g, int nsw, bool res, int occ, int tw, bool uniform, bool top, bool bot,
                         StreamArgs& a) {
-  const int H = 2 * nsw + 2, wout = SW - 2 * H, S = 2 * nsw + (res ? 1 : 0);
+  const int H = 2 * nsw + 2, wout = 2 * tw - 2 * H, S = 2 * nsw + (res ? 1 : 0);
   const int strips = (g.cols + wout - 1) / wout;
   const int ne = std::min(strips, 2), ni = strips - ne;
   const int64_t slots = (int64_t)sm_count() * std::max(occ, 1);
@@ -581,17 +614,24 @@ static void choose_seg2(const Grid& g, int nsw, bool res, int occ, bool uniform,
 
 template <typename KF>
 static cudaError_t run_k2(KF kern, int nsw, bool res, bool pro, StreamArgs a, int* nblocks) {
-  static thread_local std::vector<std::pair<const void*, int>> occ_cache;
-  const size_t smem = stream2_smem(nsw, res, pro);
+  struct Occ {
+    const void* k;
+    int tw, occ;
+  };
+  static thread_local std::vector<Occ> occ_cache;
+  const int tw = a.ci_valid ? T2 : choose_tw(a.g.cols, nsw);  // CM 2 kernels assume T2
+  const size_t smem = stream2_smem(nsw, res, pro, tw);
   int occ = -1;
   for (auto& e : occ_cache)
-    if (e.first == (const void*)kern) occ = e.second;
+    if (e.k == (const void*)kern && e.tw == tw) occ = e.occ;
   if (occ < 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the attribute is sized for the widest strip once per kernel
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)stream2_smem(nsw, res, pro, T2));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T2, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, tw, smem);
     if (e != cudaSuccess) return e;
-    occ_cache.push_back({(const void*)kern, occ});
+    occ_cache.push_back({(const void*)kern, tw, occ});
   }
   if (a.own1 <= 0) {
     a.own0 = 0;
@@ -599,12 +639,12 @@ static cudaError_t run_k2(KF kern, int nsw, bool res, bool pro, StreamArgs a, in
   }
   Grid go = a.g;
   go.rows = a.own1 - a.own0;
-  choose_seg2(go, nsw, res, occ, a.uniform != 0, a.own0 == 0, a.own1 == a.g.rows, a);
+  choose_seg2(go, nsw, res, occ, tw, a.uniform != 0, a.own0 == 0, a.own1 == a.g.rows, a);
   const int ni = a.nstrips - a.nedge;
   const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
   const dim3 grid(nctas, 1, a.g.batch);
   if (nblocks) *nblocks = nctas;
-  kern<<<grid, T2, smem, a.stream>>>(a);
+  kern<<<grid, tw, smem, a.stream>>>(a);
   return MGB_DBG(__func__);
 }
 
