@@ -23,6 +23,11 @@ namespace mgb {
 
 thread_local int64_t g_launches = 0;
 
+bool pdl_enabled() {
+  static const bool off = getenv("MGB_NO_PDL") && atoi(getenv("MGB_NO_PDL")) != 0;
+  return !off;
+}
+
 cudaError_t debug_sync(const char* what) {
   static const bool on = getenv("MGB_DEBUG_SYNC") && getenv("MGB_DEBUG_SYNC")[0] == '1';
   cudaError_t e = cudaGetLastError();
@@ -138,6 +143,8 @@ __global__ void __launch_bounds__(1024) k_finalize(int nblk, const double* __res
                                                   const double* __restrict__ fnorm2,
                                                   double* __restrict__ hist, int64_t hstride) {
   __shared__ double sh[32];
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   double v = 0.0;
   for (int q = threadIdx.x; q < nblk; q += blockDim.x) v += partials[(int64_t)b * nblk + q];
@@ -502,6 +509,8 @@ __global__ void __launch_bounds__(256) k_lu_solve(int n, const double* __restric
                                                   const double* __restrict__ f, int64_t fstride,
                                                   double* __restrict__ x, int64_t xstride) {
   extern __shared__ double xs[];
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
   const double* a = LU + (int64_t)b * n * n;
   const int32_t* pm = perm + (int64_t)b * n;
@@ -620,7 +629,8 @@ cudaError_t launch_residual(const Grid& g, Tab A, const uint8_t* mask, const dou
 cudaError_t launch_finalize(int batch, int nblk, const double* partials, double* out2,
                             const double* fnorm2, double* hist, int64_t hstride, cudaStream_t s) {
   ++g_launches;
-  k_finalize<<<batch, 1024, 0, s>>>(nblk, partials, out2, fnorm2, hist, hstride);
+  cudaError_t e = launch_pdl(k_finalize, dim3(batch), dim3(1024), 0, s, nblk, partials, out2, fnorm2, hist, hstride);
+  if (e != cudaSuccess) return e;
   return MGB_DBG(__func__);
 }
 
@@ -718,7 +728,9 @@ cudaError_t launch_lu_solve_grid(const Grid& g, int n, const double* lu, const i
     e = cudaMemsetAsync(x, 0, sizeof(double) * g.n() * g.batch, s);
     if (e != cudaSuccess) return e;
   }
-  k_lu_solve<<<g.batch, 256, sizeof(double) * (n <= 32 ? n * n : n), s>>>(n, lu, perm, actp, f, g.n(), x, g.n());
+  e = launch_pdl(k_lu_solve, dim3(g.batch), dim3(256), sizeof(double) * (n <= 32 ? n * n : n), s, n, lu, perm, actp, f,
+                 g.n(), x, g.n());
+  if (e != cudaSuccess) return e;
   return MGB_DBG(__func__);
 }
 

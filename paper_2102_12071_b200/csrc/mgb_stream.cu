@@ -220,6 +220,7 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
 // (constant-bank operands: no registers, no shared-memory traffic).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool MSK>
 __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
+  pdl_trigger();
   using P = SP<NSW, RES, PRO>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
   extern __shared__ double smem[];
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
     }
   }
   __syncthreads();
+  pdl_wait();  // u, f, ec come from the preceding kernels
 
   double w[NF][3][3];
 #pragma unroll
@@ -425,7 +427,8 @@ static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks)
   const int H = 2 * nsw + 2, wout = SWT - 2 * H;
   const dim3 grid((a.g.cols + wout - 1) / wout, (go.rows + a.seg - 1) / a.seg, a.g.batch);
   if (nblocks) *nblocks = (int)(grid.x * grid.y);
-  kern<<<grid, SWT, smem, a.stream>>>(a);
+  const cudaError_t e = launch_pdl(kern, grid, dim3(SWT), smem, a.stream, a);
+  if (e != cudaSuccess) return e;
   return MGB_DBG(__func__);
 }
 

@@ -316,6 +316,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
 // parameters (constant-bank operands; single problem).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM>
 __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArgs a) {
+  pdl_trigger();
   using P = SP2<NSW, RES>;
   constexpr int S = P::S, H = P::H;
   extern __shared__ __align__(16) double smem2[];
@@ -407,6 +408,7 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   st.norm = 0.0;
   // the first step reads the exchange slot of step t0 - 1: start it at zero
   for (int q = c.tid; q < 2 * c.xb; q += c.tw) c.xch[q] = 0.0;
+  pdl_wait();  // u, f, ec come from the preceding kernels; uo / rc may still be read there
 
   int t0 = c.R0 - S - 1;
   t0 -= m3(t0);
@@ -644,7 +646,8 @@ static cudaError_t run_k2(KF kern, int nsw, bool res, bool pro, StreamArgs a, in
   const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
   const dim3 grid(nctas, 1, a.g.batch);
   if (nblocks) *nblocks = nctas;
-  kern<<<grid, tw, smem, a.stream>>>(a);
+  const cudaError_t e = launch_pdl(kern, grid, dim3(tw), smem, a.stream, a);
+  if (e != cudaSuccess) return e;
   return MGB_DBG(__func__);
 }
 

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(TP<NSW, RES, PRO, T>::NT) k_tile(StreamArgs a)
   double* tA = E + (PRO ? EH * EH : 0); // 25 x 9 band-class tables
   double* tK = tA + NCLS * 9;
   double* red = tK + NCLS * 9;          // NT / 32
+  pdl_trigger();
   const Grid g = a.g;
   const int tid = threadIdx.x, b = blockIdx.z;
   const int64_t n = g.n();
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(TP<NSW, RES, PRO, T>::NT) k_tile(StreamArgs a)
       tK[q] = a.K.cls[(int64_t)b * NCLS * 9 + q];
     }
   }
+  pdl_wait();  // u, f, ec come from the preceding kernels
   // ---- stage 0: f and the input u over the whole region (zero outside the grid)
   for (int q = tid; q < W * W; q += NT) {
     const int li = q / W, lj = q - (q / W) * W;
@@ -228,7 +230,8 @@ cudaError_t run_tile(const StreamArgs& a, int* nblocks) {
   }
   const dim3 grid((a.g.cols + T - 1) / T, (a.g.rows + T - 1) / T, a.g.batch);
   if (nblocks) *nblocks = (int)(grid.x * grid.y);
-  kern<<<grid, TP<NSW, RES, PRO, T>::NT, smem, a.stream>>>(a);
+  const cudaError_t e = launch_pdl(kern, grid, dim3(TP<NSW, RES, PRO, T>::NT), smem, a.stream, a);
+  if (e != cudaSuccess) return e;
   return MGB_DBG("k_tile");
 }
 
