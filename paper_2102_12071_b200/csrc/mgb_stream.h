@@ -29,7 +29,8 @@ struct StreamArgs {
   // segments of a strip: the first has seg_first rows, the others seg (the last: the
   // rest); first / last segments on the grid's top / bottom are trimmed because their
   // boundary rows take the slow step variant
-  int nstrips, nedge, seg_first, nseg, seg_edge, seg_edge_first, nseg_edge;
+  // (the first seg_rem middle segments have one row more)
+  int nstrips, nedge, seg_first, nseg, seg_rem, seg_edge, seg_edge_first, nseg_edge, seg_edge_rem;
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
   cudaStream_t stream;
 };

@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   c.b = blockIdx.z;
   const int64_t n = g.n();
   // CTA -> (strip, row segment): the edge strips' CTAs first, then the interior ones
-  int strip, seg, seg1, sy;
+  int strip, seg, seg1, srem, sy, nsegs;
   {
     const int id = blockIdx.x;
     const int ne = a.nedge;
@@ -352,12 +352,16 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
       sy = id / ne;
       seg = a.seg_edge;
       seg1 = a.seg_edge_first;
+      srem = a.seg_edge_rem;
+      nsegs = a.nseg_edge;
     } else {
       const int q = id - ne * a.nseg_edge, ni = a.nstrips - ne;
       strip = 1 + q % ni;
       sy = q / ni;
       seg = a.seg;
       seg1 = a.seg_first;
+      srem = a.seg_rem;
+      nsegs = a.nseg;
     }
   }
   c.j0 = strip * WOUT;                            // first owned column (even)
@@ -367,8 +371,9 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   c.own = 2 * c.tid >= H && 2 * c.tid < H + WOUT && c.cin0;
   c.cc0 = c.cin0 ? bandc(c.c0, g.cols) : 2;       // out-of-grid columns are zeroed anyway
   c.cc1 = c.cin1 ? bandc(c.c0 + 1, g.cols) : 2;
-  c.R0 = a.own0 + (sy == 0 ? 0 : seg1 + (sy - 1) * seg);
-  c.R1 = min(a.own1 > 0 ? a.own1 : g.rows, c.R0 + (sy == 0 ? seg1 : seg));
+  c.R0 = a.own0 + (sy == 0 ? 0 : seg1 + (sy - 1) * seg + min(sy - 1, srem));
+  const int rend = a.own1 > 0 ? a.own1 : g.rows;  // the last segment takes the rest
+  c.R1 = sy == nsegs - 1 ? rend : min(rend, c.R0 + (sy == 0 ? seg1 : seg + (sy - 1 < srem ? 1 : 0)));
   const double* fb = a.f + c.b * n;
   const double* ub = ZU ? nullptr : a.u + c.b * n;
   c.uob = a.uo + c.b * n;
@@ -558,17 +563,30 @@ static int sm_count() {
 // segment counts fill whole waves of the measured occupancy with the fewest
 // pipeline fills (3S + 3 steps per segment).
 struct SegPlan {
-  int seg, first, n;
+  int seg, first, rem, n;
 };
-// n segments over R rows: first = seg - dt, middle seg, last ~ seg - db
+// n segments over R rows: first = seg - dt, middle seg (the first rem of them seg + 1),
+// last = the rest (~ seg - db)
 static SegPlan seg_plan(int R, int n, int dt, int db) {
   SegPlan p;
   p.n = std::max(1, std::min(n, R));
-  p.seg = std::max(1, (R + dt + db + p.n - 1) / p.n);
-  p.first = std::max(1, std::min(R, p.seg - dt));
-  // the plan must cover R rows with exactly n non-empty segments
-  while (p.n > 1 && p.first + (int64_t)(p.n - 2) * p.seg >= R) --p.n;
-  while (p.first + (int64_t)(p.n - 1) * p.seg < R) ++p.seg;
+  if (p.n == 1) {
+    p.seg = p.first = R;
+    p.rem = 0;
+    return p;
+  }
+  p.seg = std::max(1, (R + dt + db) / p.n);
+  p.first = std::max(1, std::min(R - (p.n - 1), p.seg - dt));
+  const int64_t mid = (int64_t)(p.n - 2) * p.seg;
+  const int64_t last = R - p.first - mid;       // before spreading the remainder
+  const int64_t want = std::max(1, p.seg - db);
+  p.rem = (int)std::max<int64_t>(0, std::min<int64_t>(p.n - 2, last - want));
+  if (R - p.first - mid - p.rem < 1) {           // degenerate: fall back to equal segments
+    p.seg = (R + p.n - 1) / p.n;
+    p.first = p.seg;
+    p.rem = 0;
+    while (p.n > 1 && (int64_t)(p.n - 1) * p.seg >= R) --p.n;
+  }
   return p;
 }
 
@@ -599,9 +617,11 @@ static void choose_seg2(const Grid& g, int nsw, bool res, int occ, int tw, bool 
       best_t = t;
       a.seg = pi.seg;
       a.seg_first = pi.first;
+      a.seg_rem = pi.rem;
       a.nseg = pi.n;
       a.seg_edge = pe.seg;
       a.seg_edge_first = pe.first;
+      a.seg_edge_rem = pe.rem;
       a.nseg_edge = pe.n;
     }
   }
@@ -610,6 +630,7 @@ static void choose_seg2(const Grid& g, int nsw, bool res, int occ, int tw, bool 
     const SegPlan p = seg_plan(g.rows, (g.rows + force_seg - 1) / force_seg, 0, 0);
     a.seg = a.seg_edge = p.seg;
     a.seg_first = a.seg_edge_first = p.first;
+    a.seg_rem = a.seg_edge_rem = p.rem;
     a.nseg = a.nseg_edge = p.n;
   }
 }
