@@ -608,7 +608,7 @@ static void choose_seg2(const Grid& g, int nsw, bool res, int occ, int tw, bool 
   a.nedge = ne;
   for (int nseg = 1; nseg <= std::max(1, g.rows / 16); ++nseg) {
     const SegPlan pi = seg_plan(g.rows, nseg, dt, db);
-    const int seg_e_target = std::max(16, (int)((pi.seg + F) / r) - F);
+    const int seg_e_target = std::max(8, (int)((pi.seg + F) / r) - F);
     const SegPlan pe = seg_plan(g.rows, (g.rows + dt + db + seg_e_target - 1) / seg_e_target, dt, db);
     const int64_t ctas = ((int64_t)(ni > 0 ? ni : 0) * pi.n + (int64_t)ne * pe.n) * g.batch;
     const int64_t waves = (ctas + slots - 1) / slots;
