@@ -9,7 +9,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 level = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 h, f_host, info = bench.build_problem(cfg, 0)
 rows, cols = h.level_info(level)[:2]
-f = torch.randn(rows, cols, dtype=torch.float64, device="cuda")
+f = torch.randn(h.batch, rows, cols, dtype=torch.float64, device="cuda")
 u = torch.zeros_like(f)
 w = h.acquire_work()
 ms = C.c_double()

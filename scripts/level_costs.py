@@ -18,7 +18,7 @@ w = h.acquire_work()
 res = []
 for l in range(h.depth - 1):
     rows, cols = h.level_info(l)[:2]
-    f = torch.randn(rows, cols, dtype=torch.float64, device="cuda")
+    f = torch.randn(h.batch, rows, cols, dtype=torch.float64, device="cuda")
     u = torch.zeros_like(f)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
