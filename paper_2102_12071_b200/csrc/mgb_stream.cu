@@ -63,6 +63,28 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Per-point planes (CM 0): the rows of A are read by stages 1, 3, 5 (8 steps apart)
+// and those of M by stages 2, 4, so the reuse lives in L2.  A plane row's last read is
+// marked evict-first so the rows still to be reused are the ones that stay.  (The same
+// hint on the cp.async ring copies makes ptxas emit an LDGSTS that faults: not used.)
+#ifndef MGB_EVH
+#define MGB_EVH 1
+#endif
+// 1: each step's plane weights are loaded into registers at the end of the previous
+// step (before its barrier), so their L2 latency overlaps the barrier and the
+// neighbour exchange instead of stalling the stage chains (2 CTAs/SM: 255 registers)
+#ifndef MGB_WPRE
+#define MGB_WPRE 1
+#endif
+// the L2 cache-policy word of createpolicy.fractional.L2::evict_first 1.0 (the value
+// CUTLASS uses for its TMA hints); an immediate, so it lands in a uniform register
+constexpr uint64_t POL_EVICT_FIRST = 0x12F0000000000000ull;
+__device__ __forceinline__ double ldg_hint(const double* ptr, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
+
 template <int NSW, bool RES, bool PRO>
 struct SP {
   static constexpr int S = 2 * NSW + (RES ? 1 : 0);  // stencil stages after the input field
@@ -102,13 +124,30 @@ struct Ctx {
   const uint8_t* mk;
 };
 
+// The nine per-point weights of stage k (odd: A, even: M) at (row, column); a plane
+// row's last read (A at stage S (PRE) / S - 1 (POST), M at stage 2 NSW) is evict-first.
+template <int NSW, bool RES>
+__device__ __forceinline__ void load_planes(const StreamArgs& a, const Ctx& c, int k, int row, double (&wt)[9]) {
+  constexpr int S = 2 * NSW + (RES ? 1 : 0);
+  const Op& op = (k & 1) ? a.A : a.K;
+  const double* base = op.planes + (int64_t)c.b * 9 * op.n + ((int64_t)row * c.g.cols + (c.cin ? c.col : 0));
+  const bool last = MGB_EVH && (k == (RES ? S : S - 1) || k == 2 * NSW);
+  if (last) {
+#pragma unroll
+    for (int o = 0; o < 9; ++o) wt[o] = ldg_hint(base + (int64_t)o * op.n, POL_EVICT_FIRST);
+  } else {
+#pragma unroll
+    for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
+  }
+}
+
 // One pipeline step (row t).  FAST: every row the step touches is an interior
 // row, every column of the CTA is an interior in-grid column, so no bounds,
 // band-class or column tests are needed.  PH = t mod 3 (window slots).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool MSK, bool FAST, int PH>
 __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, const int t,
                                             double (&w)[SP<NSW, RES, PRO>::NF][3][3], double (&hold)[NSW],
-                                            double& acc) {
+                                            double& acc, double (&wp)[SP<NSW, RES, PRO>::S][9]) {
   using P = SP<NSW, RES, PRO>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
   constexpr bool CL = CM != 0;
@@ -153,10 +192,13 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
       const bool res_stage = k & 1;
       const double init = res_stage ? c.ring_f[(row & (PDF - 1)) * SWT + c.tid] : hold[k / 2 - 1];
       if (!CL) {
-        const double* base = op.planes + (int64_t)c.b * 9 * op.n + ((int64_t)row * g.cols + (c.cin ? c.col : 0));
         double wt[9];
+        if (MGB_WPRE) {
 #pragma unroll
-        for (int o = 0; o < 9; ++o) wt[o] = __ldg(base + (int64_t)o * op.n);
+          for (int o = 0; o < 9; ++o) wt[o] = wp[k - 1][o];
+        } else {
+          load_planes<NSW, RES>(a, c, k, row, wt);
+        }
         val = res_stage ? dot9<true>(wt, w[k - 1], s0, s1, s2, init) : dot9<false>(wt, w[k - 1], s0, s1, s2, init);
       } else if (FAST) {
         const double* reg = CM == 2 ? ((k & 1) ? a.ci : a.ci + 9) : (((k & 1) ? c.tA : c.tK) + CINT * 9);
@@ -178,6 +220,14 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
 #pragma unroll
   for (int k = 0; k < NF; ++k) c.xch[(k * 2 + sl) * SWT + c.tid] = nv[k];
   if (RES) c.rlast[((t - 2 * S) & 3) * SWT + c.tid] = nv[S];
+  if (!CL && MGB_WPRE) {
+    // plane weights of step t + 1 (its stage rows are CTA-uniform)
+#pragma unroll
+    for (int k = 1; k <= S; ++k) {
+      const int row = t + 1 - 2 * k;
+      if ((unsigned)row < (unsigned)g.rows) load_planes<NSW, RES>(a, c, k, row, wp[k - 1]);
+    }
+  }
   __syncthreads();
   if (RES) {
     const int top = t - 2 * S;
@@ -219,7 +269,7 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
 // 2 = band-class tables with the interior class read from the kernel parameters
 // (constant-bank operands: no registers, no shared-memory traffic).
 template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, int CM, bool MSK>
-__global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
+__global__ void __launch_bounds__(SWT, (CM == 0 && MGB_WPRE) ? 2 : MINB) k_stream(StreamArgs a) {
   pdl_trigger();
   using P = SP<NSW, RES, PRO>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT, NF = P::NF;
@@ -277,6 +327,13 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
 #pragma unroll
   for (int m = 0; m < NSW; ++m) hold[m] = 0.0;
   double acc = 0.0;
+  double wp[S][9];  // CM 0: plane weights of the next step
+  if (CM == 0 && MGB_WPRE) {
+#pragma unroll
+    for (int k = 1; k <= S; ++k)
+#pragma unroll
+      for (int o = 0; o < 9; ++o) wp[k - 1][o] = 0.0;
+  }
 
   // steps t in [t0, t1], t0 aligned to a multiple of 3 (extra leading steps only
   // compute rows nobody needs)
@@ -324,6 +381,13 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
     __syncthreads();
   }
   for (int q = 0; q < DIST; ++q) issue();
+  if (CM == 0 && MGB_WPRE) {
+#pragma unroll
+    for (int k = 1; k <= S; ++k) {
+      const int row = t0 - 2 * k;
+      if ((unsigned)row < (unsigned)g.rows) load_planes<NSW, RES>(a, c, k, row, wp[k - 1]);
+    }
+  }
 
 #define MGB_STEP(PH_)                                                                                  \
   {                                                                                                    \
@@ -331,9 +395,9 @@ __global__ void __launch_bounds__(SWT, MINB) k_stream(StreamArgs a) {
     issue();                                                                                           \
     cp_wait<DIST>();                                                                                   \
     if (cta_fast && t - 2 * S >= 2 && t <= g.rows - 3)                                                 \
-      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, true, PH_>(a, c, t, w, hold, acc);                 \
+      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, true, PH_>(a, c, t, w, hold, acc, wp);                 \
     else                                                                                               \
-      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, false, PH_>(a, c, t, w, hold, acc);                \
+      stream_step<NSW, RES, PRO, NORM, ZU, CM, MSK, false, PH_>(a, c, t, w, hold, acc, wp);                \
   }
   for (int tb = t0; tb <= t1; tb += 3) {
     MGB_STEP(0)
