@@ -56,6 +56,12 @@ constexpr int DIST = 5;           // prefetch distance (rows ahead)
 // CTAs per SM the register budget is sized for (3 PRE CTAs fit in shared memory with
 // the compact exchange layout, but measured 40 % slower at 168 registers)
 constexpr int MINB = MGB_S2MINB, MINB_PRE = MGB_S2MINB_PRE;
+// Step loop: per-step variant dispatch, or three phases (boundary steps with dispatch,
+// the interior run with one variant, boundary steps) -- measured faster only for the
+// V(2,2) POST pass (c2 level 0: 118 -> 114 us; PRE 124 -> 130 us, c4 V(1,1) slower)
+#ifndef MGB_S2_PHASED
+#define MGB_S2_PHASED 0   // 1: phased V(2,2) POST, 2: three phases everywhere (experiments)
+#endif
 constexpr int PE = 8;             // ring of coarse rows (POST prolongation), power of two
 constexpr int NCLS = 25;
 constexpr int CINT = 12;          // interior band class (2 * 5 + 2)
@@ -443,12 +449,13 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
     const bool rv = prow >= lo_row && prow <= hi_row;
     double* du = &c.ring_u[(prow & (PD - 1)) * c.sw + c.tid];
     double* df = &c.ring_f[(prow & (PDF - 1)) * c.sw + c.tid];
+    // (a zero-size copy reads nothing: the row pointer is passed unselected)
     if (!ZU) {
-      cp_async8(du, rv && ina ? pu : ub, rv && ina);
-      cp_async8(du + c.tw, rv && inb ? pu + c.tw : ub, rv && inb);
+      cp_async8(du, pu, rv && ina);
+      cp_async8(du + c.tw, pu + c.tw, rv && inb);
     }
-    cp_async8(df, rv && ina ? pf : fb, rv && ina);
-    cp_async8(df + c.tw, rv && inb ? pf + c.tw : fb, rv && inb);
+    cp_async8(df, pf, rv && ina);
+    cp_async8(df + c.tw, pf + c.tw, rv && inb);
     // coarse row ci is first needed by fine row 2ci (as di = -1); staged with the
     // group of fine row 2ci - 2 so it is complete and published by that step's barrier
     if (PRO && !(prow & 1)) stage_e((prow >> 1) + 1);
@@ -484,11 +491,44 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
     else                                                                                   \
       step3<NSW, RES, PRO, NORM, ZU, CM, 3, PH_>(a, c, t, st);                             \
   }
-  for (int tb = t0; tb <= t1; tb += 3) {
+#define MGB_STEP2F(MODE_, PH_)                                                             \
+  {                                                                                        \
+    const int t = tb + PH_;                                                                \
+    issue();                                                                               \
+    cp_wait<DIST - 1>();                                                                   \
+    step3<NSW, RES, PRO, NORM, ZU, CM, MODE_, PH_>(a, c, t, st);                           \
+  }
+  // three phases: the leading boundary steps (general dispatch), the run of interior
+  // steps (one step variant, no per-step dispatch), the trailing ones
+  int tb = t0;
+  const int fa = 2 * S + 2, fz = min(t1, g.rows - 3);  // interior steps: rows_int
+  constexpr bool phased = MGB_S2_PHASED == 2 || (MGB_S2_PHASED == 1 && PRO && NSW == 2);
+  if (phased && cta_fast) {
+    for (; tb <= t1 && tb < fa; tb += 3) {
+      MGB_STEP2(0)
+      MGB_STEP2(1)
+      MGB_STEP2(2)
+    }
+    if (cta_int) {
+      for (; tb + 2 <= fz; tb += 3) {
+        MGB_STEP2F(0, 0)
+        MGB_STEP2F(0, 1)
+        MGB_STEP2F(0, 2)
+      }
+    } else {
+      for (; tb + 2 <= fz; tb += 3) {
+        MGB_STEP2F(1, 0)
+        MGB_STEP2F(1, 1)
+        MGB_STEP2F(1, 2)
+      }
+    }
+  }
+  for (; tb <= t1; tb += 3) {
     MGB_STEP2(0)
     MGB_STEP2(1)
     MGB_STEP2(2)
   }
+#undef MGB_STEP2F
 #undef MGB_STEP2
   cp_wait<0>();
 #ifdef MGB_CTA_PROF
