@@ -459,8 +459,9 @@ def run_ours(args):
     peak, peak_kind = measured_peak()
     # algorithmic bytes per fine point of one phase: u in, f, u out (8 B each) plus
     # the restricted residual (PRE) or coarse correction (POST) at 8 B per coarse
-    # point; + 72 B each for A and M when they are per-point planes
-    per_pt = 26 + (0 if compact else 144)
+    # point; + 72 B for M and 8 B per nonzero A entry (72, or 40 for a 5-point A whose
+    # zero corner planes are never read) when they are per-point planes
+    per_pt = 26 + (0 if compact else 72 + 8 * h.stencil_points(0))
     pass_bytes = per_pt * n * n * nb
     achieved = pass_bytes / (ms_pre.value * 1e-3) / 1e9
     achieved_post = pass_bytes / (ms_post.value * 1e-3) / 1e9

@@ -145,6 +145,10 @@ int mgb_hier_operator_planes(const mgb_hier* h, int level, const double** planes
    mgb_hier_storage_info reports whether level `level`'s A / M tables are class-compact. */
 int mgb_hier_set_storage(mgb_hier* h, int mode, void* stream);
 int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_classed);
+/* Number of operator entries per point the streaming passes read for level `level`'s
+   per-point A: 5 when its corner planes are zero everywhere (a 5-point operator,
+   checked on the device at build), else 9 (0 for class-compact A). */
+int mgb_hier_stencil_points(const mgb_hier* h, int level, int* a_points);
 /* Cycle pass structure for V(1|2, 1|2) with 1-stage smoothers: 2 (default) one
    row-streaming pass per smoothing phase (sweeps + restriction, prolongation +
    sweeps); 1: one streaming pass per sweep; 0: separate sweep / restriction /

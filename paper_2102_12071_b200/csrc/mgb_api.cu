@@ -71,6 +71,7 @@ struct LevelD {
   }
   std::vector<uint8_t> hmask;
   int64_t nact = 0;
+  bool a5 = false;         // per-point A with all-zero corner planes (5-point operator)
   ConvSm conv;             // shared-kernel convolutional smoother (conv.nl > 0 replaces K)
   bool has_smoother() const { return K != nullptr || conv.nl > 0; }
   Op opA() const { return Op{A, Acls, n, 1}; }
@@ -415,10 +416,29 @@ static int classify_table(mgb_hier* h, int l, const double* planes, int ks, doub
   return MGB_OK;
 }
 
+// Per-point A whose corner planes are zero everywhere (a 5-point operator such as
+// config 3's cell-centred diffusion): the streaming passes skip those loads.
+static int check_corners(mgb_hier* h, int l, cudaStream_t s) {
+  LevelD& lv = h->lv[l];
+  lv.a5 = false;
+  if (!lv.A || lv.Acls) return MGB_OK;
+  int* flag = nullptr;
+  MGB_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), s));
+  MGB_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  MGB_CUDA_TRY(launch_corner_check(lv.n, h->batch, lv.A, flag, s));
+  int hf = 1;
+  MGB_CUDA_TRY(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  MGB_CUDA_TRY(cudaFreeAsync(flag, s));
+  MGB_CUDA_TRY(cudaStreamSynchronize(s));
+  lv.a5 = hf == 0;
+  return MGB_OK;
+}
+
 static int classify_all(mgb_hier* h, cudaStream_t s) {
   for (int l = 0; l < h->depth(); ++l) {
     LevelD& lv = h->lv[l];
     if (int st = classify_table(h, l, lv.A, 1, &lv.Acls, s, &lv.hAcls)) return st;
+    if (int st = check_corners(h, l, s)) return st;
     if (lv.K) {
       if (int st = classify_table(h, l, lv.K, lv.ks, &lv.Kcls, s, &lv.hKcls)) return st;
     } else {
@@ -682,6 +702,14 @@ extern "C" int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classe
   if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
   if (a_classed) *a_classed = h->lv[level].Acls != nullptr;
   if (k_classed) *k_classed = h->lv[level].Kcls != nullptr;
+  return MGB_OK;
+}
+
+extern "C" int mgb_hier_stencil_points(const mgb_hier* h, int level, int* a_points) {
+  if (!h || !a_points) return fail(MGB_CONTRACT, "null argument");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  const LevelD& lv = h->lv[level];
+  *a_points = lv.Acls || !lv.A ? 0 : (lv.a5 ? 5 : 9);
   return MGB_OK;
 }
 
@@ -1248,6 +1276,7 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
   a.uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
   a.kernel = h->stream_kernel;
+  a.a5 = lv.a5 && !lv.Acls;
   for (int o = 0; o < 9; ++o) {
     a.ci[o] = lv.hAint()[o];
     a.ci[9 + o] = lv.hKint()[o];

@@ -286,6 +286,19 @@ __global__ void k_classify(Grid g, Op T, const int64_t* __restrict__ rep, int* _
   if (diff) atomicOr(flag, 1);
 }
 
+// flag |= 1 if a corner entry (planes 0, 2, 6, 8) of a k = 3 table is nonzero anywhere:
+// a 5-point operator, whose corner planes the per-point streaming passes skip
+__global__ void k_corner_check(int64_t n, int batch, const double* __restrict__ planes, int* __restrict__ flag) {
+  const int64_t total = n * batch;
+  bool nz = false;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = q / n, p = q - b * n;
+    const double* t = planes + b * 9 * n + p;
+    nz |= t[0] != 0.0 || t[2 * n] != 0.0 || t[6 * n] != 0.0 || t[8 * n] != 0.0;
+  }
+  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 __global__ void k_gather_cls(Grid g, Op T, const int64_t* __restrict__ rep, double* __restrict__ out) {
   const int b = blockIdx.x;
   for (int q = threadIdx.x; q < NCLS * T.ks * 9; q += blockDim.x) {
@@ -356,6 +369,12 @@ cudaError_t launch_classify(const Grid& g, const Op& T, const int64_t* rep, int*
   ++g_launches;
   dim3 grid((g.cols + BX - 1) / BX, (g.rows + BY - 1) / BY, g.batch);
   k_classify<<<grid, dim3(BX, BY), 0, s>>>(g, T, rep, flag);
+  return MGB_DBG(__func__);
+}
+
+cudaError_t launch_corner_check(int64_t n, int batch, const double* planes, int* flag, cudaStream_t s) {
+  ++g_launches;
+  k_corner_check<<<4 * 148, 256, 0, s>>>(n, batch, planes, flag);
   return MGB_DBG(__func__);
 }
 

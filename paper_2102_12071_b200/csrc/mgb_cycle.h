@@ -32,6 +32,7 @@ cudaError_t launch_resnorm(const Grid& g, const Op& A, const uint8_t* mask, cons
                            double* partials, cudaStream_t s);
 // band-class detection and gather (rep: 25 representative flat indices or -1)
 cudaError_t launch_classify(const Grid& g, const Op& T, const int64_t* rep, int* flag, cudaStream_t s);
+cudaError_t launch_corner_check(int64_t n, int batch, const double* planes, int* flag, cudaStream_t s);
 cudaError_t launch_gather_cls(const Grid& g, const Op& T, const int64_t* rep, double* out, cudaStream_t s);
 
 }  // namespace mgb

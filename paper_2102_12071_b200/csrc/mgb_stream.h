@@ -24,6 +24,7 @@ struct StreamArgs {
   int ci_valid;            // 1: ci holds the interior-class weights (batch == 1, classed A and M)
   int uniform;             // 1: every band class equals the interior one (ci valid everywhere)
   int kernel;              // streaming kernel: 0 auto, 1 one column per thread, 2 column pairs
+  int a5;                  // per-point A with zero corner planes: their loads are skipped
   // two-column kernel CTA map (set by its launcher): edge strips (first / last) get
   // shorter segments (their steps take the boundary-class path), listed first
   // segments of a strip: the first has seg_first rows, the others seg (the last: the

@@ -216,6 +216,13 @@ class MultigridHierarchy:
         _lib.call("mgb_hier_storage_info", self._h, l, C.byref(a), C.byref(k))
         return bool(a.value), bool(k.value)
 
+    def stencil_points(self, l: int) -> int:
+        """Operator entries per point the streaming passes read for level l's per-point
+        A: 5 (zero corner planes), 9, or 0 when A is class-compact."""
+        p = C.c_int()
+        _lib.call("mgb_hier_stencil_points", self._h, l, C.byref(p))
+        return p.value
+
     # -- smoother bookkeeping ------------------------------------------------
     def _sweeps(self, nu1, nu2):
         """Resolve (nu1, nu2) and make sure the device holds each level's smoother."""

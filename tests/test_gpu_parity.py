@@ -451,7 +451,7 @@ def test_nccl_decomposition_single_rank(monkeypatch):
 
 
 @pytest.mark.parametrize("name", ["c1_fd_conv", "c1_q1_conv", "case_var31_conv_v22", "case_lshape31_conv_v11",
-                                  "case_rot31_fc_v22", "c4_p0", "case_rect20x27_conv_v11"])
+                                  "case_rot31_fc_v22", "c4_p0", "case_rect20x27_conv_v11", "case_grf63_conv_v22"])
 def test_tile_and_stream_passes_bit_identical(name):
     """Tile-local fused passes (mid-size levels) vs row-streaming passes on every
     level: the same arithmetic, so u is bitwise equal; histories differ in the
@@ -476,6 +476,20 @@ def test_tile_and_stream_passes_bit_identical(name):
     assert_hist(runs[1][1], runs[2][1])                       # vs separate kernels: rounding only
     assert rel_err(dv.host(runs[1][0]), dv.host(runs[2][0])) <= 1e-12
     assert_hist(runs[1][1], g["history"])                     # and the reference
+
+
+def test_five_point_operator_detected():
+    """The GRF 5-point cell-centred operator (config 3's family) has zero corner planes
+    on level 0 only (its Galerkin coarse operators are 9-point); the streaming passes
+    then skip the corner reads, which the bitwise stream/tile test above covers."""
+    c = load("case_grf63_conv_v22")
+    spec = spec_of(c["mask"], float(c["golden"]["h"]))
+    h = mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"])
+    assert h.stencil_points(0) == 5
+    assert h.stencil_points(1) == 9
+    c = load("case_var31_conv_v22")
+    h = mg.build_hierarchy(mg.StencilField(spec_of(c["mask"], float(c["golden"]["h"])), c["A0"]), c["levels"])
+    assert h.stencil_points(0) in (0, 9)
 
 
 @pytest.mark.parametrize("n,nu", [(1023, 2), (1023, 1), (600, 2)])
