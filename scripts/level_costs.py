@@ -11,6 +11,8 @@ if len(sys.argv) > 2:  # streaming kernel: 0 auto, 1 one column, 2 column pairs
     h.set_stream_kernel(int(sys.argv[2]))
 if len(sys.argv) > 3:  # stream_min (points): levels below run tile passes (-1 keeps)
     h.set_passes(int(sys.argv[3]))
+if len(sys.argv) > 5:  # tile: 1 tile-local fused passes below stream_min, 0 separate kernels
+    h.set_passes(-1, int(sys.argv[5]), -1)
 if len(sys.argv) > 4:  # coarse_max (points): levels up to this run in the single-CTA coarse kernel
     h.set_passes(-1, -1, int(sys.argv[4]))
 nu = info["nu"]
