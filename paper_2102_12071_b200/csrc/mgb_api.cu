@@ -1247,18 +1247,28 @@ static int enqueue_coarse(mgb_work* w, int lc, bool zero, int nu1, int nu2, cuda
 
 // ---- row-streaming passes (mgb_stream.cu) -----------------------------------
 
+// Row streaming for levels of at least stream_min points, except batches of narrow
+// problems (< 96 columns: a strip is mostly halo and a segment mostly pipeline fill;
+// config 4's 63^2 level: tile passes 55 us vs 72 us per cycle) unless stream_min = 0
+// forces streaming everywhere.
+static bool streamed(const mgb_hier* h, int l) {
+  const LevelD& lv = h->lv[l];
+  if ((int64_t)lv.n * h->batch < h->stream_min) return false;
+  return !(h->stream_min > 0 && h->batch > 1 && lv.cols < 96);
+}
+
 // fused pass kind for level l: 0 separate kernels, 1 row streaming, 2 tile-local
 static int pass_kind(const mgb_hier* h, int l, int nu1, int nu2) {
   const LevelD& lv = h->lv[l];
   if (!h->fused || lv.ks != 1 || !(nu1 == 1 || nu1 == 2) || !(nu2 == 1 || nu2 == 2)) return 0;
-  if ((int64_t)lv.n * h->batch >= h->stream_min) return 1;
+  if (streamed(h, l)) return 1;
   return h->tile ? 2 : 0;
 }
 static bool use_stream(const mgb_hier* h, int l, int nu1, int nu2) { return pass_kind(h, l, nu1, nu2) != 0; }
 
 static cudaError_t launch_pass(const mgb_hier* h, int l, const StreamArgs& a, int nsw, bool res, bool pro,
                                bool norm, int* nb) {
-  if ((int64_t)h->lv[l].n * h->batch >= h->stream_min) return launch_stream(a, nsw, res, pro, norm, nb);
+  if (streamed(h, l)) return launch_stream(a, nsw, res, pro, norm, nb);
   return launch_tile(a, nsw, res, pro, norm, nb);
 }
 
