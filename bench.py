@@ -21,7 +21,9 @@ agglomerated coarse levels (strong scaling of the one problem).
 The value is the job's unknowns / max-over-ranks device time.
 
 `--impl reference` times the CPU oracle port of the reference algorithm (NumPy,
-oracle/mg_oracle.py) on a bounded sample of the same workload (cpu_sample()).
+oracle/mg_oracle.py) on a bounded sample of the same workload on all host cores
+(cpu_sample_replicas(): one single-threaded replica per core; config 4: a pool
+over its independent problems).
 """
 
 from __future__ import annotations
@@ -198,11 +200,11 @@ def build_problem(cfg_name, device, lo=0, hi=None):
     return h, f, info
 
 
-def cpu_sample(cfg_name, steps=1, warmup=0):
+def cpu_sample(cfg_name, steps=1, warmup=0, barrier=None):
     """Oracle port (NumPy, single thread) on a bounded sample of the config: its
     operator family at min(n, CPU_SAMPLE_N)^2 (levels scaled to reach 3x3), one
     problem, V(nu, nu) cycles with the history residual, timed like
-    hierarchy.solve (setup excluded)."""
+    hierarchy.solve (setup excluded).  barrier: replicas start timing together."""
     from oracle import mg_oracle as mo
     from paper_2102_12071_b200 import problems as gen
     cfg = CONFIGS[cfg_name]
@@ -223,6 +225,8 @@ def cpu_sample(cfg_name, steps=1, warmup=0):
     u = np.zeros((n, n))
     fn = float(np.linalg.norm(f))
     times = []
+    if barrier is not None:
+        barrier.wait()
     for s in range(warmup + steps):
         t = time.perf_counter()
         u = mo.v_cycle(h, 0, f, u, nu, nu)
@@ -290,6 +294,52 @@ def cpu_sample_pool(cfg_name, nproblems=None):
             "per_cycle_s": per_cycle_core / cores}
 
 
+def _replica_worker(cfg_name, steps, warmup, barrier, out):
+    """One single-threaded replica of cpu_sample (worker of cpu_sample_replicas): the
+    setup runs before the barrier, so every replica's timed cycles overlap."""
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    sys.path.insert(0, ROOT)
+    s = cpu_sample(cfg_name, steps=steps, warmup=warmup, barrier=barrier)
+    out.put(s["per_cycle_s"])
+
+
+def cpu_sample_replicas(cfg_name, steps=1, warmup=0, max_procs=32):
+    """Single-problem configs on all host cores: one solve of the reference is
+    single-threaded NumPy, so the host's throughput is independent replicas, one
+    per core (the reference's own concurrency model: the bench thread pool,
+    cli.py:746-752), each timing cpu_sample's cycles at the same moment; value =
+    sum over replicas of unknowns / cycle time (memory-bandwidth contention
+    between replicas included)."""
+    import multiprocessing as mpc
+    cores = max(1, min(os.cpu_count() or 1, max_procs))
+    if cores == 1:
+        return cpu_sample(cfg_name, steps=steps, warmup=warmup)
+    ctx = mpc.get_context("spawn")
+    barrier, out = ctx.Barrier(cores), ctx.Queue()
+    procs = [ctx.Process(target=_replica_worker, args=(cfg_name, steps, warmup, barrier, out)) for _ in range(cores)]
+    for p in procs:
+        p.start()
+    per = [out.get() for _ in procs]
+    for p in procs:
+        p.join()
+    cfg = CONFIGS[cfg_name]
+    n = min(cfg["n"], CPU_SAMPLE_N)
+    value = float(sum(n * n / t for t in per))
+    return {"value": value, "unit": "unknowns/s", "cores": cores, "kind": "port",
+            "sample": f"oracle/mg_oracle.py (NumPy) on {cores} concurrent single-threaded replicas, each one "
+                      f"problem of the config's operator family at {n}^2 ({gen_levels(n)} levels), "
+                      f"{steps} V({cfg['nu']},{cfg['nu']}) cycle(s) + history residual timed after {warmup} "
+                      f"warm-up (setup excluded); value = sum of the replicas' unknowns / cycle time "
+                      f"(mean cycle {np.mean(per) * 1e3:.0f} ms); cpu {cpu_model()}",
+            "per_cycle_s": float(np.mean(per)) / cores}
+
+
+def gen_levels(n):
+    from paper_2102_12071_b200 import problems as gen
+    return gen.levels_for(n)
+
+
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -316,7 +366,7 @@ def run_reference(args):
     if cfg["batch"] > 1:
         s = cpu_sample_pool(args.config)
     else:
-        s = cpu_sample(args.config, steps=max(1, args.steps), warmup=min(args.warmup, 1))
+        s = cpu_sample_replicas(args.config, steps=max(1, min(args.steps, 10)), warmup=min(args.warmup, 1))
     line = {"metric": "unknowns/sec per V-cycle (fp64)", "value": s["value"], "unit": "unknowns/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": s["per_cycle_s"] * 1e3, "higher_is_better": True,
