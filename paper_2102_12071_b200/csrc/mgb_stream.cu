@@ -85,6 +85,33 @@ __device__ __forceinline__ double ldg_hint(const double* ptr, uint64_t pol) {
   return v;
 }
 
+// CM 0: the first-use plane rows (A for stage 1, M for stage 2) are prefetched into L2
+// by the ring issue, MGB_L2PF_AHEAD steps beyond the ring's DIST rows, so the register
+// loads of every stage hit L2 (the passes were load-latency bound at 8 warps/SM)
+#ifndef MGB_L2PF
+#define MGB_L2PF 1
+#endif
+#ifndef MGB_L2PF_AHEAD
+#define MGB_L2PF_AHEAD 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const double* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p));
+}
+template <bool RES>
+__device__ __forceinline__ void prefetch_planes(const StreamArgs& a, int b, const Grid& g, int col, int rowA, int rowM) {
+  if ((unsigned)rowA < (unsigned)g.rows) {
+    const double* pa = a.A.planes + (int64_t)b * 9 * a.A.n + ((int64_t)rowA * g.cols + col);
+#pragma unroll
+    for (int o = 0; o < 9; ++o)
+      if (!(a.a5 && (o == 0 || o == 2 || o == 6 || o == 8))) prefetch_l2(pa + (int64_t)o * a.A.n);
+  }
+  if ((unsigned)rowM < (unsigned)g.rows) {
+    const double* pm = a.K.planes + (int64_t)b * 9 * a.K.n + ((int64_t)rowM * g.cols + col);
+#pragma unroll
+    for (int o = 0; o < 9; ++o) prefetch_l2(pm + (int64_t)o * a.K.n);
+  }
+}
+
 template <int NSW, bool RES, bool PRO>
 struct SP {
   static constexpr int S = 2 * NSW + (RES ? 1 : 0);  // stencil stages after the input field
@@ -367,6 +394,8 @@ __global__ void __launch_bounds__(SWT, (CM == 0 && MGB_WPRE) ? 2 : MINB) k_strea
       const bool ev = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c && cj >= 0 && cj < cols_c;
       cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + c.tid], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
     }
+    if (CM == 0 && MGB_L2PF && c.cin)
+      prefetch_planes<RES>(a, c.b, g, c.col, prow + MGB_L2PF_AHEAD - 2, prow + MGB_L2PF_AHEAD - 4);
     cp_commit();
     ++prow;
     if (!ZU) pu += cstride;
