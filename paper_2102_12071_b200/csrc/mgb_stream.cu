@@ -97,18 +97,24 @@ __device__ __forceinline__ double ldg_hint(const double* ptr, uint64_t pol) {
 __device__ __forceinline__ void prefetch_l2(const double* p) {
   asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p));
 }
-template <bool RES>
-__device__ __forceinline__ void prefetch_planes(const StreamArgs& a, int b, const Grid& g, int col, int rowA, int rowM) {
-  if ((unsigned)rowA < (unsigned)g.rows) {
-    const double* pa = a.A.planes + (int64_t)b * 9 * a.A.n + ((int64_t)rowA * g.cols + col);
+// One warp-wide pass: the warp's 32 columns of a plane row span at most three 128-byte
+// lines, touched by columns wc0, wc0 + 16 and wc0 + 31, so lane q prefetches line
+// (q mod 3) of plane item q / 3 (A's nonzero planes at rowA, then M's nine at rowM):
+// two prefetch instructions per warp and step instead of one per plane.
+__device__ __forceinline__ void prefetch_planes(const StreamArgs& a, int b, const Grid& g, int wc0, int rowA, int rowM,
+                                                int lane) {
+  const int nA = a.a5 ? 5 : 9;
 #pragma unroll
-    for (int o = 0; o < 9; ++o)
-      if (!(a.a5 && (o == 0 || o == 2 || o == 6 || o == 8))) prefetch_l2(pa + (int64_t)o * a.A.n);
-  }
-  if ((unsigned)rowM < (unsigned)g.rows) {
-    const double* pm = a.K.planes + (int64_t)b * 9 * a.K.n + ((int64_t)rowM * g.cols + col);
-#pragma unroll
-    for (int o = 0; o < 9; ++o) prefetch_l2(pm + (int64_t)o * a.K.n);
+  for (int r = 0; r < 2; ++r) {
+    const int q = lane + 32 * r, item = q / 3, part = q - 3 * item;
+    if (item >= nA + 9) break;
+    const bool isA = item < nA;
+    const int row = isA ? rowA : rowM;
+    if ((unsigned)row >= (unsigned)g.rows) continue;
+    const int plane = !isA ? item - nA : (!a.a5 ? item : (item < 2 ? 2 * item + 1 : (item == 4 ? 7 : item + 2)));
+    const int col = min(max(wc0 + (part == 0 ? 0 : (part == 1 ? 16 : 31)), 0), g.cols - 1);
+    const Op& op = isA ? a.A : a.K;
+    prefetch_l2(op.planes + (int64_t)b * 9 * op.n + (int64_t)plane * op.n + ((int64_t)row * g.cols + col));
   }
 }
 
@@ -394,8 +400,8 @@ __global__ void __launch_bounds__(SWT, (CM == 0 && MGB_WPRE) ? 2 : MINB) k_strea
       const bool ev = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c && cj >= 0 && cj < cols_c;
       cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + c.tid], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
     }
-    if (CM == 0 && MGB_L2PF && c.cin)
-      prefetch_planes<RES>(a, c.b, g, c.col, prow + MGB_L2PF_AHEAD - 2, prow + MGB_L2PF_AHEAD - 4);
+    if (CM == 0 && MGB_L2PF)
+      prefetch_planes(a, c.b, g, c.col - (c.tid & 31), prow + MGB_L2PF_AHEAD - 2, prow + MGB_L2PF_AHEAD - 4, c.tid & 31);
     cp_commit();
     ++prow;
     if (!ZU) pu += cstride;
