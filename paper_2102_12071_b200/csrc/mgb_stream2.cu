@@ -143,9 +143,20 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     const int iL = max(c.tid - 1, 0), iR = min(c.tid + 1, c.tw - 1);
 #pragma unroll
     for (int j = 0; j < NX; ++j) {
+      if (ZU && j <= 1) continue;
       const double* xr = &c.xch[slp * c.xb + j * c.sw];
       L[j] = (RES && j == S) ? 0.0 : xr[c.tw + iL];
       R[j] = xr[iR];
+    }
+    if (ZU) {
+      // zero start: field 1 (the first residual f - A 0) is f itself, so stage 2 takes
+      // the neighbours of its input row t - 3 straight from the f ring (out-of-grid
+      // columns and rows outside the pass's range are zero-filled there, as the
+      // computed field would be); fields 0 and 1 are never exchanged
+      const double* fr = &c.ring_f[((t - 3) & (PDF - 1)) * c.sw];
+      L[0] = R[0] = 0.0;
+      L[1] = fr[max(2 * c.tid - 1, 0)];
+      R[1] = fr[min(2 * c.tid + 2, c.sw - 1)];
     }
   }
   double out[S + 1][2];
@@ -154,6 +165,13 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
   for (int k = 1; k <= S; ++k) {
     const bool resid = k & 1;
     const int x = t - 2 * k + 1;
+    double v0, v1;
+    if (ZU && k == 1) {
+      // zero start: f - A 0 = f (the chain fma(-w, 0, f) returns f), row t - 2
+      const double2 fv = *reinterpret_cast<const double2*>(&c.ring_f[((t - 2) & (PDF - 1)) * c.sw + 2 * c.tid]);
+      v0 = fv.x;
+      v1 = fv.y;
+    } else {
     const int sN = m3(PH - 2 * k + 2), sM = m3(PH - 2 * k + 1), sB = m3(PH - 2 * k);  // rows x+1, x, x-1
     const double in0 = L[k - 1], in1 = st.cur[k - 1][0], in2 = st.cur[k - 1][1], in3 = R[k - 1];
     // seed of the new chain (row x + 1): f, or the u the update adds to
@@ -210,9 +228,11 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
     s0 = FMS(wN0[2], in2, s0);
     s1 = FMS(wN1[2], in3, s1);
 #undef FMS
-    double v0 = A[sB][0], v1 = A[sB][1];
+    v0 = A[sB][0];
+    v1 = A[sB][1];
     A[sN][0] = s0;   // slot of row x + 1 (was row x - 2, long complete)
     A[sN][1] = s1;
+    }
     const int row = x - 1;  // = t - 2k
     if (!FAST) {
       const bool rv = (unsigned)row < (unsigned)g.rows;
@@ -302,6 +322,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
   const int sl = t & 1;
 #pragma unroll
   for (int j = 0; j < NX; ++j) {
+    if (ZU && j <= 1) continue;
     c.xch[sl * c.xb + j * c.sw + c.tid] = out[j][0];
     if (!(RES && j == S)) c.xch[sl * c.xb + j * c.sw + c.tw + c.tid] = out[j][1];
   }
