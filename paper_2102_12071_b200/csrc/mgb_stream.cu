@@ -228,7 +228,9 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
       const Op& op = (k & 1) ? a.A : a.K;
       const bool res_stage = k & 1;
       const double init = res_stage ? c.ring_f[(row & (PDF - 1)) * SWT + c.tid] : hold[k / 2 - 1];
-      if (!CL) {
+      if (ZU && k == 1) {
+        val = init;  // zero start: r = f - A 0 = f (as the tile passes)
+      } else if (!CL) {
         double wt[9];
         if (MGB_WPRE) {
 #pragma unroll
@@ -260,7 +262,7 @@ __device__ __forceinline__ void stream_step(const StreamArgs& a, const Ctx& c, c
   if (!CL && MGB_WPRE) {
     // plane weights of step t + 1 (its stage rows are CTA-uniform)
 #pragma unroll
-    for (int k = 1; k <= S; ++k) {
+    for (int k = ZU ? 2 : 1; k <= S; ++k) {
       const int row = t + 1 - 2 * k;
       if ((unsigned)row < (unsigned)g.rows) load_planes<NSW, RES>(a, c, k, row, wp[k - 1]);
     }
@@ -401,7 +403,8 @@ __global__ void __launch_bounds__(SWT, (CM == 0 && MGB_WPRE) ? 2 : MINB) k_strea
       cp_async8(&c.ring_e[(ci & (PE - 1)) * EW + c.tid], ev ? ecb + (int64_t)ci * cols_c + cj : ecb, ev);
     }
     if (CM == 0 && MGB_L2PF)
-      prefetch_planes(a, c.b, g, c.col - (c.tid & 31), prow + MGB_L2PF_AHEAD - 2, prow + MGB_L2PF_AHEAD - 4, c.tid & 31);
+      prefetch_planes(a, c.b, g, c.col - (c.tid & 31), prow + MGB_L2PF_AHEAD - (ZU ? 6 : 2),
+                      prow + MGB_L2PF_AHEAD - 4, c.tid & 31);  // zero start: A first read by stage 3
     cp_commit();
     ++prow;
     if (!ZU) pu += cstride;
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(SWT, (CM == 0 && MGB_WPRE) ? 2 : MINB) k_strea
   for (int q = 0; q < DIST; ++q) issue();
   if (CM == 0 && MGB_WPRE) {
 #pragma unroll
-    for (int k = 1; k <= S; ++k) {
+    for (int k = ZU ? 2 : 1; k <= S; ++k) {
       const int row = t0 - 2 * k;
       if ((unsigned)row < (unsigned)g.rows) load_planes<NSW, RES>(a, c, k, row, wp[k - 1]);
     }
