@@ -120,6 +120,8 @@ struct St3 {
   double cur[NX][2];      // own values of field j published at the previous step
   double prev[NSW][2];    // own values of fields 0, 2, .. published two steps back
   double racc;            // open restriction sum (coarse row being accumulated)
+  double eA0, eA1;        // POST: coarse correction row t >> 1 at columns m - 1, m (registers:
+  double eB0, eB1;        // each coarse row is read from ring_e once), and row (t >> 1) - 1
   double norm;            // history: sum of squares of the input residual
 };
 
@@ -290,24 +292,30 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Ctx2& c, const 
       u0 = v.x;
       u1 = v.y;
     }
+    if (PRO && !(t & 1)) {
+      // coarse row t/2 enters (staged in ring_e, entry q = coarse column cjb + q; read
+      // once, kept in registers for fine rows t, t + 1, t + 2); row t/2 - 1 moves down
+      st.eB0 = st.eA0;
+      st.eB1 = st.eA1;
+      const double* ea = c.ring_e + ((t >> 1) & (PE - 1)) * c.ew;
+      st.eA0 = ea[c.tid];
+      st.eA1 = ea[c.tid + 1];
+    }
     if (PRO && rvr) {
-      // u += P ec, coarse rows staged in ring_e (entry q = coarse column cjb + q);
-      // the k_stream loop order: di = -1, 0, 1 (row parity), dj = -1, 0, 1 (column parity)
+      // u += P ec; the k_stream loop order: di = -1, 0, 1 (row parity), dj = -1, 0, 1
+      // (column parity)
       double p0 = 0.0, p1 = 0.0;
       if (t & 1) {
-        const double* er = c.ring_e + (((t - 1) >> 1) & (PE - 1)) * c.ew;
-        p0 = fma(0.25, er[c.tid + 1], p0);   // (di 0, dj -1): coarse m
-        p0 = fma(0.25, er[c.tid], p0);       // (di 0, dj +1): coarse m - 1
-        p1 = fma(0.5, er[c.tid + 1], p1);    // (di 0, dj 0)
+        p0 = fma(0.25, st.eA1, p0);   // (di 0, dj -1): coarse row (t - 1)/2, column m
+        p0 = fma(0.25, st.eA0, p0);   // (di 0, dj +1): column m - 1
+        p1 = fma(0.5, st.eA1, p1);    // (di 0, dj 0)
       } else {
-        const double* ea = c.ring_e + ((t >> 1) & (PE - 1)) * c.ew;        // di = -1: coarse row t/2
-        const double* eb = c.ring_e + (((t - 2) >> 1) & (PE - 1)) * c.ew;  // di = +1: coarse row t/2 - 1
-        p0 = fma(0.125, ea[c.tid + 1], p0);
-        p0 = fma(0.125, ea[c.tid], p0);
-        p1 = fma(0.25, ea[c.tid + 1], p1);
-        p0 = fma(0.125, eb[c.tid + 1], p0);
-        p0 = fma(0.125, eb[c.tid], p0);
-        p1 = fma(0.25, eb[c.tid + 1], p1);
+        p0 = fma(0.125, st.eA1, p0);  // di = -1: coarse row t/2
+        p0 = fma(0.125, st.eA0, p0);
+        p1 = fma(0.25, st.eA1, p1);
+        p0 = fma(0.125, st.eB1, p0);  // di = +1: coarse row t/2 - 1
+        p0 = fma(0.125, st.eB0, p0);
+        p1 = fma(0.25, st.eB1, p1);
       }
       u0 += p0;
       u1 += p1;
@@ -439,6 +447,7 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   for (int m = 0; m < NSW; ++m) st.prev[m][0] = st.prev[m][1] = 0.0;
   st.racc = 0.0;
   st.norm = 0.0;
+  st.eA0 = st.eA1 = st.eB0 = st.eB1 = 0.0;
   // the first step reads the exchange slot of step t0 - 1: start it at zero
   for (int q = c.tid; q < 2 * c.xb; q += c.tw) c.xch[q] = 0.0;
   pdl_wait();  // u, f, ec come from the preceding kernels; uo / rc may still be read there
@@ -490,6 +499,10 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
     cp_commit();
     cp_wait<0>();
     __syncthreads();
+    // the register copy of coarse row (t0 - 1) >> 1, as if step t0 - 1 had run
+    const double* ea = c.ring_e + (((t0 - 1) >> 1) & (PE - 1)) * c.ew;
+    st.eA0 = ea[c.tid];
+    st.eA1 = ea[c.tid + 1];
   }
   for (int q = 0; q < DIST; ++q) issue();
   // ring rows are copied by other threads than the ones reading the pair: row t

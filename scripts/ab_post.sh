@@ -1,0 +1,10 @@
+# POST: coarse correction rows in registers (default lib) vs three ring_e reads per row (experiments/lib_base.so)
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_gpu.log
+for rep in 1 2; do
+for L in paper_2102_12071_b200/libmgb.so experiments/lib_base.so; do
+  for cfg in c2 c4; do
+    MGB_LIB_PATH=$PWD/$L timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu > gpurun_out/g.log 2>&1
+    echo "$L $cfg $(tail -1 gpurun_out/g.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"], d["roofline"]["launch_ms"], d["roofline"]["post"]["launch_ms"], d["history_last"])' 2>&1 | tail -1)"
+  done
+done
+done
