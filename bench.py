@@ -56,7 +56,8 @@ CONFIGS = {
                net="net_conv_c5.json",
                desc="rotated FD eps=0.01 theta=pi/3, band-class hierarchy (no per-point tables)"),
 }
-CPU_SAMPLE_N = 1023                  # bounded CPU sample: same operator family at <= 1023^2
+# bounded CPU sample: same operator family at <= 1023^2 (MGB_CPU_SAMPLE_N: smaller, for tests)
+CPU_SAMPLE_N = int(os.environ.get("MGB_CPU_SAMPLE_N", "1023"))
 
 
 def cycle_bytes_per_fine_unknown(n, levels, nu1, nu2):

@@ -1,0 +1,36 @@
+"""The reference arm of bench.py (--impl reference): the CPU oracle port on all host
+cores, one JSON line with the contract's keys.  Small sample grid so it runs on CPU."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _run(args, n):
+    env = dict(os.environ, MGB_CPU_SAMPLE_N=str(n))
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", *args],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_reference_arm_line_uses_all_cores():
+    d = _run(["--steps", "2", "--warmup", "1"], 63)
+    assert d["impl"] == "reference"
+    assert d["metric"] == "unknowns/sec per V-cycle (fp64)" and d["unit"] == "unknowns/s"
+    assert d["higher_is_better"] is True and d["value"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["value"] == d["value"]
+    assert cb["cores"] == max(1, min(os.cpu_count() or 1, 32))
+    assert d["e2e"] == {"value": d["value"], "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"].startswith("c2:") and d["config"]["sample_n"] == 63
+
+
+def test_reference_arm_other_ranks_exit_without_work():
+    env = dict(os.environ, MGB_CPU_SAMPLE_N="63", RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
+                       capture_output=True, text=True, env=env, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip() == ""
