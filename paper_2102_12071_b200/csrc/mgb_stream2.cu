@@ -44,9 +44,16 @@ namespace {
 #define MGB_S2T 128
 #endif
 constexpr int T2 = MGB_S2T;       // widest strip: threads per CTA (column pairs)
+#ifndef MGB_S2DIST
+#define MGB_S2DIST 5
+#endif
+#ifndef MGB_S2PDF
+#define MGB_S2PDF 16
+#endif
 constexpr int PD = 8;             // prefetch ring depth (rows) for u (power of two)
-constexpr int PDF = 16;           // ring depth for f: rows t-10 .. t+DIST
-constexpr int DIST = 5;           // prefetch distance (rows ahead)
+constexpr int PDF = MGB_S2PDF;    // ring depth for f: rows t-10 .. t+DIST
+constexpr int DIST = MGB_S2DIST;  // prefetch distance (rows ahead)
+static_assert(PDF >= 11 + DIST && PD >= DIST + 1, "ring depths");
 #ifndef MGB_S2MINB
 #define MGB_S2MINB 2
 #endif
