@@ -131,7 +131,22 @@ __global__ void __launch_bounds__(TP<NSW, RES, PRO, T>::NT) k_tile(StreamArgs a)
   for (int k = 1; k <= S; ++k) {
     const int lo = k, wk = W - 2 * k;
     const bool res_stage = k & 1;
-    const double* src = res_stage ? U : R;  // the stage's input field
+    // zero start without a mask: r = f - A 0 = f is F itself (zero outside the grid),
+    // so stage 1 only accumulates the history norm and stage 2 reads F
+    constexpr bool ZF = ZU && !MSK;
+    if (ZF && k == 1) {
+      if (NORM) {
+        for (int q = tid; q < wk * wk; q += NT) {
+          const int li = lo + q / wk, lj = lo + q - (q / wk) * wk;
+          const int i = gi0 + li, j = gj0 + lj;
+          const bool in = (unsigned)i < (unsigned)g.rows && (unsigned)j < (unsigned)g.cols;
+          const bool own = in && li >= S && li < S + T && lj >= S && lj < S + T;
+          if (own) acc = fma(F[li * W + lj], F[li * W + lj], acc);
+        }
+      }
+      continue;
+    }
+    const double* src = res_stage ? U : ((ZF && k == 2) ? F : R);  // the stage's input field
     const Op& op = res_stage ? a.A : a.K;
     for (int q = tid; q < wk * wk; q += NT) {
       const int li = lo + q / wk, lj = lo + q - (q / wk) * wk;
