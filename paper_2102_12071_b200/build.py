@@ -28,8 +28,13 @@ def nvcc_path() -> str:
 
 
 def flags():
-    # -fmad=false: no multiply-add contraction, so every a + w*u is rounded like
-    # NumPy's elementwise evaluation (bit-identical stencil/transfer/RAP results).
+    # -fmad=false: no implicit multiply-add contraction, so the stateless ops
+    # (k_apply, k_restrict, k_prolong, k_galerkin, the conv-smoother layers) round
+    # every a + w*u like NumPy's elementwise evaluation and are bit-identical to the
+    # reference.  The fused cycle passes call fma() explicitly (mgb_dot.h,
+    # mgb_stream2.cu), which -fmad=false does not suppress: they are bitwise equal
+    # to each other (stream == tile == DD) and agree with the reference to
+    # rounding (histories and u within 1e-10 relative).
     return ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
             "-Xcompiler", "-fvisibility=hidden", "-cudart", "static", "-I", os.path.join(ROOT, "include")]
 

@@ -1589,6 +1589,22 @@ extern "C" int mgb_run_cycles(const mgb_hier* h, mgb_work* w, const double* f_de
   return launch_graph(w, key, S(stream));
 }
 
+// History staging of the host-buffer calls: hh (and hh2, the second staging set
+// of the pipelined call) always share one capacity hh_cap >= nh; growing it
+// reallocates both, so neither call can launch a graph whose history writes
+// exceed the buffer (graphs are keyed on the buffer pointer).
+static int ensure_hist(mgb_work* w, int64_t nh, bool second) {
+  if (nh > w->hh_cap) {
+    dfree(w->hh);
+    dfree(w->hh2);
+    w->hh_cap = 0;
+    MGB_CUDA_TRY(dalloc(&w->hh, (size_t)nh));
+    w->hh_cap = nh;
+  }
+  if (second && !w->hh2) MGB_CUDA_TRY(dalloc(&w->hh2, (size_t)w->hh_cap));
+  return MGB_OK;
+}
+
 extern "C" int mgb_run_cycles_host(const mgb_hier* h, mgb_work* w, const double* f_host, double* u_host,
                                    int nu1, int nu2, int cycles, int u_zero, double* history_host,
                                    void* stream) {
@@ -1602,11 +1618,7 @@ extern "C" int mgb_run_cycles_host(const mgb_hier* h, mgb_work* w, const double*
   if (!w->hf) MGB_CUDA_TRY(dalloc(&w->hf, cnt));
   if (!w->hu) MGB_CUDA_TRY(dalloc(&w->hu, cnt));
   const int64_t nh = (int64_t)h->batch * (cycles + 1);
-  if (nh > w->hh_cap) {
-    dfree(w->hh);
-    MGB_CUDA_TRY(dalloc(&w->hh, (size_t)nh));
-    w->hh_cap = nh;
-  }
+  if (int st = ensure_hist(w, nh, false)) return st;
   MGB_CUDA_TRY(cudaMemcpyAsync(w->hf, f_host, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
   if (!u_zero) MGB_CUDA_TRY(cudaMemcpyAsync(w->hu, u_host, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
   GraphKey key{w->hf, w->hu, nu1, nu2, cycles, u_zero ? 1 : 0, 0, w->hh};
@@ -1638,13 +1650,7 @@ extern "C" int mgb_run_cycles_host_many(const mgb_hier* h, mgb_work* w, int coun
   if (!w->hu) MGB_CUDA_TRY(dalloc(&w->hu, cnt));
   if (!w->hf2) MGB_CUDA_TRY(dalloc(&w->hf2, cnt));
   if (!w->hu2) MGB_CUDA_TRY(dalloc(&w->hu2, cnt));
-  if (nh > w->hh_cap) {
-    dfree(w->hh);
-    dfree(w->hh2);
-    MGB_CUDA_TRY(dalloc(&w->hh, (size_t)nh));
-    w->hh_cap = nh;
-  }
-  if (!w->hh2) MGB_CUDA_TRY(dalloc(&w->hh2, (size_t)w->hh_cap));
+  if (int st = ensure_hist(w, nh, true)) return st;
   if (!w->cin) MGB_CUDA_TRY(cudaStreamCreateWithFlags(&w->cin, cudaStreamNonBlocking));
   if (!w->cout) MGB_CUDA_TRY(cudaStreamCreateWithFlags(&w->cout, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b)

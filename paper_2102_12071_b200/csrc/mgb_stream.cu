@@ -511,17 +511,24 @@ static int choose_seg(const Grid& g, int nsw, bool res, int occ) {
 
 template <typename KF>
 static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks) {
-  static thread_local std::vector<std::pair<const void*, int>> occ_cache;
+  // the >48 KB shared-memory attribute and the occupancy are per device
+  struct Occ {
+    const void* k;
+    int dev, occ;
+  };
+  static thread_local std::vector<Occ> occ_cache;
   const size_t smem = stream_smem(nsw, res);
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
   int occ = -1;
   for (auto& e : occ_cache)
-    if (e.first == (const void*)kern) occ = e.second;
+    if (e.k == (const void*)kern && e.dev == dev) occ = e.occ;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, SWT, smem);
     if (e != cudaSuccess) return e;
-    occ_cache.push_back({(const void*)kern, occ});
+    occ_cache.push_back({(const void*)kern, dev, occ});
   }
   static const int force_seg = getenv("MGB_SEG") ? atoi(getenv("MGB_SEG")) : 0;  // experiments only
   if (a.own1 <= 0) {

@@ -728,14 +728,17 @@ template <typename KF>
 static cudaError_t run_k2(KF kern, int nsw, bool res, bool pro, StreamArgs a, int* nblocks) {
   struct Occ {
     const void* k;
-    int tw, occ;
+    int dev, tw, occ;
   };
+  // the >48 KB shared-memory attribute and the occupancy are per device
   static thread_local std::vector<Occ> occ_cache;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
   const int tw = a.ci_valid ? T2 : choose_tw(a.g.cols, nsw);  // CM 2 kernels assume T2
   const size_t smem = stream2_smem(nsw, res, pro, tw);
   int occ = -1;
   for (auto& e : occ_cache)
-    if (e.k == (const void*)kern && e.tw == tw) occ = e.occ;
+    if (e.k == (const void*)kern && e.dev == dev && e.tw == tw) occ = e.occ;
   if (occ < 0) {
     // the attribute is sized for the widest strip once per kernel
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -743,7 +746,7 @@ static cudaError_t run_k2(KF kern, int nsw, bool res, bool pro, StreamArgs a, in
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, tw, smem);
     if (e != cudaSuccess) return e;
-    occ_cache.push_back({(const void*)kern, tw, occ});
+    occ_cache.push_back({(const void*)kern, dev, tw, occ});
   }
   if (a.own1 <= 0) {
     a.own0 = 0;

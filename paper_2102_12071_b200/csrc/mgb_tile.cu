@@ -19,6 +19,7 @@
 // Reference: v_cycle hierarchy.py:96-111 with RepeatedSmoother cli.py:365-377,
 // apply_stencil grid.py:216-226, inferred_apply smoothers.py:325-343, restrict
 // transfer.py:108-121, prolong transfer.py:124-147, history hierarchy.py:129-141.
+#include <atomic>
 #include <algorithm>
 #include <cstdlib>
 
@@ -238,11 +239,14 @@ template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool CLS, bool MSK, i
 cudaError_t run_tile(const StreamArgs& a, int* nblocks) {
   auto kern = k_tile<NSW, RES, PRO, NORM, ZU, CLS, MSK, T>;
   constexpr size_t smem = tile_smem<NSW, RES, PRO, T>();
-  static bool attr = false;  // per instantiation
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};  // per instantiation: one bit per device set up
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.fetch_or(bit, std::memory_order_acq_rel);
   }
   const dim3 grid((a.g.cols + T - 1) / T, (a.g.rows + T - 1) / T, a.g.batch);
   if (nblocks) *nblocks = (int)(grid.x * grid.y);

@@ -275,15 +275,42 @@ class MultigridHierarchy:
         self._installed[l] = sm
 
     # -- device-resident entry points (torch CUDA tensors) -------------------
+    def _check_dev(self, x, name: str, count: int | None = None):
+        """The C-ABI takes raw pointers: refuse anything but a C-contiguous fp64
+        CUDA tensor on this hierarchy's device holding exactly `count` values
+        (default: one level-0 grid function per problem; histories: at least)."""
+        t = dv.torch()
+        if not isinstance(x, t.Tensor):
+            raise ContractError(f"{name} must be a CUDA tensor")
+        if x.dtype != t.float64:
+            raise ContractError(f"{name} must be float64, got {x.dtype}")
+        if not x.is_cuda or x.device.index != self.device:
+            raise ContractError(f"{name} must live on cuda:{self.device}, got {x.device}")
+        if not x.is_contiguous():
+            raise ContractError(f"{name} must be contiguous")
+        spec = self.levels[0].spec
+        if count is None:
+            want = self.batch * spec.rows * spec.cols
+            shapes = [(self.batch, spec.rows, spec.cols)] + ([(spec.rows, spec.cols)] if self.batch == 1 else [])
+            if x.numel() != want or tuple(x.shape) not in shapes:
+                raise ContractError(f"{name} has shape {tuple(x.shape)}, expected {shapes[0]}")
+        elif x.numel() < count:
+            raise ContractError(f"{name} holds {x.numel()} values, needs {count}")
+
     def run_cycles(self, f, u, cycles: int, nu1: int | None = None, nu2: int | None = None,
                    history=None, u_zero: bool = False):
         """Fixed-count V(nu1, nu2) loop entirely on the device: f, u are
         (batch, rows, cols) or (rows, cols) fp64 CUDA tensors; returns the
         (batch, cycles + 1) relative-residual history tensor (no host sync)."""
         nu1, nu2 = self._sweeps(nu1, nu2)
+        if cycles < 0:
+            raise ConfigError("cycles must be non-negative")
         t = dv.torch()
+        self._check_dev(f, "f")
+        self._check_dev(u, "u")
         if history is None:
             history = t.empty((self.batch, cycles + 1), dtype=t.float64, device=f.device)
+        self._check_dev(history, "history", self.batch * (cycles + 1))
         w = self.acquire_work()
         try:
             _lib.call("mgb_run_cycles", self._h, w, dv.ptr(f), dv.ptr(u), nu1, nu2, int(cycles),
@@ -292,6 +319,23 @@ class MultigridHierarchy:
         finally:
             self.release_work(w)
         return history
+
+    def _check_host(self, fs, us, hs, cycles: int):
+        if cycles < 0:
+            raise ConfigError("cycles must be non-negative")
+        spec = self.levels[0].spec
+        want = self.batch * spec.rows * spec.cols
+        if len(hs) != len(fs):
+            raise ContractError("one history buffer per solve")
+        for a in list(fs) + list(us) + list(hs):
+            if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ContractError("host buffers must be C-contiguous float64")
+        for a in list(fs) + list(us):
+            if a.size != want:
+                raise ContractError(f"host grid buffer holds {a.size} values, expected {want}")
+        for a in hs:
+            if a.size < self.batch * (cycles + 1):
+                raise ContractError(f"history buffer holds {a.size} values, needs {self.batch * (cycles + 1)}")
 
     def run_cycles_host(self, f_host: np.ndarray, u_host: np.ndarray, cycles: int, nu1: int | None = None,
                         nu2: int | None = None, history_host: np.ndarray | None = None, u_zero: bool = False,
@@ -302,9 +346,7 @@ class MultigridHierarchy:
         nu1, nu2 = self._sweeps(nu1, nu2)
         if history_host is None:
             history_host = np.empty((self.batch, cycles + 1))
-        for a in (f_host, u_host, history_host):
-            if a.dtype != np.float64 or not a.flags.c_contiguous:
-                raise ContractError("host buffers must be C-contiguous float64")
+        self._check_host([f_host], [u_host], [history_host], cycles)
         w = self.acquire_work()
         try:
             _lib.call("mgb_run_cycles_host", self._h, w, f_host.ctypes.data_as(_lib.P),
@@ -327,9 +369,7 @@ class MultigridHierarchy:
             raise ContractError("f_hosts and u_hosts differ in length")
         if history_hosts is None:
             history_hosts = [np.empty((self.batch, cycles + 1)) for _ in range(count)]
-        for a in list(f_hosts) + list(u_hosts) + list(history_hosts):
-            if a.dtype != np.float64 or not a.flags.c_contiguous:
-                raise ContractError("host buffers must be C-contiguous float64")
+        self._check_host(f_hosts, u_hosts, history_hosts, cycles)
         arr = lambda xs: (C.c_void_p * max(count, 1))(*[x.ctypes.data for x in xs])  # noqa: E731
         fp, up, hp = arr(f_hosts), arr(u_hosts), arr(history_hosts)
         w = self.acquire_work()
@@ -343,6 +383,8 @@ class MultigridHierarchy:
 
     def solve_device(self, f, u, tol: float = 1e-6, max_iter: int = 100, nu1=None, nu2=None) -> SolveReport:
         nu1, nu2 = self._sweeps(nu1, nu2)
+        self._check_dev(f, "f")
+        self._check_dev(u, "u")
         hist = np.zeros(max_iter + 1)
         nh, it, conv, secs = C.c_int(), C.c_int(), C.c_int(), C.c_double()
         w = self.acquire_work()

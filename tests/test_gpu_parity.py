@@ -195,16 +195,22 @@ def test_solve_report_contract():
 
 
 def test_solve_divergence_raises():
-    """the pi/6-trained net diverges on a pi/3 operator -> NonConvergedError."""
+    """hierarchy.py:142-144: history > 1e6 max(r0, tol) -> NonConvergedError.  An
+    over-relaxed Jacobi smoother (omega = 3 > 2) diverges deterministically; the
+    oracle (same guard) raises at the same iteration."""
     n = 63
+    A = gen.rotated_fd(n, math.pi / 3, 0.01)
     spec = mg.full_spec(n)
-    h = _equip(mg.build_hierarchy(mg.StencilField(spec, gen.rotated_fd(n, math.pi / 3, 0.01)), 5), "conv")
-    F = mg.GridFunction(spec, gen.uniform_rhs(n, 0))
-    try:
-        mg.solve(h, F, tol=1e-12, max_iter=200)
-    except mg.NonConvergedError:
-        return
-    pytest.skip("did not diverge at this size")
+    h = mg.equip_classical(mg.build_hierarchy(mg.StencilField(spec, A), 5), "jacobi", omega=3.0)
+    f = gen.uniform_rhs(n, 0)
+    with pytest.raises(mg.NonConvergedError) as ei:
+        mg.solve(h, mg.GridFunction(spec, f), tol=1e-12, max_iter=200)
+    with pytest.raises(mo.OracleError) as eo:
+        mo.solve(mo.equip_jacobi(mo.build_hierarchy(A, 5), omega=3.0), f, tol=1e-12, max_iter=200)
+    assert "NonConvergedError" in str(eo.value)
+    import re
+    it = [re.search(r"iteration (\d+)", str(e.value)) for e in (ei, eo)]
+    assert all(it) and it[0].group(1) == it[1].group(1), (str(ei.value), str(eo.value))
 
 
 def test_coarse_solve_exact():
