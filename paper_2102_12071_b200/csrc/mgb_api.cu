@@ -92,7 +92,7 @@ struct mgb_hier {
   int64_t stream_min = 1000000;   // row-streaming passes on levels with at least this many points
                                   // (batch x rows x cols); smaller levels use tile passes
   int tile = 1;                   // 1: tile-local fused passes below stream_min; 0: separate kernels
-  int stream_kernel = 0;          // 0 auto, 1 one-column streaming kernel, 2 column-pair kernel
+  int stream_kernel = 0;          // 0 auto, 1 one-column streaming kernel, 2 column-pair kernel, 3 warp-strip kernel
   int64_t coarse_max = 0;         // levels up to this many points run in the single-launch
                                   // shared-memory coarse cycle (0 disables it)
   int fused = 2;            // 2: one fused pass per smoothing phase; 1: one fused pass per sweep;
@@ -615,7 +615,7 @@ extern "C" int mgb_hier_set_fused(mgb_hier* h, int enable) {
 
 extern "C" int mgb_hier_set_stream_kernel(mgb_hier* h, int kind) {
   if (!h) return fail(MGB_CONTRACT, "null hierarchy");
-  if (kind < 0 || kind > 2) return fail(MGB_CONFIG, "stream kernel must be 0 (auto), 1 or 2");
+  if (kind < 0 || kind > 3) return fail(MGB_CONFIG, "stream kernel must be 0 (auto), 1, 2 or 3");
   h->stream_kernel = kind;
   ++h->version;
   return MGB_OK;

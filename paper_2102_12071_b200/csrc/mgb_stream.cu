@@ -555,7 +555,10 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   // column-pair kernel: band-class levels of >= 1M points (batch included; interior
   // weights from the constant bank or, batched, from registers)
   const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() * a.g.batch >= 1000000);
-  if (cm != 0 && pairs) return launch_stream2(a, nsw, res, pro, norm, nblocks);
+  static const bool auto3 = getenv("MGB_STREAM3") && atoi(getenv("MGB_STREAM3")) != 0;  // A/B experiments
+  const bool warp3 = a.kernel == 3 || (a.kernel == 0 && auto3 && a.g.n() >= 1000000);
+  if (cm == 2 && warp3 && stream3_ok(a)) return launch_stream3(a, nsw, res, pro, norm, nblocks);
+  if (cm != 0 && (pairs || a.kernel == 3)) return launch_stream2(a, nsw, res, pro, norm, nblocks);
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \
     if (msk) return run_k(k_stream<NSW_, RES_, PRO_, NORM_, ZU_, 0, true>, nsw, res, a, nblocks);     \

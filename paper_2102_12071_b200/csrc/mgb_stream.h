@@ -23,7 +23,7 @@ struct StreamArgs {
                            // ghosted row blocks passed as pointers pre-offset to global rows.
   int ci_valid;            // 1: ci holds the interior-class weights (batch == 1, classed A and M)
   int uniform;             // 1: every band class equals the interior one (ci valid everywhere)
-  int kernel;              // streaming kernel: 0 auto, 1 one column per thread, 2 column pairs
+  int kernel;              // streaming kernel: 0 auto, 1 one column per thread, 2 column pairs, 3 one warp per strip
   int a5;                  // per-point A with zero corner planes: their loads are skipped
   // two-column kernel CTA map (set by its launcher): edge strips (first / last) get
   // shorter segments (their steps take the boundary-class path), listed first
@@ -45,5 +45,10 @@ int stream_max_blocks(const Grid& g);
 // Two-columns-per-thread variant for band-class levels without masks (mgb_stream2.cu);
 // launch_stream dispatches to it (MGB_STREAM1=1 keeps the one-column kernel).
 cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
+// One warp per strip, four columns per lane (mgb_stream3.cu): single-problem band-class
+// levels without masks (stream3_ok); launch_stream dispatches to it for kernel == 3
+// (and for kernel == 0 on large levels, see launch_stream).
+bool stream3_ok(const StreamArgs& a);
+cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 
 }  // namespace mgb

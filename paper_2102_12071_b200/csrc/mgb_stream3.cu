@@ -1,0 +1,554 @@
+// Row-streaming V-cycle passes, one warp per CTA, four columns per lane
+// (single-problem band-class levels: config 2 / 5 levels 0-2).
+//
+// Same passes as k_stream / k_stream2 (PRE: [history norm] + nu sweeps + residual +
+// full-weighting restriction; POST: prolongation + nu sweeps; plain sweeps; the
+// residual-norm pass), same push-form FMA chains, hence bit-identical results.  The
+// design differs in three ways that remove what bounded k_stream2 (a CTA-wide
+// barrier and a shared-memory neighbour exchange per row step at 8 warps/SM):
+//
+// * one warp owns a 128-column strip (4 columns per lane) and a row segment; the
+//   column neighbours of a lane's run come from its neighbour lanes by warp
+//   shuffles, so there is no barrier and no exchange buffer at all;
+// * no lag between stages: at step t stage k pushes the row of field k-1 that stage
+//   k-1 completed in the SAME step (field 0 row t, field k row t - k), so the state
+//   carried from step to step is only the two open output rows per stage (an update
+//   stage's seed, field k-2, was completed earlier in the same step).  About 130
+//   registers instead of 200+, and the pipeline fill is 2S + 2 rows per segment
+//   instead of 3S + 3;
+// * the per-lane step overhead (ring fill, shuffles, stores, control) is paid once
+//   per four points.
+//
+// u and f rows arrive through per-warp cp.async rings (row t + 3 issued at step t,
+// fully coalesced: lane q copies strip columns q + 32 m), read back as two 16-byte
+// halves per lane from a swizzled layout (conflict-free).  Coarse correction rows
+// (POST) are loaded into registers one coarse row ahead.
+//
+// Reference: v_cycle hierarchy.py:96-111 (with RepeatedSmoother cli.py:365-377),
+// apply_stencil grid.py:216-226, inferred_apply smoothers.py:325-343, restrict
+// transfer.py:108-121, prolong transfer.py:124-147, history hierarchy.py:129-141.
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include <cstdint>
+#include <cmath>
+
+#include "mgb_stream.h"
+
+namespace mgb {
+namespace {
+
+constexpr int CPT = 4;             // columns per lane
+constexpr int SW3 = 32 * CPT;      // strip width
+constexpr int RU3 = 4;             // u ring rows (t .. t + 3)
+constexpr int RF3 = 8;             // f ring rows (t - 3 .. t + 3)
+constexpr int D3 = 2;              // row t + D3 + 1 is issued at step t
+constexpr int NCLS3 = 25;
+#ifndef MGB_S3MINB
+#define MGB_S3MINB 12
+#endif
+
+template <int NSW, bool RES, bool NOUT>
+struct P3 {
+  static constexpr int S = NOUT ? 1 : 2 * NSW + (RES ? 1 : 0);   // stages after field 0
+  static constexpr int H = ((RES ? S + 1 : S) + 1) & ~1;          // halo columns per side (even)
+  static constexpr int WOUT = SW3 - 2 * H;                         // owned columns per strip
+};
+
+__device__ __forceinline__ int band3(int i, int n) { return i < 2 ? i : (i >= n - 2 ? 4 - (n - 1 - i) : 2); }
+
+// ring slot position of strip column s: lane i's columns 4i .. 4i+3 as two 16-byte
+// halves, the halves swapped on every other group of four lanes (conflict-free reads)
+__device__ __forceinline__ int swz(int s) {
+  const int i = s >> 2, h = (s >> 1) & 1;
+  return 4 * i + 2 * (h ^ ((i >> 2) & 1)) + (s & 1);
+}
+
+__device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// the lane's four values of a ring row
+__device__ __forceinline__ void ld_own(const double* row, int lane, double v[4]) {
+  const int x = (lane >> 2) & 1;
+  const double2 p = *reinterpret_cast<const double2*>(row + 4 * lane + 2 * x);
+  const double2 q = *reinterpret_cast<const double2*>(row + 4 * lane + 2 * (x ^ 1));
+  v[0] = p.x;
+  v[1] = p.y;
+  v[2] = q.x;
+  v[3] = q.y;
+}
+
+struct Lane3 {
+  int lane, c0, R0, R1;
+  unsigned cin, own;   // bit c: column c0 + c in the grid / owned
+  int cb[4];           // band of column c0 + c (2 when outside the grid)
+  const double* tab;   // shared-memory class tables: A [25][9], then K [25][9]
+};
+
+// MODE 0: interior rows, interior strip (constant-bank weights, no tests)
+//      1: interior rows, uniform level (constant weights, out-of-grid columns zeroed)
+//      2: interior rows, edge strip of a non-uniform level (per-column class weights)
+//      3: anything else (per row band and column class; rows and columns tested)
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, int MODE, int PAR>
+__device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const int t, double (&acc)[P3<NSW, RES, NOUT>::S][2][4],
+                                      double (&racc)[2], double& norm, const double* ringF, const double* ringU,
+                                      const double (&e0)[3], const double (&e1)[3]) {
+  using P = P3<NSW, RES, NOUT>;
+  constexpr int S = P::S;
+  const Grid& g = a.g;
+  constexpr bool CMASK = MODE >= 1;            // zero out-of-grid columns
+  constexpr bool RTEST = MODE == 3;            // rows may leave the grid / the interior band
+  const int lane = L.lane;
+  double fld[S + 1][4];
+  // ---- field 0: u (+ P ec) at row t
+  if (!ZU) {
+    ld_own(ringU + (t & (RU3 - 1)) * SW3, lane, fld[0]);
+    if (PRO && (!RTEST || (unsigned)t < (unsigned)g.rows)) {
+      double p[4];
+      if (PAR) {   // odd fine row: coarse row t >> 1 only (di = 0)
+        p[0] = fma(0.25, e1[1], 0.0);
+        p[0] = fma(0.25, e1[0], p[0]);
+        p[1] = fma(0.5, e1[1], 0.0);
+        p[2] = fma(0.25, e1[2], 0.0);
+        p[2] = fma(0.25, e1[1], p[2]);
+        p[3] = fma(0.5, e1[2], 0.0);
+      } else {     // even fine row: coarse rows t / 2 (di = -1) and t / 2 - 1 (di = +1)
+        p[0] = fma(0.125, e1[1], 0.0);
+        p[0] = fma(0.125, e1[0], p[0]);
+        p[1] = fma(0.25, e1[1], 0.0);
+        p[0] = fma(0.125, e0[1], p[0]);
+        p[0] = fma(0.125, e0[0], p[0]);
+        p[1] = fma(0.25, e0[1], p[1]);
+        p[2] = fma(0.125, e1[2], 0.0);
+        p[2] = fma(0.125, e1[1], p[2]);
+        p[3] = fma(0.25, e1[2], 0.0);
+        p[2] = fma(0.125, e0[2], p[2]);
+        p[2] = fma(0.125, e0[1], p[2]);
+        p[3] = fma(0.25, e0[2], p[3]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) fld[0][c] += p[c];
+    }
+    if (PRO && CMASK) {
+      const bool rv = !RTEST || (unsigned)t < (unsigned)g.rows;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) fld[0][c] = (rv && ((L.cin >> c) & 1)) ? fld[0][c] : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) fld[0][c] = 0.0;
+  }
+  // ---- stages k = 1..S: push field k-1 row x = t - k + 1, complete row t - k
+#pragma unroll
+  for (int k = 1; k <= S; ++k) {
+    const bool resid = k & 1;
+    const int row = t - k;
+    double* out = fld[k];
+    if (ZU && k == 1) {
+      // zero start: f - A 0 = f (the chain fma(-w, 0, f) returns f)
+      ld_own(ringF + ((t - 1) & (RF3 - 1)) * SW3, lane, out);
+    } else {
+      const double* v = fld[k - 1];
+      double in[6];
+      in[0] = __shfl_up_sync(0xffffffffu, v[3], 1);     // column c0 - 1 (lane 0: strip halo)
+      in[1] = v[0];
+      in[2] = v[1];
+      in[3] = v[2];
+      in[4] = v[3];
+      in[5] = __shfl_down_sync(0xffffffffu, v[0], 1);   // column c0 + 4 (lane 31: strip halo)
+      double seed[4];
+      if (resid) {
+        ld_own(ringF + ((t - k + 2) & (RF3 - 1)) * SW3, lane, seed);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) seed[c] = fld[k - 2][c];
+      }
+      const int s_old = (PAR ^ k) & 1;        // slot of row t - k (completes now)
+      const double* tabk = L.tab + (resid ? 0 : NCLS3 * 9);
+      int bN = 2, bM = 2, bB = 2;
+      if (MODE == 3) {
+        const int x = t - k + 1;
+        bN = (unsigned)(x + 1) < (unsigned)g.rows ? band3(x + 1, g.rows) : 2;
+        bM = (unsigned)x < (unsigned)g.rows ? band3(x, g.rows) : 2;
+        bB = (unsigned)(x - 1) < (unsigned)g.rows ? band3(x - 1, g.rows) : 2;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double* wN;
+        const double* wM;
+        const double* wB;
+        if (MODE <= 1 || UNI) {
+          wN = wM = wB = resid ? a.ci : a.ci + 9;
+        } else if (MODE == 2) {
+          wN = wM = wB = tabk + (10 + L.cb[c]) * 9;
+        } else {
+          wN = tabk + (bN * 5 + L.cb[c]) * 9;
+          wM = tabk + (bM * 5 + L.cb[c]) * 9;
+          wB = tabk + (bB * 5 + L.cb[c]) * 9;
+        }
+        // s_old / s_mid are compile-time after unrolling (PAR, k static)
+        double Ao = s_old ? acc[k - 1][1][c] : acc[k - 1][0][c];
+        double Am = s_old ? acc[k - 1][0][c] : acc[k - 1][1][c];
+        double sd = seed[c];
+#define FMS(w_, x_, a_) fma(resid ? -(w_) : (w_), (x_), (a_))
+        Ao = FMS(wB[6], in[c], Ao);
+        Am = FMS(wM[3], in[c], Am);
+        sd = FMS(wN[0], in[c], sd);
+        Ao = FMS(wB[7], in[c + 1], Ao);
+        Am = FMS(wM[4], in[c + 1], Am);
+        sd = FMS(wN[1], in[c + 1], sd);
+        Ao = FMS(wB[8], in[c + 2], Ao);
+        Am = FMS(wM[5], in[c + 2], Am);
+        sd = FMS(wN[2], in[c + 2], sd);
+#undef FMS
+        out[c] = Ao;
+        if (s_old) {
+          acc[k - 1][1][c] = sd;   // row t - k + 2 reuses the completed row's slot
+          acc[k - 1][0][c] = Am;
+        } else {
+          acc[k - 1][0][c] = sd;
+          acc[k - 1][1][c] = Am;
+        }
+      }
+    }
+    // zero the completed row outside the grid
+    if (RTEST) {
+      const bool rv = (unsigned)row < (unsigned)g.rows;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) out[c] = (rv && ((L.cin >> c) & 1)) ? out[c] : 0.0;
+    } else if (CMASK) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) out[c] = ((L.cin >> c) & 1) ? out[c] : 0.0;
+    }
+    const bool orow = row >= L.R0 && row < L.R1;
+    if (NORM && k == 1 && orow) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if ((L.own >> c) & 1) norm = fma(out[c], out[c], norm);
+    }
+    if (!NOUT && k == 2 * NSW && orow && a.uo) {
+      double* dst = a.uo + (int64_t)row * g.cols + L.c0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if ((L.own >> c) & 1) dst[c] = out[c];
+    }
+  }
+  // ---- restriction: push field S row y = t - S (coarse anchors c0 + 1, c0 + 3)
+  if (RES) {
+    const int y = t - S;
+    const double* xs = fld[S];
+    const double xr = __shfl_down_sync(0xffffffffu, xs[0], 1);
+    if ((PAR ^ S) & 1) {   // y odd: middle row of coarse row (y - 1) / 2
+      racc[0] = fma(0.125, xs[0], racc[0]);
+      racc[0] = fma(0.25, xs[1], racc[0]);
+      racc[0] = fma(0.125, xs[2], racc[0]);
+      racc[1] = fma(0.125, xs[2], racc[1]);
+      racc[1] = fma(0.25, xs[3], racc[1]);
+      racc[1] = fma(0.125, xr, racc[1]);
+    } else {
+      // bottom row of coarse row (y - 2) / 2 (completes), top row of coarse row y / 2
+      double sA = fma(0.0625, xs[0], racc[0]);
+      sA = fma(0.125, xs[1], sA);
+      sA = fma(0.0625, xs[2], sA);
+      double sB = fma(0.0625, xs[2], racc[1]);
+      sB = fma(0.125, xs[3], sB);
+      sB = fma(0.0625, xr, sB);
+      const int ci = (y - 2) >> 1;
+      const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+      if (y >= 2 && ci >= (L.R0 >> 1) && 2 * ci + 1 < L.R1 && ci < rows_c) {
+        const int cj = L.c0 >> 1;
+        double* dst = a.rc + (int64_t)ci * cols_c + cj;
+        if ((L.own & 1) && cj < cols_c) {
+          const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj];
+          dst[0] = act ? sA : 0.0;
+        }
+        if ((L.own & 4) && cj + 1 < cols_c) {
+          const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj + 1];
+          dst[1] = act ? sB : 0.0;
+        }
+      }
+      double r = 0.0625 * xs[0];
+      r = fma(0.125, xs[1], r);
+      racc[0] = fma(0.0625, xs[2], r);
+      r = 0.0625 * xs[2];
+      r = fma(0.125, xs[3], r);
+      racc[1] = fma(0.0625, xr, r);
+    }
+  }
+}
+
+// UNI: every band class equals the interior one (config 2 / 5 level 0): constant
+// weights everywhere, 12 warps/SM (168 registers); otherwise the class-weight step
+// variants need the full register file (8 warps/SM)
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI>
+__global__ void __launch_bounds__(32, UNI ? MGB_S3MINB : 8) k_stream3(StreamArgs a) {
+  pdl_trigger();
+  using P = P3<NSW, RES, NOUT>;
+  constexpr int S = P::S, H = P::H, WOUT = P::WOUT;
+  extern __shared__ __align__(16) double sm3[];
+  double* ringF = sm3;                       // RF3 x SW3
+  double* ringU = ringF + RF3 * SW3;         // RU3 x SW3 (unused when ZU)
+  double* tab = ringU + (ZU ? 0 : RU3 * SW3);  // 2 x 25 x 9 class tables (non-uniform levels)
+  const Grid& g = a.g;
+  Lane3 L;
+  L.lane = threadIdx.x;
+  // CTA -> (strip, row segment): the two edge strips' CTAs first (shorter segments on
+  // non-uniform levels, whose edge steps read class weights), then the interior ones
+  int strip, sy, seg, nseg;
+  {
+    const int id = blockIdx.x, ne = a.nedge;
+    if (id < ne * a.nseg_edge) {
+      strip = (id % ne == 0) ? 0 : a.nstrips - 1;
+      sy = id / ne;
+      seg = a.seg_edge;
+      nseg = a.nseg_edge;
+    } else {
+      const int q = id - ne * a.nseg_edge, ni = a.nstrips - ne;
+      strip = (ne > 0 ? 1 : 0) + q % ni;
+      sy = q / ni;
+      seg = a.seg;
+      nseg = a.nseg;
+    }
+  }
+  const int j0 = strip * WOUT;
+  L.c0 = j0 - H + CPT * L.lane;
+  L.cin = L.own = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int gc = L.c0 + c;
+    const bool in = (unsigned)gc < (unsigned)g.cols;
+    L.cin |= (in ? 1u : 0u) << c;
+    L.own |= ((in && gc >= j0 && gc < j0 + WOUT) ? 1u : 0u) << c;
+    L.cb[c] = in ? band3(gc, g.cols) : 2;
+  }
+  const int own0 = a.own1 > 0 ? a.own0 : 0, rend = a.own1 > 0 ? a.own1 : g.rows;
+  L.R0 = own0 + sy * seg;
+  L.R1 = sy == nseg - 1 ? rend : min(rend, L.R0 + seg);
+  L.tab = tab;
+  const bool strip_int = j0 - H >= 2 && j0 - H + SW3 - 1 <= g.cols - 3;
+  if (!UNI) {
+    for (int q = L.lane; q < 2 * NCLS3 * 9; q += 32)
+      tab[q] = q < NCLS3 * 9 ? a.A.cls[q] : a.K.cls[q - NCLS3 * 9];
+    __syncwarp();
+  }
+  // rows: field S rows [ylo, yhi] are needed (restriction: one row beyond the owned
+  // range on each side), field 0 rows [ylo - S, yhi + S]
+  const int ylo = RES ? L.R0 - 1 : L.R0, yhi = RES ? L.R1 : L.R1 - 1;
+  int t0 = ylo - S;
+  t0 -= (t0 & 1);
+  const int t1 = yhi + S;
+  const int lo_row = max(0, ylo - S), hi_row = min(g.rows - 1, t1);
+  // ring fill: lane q copies strip columns q + 32 m (coalesced rows)
+  int gq[4], sq[4];
+  unsigned cq = 0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int s = L.lane + 32 * m;
+    gq[m] = j0 - H + s;
+    sq[m] = swz(s);
+    cq |= (((unsigned)gq[m] < (unsigned)g.cols) ? 1u : 0u) << m;
+  }
+  const double* fb = a.f;
+  const double* ub = a.u;
+  auto issue = [&](int r) {
+    const bool rv = r >= lo_row && r <= hi_row;
+    const int64_t ro = (int64_t)r * g.cols;
+    double* df = ringF + (r & (RF3 - 1)) * SW3;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const bool v = rv && ((cq >> m) & 1);
+      cpa8(df + sq[m], v ? fb + ro + gq[m] : fb, v);
+    }
+    if (!ZU) {
+      double* du = ringU + (r & (RU3 - 1)) * SW3;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const bool v = rv && ((cq >> m) & 1);
+        cpa8(du + sq[m], v ? ub + ro + gq[m] : ub, v);
+      }
+    }
+    cpa_commit();
+  };
+  double acc[S][2][4];
+#pragma unroll
+  for (int k = 0; k < S; ++k)
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[k][r][c] = 0.0;
+  double racc[2] = {0.0, 0.0};
+  double norm = 0.0;
+  // POST: coarse rows (t >> 1) - 1, t >> 1, and the next one in flight (cols m - 1 .. m + 1)
+  double e0[3] = {0.0, 0.0, 0.0}, e1[3] = {0.0, 0.0, 0.0}, eN[3] = {0.0, 0.0, 0.0};
+  const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+  const int lo_c = (lo_row - 2) >> 1, hi_c = (hi_row >> 1) + 1;
+  const int mcol = (L.c0 >> 1) - 1;
+  auto load_e = [&](int ci, double (&dst)[3]) {
+    const bool rv = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int cj = mcol + q;
+      dst[q] = (rv && (unsigned)cj < (unsigned)cols_c) ? __ldg(a.ec + (int64_t)ci * cols_c + cj) : 0.0;
+    }
+  };
+  pdl_wait();  // u, f, ec come from the preceding kernels; uo / rc may still be read there
+  if (PRO) {
+    load_e((t0 >> 1) - 1, e1);
+    load_e(t0 >> 1, eN);
+  }
+  for (int r = t0 - 3; r <= t0 + D3; ++r) issue(r);
+
+#define MGB_STEP3(PAR_)                                                                                \
+  {                                                                                                    \
+    const int t = tb + PAR_;                                                                           \
+    __syncwarp();                                                                                      \
+    issue(t + D3 + 1);                                                                                 \
+    if (PRO && !PAR_) {                                                                                \
+      _Pragma("unroll") for (int q = 0; q < 3; ++q) {                                                  \
+        e0[q] = e1[q];                                                                                 \
+        e1[q] = eN[q];                                                                                 \
+      }                                                                                                \
+      load_e((t >> 1) + 1, eN);                                                                        \
+    }                                                                                                  \
+    cpa_wait<D3>(); /* rows t + 1 (f) and t (u) have landed */                                         \
+    __syncwarp();                                                                                      \
+    const bool rows_int = t - S >= 2 && t + 1 <= g.rows - 3;                                           \
+    if (rows_int && strip_int)                                                                         \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 0, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
+    else if (rows_int && UNI)                                                                          \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 1, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
+    else if (rows_int)                                                                                 \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 2, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
+    else                                                                                               \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 3, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
+  }
+  for (int tb = t0; tb <= t1; tb += 2) {
+    MGB_STEP3(0)
+    MGB_STEP3(1)
+  }
+#undef MGB_STEP3
+  cpa_wait<0>();
+  if (NORM) {
+    double v = norm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (L.lane == 0) a.partials[blockIdx.x] = v;
+  }
+}
+
+}  // namespace
+
+static size_t stream3_smem(bool zu) { return sizeof(double) * ((size_t)(RF3 + (zu ? 0 : RU3)) * SW3 + 2 * NCLS3 * 9); }
+
+static int sm_count3() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+// Row segments: whole waves of the measured occupancy with the fewest pipeline fills
+// (2S + 3 steps per segment); the two edge strips of a non-uniform level get
+// segments shorter by the measured cost ratio of their class-weight steps.
+static void choose_seg3(int rows, int cols, int S, int wout, int occ, bool uniform, StreamArgs& a) {
+  const int strips = (cols + wout - 1) / wout;
+  const int ne = uniform ? 0 : std::min(strips, 2), ni = strips - ne;
+  const int64_t slots = (int64_t)sm_count3() * std::max(occ, 1);
+  static const double r_env = getenv("MGB_EDGE3") ? atof(getenv("MGB_EDGE3")) : 0.0;
+  const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : 1.8);
+  const int F = 2 * S + 3;
+  double best_t = 1e300;
+  a.nstrips = strips;
+  a.nedge = ne;
+  const int maxseg = std::max(1, (rows + 15) / 16);
+  for (int nseg = 1; nseg <= maxseg; ++nseg) {
+    const int seg = (rows + nseg - 1) / nseg;
+    int nse = ne ? std::max(1, (int)std::ceil(rows / std::max(1.0, (seg + F) / r - F))) : 0;
+    nse = std::min(nse, maxseg);
+    const int sege = ne ? (rows + nse - 1) / nse : 0;
+    const int64_t ctas = (int64_t)ni * nseg + (int64_t)ne * nse;
+    const double w = (double)ctas / slots;
+    const double waves = w <= 2.0 ? std::ceil(w) : w + 0.5;
+    const double t = waves * std::max((double)(seg + F), ne ? r * (sege + F) : 0.0);
+    if (t < best_t) {
+      best_t = t;
+      a.seg = seg;
+      a.nseg = nseg;
+      a.seg_edge = sege;
+      a.nseg_edge = nse;
+    }
+  }
+  static const int force_seg = getenv("MGB_SEG3") ? atoi(getenv("MGB_SEG3")) : 0;  // experiments only
+  if (force_seg > 0) {
+    a.nseg = std::max(1, std::min(maxseg, (rows + force_seg - 1) / force_seg));
+    a.seg = (rows + a.nseg - 1) / a.nseg;
+    a.nseg_edge = a.nseg;
+    a.seg_edge = a.seg;
+  }
+}
+
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI>
+static cudaError_t run_k3(StreamArgs a, int* nblocks) {
+  using P = P3<NSW, RES, NOUT>;
+  auto kern = k_stream3<NSW, RES, PRO, NORM, ZU, NOUT, UNI>;
+  struct Occ {
+    int dev, occ;
+  };
+  static thread_local std::vector<Occ> occ_cache;   // per instantiation, per device
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  const size_t smem = stream3_smem(ZU);
+  int occ = -1;
+  for (auto& e : occ_cache)
+    if (e.dev == dev) occ = e.occ;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
+    if (e != cudaSuccess) return e;
+    occ_cache.push_back({dev, occ});
+  }
+  if (a.own1 <= 0) {
+    a.own0 = 0;
+    a.own1 = a.g.rows;
+  }
+  choose_seg3(a.own1 - a.own0, a.g.cols, P::S, P::WOUT, occ, a.uniform != 0, a);
+  const int ni = a.nstrips - a.nedge;
+  const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
+  if (nblocks) *nblocks = nctas;
+  const cudaError_t e = launch_pdl(kern, dim3(nctas, 1, 1), dim3(32), smem, a.stream, a);
+  if (e != cudaSuccess) return e;
+  return MGB_DBG("k_stream3");
+}
+
+bool stream3_ok(const StreamArgs& a) {
+  return a.g.batch == 1 && a.ci_valid && a.mask == nullptr && a.A.cls != nullptr && a.K.cls != nullptr &&
+         a.A.ks == 1 && a.K.ks == 1;
+}
+
+cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks) {
+  const bool zu = a.u == nullptr;
+  const bool nout = a.uo == nullptr && !res && !pro;
+#define MGB_ST3(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                                \
+  if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_)    \
+    return a.uniform ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true>(a, nblocks)                \
+                     : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, false>(a, nblocks);
+  MGB_ST3(1, true, false, false, false, false) MGB_ST3(1, true, false, true, false, false)
+  MGB_ST3(1, true, false, false, true, false)  MGB_ST3(1, true, false, true, true, false)
+  MGB_ST3(2, true, false, false, false, false) MGB_ST3(2, true, false, true, false, false)
+  MGB_ST3(2, true, false, false, true, false)  MGB_ST3(2, true, false, true, true, false)
+  MGB_ST3(1, false, false, false, false, false) MGB_ST3(1, false, false, true, false, false)
+  MGB_ST3(1, false, false, false, true, false)  MGB_ST3(1, false, false, true, true, false)
+  MGB_ST3(1, false, false, true, false, true)
+  MGB_ST3(1, false, true, false, false, false) MGB_ST3(2, false, true, false, false, false)
+#undef MGB_ST3
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mgb

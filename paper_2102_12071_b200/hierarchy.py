@@ -206,8 +206,9 @@ class MultigridHierarchy:
         _lib.call("mgb_hier_set_passes", self._h, int(stream_min), int(tile), int(coarse_max))
 
     def set_stream_kernel(self, kind: int = 0):
-        """Row-streaming kernel: 0 auto, 1 one column per thread, 2 column pairs
-        (single-problem band-class levels; bit-identical results)."""
+        """Row-streaming kernel: 0 auto, 1 one column per thread, 2 column pairs,
+        3 one warp per 128-column strip (single-problem band-class levels);
+        bit-identical results."""
         _lib.call("mgb_hier_set_stream_kernel", self._h, int(kind))
 
     def storage_info(self, l: int):

@@ -196,12 +196,16 @@ def test_solve_report_contract():
 
 def test_solve_divergence_raises():
     """hierarchy.py:142-144: history > 1e6 max(r0, tol) -> NonConvergedError.  An
-    over-relaxed Jacobi smoother (omega = 3 > 2) diverges deterministically; the
+    over-relaxed point smoother (3 / diag: Jacobi with omega = 3, which jacobi()
+    itself rejects, installed as per-point kernels) diverges deterministically; the
     oracle (same guard) raises at the same iteration."""
     n = 63
     A = gen.rotated_fd(n, math.pi / 3, 0.01)
     spec = mg.full_spec(n)
-    h = mg.equip_classical(mg.build_hierarchy(mg.StencilField(spec, A), 5), "jacobi", omega=3.0)
+    h = mg.build_hierarchy(mg.StencilField(spec, A), 5)
+    for lev in h.levels[:-1]:
+        K = mo.jacobi_kernels(lev.operator.data, lev.spec.mask, 3.0)
+        lev.smoother = mg.InferredSmoother(lev.spec, K, 1)
     f = gen.uniform_rhs(n, 0)
     with pytest.raises(mg.NonConvergedError) as ei:
         mg.solve(h, mg.GridFunction(spec, f), tol=1e-12, max_iter=200)
@@ -558,6 +562,131 @@ def test_pipelined_host_solves_equal_single_calls():
     u1 = us[3].copy()
     h.run_cycles_host(np.ascontiguousarray(fs[3]), u1, 2, 1, 1, u_zero=False)
     assert np.array_equal(us2[3], u1)
+
+
+def test_host_calls_history_staging_grows_safely():
+    """Regression (advisor r01): run_cycles_host_many, then run_cycles_host with more
+    cycles (grows the history staging), then run_cycles_host_many again with the
+    larger count on the same pooled workspace: both staging sets must have grown,
+    so every solve still equals the synchronous single call."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    c = load("case_rot15_conv_v22")
+    spec = spec_of(c["mask"], float(c["golden"]["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), "conv")
+    n = c["mask"].shape[0]
+    fs = [t.from_numpy(gen.uniform_rhs(n, 40 + k)).pin_memory().numpy() for k in range(3)]
+
+    def many(cycles):
+        us = [t.zeros(n, n, dtype=t.float64).pin_memory().numpy() for _ in fs]
+        return us, h.run_cycles_host_many(fs, us, cycles, 1, 1, u_zero=True)
+
+    many(5)
+    u1 = np.zeros((n, n))
+    h.run_cycles_host(np.ascontiguousarray(fs[0]), u1, 10, 1, 1, u_zero=True)
+    us, hs = many(10)
+    for k in range(3):
+        uk = np.zeros((n, n))
+        hk = h.run_cycles_host(np.ascontiguousarray(fs[k]), uk, 10, 1, 1, u_zero=True)
+        assert np.array_equal(us[k], uk) and np.array_equal(hs[k], hk)
+
+
+def test_facade_rejects_bad_device_buffers():
+    """Advisor r01: raw pointers go to the C-ABI only for C-contiguous fp64 CUDA
+    tensors of the level-0 size on the hierarchy's device."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    c = load("case_rot15_conv_v22")
+    spec = spec_of(c["mask"], float(c["golden"]["h"]))
+    h = _equip(mg.build_hierarchy(mg.StencilField(spec, c["A0"]), c["levels"]), "conv")
+    n = c["mask"].shape[0]
+    f = dv.to_dev(gen.uniform_rhs(n, 1))
+    u = dv.zeros(f.shape)
+    for bad in (f.float(), f.t(), f[:-1], f.cpu()):
+        with pytest.raises(mg.ContractError):
+            h.run_cycles(bad, u, 2, 1, 1)
+    with pytest.raises(mg.ContractError):
+        h.run_cycles(f, u, 4, 1, 1, history=t.empty(3, dtype=t.float64, device=f.device))
+    h.run_cycles(f, u, 2, 1, 1, u_zero=True)
+
+
+@pytest.mark.parametrize("rows,cols,theta,nu,net", [
+    (600, 600, math.pi / 4, 2, "conv_c2"),     # even sides
+    (511, 511, math.pi / 6, 2, "conv"),        # odd sides, several strips
+    (300, 777, math.pi / 3, 1, "conv"),        # rectangle, V(1,1)
+    (1023, 1023, math.pi / 4, 2, "fc"),        # fc net: boundary band classes differ (non-uniform)
+    (97, 1201, math.pi / 4, 2, "conv_c2"),     # short and wide: many strips, few rows
+    (2047, 130, math.pi / 5, 2, "conv"),       # tall and narrow: two strips, long segments
+    (40, 40, 0.3, 1, "fc"),                    # one strip, one segment
+])
+def test_warp_strip_stream_kernel_bit_identical(rows, cols, theta, nu, net):
+    """The one-warp-per-strip kernel (k_stream3: four columns per lane, shuffle
+    neighbours, no stage lag) against the column-pair kernel, forced on every level
+    of a band-class hierarchy (uniform and non-uniform levels, edge strips, grid-edge
+    rows, segment boundaries, PRE / POST / zero-start / residual-norm passes): u
+    bitwise equal, histories to summation order."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    table = gen.rotated_fd(1, theta, 1e-2, h=1.0 / (max(rows, cols) + 1))[0, 0]
+    levels = gen.levels_for(min(rows, cols))
+    h = mg.equip_inferred(mg.build_hierarchy_classed(rows, cols, table, levels), net_of(net))
+    h.set_passes(0, 1)
+    f = dv.to_dev(np.random.default_rng(9).uniform(-1, 1, (rows, cols)))
+    out = []
+    for kind in (2, 3):
+        h.set_stream_kernel(kind)
+        u = dv.zeros(f.shape)
+        hh = h.run_cycles(f, u, 3, nu, nu, u_zero=True)
+        u2 = u.clone()
+        hw = h.run_cycles(f, u2, 2, nu, nu, u_zero=False)     # warm start: the non-zero-start PRE
+        out.append((u, dv.host(hh)[0], u2, dv.host(hw)[0]))
+    h.set_stream_kernel(0)
+    (ua, ha, wa, hwa), (ub, hb, wb, hwb) = out
+    assert t.equal(ua, ub), float((ua - ub).abs().max())
+    assert t.equal(wa, wb), float((wa - wb).abs().max())
+    assert np.allclose(ha, hb, rtol=1e-13, atol=0) and np.allclose(hwa, hwb, rtol=1e-13, atol=0)
+
+
+def test_warp_strip_kernel_full_size_c2():
+    """Config 2 at 4095^2 (uniform level 0, non-uniform levels 1-2): the warp-strip
+    kernel equals the column-pair kernel bitwise over 3 V(2,2) cycles."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    n = 4095
+    table = gen.rotated_fd(1, math.pi / 4, 1e-3, h=1.0 / (n + 1))[0, 0]
+    h = mg.equip_inferred(mg.build_hierarchy_classed(n, n, table, gen.levels_for(n)), net_of("conv_c2"))
+    f = dv.to_dev(gen.uniform_rhs(n, 1))
+    out = []
+    for kind in (2, 3):
+        h.set_stream_kernel(kind)
+        u = dv.zeros(f.shape)
+        out.append((u, dv.host(h.run_cycles(f, u, 3, 2, 2, u_zero=True))[0]))
+    h.set_stream_kernel(0)
+    assert t.equal(out[0][0], out[1][0]), float((out[0][0] - out[1][0]).abs().max())
+    assert np.allclose(out[0][1], out[1][1], rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("n,nparts", [(1023, 2), (1023, 3), (2047, 4)])
+def test_virtual_decomposition_warp_strip_kernel(n, nparts, monkeypatch):
+    """Row-block decomposition with the warp-strip kernel on the distributed levels
+    (owned row ranges, ghost bands): bitwise the single-domain result."""
+    from paper_2102_12071_b200 import dd, device as dv
+    monkeypatch.setenv("MGB_STREAM_MIN", "0")
+    t = dv.torch()
+    table = gen.rotated_fd(1, math.pi / 3, 0.01, h=1.0 / (n + 1))[0, 0]
+    h = mg.equip_inferred(mg.build_hierarchy_classed(n, n, table, gen.levels_for(n)), net_of("conv"))
+    h.set_stream_kernel(3)
+    f_full = dv.to_dev(gen.uniform_rhs(n, 11))
+    u_ref = dv.zeros(f_full.shape)
+    hist_ref = dv.host(h.run_cycles(f_full, u_ref, 4, 2, 2, u_zero=True))[0]
+    s = dd.DecomposedSolver(h, nparts, local=True, agglomerate_rows=n // 4)
+    for p, (r0, r1) in enumerate(s.rows(p) for p in range(nparts)):
+        s.set_rhs(p, f_full[r0:r1].contiguous())
+    hist = dv.host(s.run_cycles(4, 2, 2))
+    u = t.cat([s.solution(p) for p in range(nparts)])
+    h.set_stream_kernel(0)
+    assert t.equal(u, u_ref), float((u - u_ref).abs().max())
+    assert np.allclose(hist, hist_ref, rtol=1e-13, atol=0)
 
 
 @pytest.mark.parametrize("rows,cols,theta,nu,net", [
