@@ -147,6 +147,11 @@ struct mgb_work {
   int64_t hist_pinned_cap = 0;
   cudaStream_t cin = nullptr, cout = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  // padded copies of level 0 (pad_layout, mgb_stream.h) for the warp-strip passes of a
+  // run_cycles solve: f, u and the ping-pong partner; pad0 is set while such a solve is
+  // enqueued (stream_args / vcycle_rec then address level 0 through them)
+  double *pf0 = nullptr, *pu0 = nullptr, *pt0 = nullptr;
+  bool pad0 = false;
   std::vector<GraphEntry> graphs;
   int graph_version = -1;   // hierarchy version the cached graphs were captured against
   int64_t last_launches = 0;
@@ -165,6 +170,12 @@ struct mgb_work {
     dfree(hf2);
     dfree(hu2);
     dfree(hh2);
+    for (double** p : {&pf0, &pu0, &pt0})
+      if (*p) {
+        double* base = *p - pad_offset(h->lv[0].cols);
+        dfree(base);
+        *p = nullptr;
+      }
     if (hist_pinned) cudaFreeHost(hist_pinned);
     for (int b = 0; b < 2; ++b)
       for (cudaEvent_t e : {ev_in[b], ev_done[b], ev_out[b]})
@@ -1287,6 +1298,10 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   a.uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
   a.kernel = h->stream_kernel;
   a.a5 = lv.a5 && !lv.Acls;
+  if (l == 0 && w->pad0) {
+    a.ld = pad_pitch(lv.cols);
+    a.padded = 1;
+  }
   for (int o = 0; o < 9; ++o) {
     a.ci[o] = lv.hAint()[o];
     a.ci[9 + o] = lv.hKint()[o];
@@ -1380,7 +1395,7 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
     return MGB_OK;
   }
   double* cur = u;
-  double* oth = w->t[l];
+  double* oth = (l == 0 && w->pad0) ? w->pt0 : w->t[l];
   const Grid g = h->grid(l);
   const bool fuse_norm = hist && nu1 > 0 && lv.ks == 1;
   if (use_stream(h, l, nu1, nu2)) {
@@ -1422,10 +1437,46 @@ static int enqueue_vcycle(mgb_work* w, int l, const double* f, double* u, int nu
                           bool zero = false, double* hist = nullptr, int64_t hstride = 0) {
   double* res = nullptr;
   if (int st = vcycle_rec(w, l, f, u, zero, nu1, nu2, s, &res, hist, hstride)) return st;
-  if (res != u)
-    MGB_CUDA_TRY(cudaMemcpyAsync(u, res, sizeof(double) * w->h->batch * w->h->lv[l].n,
-                                 cudaMemcpyDeviceToDevice, s));
+  if (res != u) {
+    if (l == 0 && w->pad0) {   // both padded level-0 buffers: copy whole allocations (margins are zero)
+      const int cols = w->h->lv[0].cols;
+      MGB_CUDA_TRY(cudaMemcpyAsync(u - pad_offset(cols), res - pad_offset(cols),
+                                   sizeof(double) * pad_elems(w->h->lv[0].rows, cols), cudaMemcpyDeviceToDevice, s));
+    } else {
+      MGB_CUDA_TRY(cudaMemcpyAsync(u, res, sizeof(double) * w->h->batch * w->h->lv[l].n,
+                                   cudaMemcpyDeviceToDevice, s));
+    }
+  }
   return MGB_OK;
+}
+
+// Level 0 of a run_cycles solve runs on padded copies when its passes are the
+// warp-strip kernel's (single problem, uniform band classes, streamed, fused).
+static bool level0_padded(const mgb_hier* h, int nu1, int nu2) {
+  const LevelD& l0 = h->lv[0];
+  return h->batch == 1 && h->depth() > 1 && pass_kind(h, 0, nu1, nu2) == 1 && l0.ks == 1 && l0.Acls && l0.Kcls &&
+         !l0.mask && l0.conv.nl == 0 && l0.uniform() &&
+         warp_strip_selected(h->stream_kernel, l0.n, h->batch, true);
+}
+
+static int ensure_pad0(mgb_work* w) {
+  const LevelD& l0 = w->h->lv[0];
+  for (double** p : {&w->pf0, &w->pu0, &w->pt0}) {
+    if (*p) continue;
+    double* base = nullptr;
+    MGB_CUDA_TRY(dalloc(&base, (size_t)pad_elems(l0.rows, l0.cols)));
+    MGB_CUDA_TRY(cudaMemset(base, 0, sizeof(double) * pad_elems(l0.rows, l0.cols)));
+    *p = base + pad_offset(l0.cols);
+  }
+  return MGB_OK;
+}
+
+// dense <-> padded level-0 copies (2-D copies: the margins are never touched)
+static cudaError_t pad0_copy(const mgb_hier* h, double* dst, bool dst_padded, const double* src, bool src_padded,
+                             cudaStream_t s) {
+  const LevelD& l0 = h->lv[0];
+  const size_t P = sizeof(double) * pad_pitch(l0.cols), D = sizeof(double) * l0.cols;
+  return cudaMemcpy2DAsync(dst, dst_padded ? P : D, src, src_padded ? P : D, D, l0.rows, cudaMemcpyDeviceToDevice, s);
 }
 
 static int check_equipped(const mgb_hier* h) {
@@ -1474,6 +1525,8 @@ extern "C" int mgb_smooth(const mgb_hier* h, mgb_work* w, int level, const doubl
 static int coarse_first_level(const mgb_hier* h);
 
 int prepare_work(mgb_work* w) {
+  if (level0_padded(w->h, 2, 2) || level0_padded(w->h, 1, 1))
+    if (int st = ensure_pad0(w)) return st;
   for (int l = 0; l + 1 < w->h->depth(); ++l)
     if (w->h->lv[l].ks > 1 || w->h->lv[l].conv.nl > 0)
       if (int st = ensure_generic(w, l)) return st;
@@ -1482,6 +1535,38 @@ int prepare_work(mgb_work* w) {
     for (int l = lc; l < w->h->depth(); ++l)
       if (!w->r[l]) MGB_CUDA_TRY(dalloc(&w->r[l], (size_t)w->h->batch * w->h->lv[l].n));
   return MGB_OK;
+}
+
+// run_cycles (mode 0): history entry c (residual of the input of cycle c) is folded
+// into cycle c's first pre-sweep; the last entry needs its own residual pass.  When
+// level 0 runs warp-strip passes, the cycles work on padded copies of f and u (staged
+// in / out once per solve, 2 x 2 x 8 B per point: ~2 % of a 10-cycle solve).
+static int enqueue_run(mgb_work* w, const GraphKey& key, cudaStream_t cs) {
+  const mgb_hier* h = w->h;
+  const int64_t nb = h->batch * (int64_t)h->lv[0].n;
+  int st = MGB_OK;
+  if (key.u_zero && key.cycles == 0) {
+    cudaError_t e = cudaMemsetAsync(key.u, 0, sizeof(double) * nb, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "memset");
+  }
+  if (!(key.u_zero && key.cycles > 0 && pre_gives_fnorm(h, key.nu1, key.nu2)))
+    if ((st = enqueue_fnorm(w, key.f, cs))) return st;
+  const bool pad = key.cycles > 0 && level0_padded(h, key.nu1, key.nu2) && w->pf0;
+  const double* f = key.f;
+  double* u = key.u;
+  if (pad) {
+    MGB_CUDA_TRY(pad0_copy(h, w->pf0, true, key.f, false, cs));
+    if (!key.u_zero) MGB_CUDA_TRY(pad0_copy(h, w->pu0, true, key.u, false, cs));
+    f = w->pf0;
+    u = w->pu0;
+  }
+  w->pad0 = pad;
+  for (int c = 0; c < key.cycles && !st; ++c)
+    st = enqueue_vcycle(w, 0, f, u, key.nu1, key.nu2, cs, key.u_zero && c == 0, key.hist + c, key.cycles + 1);
+  if (!st) st = enqueue_resnorm(w, f, u, key.hist + key.cycles, key.cycles + 1, cs);
+  w->pad0 = false;
+  if (!st && pad) MGB_CUDA_TRY(pad0_copy(h, key.u, false, w->pu0, true, cs));
+  return st;
 }
 
 static int get_graph(mgb_work* w, const GraphKey& key, GraphEntry** out) {
@@ -1502,18 +1587,8 @@ static int get_graph(mgb_work* w, const GraphKey& key, GraphEntry** out) {
     int st = MGB_OK;
     const int64_t nb = w->h->batch * (int64_t)w->h->lv[0].n;
     if (key.mode == 0) {
-      // history entry c (residual of the input of cycle c) is folded into cycle c's
-      // first pre-sweep; the last entry needs its own residual pass
-      if (key.u_zero && key.cycles == 0) {
-        cudaError_t e = cudaMemsetAsync(key.u, 0, sizeof(double) * nb, w->cap);
-        if (e != cudaSuccess) st = cuda_fail(e, "memset");
-      }
-      if (!st && !(key.u_zero && key.cycles > 0 && pre_gives_fnorm(w->h, key.nu1, key.nu2)))
-        st = enqueue_fnorm(w, key.f, w->cap);
-      for (int c = 0; c < key.cycles && !st; ++c)
-        st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap, key.u_zero && c == 0,
-                            key.hist + c, key.cycles + 1);
-      if (!st) st = enqueue_resnorm(w, key.f, key.u, key.hist + key.cycles, key.cycles + 1, w->cap);
+      (void)nb;
+      st = enqueue_run(w, key, w->cap);
     } else {
       st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap);
       if (!st) st = enqueue_resnorm(w, key.f, key.u, w->scratch, 4, w->cap);
@@ -1545,16 +1620,8 @@ static int enqueue_key(mgb_work* w, const GraphKey& key, cudaStream_t cs) {
   int st = MGB_OK;
   const int64_t nb = w->h->batch * (int64_t)w->h->lv[0].n;
   if (key.mode == 0) {
-    if (key.u_zero && key.cycles == 0) {
-      cudaError_t e = cudaMemsetAsync(key.u, 0, sizeof(double) * nb, cs);
-      if (e != cudaSuccess) st = cuda_fail(e, "memset");
-    }
-    if (!st && !(key.u_zero && key.cycles > 0 && pre_gives_fnorm(w->h, key.nu1, key.nu2)))
-      st = enqueue_fnorm(w, key.f, cs);
-    for (int c = 0; c < key.cycles && !st; ++c)
-      st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, cs, key.u_zero && c == 0, key.hist + c,
-                          key.cycles + 1);
-    if (!st) st = enqueue_resnorm(w, key.f, key.u, key.hist + key.cycles, key.cycles + 1, cs);
+    (void)nb;
+    st = enqueue_run(w, key, cs);
   } else {
     st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, cs);
     if (!st) st = enqueue_resnorm(w, key.f, key.u, w->scratch, 4, cs);
@@ -1765,6 +1832,20 @@ extern "C" int mgb_time_pass(const mgb_hier* h, mgb_work* w, int level, int pass
   MGB_CUDA_TRY(cudaEventCreate(&e1));
   const bool stream_pass = use_stream(h, level, nu, nu);
   double* bufs[2] = {u_dev, w->t[level]};
+  // level 0 of run_cycles solves: the warp-strip passes on the padded copies
+  const bool pad = level == 0 && stream_pass && level0_padded(h, nu, nu) && w->pf0;
+  if (pad) {
+    MGB_CUDA_TRY(pad0_copy(h, w->pf0, true, f_dev, false, s));
+    MGB_CUDA_TRY(pad0_copy(h, w->pu0, true, u_dev, false, s));
+    f_dev = w->pf0;
+    bufs[0] = w->pu0;
+    bufs[1] = w->pt0;
+  }
+  struct Pad0Scope {   // level 0 addressed through the padded copies for this call only
+    mgb_work* w;
+    ~Pad0Scope() { w->pad0 = false; }
+  } pad_scope{w};
+  w->pad0 = pad;
   int st = MGB_OK;
   auto one = [&](int r) -> int {
     double* cur = bufs[r & 1];

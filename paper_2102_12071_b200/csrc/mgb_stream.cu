@@ -546,6 +546,17 @@ static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks)
   return MGB_DBG(__func__);
 }
 
+// The warp-strip kernel (mgb_stream3.cu) runs where it is forced (kernel 3) and, by
+// default, on single-problem uniform band-class levels of at least 1M points (config
+// 2 / 5 level 0); MGB_STREAM3=0 / 1 turns the default off / extends it to every
+// single-problem band-class level of that size (A/B experiments).
+bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform) {
+  static const int env = getenv("MGB_STREAM3") ? atoi(getenv("MGB_STREAM3")) : -1;
+  if (kernel == 3) return true;
+  if (kernel != 0 || batch != 1 || n < 1000000 || env == 0) return false;
+  return uniform || env == 1;
+}
+
 cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks) {
   const bool zu = a.u == nullptr;
   const bool msk = a.mask != nullptr;
@@ -555,9 +566,8 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   // column-pair kernel: band-class levels of >= 1M points (batch included; interior
   // weights from the constant bank or, batched, from registers)
   const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() * a.g.batch >= 1000000);
-  static const bool auto3 = getenv("MGB_STREAM3") && atoi(getenv("MGB_STREAM3")) != 0;  // A/B experiments
-  const bool warp3 = a.kernel == 3 || (a.kernel == 0 && auto3 && a.g.n() >= 1000000);
-  if (cm == 2 && warp3 && stream3_ok(a)) return launch_stream3(a, nsw, res, pro, norm, nblocks);
+  if (cm == 2 && warp_strip_selected(a.kernel, a.g.n(), a.g.batch, a.uniform != 0) && stream3_ok(a))
+    return launch_stream3(a, nsw, res, pro, norm, nblocks);
   if (cm != 0 && (pairs || a.kernel == 3)) return launch_stream2(a, nsw, res, pro, norm, nblocks);
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_) {                     \

@@ -32,9 +32,21 @@ struct StreamArgs {
   // boundary rows take the slow step variant
   // (the first seg_rem middle segments have one row more)
   int nstrips, nedge, seg_first, nseg, seg_rem, seg_edge, seg_edge_first, nseg_edge, seg_edge_rem;
+  // warp-strip kernel only: row pitch (elements) of f, u and uo (0: cols), and whether
+  // they use the padded level layout (pad_layout(): 16-byte aligned rows, zero margins of
+  // PAD_ROWS rows and PAD_LCOLS / >= 122 columns around the grid, margins never written)
+  int64_t ld;
+  int padded;
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
   cudaStream_t stream;
 };
+
+// Padded level layout of the warp-strip kernel: rows [-PAD_ROWS, rows + PAD_ROWS) x
+// columns [-PAD_LCOLS, pitch - PAD_LCOLS); the base pointer addresses (0, 0).
+constexpr int PAD_ROWS = 8, PAD_LCOLS = 8;
+inline int64_t pad_pitch(int cols) { return ((int64_t)PAD_LCOLS + cols + 122 + 15) / 16 * 16; }
+inline int64_t pad_elems(int rows, int cols) { return ((int64_t)rows + 2 * PAD_ROWS) * pad_pitch(cols); }
+inline int64_t pad_offset(int cols) { return (int64_t)PAD_ROWS * pad_pitch(cols) + PAD_LCOLS; }
 
 // PRE: res = true, pro = false (norm optional, u null = zero start);
 // plain sweeps: res = pro = false, nsw = 1 (norm optional);
@@ -49,6 +61,7 @@ cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, boo
 // levels without masks (stream3_ok); launch_stream dispatches to it for kernel == 3
 // (and for kernel == 0 on large levels, see launch_stream).
 bool stream3_ok(const StreamArgs& a);
+bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform);
 cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 
 }  // namespace mgb

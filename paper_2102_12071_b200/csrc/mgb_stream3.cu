@@ -40,13 +40,21 @@ namespace {
 
 constexpr int CPT = 4;             // columns per lane
 constexpr int SW3 = 32 * CPT;      // strip width
-constexpr int RU3 = 4;             // u ring rows (t .. t + 3)
-constexpr int RF3 = 8;             // f ring rows (t - 3 .. t + 3)
-constexpr int D3 = 2;              // row t + D3 + 1 is issued at step t
-constexpr int NCLS3 = 25;
-#ifndef MGB_S3MINB
-#define MGB_S3MINB 12
+#ifndef MGB_S3NR
+#define MGB_S3NR 2
 #endif
+#ifndef MGB_S3DG
+#define MGB_S3DG 2
+#endif
+#ifndef MGB_S3MINB
+#define MGB_S3MINB 8
+#endif
+constexpr int NR3 = MGB_S3NR;      // rows entering per step
+constexpr int DG3 = MGB_S3DG;      // ring groups (of NR3 rows) in flight beyond the next one
+constexpr int RU3 = 8;             // u ring rows (t .. t + NR (DG + 2) - 1)
+constexpr int RF3 = 16;            // f ring rows (t - 4 .. t + NR (DG + 2) - 1)
+static_assert(NR3 * (DG3 + 2) <= RU3 && NR3 * (DG3 + 2) + 4 <= RF3, "ring depths");
+constexpr int NCLS3 = 25;
 
 template <int NSW, bool RES, bool NOUT>
 struct P3 {
@@ -64,9 +72,15 @@ __device__ __forceinline__ int swz(int s) {
   return 4 * i + 2 * (h ^ ((i >> 2) & 1)) + (s & 1);
 }
 
-__device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+__device__ __forceinline__ void cpa8s(unsigned sa, const double* gmem, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cpa8f(unsigned sa, const double* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa16(unsigned sa, const double* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
                : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
@@ -86,211 +100,272 @@ __device__ __forceinline__ void ld_own(const double* row, int lane, double v[4])
 
 struct Lane3 {
   int lane, c0, R0, R1;
+  int64_t ld;          // row pitch of f, u, uo
   unsigned cin, own;   // bit c: column c0 + c in the grid / owned
   int cb[4];           // band of column c0 + c (2 when outside the grid)
   const double* tab;   // shared-memory class tables: A [25][9], then K [25][9]
+  int lo_c, hi_c, mcol;  // POST: coarse rows that may be read, first coarse column of the lane
 };
 
-// MODE 0: interior rows, interior strip (constant-bank weights, no tests)
-//      1: interior rows, uniform level (constant weights, out-of-grid columns zeroed)
+// POST: the lane's coarse correction values (columns m - 1 .. m + 1) of coarse row ci
+__device__ __forceinline__ void load_e3(const StreamArgs& a, const Lane3& L, int ci, double (&dst)[3]) {
+  const int rows_c = a.g.rows / 2, cols_c = a.g.cols / 2;
+  const bool rv = ci >= 0 && ci < rows_c && ci >= L.lo_c && ci <= L.hi_c;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int cj = L.mcol + q;
+    dst[q] = (rv && (unsigned)cj < (unsigned)cols_c) ? __ldg(a.ec + (int64_t)ci * cols_c + cj) : 0.0;
+  }
+}
+
+// One pipeline step: field-0 rows t .. t + NR - 1 enter; stage k completes rows
+// t - k .. t - k + NR - 1.  P0 = t mod 2 (static).
+// MODE 0: interior rows, interior strip, inside the segment (constant-bank weights, no
+//         row or column tests: only the lane-constant column ownership of outputs)
+//      1: interior rows, uniform level or interior strip (constant weights; out-of-grid
+//         columns zeroed, output rows tested against the segment)
 //      2: interior rows, edge strip of a non-uniform level (per-column class weights)
 //      3: anything else (per row band and column class; rows and columns tested)
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, int MODE, int PAR>
-__device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const int t, double (&acc)[P3<NSW, RES, NOUT>::S][2][4],
-                                      double (&racc)[2], double& norm, const double* ringF, const double* ringU,
-                                      const double (&e0)[3], const double (&e1)[3]) {
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, bool ZA, bool ALN, int NR, int MODE, int P0>
+__device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const int t,
+                                      double (&acc)[P3<NSW, RES, NOUT>::S][2][4], double (&racc)[2], double& norm,
+                                      const double* ringF, const double* ringU, double (&e0)[3], double (&e1)[3],
+                                      double (&eN)[3]) {
   using P = P3<NSW, RES, NOUT>;
   constexpr int S = P::S;
   const Grid& g = a.g;
   constexpr bool CMASK = MODE >= 1;            // zero out-of-grid columns
   constexpr bool RTEST = MODE == 3;            // rows may leave the grid / the interior band
   const int lane = L.lane;
-  double fld[S + 1][4];
-  // ---- field 0: u (+ P ec) at row t
-  if (!ZU) {
-    ld_own(ringU + (t & (RU3 - 1)) * SW3, lane, fld[0]);
-    if (PRO && (!RTEST || (unsigned)t < (unsigned)g.rows)) {
-      double p[4];
-      if (PAR) {   // odd fine row: coarse row t >> 1 only (di = 0)
-        p[0] = fma(0.25, e1[1], 0.0);
-        p[0] = fma(0.25, e1[0], p[0]);
-        p[1] = fma(0.5, e1[1], 0.0);
-        p[2] = fma(0.25, e1[2], 0.0);
-        p[2] = fma(0.25, e1[1], p[2]);
-        p[3] = fma(0.5, e1[2], 0.0);
-      } else {     // even fine row: coarse rows t / 2 (di = -1) and t / 2 - 1 (di = +1)
-        p[0] = fma(0.125, e1[1], 0.0);
-        p[0] = fma(0.125, e1[0], p[0]);
-        p[1] = fma(0.25, e1[1], 0.0);
-        p[0] = fma(0.125, e0[1], p[0]);
-        p[0] = fma(0.125, e0[0], p[0]);
-        p[1] = fma(0.25, e0[1], p[1]);
-        p[2] = fma(0.125, e1[2], 0.0);
-        p[2] = fma(0.125, e1[1], p[2]);
-        p[3] = fma(0.25, e1[2], 0.0);
-        p[2] = fma(0.125, e0[2], p[2]);
-        p[2] = fma(0.125, e0[1], p[2]);
-        p[3] = fma(0.25, e0[2], p[3]);
+  double fld[S + 1][NR][4];
+  // ---- field 0: u (+ P ec) at rows t + j
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int row = t + j;
+    const bool podd = (P0 + j) & 1;
+    if (ZU) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) fld[0][j][c] = 0.0;
+      continue;
+    }
+    ld_own(ringU + (row & (RU3 - 1)) * SW3, lane, fld[0][j]);
+    if (PRO) {
+      if (!podd) {   // coarse row row / 2 enters: rows row/2 - 1, row/2 in e0, e1; the next in flight
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          e0[q] = e1[q];
+          e1[q] = eN[q];
+        }
+        load_e3(a, L, (row >> 1) + 1, eN);
       }
+      if (!RTEST || (unsigned)row < (unsigned)g.rows) {
+        double p[4];
+        if (podd) {   // odd fine row: coarse row row >> 1 only (di = 0)
+          p[0] = fma(0.25, e1[1], 0.0);
+          p[0] = fma(0.25, e1[0], p[0]);
+          p[1] = fma(0.5, e1[1], 0.0);
+          p[2] = fma(0.25, e1[2], 0.0);
+          p[2] = fma(0.25, e1[1], p[2]);
+          p[3] = fma(0.5, e1[2], 0.0);
+        } else {      // even fine row: coarse rows row / 2 (di = -1) and row / 2 - 1 (di = +1)
+          p[0] = fma(0.125, e1[1], 0.0);
+          p[0] = fma(0.125, e1[0], p[0]);
+          p[1] = fma(0.25, e1[1], 0.0);
+          p[0] = fma(0.125, e0[1], p[0]);
+          p[0] = fma(0.125, e0[0], p[0]);
+          p[1] = fma(0.25, e0[1], p[1]);
+          p[2] = fma(0.125, e1[2], 0.0);
+          p[2] = fma(0.125, e1[1], p[2]);
+          p[3] = fma(0.25, e1[2], 0.0);
+          p[2] = fma(0.125, e0[2], p[2]);
+          p[2] = fma(0.125, e0[1], p[2]);
+          p[3] = fma(0.25, e0[2], p[3]);
+        }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) fld[0][c] += p[c];
+        for (int c = 0; c < 4; ++c) fld[0][j][c] += p[c];
+      }
+      if (CMASK) {
+        const bool rv = !RTEST || (unsigned)row < (unsigned)g.rows;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fld[0][j][c] = (rv && ((L.cin >> c) & 1)) ? fld[0][j][c] : 0.0;
+      }
     }
-    if (PRO && CMASK) {
-      const bool rv = !RTEST || (unsigned)t < (unsigned)g.rows;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) fld[0][c] = (rv && ((L.cin >> c) & 1)) ? fld[0][c] : 0.0;
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) fld[0][c] = 0.0;
   }
-  // ---- stages k = 1..S: push field k-1 row x = t - k + 1, complete row t - k
+  // ---- stages k = 1..S: push field k-1 rows t - k + 1 + j, complete rows t - k + j
 #pragma unroll
   for (int k = 1; k <= S; ++k) {
     const bool resid = k & 1;
-    const int row = t - k;
-    double* out = fld[k];
-    if (ZU && k == 1) {
-      // zero start: f - A 0 = f (the chain fma(-w, 0, f) returns f)
-      ld_own(ringF + ((t - 1) & (RF3 - 1)) * SW3, lane, out);
-    } else {
-      const double* v = fld[k - 1];
-      double in[6];
-      in[0] = __shfl_up_sync(0xffffffffu, v[3], 1);     // column c0 - 1 (lane 0: strip halo)
-      in[1] = v[0];
-      in[2] = v[1];
-      in[3] = v[2];
-      in[4] = v[3];
-      in[5] = __shfl_down_sync(0xffffffffu, v[0], 1);   // column c0 + 4 (lane 31: strip halo)
-      double seed[4];
-      if (resid) {
-        ld_own(ringF + ((t - k + 2) & (RF3 - 1)) * SW3, lane, seed);
+    const double* tabk = L.tab + (resid ? 0 : NCLS3 * 9);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int row = t - k + j;
+      double* out = fld[k][j];
+      if (ZU && k == 1) {
+        // zero start: f - A 0 = f (the chain fma(-w, 0, f) returns f)
+        ld_own(ringF + (row & (RF3 - 1)) * SW3, lane, out);
       } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) seed[c] = fld[k - 2][c];
-      }
-      const int s_old = (PAR ^ k) & 1;        // slot of row t - k (completes now)
-      const double* tabk = L.tab + (resid ? 0 : NCLS3 * 9);
-      int bN = 2, bM = 2, bB = 2;
-      if (MODE == 3) {
-        const int x = t - k + 1;
-        bN = (unsigned)(x + 1) < (unsigned)g.rows ? band3(x + 1, g.rows) : 2;
-        bM = (unsigned)x < (unsigned)g.rows ? band3(x, g.rows) : 2;
-        bB = (unsigned)(x - 1) < (unsigned)g.rows ? band3(x - 1, g.rows) : 2;
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double* wN;
-        const double* wM;
-        const double* wB;
-        if (MODE <= 1 || UNI) {
-          wN = wM = wB = resid ? a.ci : a.ci + 9;
-        } else if (MODE == 2) {
-          wN = wM = wB = tabk + (10 + L.cb[c]) * 9;
+        const double* v = fld[k - 1][j];
+        double in[6];
+        in[0] = __shfl_up_sync(0xffffffffu, v[3], 1);     // column c0 - 1 (lane 0: strip halo)
+        in[1] = v[0];
+        in[2] = v[1];
+        in[3] = v[2];
+        in[4] = v[3];
+        in[5] = __shfl_down_sync(0xffffffffu, v[0], 1);   // column c0 + 4 (lane 31: strip halo)
+        double seed[4];
+        if (resid) {
+          ld_own(ringF + ((row + 2) & (RF3 - 1)) * SW3, lane, seed);
         } else {
-          wN = tabk + (bN * 5 + L.cb[c]) * 9;
-          wM = tabk + (bM * 5 + L.cb[c]) * 9;
-          wB = tabk + (bB * 5 + L.cb[c]) * 9;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) seed[c] = fld[k - 2][j][c];
         }
-        // s_old / s_mid are compile-time after unrolling (PAR, k static)
-        double Ao = s_old ? acc[k - 1][1][c] : acc[k - 1][0][c];
-        double Am = s_old ? acc[k - 1][0][c] : acc[k - 1][1][c];
-        double sd = seed[c];
+        const int s_old = (P0 + j + k) & 1;   // slot of row t - k + j (completes now); static
+        int bN = 2, bM = 2, bB = 2;
+        if (MODE == 3) {
+          const int x = row + 1;              // the input row
+          bN = (unsigned)(x + 1) < (unsigned)g.rows ? band3(x + 1, g.rows) : 2;
+          bM = (unsigned)x < (unsigned)g.rows ? band3(x, g.rows) : 2;
+          bB = (unsigned)(x - 1) < (unsigned)g.rows ? band3(x - 1, g.rows) : 2;
+        }
+        const double* wN[4];
+        const double* wM[4];
+        const double* wB[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (MODE <= 1 || UNI) {
+            wN[c] = wM[c] = wB[c] = resid ? a.ci : a.ci + 9;
+          } else if (MODE == 2) {
+            wN[c] = wM[c] = wB[c] = tabk + (10 + L.cb[c]) * 9;
+          } else {
+            wN[c] = tabk + (bN * 5 + L.cb[c]) * 9;
+            wM[c] = tabk + (bM * 5 + L.cb[c]) * 9;
+            wB[c] = tabk + (bB * 5 + L.cb[c]) * 9;
+          }
+        }
+        double (&Ao)[4] = acc[k - 1][s_old];        // row t - k + j: its bottom terms complete it
+        double (&Am)[4] = acc[k - 1][s_old ^ 1];    // row t - k + j + 1: middle terms
 #define FMS(w_, x_, a_) fma(resid ? -(w_) : (w_), (x_), (a_))
-        Ao = FMS(wB[6], in[c], Ao);
-        Am = FMS(wM[3], in[c], Am);
-        sd = FMS(wN[0], in[c], sd);
-        Ao = FMS(wB[7], in[c + 1], Ao);
-        Am = FMS(wM[4], in[c + 1], Am);
-        sd = FMS(wN[1], in[c + 1], sd);
-        Ao = FMS(wB[8], in[c + 2], Ao);
-        Am = FMS(wM[5], in[c + 2], Am);
-        sd = FMS(wN[2], in[c + 2], sd);
+        // critical path first (the completed row feeds the next stage through shuffles),
+        // one wave of four independent chains per weight; every chain keeps
+        // stencil_dot's term order
+#pragma unroll
+        for (int o = 6; o < 9; ++o)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (!(ZA && resid && o == 6)) Ao[c] = FMS(wB[c][o], in[c + o - 6], Ao[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = Ao[c];
+#pragma unroll
+        for (int o = 3; o < 6; ++o)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) Am[c] = FMS(wM[c][o], in[c + o - 3], Am[c]);
+#pragma unroll
+        for (int o = 0; o < 3; ++o)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (!(ZA && resid && o == 2)) seed[c] = FMS(wN[c][o], in[c + o], seed[c]);
 #undef FMS
-        out[c] = Ao;
-        if (s_old) {
-          acc[k - 1][1][c] = sd;   // row t - k + 2 reuses the completed row's slot
-          acc[k - 1][0][c] = Am;
-        } else {
-          acc[k - 1][0][c] = sd;
-          acc[k - 1][1][c] = Am;
+        // row t - k + j + 2 reuses the completed row's slot
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Ao[c] = seed[c];
+      }
+      // zero the completed row outside the grid
+      if (RTEST) {
+        const bool rv = (unsigned)row < (unsigned)g.rows;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = (rv && ((L.cin >> c) & 1)) ? out[c] : 0.0;
+      } else if (CMASK) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = ((L.cin >> c) & 1) ? out[c] : 0.0;
+      }
+      // MODE 0 steps lie inside the segment (every output row owned): no row tests
+      const bool orow = MODE == 0 || (row >= L.R0 && row < L.R1);
+      if (NORM && k == 1) {
+        // branch-free: excluded points add an exact +0 (the partial sum stays >= +0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double v = (orow && ((L.own >> c) & 1)) ? out[c] : 0.0;
+          norm = fma(v, v, norm);
         }
       }
-    }
-    // zero the completed row outside the grid
-    if (RTEST) {
-      const bool rv = (unsigned)row < (unsigned)g.rows;
+      if (!NOUT && k == 2 * NSW && orow && (MODE == 0 || a.uo)) {
+        double* dst = a.uo + (int64_t)row * L.ld + L.c0;
+#ifdef MGB_S3_NOSTORE
+        if (out[0] == 1.2345e300)   // experiment builds only: (practically) no HBM writes
+#endif
+        if (ALN) {
+          // padded layout: 16-byte aligned pairs (c0 even), owned pairs whole (even bounds)
+          if (L.own & 1) *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
+          if (L.own & 4) *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
+        } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) out[c] = (rv && ((L.cin >> c) & 1)) ? out[c] : 0.0;
-    } else if (CMASK) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) out[c] = ((L.cin >> c) & 1) ? out[c] : 0.0;
-    }
-    const bool orow = row >= L.R0 && row < L.R1;
-    if (NORM && k == 1 && orow) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if ((L.own >> c) & 1) norm = fma(out[c], out[c], norm);
-    }
-    if (!NOUT && k == 2 * NSW && orow && a.uo) {
-      double* dst = a.uo + (int64_t)row * g.cols + L.c0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if ((L.own >> c) & 1) dst[c] = out[c];
+          for (int c = 0; c < 4; ++c)
+            if ((L.own >> c) & 1) dst[c] = out[c];
+        }
+      }
     }
   }
-  // ---- restriction: push field S row y = t - S (coarse anchors c0 + 1, c0 + 3)
+  // ---- restriction: push field S rows y = t - S + j (coarse anchors c0 + 1, c0 + 3)
   if (RES) {
-    const int y = t - S;
-    const double* xs = fld[S];
-    const double xr = __shfl_down_sync(0xffffffffu, xs[0], 1);
-    if ((PAR ^ S) & 1) {   // y odd: middle row of coarse row (y - 1) / 2
-      racc[0] = fma(0.125, xs[0], racc[0]);
-      racc[0] = fma(0.25, xs[1], racc[0]);
-      racc[0] = fma(0.125, xs[2], racc[0]);
-      racc[1] = fma(0.125, xs[2], racc[1]);
-      racc[1] = fma(0.25, xs[3], racc[1]);
-      racc[1] = fma(0.125, xr, racc[1]);
-    } else {
-      // bottom row of coarse row (y - 2) / 2 (completes), top row of coarse row y / 2
-      double sA = fma(0.0625, xs[0], racc[0]);
-      sA = fma(0.125, xs[1], sA);
-      sA = fma(0.0625, xs[2], sA);
-      double sB = fma(0.0625, xs[2], racc[1]);
-      sB = fma(0.125, xs[3], sB);
-      sB = fma(0.0625, xr, sB);
-      const int ci = (y - 2) >> 1;
-      const int rows_c = g.rows / 2, cols_c = g.cols / 2;
-      if (y >= 2 && ci >= (L.R0 >> 1) && 2 * ci + 1 < L.R1 && ci < rows_c) {
-        const int cj = L.c0 >> 1;
-        double* dst = a.rc + (int64_t)ci * cols_c + cj;
-        if ((L.own & 1) && cj < cols_c) {
-          const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj];
-          dst[0] = act ? sA : 0.0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int y = t - S + j;
+      const double* xs = fld[S][j];
+      const double xr = __shfl_down_sync(0xffffffffu, xs[0], 1);
+      if ((P0 + j + S) & 1) {   // y odd: middle row of coarse row (y - 1) / 2
+        racc[0] = fma(0.125, xs[0], racc[0]);
+        racc[0] = fma(0.25, xs[1], racc[0]);
+        racc[0] = fma(0.125, xs[2], racc[0]);
+        racc[1] = fma(0.125, xs[2], racc[1]);
+        racc[1] = fma(0.25, xs[3], racc[1]);
+        racc[1] = fma(0.125, xr, racc[1]);
+      } else {
+        // bottom row of coarse row (y - 2) / 2 (completes), top row of coarse row y / 2
+        double sA = fma(0.0625, xs[0], racc[0]);
+        sA = fma(0.125, xs[1], sA);
+        sA = fma(0.0625, xs[2], sA);
+        double sB = fma(0.0625, xs[2], racc[1]);
+        sB = fma(0.125, xs[3], sB);
+        sB = fma(0.0625, xr, sB);
+        const int ci = (y - 2) >> 1;
+        const int rows_c = g.rows / 2, cols_c = g.cols / 2;
+        if (MODE == 0 || (y >= 2 && ci >= (L.R0 >> 1) && 2 * ci + 1 < L.R1 && ci < rows_c)) {
+          const int cj = L.c0 >> 1;
+          double* dst = a.rc + (int64_t)ci * cols_c + cj;
+          if ((L.own & 1) && cj < cols_c) {
+            const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj];
+            dst[0] = act ? sA : 0.0;
+          }
+          if ((L.own & 4) && cj + 1 < cols_c) {
+            const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj + 1];
+            dst[1] = act ? sB : 0.0;
+          }
         }
-        if ((L.own & 4) && cj + 1 < cols_c) {
-          const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj + 1];
-          dst[1] = act ? sB : 0.0;
-        }
+        double r = 0.0625 * xs[0];
+        r = fma(0.125, xs[1], r);
+        racc[0] = fma(0.0625, xs[2], r);
+        r = 0.0625 * xs[2];
+        r = fma(0.125, xs[3], r);
+        racc[1] = fma(0.0625, xr, r);
       }
-      double r = 0.0625 * xs[0];
-      r = fma(0.125, xs[1], r);
-      racc[0] = fma(0.0625, xs[2], r);
-      r = 0.0625 * xs[2];
-      r = fma(0.125, xs[3], r);
-      racc[1] = fma(0.0625, xr, r);
     }
   }
 }
 
 // UNI: every band class equals the interior one (config 2 / 5 level 0): constant
-// weights everywhere, 12 warps/SM (168 registers); otherwise the class-weight step
-// variants need the full register file (8 warps/SM)
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI>
-__global__ void __launch_bounds__(32, UNI ? MGB_S3MINB : 8) k_stream3(StreamArgs a) {
+// weights everywhere.  NR rows enter per step (one ring group, one wait per step);
+// the register file holds 8 warps/SM at MINB 8.
+// ZA (uniform levels only): the operator's anti-diagonal corners A[-1][+1], A[+1][-1]
+// are exact zeros (the rotated finite-difference stencil, problems.py:45-52): their
+// FMAs are skipped (adding an exact zero product leaves every chain's value unchanged).
+// ALN: f, u, uo use the padded layout (16-byte copies bypassing L1, 128-bit stores, no
+// column predicates: the margins read as zeros).
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, bool ZA, bool ALN>
+__global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
   pdl_trigger();
   using P = P3<NSW, RES, NOUT>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT;
+  constexpr int NR = NR3;
   extern __shared__ __align__(16) double sm3[];
   double* ringF = sm3;                       // RF3 x SW3
   double* ringU = ringF + RF3 * SW3;         // RU3 x SW3 (unused when ZU)
@@ -331,6 +406,7 @@ __global__ void __launch_bounds__(32, UNI ? MGB_S3MINB : 8) k_stream3(StreamArgs
   L.R0 = own0 + sy * seg;
   L.R1 = sy == nseg - 1 ? rend : min(rend, L.R0 + seg);
   L.tab = tab;
+  L.ld = a.ld > 0 ? a.ld : g.cols;
   const bool strip_int = j0 - H >= 2 && j0 - H + SW3 - 1 <= g.cols - 3;
   if (!UNI) {
     for (int q = L.lane; q < 2 * NCLS3 * 9; q += 32)
@@ -338,41 +414,63 @@ __global__ void __launch_bounds__(32, UNI ? MGB_S3MINB : 8) k_stream3(StreamArgs
     __syncwarp();
   }
   // rows: field S rows [ylo, yhi] are needed (restriction: one row beyond the owned
-  // range on each side), field 0 rows [ylo - S, yhi + S]
+  // range on each side), field 0 rows [ylo - S, yhi + S]; steps start at a multiple of NR
   const int ylo = RES ? L.R0 - 1 : L.R0, yhi = RES ? L.R1 : L.R1 - 1;
   int t0 = ylo - S;
-  t0 -= (t0 & 1);
+  t0 -= (t0 & 1);   // even: static row parities (NR = 2 steps, or the two-step unroll)
   const int t1 = yhi + S;
   const int lo_row = max(0, ylo - S), hi_row = min(g.rows - 1, t1);
-  // ring fill: lane q copies strip columns q + 32 m (coalesced rows)
-  int gq[4], sq[4];
+  L.lo_c = (lo_row - 2) >> 1;
+  L.hi_c = (hi_row >> 1) + 1;
+  L.mcol = (L.c0 >> 1) - 1;
+  // ring fill: lane q copies strip columns q + 32 m (coalesced rows) to the ring
+  // positions swz(q + 32 m) = swz(q) + 32 m; rows outside [lo_row, hi_row] and columns
+  // outside the grid are zero-filled (size-0 copies).  Padded layout: lane q copies the
+  // 16-byte column pairs q and q + 32 (positions swz(2q), swz(2q + 64) = swz(2q) + 64),
+  // the margins supplying the zeros outside the grid.
+  const int colq = j0 - H + (ALN ? 2 : 1) * L.lane;
+  const unsigned sF = (unsigned)__cvta_generic_to_shared(ringF + swz((ALN ? 2 : 1) * L.lane));
+  const unsigned sU = (unsigned)__cvta_generic_to_shared(ringU + swz((ALN ? 2 : 1) * L.lane));
+  const bool cols_all = j0 - H >= 0 && j0 - H + SW3 <= g.cols;   // every strip column in the grid
   unsigned cq = 0;
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const int s = L.lane + 32 * m;
-    gq[m] = j0 - H + s;
-    sq[m] = swz(s);
-    cq |= (((unsigned)gq[m] < (unsigned)g.cols) ? 1u : 0u) << m;
-  }
+  for (int m = 0; m < 4; ++m) cq |= (((unsigned)(colq + 32 * m) < (unsigned)g.cols) ? 1u : 0u) << m;
   const double* fb = a.f;
   const double* ub = a.u;
-  auto issue = [&](int r) {
+  auto issue_row = [&](int r) {
+#ifdef MGB_S3_NOLOAD
+    return;   // experiment builds only: no HBM reads (compute-only timing)
+#endif
     const bool rv = r >= lo_row && r <= hi_row;
-    const int64_t ro = (int64_t)r * g.cols;
-    double* df = ringF + (r & (RF3 - 1)) * SW3;
+    const int64_t ro = (int64_t)r * L.ld + colq;
+    const unsigned of = sF + (unsigned)((r & (RF3 - 1)) * SW3 * 8);
+    const unsigned ou = sU + (unsigned)((r & (RU3 - 1)) * SW3 * 8);
+    if (ALN) {
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const bool v = rv && ((cq >> m) & 1);
-      cpa8(df + sq[m], v ? fb + ro + gq[m] : fb, v);
-    }
-    if (!ZU) {
-      double* du = ringU + (r & (RU3 - 1)) * SW3;
+      for (int m = 0; m < 2; ++m) {
+        cpa16(of + 512 * m, rv ? fb + ro + 64 * m : fb, rv);
+        if (!ZU) cpa16(ou + 512 * m, rv ? ub + ro + 64 * m : ub, rv);
+      }
+    } else if (rv && cols_all) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) cpa8f(of + 256 * m, fb + ro + 32 * m);
+      if (!ZU) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) cpa8f(ou + 256 * m, ub + ro + 32 * m);
+      }
+    } else {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const bool v = rv && ((cq >> m) & 1);
-        cpa8(du + sq[m], v ? ub + ro + gq[m] : ub, v);
+        cpa8s(of + 256 * m, v ? fb + ro + 32 * m : fb, v);
+        if (!ZU) cpa8s(ou + 256 * m, v ? ub + ro + 32 * m : ub, v);
       }
     }
+  };
+  // ring group s: rows s NR .. s NR + NR - 1
+  auto issue = [&](int s) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) issue_row(s * NR + j);
     cpa_commit();
   };
   double acc[S][2][4];
@@ -384,53 +482,45 @@ __global__ void __launch_bounds__(32, UNI ? MGB_S3MINB : 8) k_stream3(StreamArgs
       for (int c = 0; c < 4; ++c) acc[k][r][c] = 0.0;
   double racc[2] = {0.0, 0.0};
   double norm = 0.0;
-  // POST: coarse rows (t >> 1) - 1, t >> 1, and the next one in flight (cols m - 1 .. m + 1)
+  // POST: coarse rows (t >> 1) - 1, t >> 1 (e0, e1) and the next one in flight (eN)
   double e0[3] = {0.0, 0.0, 0.0}, e1[3] = {0.0, 0.0, 0.0}, eN[3] = {0.0, 0.0, 0.0};
-  const int rows_c = g.rows / 2, cols_c = g.cols / 2;
-  const int lo_c = (lo_row - 2) >> 1, hi_c = (hi_row >> 1) + 1;
-  const int mcol = (L.c0 >> 1) - 1;
-  auto load_e = [&](int ci, double (&dst)[3]) {
-    const bool rv = ci >= 0 && ci < rows_c && ci >= lo_c && ci <= hi_c;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int cj = mcol + q;
-      dst[q] = (rv && (unsigned)cj < (unsigned)cols_c) ? __ldg(a.ec + (int64_t)ci * cols_c + cj) : 0.0;
-    }
-  };
   pdl_wait();  // u, f, ec come from the preceding kernels; uo / rc may still be read there
   if (PRO) {
-    load_e((t0 >> 1) - 1, e1);
-    load_e(t0 >> 1, eN);
+    load_e3(a, L, (t0 >> 1) - 1, e1);
+    load_e3(a, L, t0 >> 1, eN);
   }
-  for (int r = t0 - 3; r <= t0 + D3; ++r) issue(r);
+  // groups of rows t0 - 4 .. : the residual seeds reach back to row t - 3
+  const int s0 = t0 / NR - (4 + NR - 1) / NR;
+  const int sstart = t0 / NR;
+  for (int s = s0; s <= sstart + DG3; ++s) issue(s);
 
-#define MGB_STEP3(PAR_)                                                                                \
-  {                                                                                                    \
-    const int t = tb + PAR_;                                                                           \
-    __syncwarp();                                                                                      \
-    issue(t + D3 + 1);                                                                                 \
-    if (PRO && !PAR_) {                                                                                \
-      _Pragma("unroll") for (int q = 0; q < 3; ++q) {                                                  \
-        e0[q] = e1[q];                                                                                 \
-        e1[q] = eN[q];                                                                                 \
-      }                                                                                                \
-      load_e((t >> 1) + 1, eN);                                                                        \
-    }                                                                                                  \
-    cpa_wait<D3>(); /* rows t + 1 (f) and t (u) have landed */                                         \
-    __syncwarp();                                                                                      \
-    const bool rows_int = t - S >= 2 && t + 1 <= g.rows - 3;                                           \
-    if (rows_int && strip_int)                                                                         \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 0, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
-    else if (rows_int && UNI)                                                                          \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 1, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
-    else if (rows_int)                                                                                 \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 2, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
-    else                                                                                               \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, 3, PAR_>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1); \
+#define MGB_STEP3(P0_)                                                                                       \
+  {                                                                                                          \
+    const int t = tb + (P0_) * NR;                                                                           \
+    __syncwarp();                                                                                            \
+    issue(t / NR + 1 + DG3);                                                                                 \
+    cpa_wait<DG3>(); /* f rows up to t + NR and u rows t .. t + NR - 1 have landed */                       \
+    __syncwarp();                                                                                            \
+    const bool rows_int = t - S >= 2 && t + NR <= g.rows - 3;                                                \
+    /* core: every row an output of this step touches is owned (norm, u, coarse rows) */                    \
+    const bool core = t - S - 2 >= L.R0 && t + NR <= L.R1 - 1;                                               \
+    if (rows_int && strip_int && core && (NOUT || a.uo))                                                     \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
+    else if (rows_int && (UNI || strip_int))                                                                 \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
+    else if (rows_int)                                                                                       \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 2, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
+    else                                                                                                     \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 3, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
   }
-  for (int tb = t0; tb <= t1; tb += 2) {
-    MGB_STEP3(0)
-    MGB_STEP3(1)
+  // t0 is even: with one row per step, unroll two steps so each step's parity is static
+  if (NR == 2) {
+    for (int tb = t0; tb <= t1; tb += NR) MGB_STEP3(0)
+  } else {
+    for (int tb = t0; tb <= t1; tb += 2 * NR) {
+      MGB_STEP3(0)
+      MGB_STEP3(1)
+    }
   }
 #undef MGB_STEP3
   cpa_wait<0>();
@@ -444,7 +534,9 @@ __global__ void __launch_bounds__(32, UNI ? MGB_S3MINB : 8) k_stream3(StreamArgs
 
 }  // namespace
 
-static size_t stream3_smem(bool zu) { return sizeof(double) * ((size_t)(RF3 + (zu ? 0 : RU3)) * SW3 + 2 * NCLS3 * 9); }
+static size_t stream3_smem(bool zu, bool uni) {
+  return sizeof(double) * ((size_t)(RF3 + (zu ? 0 : RU3)) * SW3 + (uni ? 0 : 2 * NCLS3 * 9));
+}
 
 static int sm_count3() {
   int dev = 0, sms = 0;
@@ -462,7 +554,7 @@ static void choose_seg3(int rows, int cols, int S, int wout, int occ, bool unifo
   const int64_t slots = (int64_t)sm_count3() * std::max(occ, 1);
   static const double r_env = getenv("MGB_EDGE3") ? atof(getenv("MGB_EDGE3")) : 0.0;
   const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : 1.8);
-  const int F = 2 * S + 3;
+  const int F = 2 * S + 2 + NR3;
   double best_t = 1e300;
   a.nstrips = strips;
   a.nedge = ne;
@@ -493,17 +585,17 @@ static void choose_seg3(int rows, int cols, int S, int wout, int occ, bool unifo
   }
 }
 
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI>
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, bool ZA, bool ALN>
 static cudaError_t run_k3(StreamArgs a, int* nblocks) {
   using P = P3<NSW, RES, NOUT>;
-  auto kern = k_stream3<NSW, RES, PRO, NORM, ZU, NOUT, UNI>;
+  auto kern = k_stream3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN>;
   struct Occ {
     int dev, occ;
   };
   static thread_local std::vector<Occ> occ_cache;   // per instantiation, per device
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
-  const size_t smem = stream3_smem(ZU);
+  const size_t smem = stream3_smem(ZU, UNI);
   int occ = -1;
   for (auto& e : occ_cache)
     if (e.dev == dev) occ = e.occ;
@@ -535,10 +627,15 @@ bool stream3_ok(const StreamArgs& a) {
 cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks) {
   const bool zu = a.u == nullptr;
   const bool nout = a.uo == nullptr && !res && !pro;
+  static const bool no_za = getenv("MGB_NO_ZA") && atoi(getenv("MGB_NO_ZA")) != 0;   // A/B experiments
+  const bool za = !no_za && a.ci[2] == 0.0 && a.ci[6] == 0.0;   // uniform: every class is the interior one
 #define MGB_ST3(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                                \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_)    \
-    return a.uniform ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true>(a, nblocks)                \
-                     : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, false>(a, nblocks);
+    return !a.uniform  ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, false, false, false>(a, nblocks) \
+           : !a.padded ? (za ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, true, false>(a, nblocks)  \
+                             : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, false, false>(a, nblocks)) \
+           : za        ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, true, true>(a, nblocks)       \
+                       : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, false, true>(a, nblocks);
   MGB_ST3(1, true, false, false, false, false) MGB_ST3(1, true, false, true, false, false)
   MGB_ST3(1, true, false, false, true, false)  MGB_ST3(1, true, false, true, true, false)
   MGB_ST3(2, true, false, false, false, false) MGB_ST3(2, true, false, true, false, false)

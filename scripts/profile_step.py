@@ -12,6 +12,8 @@ import bench  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 h, f_host, info = bench.build_problem(cfg, 0)
+if os.environ.get("MGB_KIND"):   # streaming kernel kind (0 auto, 1, 2, 3)
+    h.set_stream_kernel(int(os.environ["MGB_KIND"]))
 f = torch.from_numpy(f_host).cuda()
 u = torch.zeros_like(f)
 for _ in range(2):
