@@ -160,3 +160,82 @@ def levels_for(n: int, coarsest: int = 3) -> int:
         n //= 2
         lv += 1
     return lv
+
+
+# ---------------------------------------------------------------------------
+# reference problem families as StencilField objects (problems.py:45-152): what the
+# command-line front end assembles.  Host-side, once per run.
+
+def build_geometry(kind: str, n: int, spacing: float | None = None):
+    """problems.py:98-120: GridSpec of a named domain."""
+    from .errors import ConfigError
+    from .grid import GridSpec
+    try:
+        mask = geometry_mask(kind, n)
+    except ValueError:
+        raise ConfigError(f"unknown geometry {kind!r}") from None
+    return GridSpec(n, n, 1.0 / (n + 1) if spacing is None else spacing, mask)
+
+
+def assemble_rotated_laplacian(spec, angle: float, anisotropy: float):
+    """problems.py:45-52: one constant table on every point of `spec`."""
+    from .errors import ConfigError
+    from .grid import constant_stencil
+    if anisotropy <= 0.0:
+        raise ConfigError(f"anisotropy must be positive, got {anisotropy}")
+    a, b, c = rotated_coefficients(angle, anisotropy)
+    return constant_stencil(spec, (a * _SXX + c * _SYY - b * _SXY) / (spec.spacing * spec.spacing))
+
+
+def assemble_variable_diffusion(spec, kappa: float):
+    """problems.py:62-95: bilinear elements for -div(g grad u), g = sin(kappa pi x y)
+    + 1.1 sampled at the four cell midpoints around each node, scaled by 1 / h^2;
+    identity rows at inactive points."""
+    from .errors import NumericError
+    from .grid import StencilField
+    h = spec.spacing
+    y = (np.arange(spec.rows, dtype=float)[:, None] + 1.0) * h
+    x = (np.arange(spec.cols, dtype=float)[None, :] + 1.0) * h
+    g = {(sy, sx): np.sin(kappa * math.pi * (x + 0.5 * sx * h) * (y + 0.5 * sy * h)) + 1.1
+         for sy in (-1, 1) for sx in (-1, 1)}
+    lo = min(float(q.min()) for q in g.values())
+    if lo <= 0.0:
+        raise NumericError(f"diffusion coefficient not elliptic, min sample {lo}")
+    s = 1.0 / (3.0 * h * h)
+    data = np.zeros((spec.rows, spec.cols, 3, 3))
+    for (sy, sx), q in g.items():
+        data[:, :, 1 + sy, 1 + sx] = -q * s                 # corner neighbours: one cell each
+    for sy in (-1, 1):                                       # edge neighbours: two cells each
+        data[:, :, 1 + sy, 1] = -(g[(sy, -1)] + g[(sy, 1)]) * 0.5 * s
+    for sx in (-1, 1):
+        data[:, :, 1, 1 + sx] = -(g[(-1, sx)] + g[(1, sx)]) * 0.5 * s
+    data[:, :, 1, 1] = 2.0 * (g[(1, 1)] + g[(1, -1)] + g[(-1, -1)] + g[(-1, 1)]) * s   # ne + nw + sw + se
+    data[~spec.mask] = 0.0
+    data[~spec.mask, 1, 1] = 1.0
+    return StencilField(spec, data)
+
+
+class ProblemSpec:
+    """problems.py:123-146: (family, n, geometry, angle, anisotropy, kappa)."""
+
+    FIELDS = ("family", "n", "geometry", "angle", "anisotropy", "kappa")
+
+    def __init__(self, family: str, n: int, geometry: str = "square", angle: float = 0.0,
+                 anisotropy: float = 100.0, kappa: float = 1.0):
+        self.family, self.n, self.geometry = family, int(n), geometry
+        self.angle, self.anisotropy, self.kappa = float(angle), float(anisotropy), float(kappa)
+
+    def asdict(self) -> dict:
+        return {k: getattr(self, k) for k in self.FIELDS}
+
+    def grid(self):
+        return build_geometry(self.geometry, self.n)
+
+    def assemble(self, spec=None):
+        from .errors import ConfigError
+        spec = self.grid() if spec is None else spec
+        if self.family == "rotated":
+            return assemble_rotated_laplacian(spec, self.angle, self.anisotropy)
+        if self.family == "variable":
+            return assemble_variable_diffusion(spec, self.kappa)
+        raise ConfigError(f"unknown problem family {self.family!r}")
