@@ -41,18 +41,19 @@ namespace {
 constexpr int CPT = 4;             // columns per lane
 constexpr int SW3 = 32 * CPT;      // strip width
 #ifndef MGB_S3NR
-#define MGB_S3NR 2
+#define MGB_S3NR 1
 #endif
 #ifndef MGB_S3DG
 #define MGB_S3DG 2
 #endif
 #ifndef MGB_S3MINB
-#define MGB_S3MINB 8
+#define MGB_S3MINB 12
 #endif
 constexpr int NR3 = MGB_S3NR;      // rows entering per step
 constexpr int DG3 = MGB_S3DG;      // ring groups (of NR3 rows) in flight beyond the next one
-constexpr int RU3 = 8;             // u ring rows (t .. t + NR (DG + 2) - 1)
-constexpr int RF3 = 16;            // f ring rows (t - 4 .. t + NR (DG + 2) - 1)
+constexpr int pow2_at_least(int v) { return v <= 1 ? 1 : 2 * pow2_at_least((v + 1) / 2); }
+constexpr int RU3 = pow2_at_least(NR3 * (DG3 + 2));       // u ring rows (t .. t + NR (DG + 2) - 1)
+constexpr int RF3 = pow2_at_least(NR3 * (DG3 + 2) + 4);   // f ring rows (t - 4 .. t + NR (DG + 2) - 1)
 static_assert(NR3 * (DG3 + 2) <= RU3 && NR3 * (DG3 + 2) + 4 <= RF3, "ring depths");
 constexpr int NCLS3 = 25;
 
