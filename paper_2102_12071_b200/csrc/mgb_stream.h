@@ -43,7 +43,7 @@ struct StreamArgs {
 
 // Padded level layout of the warp-strip kernel: rows [-PAD_ROWS, rows + PAD_ROWS) x
 // columns [-PAD_LCOLS, pitch - PAD_LCOLS); the base pointer addresses (0, 0).
-constexpr int PAD_ROWS = 8, PAD_LCOLS = 8;
+constexpr int PAD_ROWS = 16, PAD_LCOLS = 8;
 inline int64_t pad_pitch(int cols) { return ((int64_t)PAD_LCOLS + cols + 122 + 15) / 16 * 16; }
 inline int64_t pad_elems(int rows, int cols) { return ((int64_t)rows + 2 * PAD_ROWS) * pad_pitch(cols); }
 inline int64_t pad_offset(int cols) { return (int64_t)PAD_ROWS * pad_pitch(cols) + PAD_LCOLS; }

@@ -84,6 +84,9 @@ __device__ __forceinline__ void cpa16(unsigned sa, const double* gmem, bool vali
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
                : "memory");
 }
+__device__ __forceinline__ void cpa16f(unsigned sa, const double* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -106,6 +109,7 @@ struct Lane3 {
   int cb[4];           // band of column c0 + c (2 when outside the grid)
   const double* tab;   // shared-memory class tables: A [25][9], then K [25][9]
   int lo_c, hi_c, mcol;  // POST: coarse rows that may be read, first coarse column of the lane
+  double* uo_t;          // uo at (row t - 2 NSW, column c0) of the current step (advanced per step)
 };
 
 // POST: the lane's coarse correction values (columns m - 1 .. m + 1) of coarse row ci
@@ -282,15 +286,13 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
       // MODE 0 steps lie inside the segment (every output row owned): no row tests
       const bool orow = MODE == 0 || (row >= L.R0 && row < L.R1);
       if (NORM && k == 1) {
-        // branch-free: excluded points add an exact +0 (the partial sum stays >= +0)
+        // excluded points are skipped (adding their exact +0 would leave the same bits)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const double v = (orow && ((L.own >> c) & 1)) ? out[c] : 0.0;
-          norm = fma(v, v, norm);
-        }
+        for (int c = 0; c < 4; ++c)
+          if (orow && ((L.own >> c) & 1)) norm = fma(out[c], out[c], norm);
       }
       if (!NOUT && k == 2 * NSW && orow && (MODE == 0 || a.uo)) {
-        double* dst = a.uo + (int64_t)row * L.ld + L.c0;
+        double* dst = L.uo_t + (int64_t)j * L.ld;   // row t - 2 NSW + j
 #ifdef MGB_S3_NOSTORE
         if (out[0] == 1.2345e300)   // experiment builds only: (practically) no HBM writes
 #endif
@@ -438,24 +440,34 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
   for (int m = 0; m < 4; ++m) cq |= (((unsigned)(colq + 32 * m) < (unsigned)g.cols) ? 1u : 0u) << m;
   const double* fb = a.f;
   const double* ub = a.u;
-  auto issue_row = [&](int r) {
+  // padded layout: every row a segment touches ([-11, rows + 8], inside the PAD_ROWS margins)
+  // and every strip column is addressable and the margins hold zeros, so the copies need no
+  // predicate; rows are issued in sequence, so the source pointers just advance by the pitch
+  const double* fnx = nullptr;
+  const double* unx = nullptr;
+  auto issue_row = [&](int r, bool wu) {
 #ifdef MGB_S3_NOLOAD
     return;   // experiment builds only: no HBM reads (compute-only timing)
 #endif
-    const bool rv = r >= lo_row && r <= hi_row;
-    const int64_t ro = (int64_t)r * L.ld + colq;
     const unsigned of = sF + (unsigned)((r & (RF3 - 1)) * SW3 * 8);
     const unsigned ou = sU + (unsigned)((r & (RU3 - 1)) * SW3 * 8);
     if (ALN) {
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        cpa16(of + 512 * m, rv ? fb + ro + 64 * m : fb, rv);
-        if (!ZU) cpa16(ou + 512 * m, rv ? ub + ro + 64 * m : ub, rv);
+      cpa16f(of, fnx);
+      cpa16f(of + 512, fnx + 64);
+      fnx += L.ld;
+      if (!ZU && wu) {
+        cpa16f(ou, unx);
+        cpa16f(ou + 512, unx + 64);
+        unx += L.ld;
       }
-    } else if (rv && cols_all) {
+      return;
+    }
+    const bool rv = r >= lo_row && r <= hi_row;
+    const int64_t ro = (int64_t)r * L.ld + colq;
+    if (rv && cols_all) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) cpa8f(of + 256 * m, fb + ro + 32 * m);
-      if (!ZU) {
+      if (!ZU && wu) {
 #pragma unroll
         for (int m = 0; m < 4; ++m) cpa8f(ou + 256 * m, ub + ro + 32 * m);
       }
@@ -464,14 +476,16 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
       for (int m = 0; m < 4; ++m) {
         const bool v = rv && ((cq >> m) & 1);
         cpa8s(of + 256 * m, v ? fb + ro + 32 * m : fb, v);
-        if (!ZU) cpa8s(ou + 256 * m, v ? ub + ro + 32 * m : ub, v);
+        if (!ZU && wu) cpa8s(ou + 256 * m, v ? ub + ro + 32 * m : ub, v);
       }
     }
   };
   // ring group s: rows s NR .. s NR + NR - 1
-  auto issue = [&](int s) {
+  // wu: with the u rows (the groups before t0 carry f rows only: u rows before t0 are
+  // never read, and copying them would race with rows t0 .. for the same ring slots)
+  auto issue = [&](int s, bool wu) {
 #pragma unroll
-    for (int j = 0; j < NR; ++j) issue_row(s * NR + j);
+    for (int j = 0; j < NR; ++j) issue_row(s * NR + j, wu);
     cpa_commit();
   };
   double acc[S][2][4];
@@ -493,13 +507,18 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
   // groups of rows t0 - 4 .. : the residual seeds reach back to row t - 3
   const int s0 = t0 / NR - (4 + NR - 1) / NR;
   const int sstart = t0 / NR;
-  for (int s = s0; s <= sstart + DG3; ++s) issue(s);
+  if (ALN) {
+    fnx = fb + (int64_t)(s0 * NR) * L.ld + colq;
+    if (!ZU) unx = ub + (int64_t)t0 * L.ld + colq;
+  }
+  for (int s = s0; s <= sstart + DG3; ++s) issue(s, s >= sstart);
+  L.uo_t = NOUT || !a.uo ? nullptr : a.uo + (int64_t)(t0 - 2 * NSW) * L.ld + L.c0;
 
 #define MGB_STEP3(P0_)                                                                                       \
   {                                                                                                          \
     const int t = tb + (P0_) * NR;                                                                           \
     __syncwarp();                                                                                            \
-    issue(t / NR + 1 + DG3);                                                                                 \
+    issue(t / NR + 1 + DG3, true);                                                                           \
     cpa_wait<DG3>(); /* f rows up to t + NR and u rows t .. t + NR - 1 have landed */                       \
     __syncwarp();                                                                                            \
     const bool rows_int = t - S >= 2 && t + NR <= g.rows - 3;                                                \
@@ -513,6 +532,7 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
       step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 2, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
     else                                                                                                     \
       step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 3, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
+    L.uo_t += NR * L.ld;                                                                                     \
   }
   // t0 is even: with one row per step, unroll two steps so each step's parity is static
   if (NR == 2) {
