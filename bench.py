@@ -201,27 +201,92 @@ def build_problem(cfg_name, device, lo=0, hi=None):
     return h, f, info
 
 
-def cpu_sample(cfg_name, steps=1, warmup=0, barrier=None):
-    """Oracle port (NumPy, single thread) on a bounded sample of the config: its
-    operator family at min(n, CPU_SAMPLE_N)^2 (levels scaled to reach 3x3), one
-    problem, V(nu, nu) cycles with the history residual, timed like
-    hierarchy.solve (setup excluded).  barrier: replicas start timing together."""
+def _band(n):
+    """Band index of every row / column: 0, 1 for the first two, 2 inside, 3, 4 for the last two."""
+    b = np.full(n, 2)
+    b[:2] = (0, 1)
+    b[-2:] = (3, 4)
+    return b
+
+
+def oracle_hierarchy_constant(table, n, levels, net):
+    """Oracle hierarchy (oracle/mg_oracle.py types) of a constant-coefficient operator
+    at full size without the oracle's O(n^2 x 200 flop) setup: away from the boundary a
+    constant-coefficient Galerkin chain is constant, and within two points of it it
+    depends only on the band (first two rows / columns, interior, last two), so every
+    level's operator is 5 x 5 class tables.  The class tables of the next level come from
+    the oracle's own galerkin() on a 15 x 15 expansion (-> 7 x 7: its rows 0, 1, 3, 5, 6
+    are the five bands); the conv net maps a point's own table, so the kernels are the
+    net's outputs on the 25 class tables.  Levels of at most 63 points per side use the
+    oracle's functions directly.  The operators equal mo.build_hierarchy's bit for bit and
+    the kernels mo.equip_inferred's to one unit in the last place (BLAS blocks the net's
+    last matmul differently for 25 rows; tests/test_bench_reference.py); only the timed
+    cycle, which runs the oracle's v_cycle on these per-point arrays, is measured."""
+    from oracle import mg_oracle as mo
+    if net.variant != "conv":
+        raise ValueError("class expansion needs the conv variant (features = the point's own table)")
+    ones = lambda m: np.ones((m, m), dtype=bool)  # noqa: E731
+    pick = np.array([0, 1, 3, 5, 6])
+    cls = np.broadcast_to(np.asarray(table, dtype=float), (5, 5, 3, 3)).copy()
+    expand = lambda c, m: np.ascontiguousarray(c[_band(m)[:, None], _band(m)[None, :]])  # noqa: E731
+    ops, kernels, masks, size = [], [], [], n
+    for l in range(levels):
+        masks.append(ones(size))
+        if l > 0 and ops[-1].shape[0] <= 63:
+            ops.append(mo.galerkin(ops[-1], masks[-2], masks[-1]))
+            cls = None
+        else:
+            if l > 0:
+                cls = mo.galerkin(expand(cls, 15), ones(15), ones(7))[pick[:, None], pick[None, :]]
+            ops.append(expand(cls, size))
+        if l < levels - 1:
+            if cls is not None:
+                kernels.append(expand(mo.infer_kernels(net, np.ascontiguousarray(cls), ones(5)), size))
+            else:
+                kernels.append(mo.infer_kernels(net, ops[-1], masks[-1]))
+        size //= 2
+    lu, perm = mo.lu_factor(mo.materialize(ops[-1], masks[-1]))
+    return mo.Hierarchy(ops, masks, lu, perm, kernels, net.slope)
+
+
+def cpu_sample_n(cfg):
+    """Grid size of the CPU sample: the config's own n where one solve fits host memory
+    and minutes (constant-coefficient configs up to 4095^2 through
+    oracle_hierarchy_constant: config 2 at full size), else CPU_SAMPLE_N."""
+    if "MGB_CPU_SAMPLE_N" in os.environ:
+        return min(cfg["n"], CPU_SAMPLE_N)
+    if cfg["op"] in ("rot", "rot_classed"):
+        return min(cfg["n"], 4095)
+    return min(cfg["n"], CPU_SAMPLE_N)
+
+
+def cpu_sample(cfg_name, steps=1, warmup=0, barrier=None, n=None):
+    """Oracle port (NumPy, single thread) on a bounded sample of the config: one
+    problem of its operator family at cpu_sample_n(cfg)^2 (levels scaled to reach 3x3),
+    V(nu, nu) cycles with the history residual, timed like hierarchy.solve (setup
+    excluded).  barrier: replicas start timing together."""
     from oracle import mg_oracle as mo
     from paper_2102_12071_b200 import problems as gen
     cfg = CONFIGS[cfg_name]
-    n = min(cfg["n"], CPU_SAMPLE_N)
+    n = cpu_sample_n(cfg) if n is None else min(n, cfg["n"])
     levels = gen.levels_for(n)
     nu = cfg["nu"]
-    if cfg["op"] in ("rot", "rot_classed"):
-        A, f = gen.rotated_fd(n, cfg["theta"], cfg["eps"]), gen.uniform_rhs(n, cfg["seed"])
-    elif cfg["op"] == "grf":
-        A, f = gen.grf_diffusion_5pt(n, seed=cfg["seed"]), gen.uniform_rhs(n, cfg["seed"])
-    else:
-        eps, theta = gen.batch_parameters(cfg["batch"], seed=cfg["seed"])
-        A, f = gen.rotated_fd(n, theta[0], eps[0]), gen.uniform_rhs(n, [4, 0])
+    net = mo.load_net_json(os.path.join(ROOT, "paper_2102_12071_b200", "data", cfg["net"]))
     t0 = time.perf_counter()
-    h = mo.build_hierarchy(A, levels)
-    mo.equip_inferred(h, mo.load_net_json(os.path.join(ROOT, "paper_2102_12071_b200", "data", cfg["net"])))
+    if cfg["op"] in ("rot", "rot_classed"):
+        f = gen.uniform_rhs(n, cfg["seed"])
+        if n > 1023:
+            h = oracle_hierarchy_constant(gen.rotated_fd(1, cfg["theta"], cfg["eps"], h=1.0 / (n + 1))[0, 0], n, levels, net)
+        else:
+            h = mo.equip_inferred(mo.build_hierarchy(gen.rotated_fd(n, cfg["theta"], cfg["eps"]), levels), net)
+    else:
+        if cfg["op"] == "grf":
+            A, f = gen.grf_diffusion_5pt(n, seed=cfg["seed"]), gen.uniform_rhs(n, cfg["seed"])
+        else:
+            eps, theta = gen.batch_parameters(cfg["batch"], seed=cfg["seed"])
+            A, f = gen.rotated_fd(n, theta[0], eps[0]), gen.uniform_rhs(n, [4, 0])
+        h = mo.equip_inferred(mo.build_hierarchy(A, levels), net)
+    A = h.ops[0]
     setup = time.perf_counter() - t0
     u = np.zeros((n, n))
     fn = float(np.linalg.norm(f))
@@ -240,7 +305,7 @@ def cpu_sample(cfg_name, steps=1, warmup=0, barrier=None):
             "sample": f"oracle/mg_oracle.py (NumPy, 1 thread) V({nu},{nu}) cycle + history residual on the "
                       f"config's operator family at {n}^2 ({levels} levels), {len(times)} cycle(s) timed, "
                       f"setup {setup:.1f}s excluded; cpu {cpu_model()}",
-            "per_cycle_s": per_cycle}
+            "per_cycle_s": per_cycle, "n": n, "same_size": n == cfg["n"]}
 
 
 def _c4_problem_cycle(i):
@@ -295,37 +360,49 @@ def cpu_sample_pool(cfg_name, nproblems=None):
             "per_cycle_s": per_cycle_core / cores}
 
 
-def _replica_worker(cfg_name, steps, warmup, barrier, out):
+def _replica_worker(cfg_name, steps, warmup, barrier, out, n=None):
     """One single-threaded replica of cpu_sample (worker of cpu_sample_replicas): the
     setup runs before the barrier, so every replica's timed cycles overlap."""
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
     sys.path.insert(0, ROOT)
-    s = cpu_sample(cfg_name, steps=steps, warmup=warmup, barrier=barrier)
+    s = cpu_sample(cfg_name, steps=steps, warmup=warmup, barrier=barrier, n=n)
     out.put(s["per_cycle_s"])
 
 
-def cpu_sample_replicas(cfg_name, steps=1, warmup=0, max_procs=32):
+def host_mem_available_gb():
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable"):
+                return float(ln.split()[1]) / 1e6
+    except Exception:
+        pass
+    return 16.0
+
+
+def cpu_sample_replicas(cfg_name, steps=1, warmup=0, max_procs=32, n=None):
     """Single-problem configs on all host cores: one solve of the reference is
     single-threaded NumPy, so the host's throughput is independent replicas, one
     per core (the reference's own concurrency model: the bench thread pool,
     cli.py:746-752), each timing cpu_sample's cycles at the same moment; value =
     sum over replicas of unknowns / cycle time (memory-bandwidth contention
-    between replicas included)."""
+    between replicas included).  Replicas are capped by host memory (a 4095^2
+    oracle solve holds about 4.5 GB)."""
     import multiprocessing as mpc
-    cores = max(1, min(os.cpu_count() or 1, max_procs))
+    cfg = CONFIGS[cfg_name]
+    n = cpu_sample_n(cfg) if n is None else min(n, cfg["n"])
+    per_replica_gb = 6.0 * (n / 4095.0) ** 2 + 0.3
+    cores = max(1, min(os.cpu_count() or 1, max_procs, int(0.8 * host_mem_available_gb() / per_replica_gb)))
     if cores == 1:
-        return cpu_sample(cfg_name, steps=steps, warmup=warmup)
+        return cpu_sample(cfg_name, steps=steps, warmup=warmup, n=n)
     ctx = mpc.get_context("spawn")
     barrier, out = ctx.Barrier(cores), ctx.Queue()
-    procs = [ctx.Process(target=_replica_worker, args=(cfg_name, steps, warmup, barrier, out)) for _ in range(cores)]
+    procs = [ctx.Process(target=_replica_worker, args=(cfg_name, steps, warmup, barrier, out, n)) for _ in range(cores)]
     for p in procs:
         p.start()
     per = [out.get() for _ in procs]
     for p in procs:
         p.join()
-    cfg = CONFIGS[cfg_name]
-    n = min(cfg["n"], CPU_SAMPLE_N)
     value = float(sum(n * n / t for t in per))
     return {"value": value, "unit": "unknowns/s", "cores": cores, "kind": "port",
             "sample": f"oracle/mg_oracle.py (NumPy) on {cores} concurrent single-threaded replicas, each one "
@@ -333,7 +410,7 @@ def cpu_sample_replicas(cfg_name, steps=1, warmup=0, max_procs=32):
                       f"{steps} V({cfg['nu']},{cfg['nu']}) cycle(s) + history residual timed after {warmup} "
                       f"warm-up (setup excluded); value = sum of the replicas' unknowns / cycle time "
                       f"(mean cycle {np.mean(per) * 1e3:.0f} ms); cpu {cpu_model()}",
-            "per_cycle_s": float(np.mean(per)) / cores}
+            "per_cycle_s": float(np.mean(per)) / cores, "n": n, "same_size": n == cfg["n"]}
 
 
 def gen_levels(n):
@@ -359,23 +436,37 @@ def workload_desc(cfg_name):
 
 
 def run_reference(args):
+    """The reference arm: the oracle port on all host cores at the config's own grid size
+    where that is feasible (cpu_sample_n: config 2 at its full 4095^2, about 26 s per
+    cycle and 4.5 GB per replica, so one or two timed cycles), with the quick 1023^2
+    sample of round 1 kept beside it as `sample_1023`."""
     from paper_2102_12071_b200 import dist as D
     world, rank, local = D.env()
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
+    extra = None
     if cfg["batch"] > 1:
         s = cpu_sample_pool(args.config)
     else:
-        s = cpu_sample_replicas(args.config, steps=max(1, min(args.steps, 10)), warmup=min(args.warmup, 1))
+        n = cpu_sample_n(cfg)
+        big = n > 1023
+        s = cpu_sample_replicas(args.config, steps=max(1, min(args.steps, 2 if big else 10)),
+                                warmup=0 if big else min(args.warmup, 1))
+        if big:
+            q = cpu_sample_replicas(args.config, steps=max(1, min(args.steps, 5)), warmup=1, n=1023)
+            extra = {"value": q["value"], "unit": "unknowns/s", "cores": q["cores"], "n": 1023}
+    n_s = s.get("n", cfg["n"])
     line = {"metric": "unknowns/sec per V-cycle (fp64)", "value": s["value"], "unit": "unknowns/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": s["per_cycle_s"] * 1e3, "higher_is_better": True,
             "scaling": "strong" if cfg["batch"] > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators)", "impl": "reference",
-            "config": {"workload": workload_desc(args.config), "sample_n": min(cfg["n"], CPU_SAMPLE_N)},
+            "config": {"workload": workload_desc(args.config), "sample_n": n_s, "same_size": n_s == cfg["n"]},
             "cpu_baseline": {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": s["value"], "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if extra:
+        line["sample_1023"] = extra
     print(json.dumps(line), flush=True)
     return 0
 
@@ -555,9 +646,20 @@ def run_ours(args):
         cpu = cpu_sample_pool(args.config) if batched else cpu_sample(args.config, steps=1)
     if rank == 0:
         bpu = cycle_bytes_per_fine_unknown(n, levels, nu, nu)
-        # which streaming kernel runs level 0 (mgb_stream.cu launch_stream dispatch)
-        kname = ("k_stream2 (column pairs, push-form chains)" if compact and nb == 1 and n * n >= (2 << 20)
-                 else "k_stream (one column per thread)")
+        kname = h.pass_kernel(0, nu)   # the kernel launch_pass dispatches level 0 to
+        # compulsory traffic of one fused cycle: per level a PRE pass (u, f in; u out; the
+        # restricted residual at 8 B per coarse point; on levels >= 1 the start is zero, so
+        # u is not read) and a POST pass (u, f, coarse correction in; u out), plus the
+        # per-point tables where a level streams them; the history residual pass of the
+        # last cycle (u, f in) is spread over the cycles
+        cyc_bytes = 0.0
+        for l in range(levels - 1):
+            nl = (n >> l) ** 2
+            tables = 0 if all(h.storage_info(l)) else 72 + 8 * h.stencil_points(l)
+            pre = (26 if l == 0 else 18) + tables
+            cyc_bytes += nl * nb * (pre + 26 + tables)
+        cyc_bytes += 16.0 * n * n * nb / cycles
+        cyc_s = ms_max * 1e-3 / cycles
         hl = hist_all[:, -1]
         line = {
             "metric": "unknowns/sec per V-cycle (fp64)", "value": value, "unit": "unknowns/s",
@@ -578,6 +680,13 @@ def run_ours(args):
                          "post": {"kernel": f"{kname} POST, level 0 (prolongation + sweeps)",
                                   "achieved": achieved_post, "frac": achieved_post / peak,
                                   "launch_ms": ms_post.value}},
+            "cycle_roofline": {"bound": "hbm", "bytes_per_cycle": cyc_bytes, "cycle_ms": cyc_s * 1e3,
+                               "achieved": cyc_bytes / cyc_s / 1e9, "peak": peak, "unit": "GB/s",
+                               "frac": cyc_bytes / cyc_s / 1e9 / peak,
+                               "model": "compulsory bytes of the fused passes of every level (26 B per point per "
+                                        "pass, 18 B for the zero-start PRE of levels >= 1, + per-point tables where "
+                                        "streamed) / measured cycle time; levels >= 1 are L2-resident, so this is a "
+                                        "lower bound on how far the whole cycle is from streaming at HBM speed"},
             "cycle_model": {"survey_bytes_per_fine_unknown": 172.6 if compact else bpu,
                             "survey_model": "compact (SURVEY 8(d))" if compact else "per-point (SURVEY 8(d))",
                             "effective_GBps": value / world * (172.6 if compact else bpu) / 1e9},

@@ -149,6 +149,11 @@ int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_c
    per-point A: 5 when its corner planes are zero everywhere (a 5-point operator,
    checked on the device at build), else 9 (0 for class-compact A). */
 int mgb_hier_stencil_points(const mgb_hier* h, int level, int* a_points);
+/* Which kernel runs level `level`'s fused V(nu, nu) passes (measurement labels):
+   0 separate sweep / restriction / prolongation kernels, 1 k_stream (one column per
+   thread), 2 k_stream2 (column pairs), 3 k_stream3 (one warp per 128-column strip),
+   4 k_tile (tile-local passes). */
+int mgb_hier_pass_kernel(const mgb_hier* h, int level, int nu, int* kind);
 /* Cycle pass structure for V(1|2, 1|2) with 1-stage smoothers: 2 (default) one
    row-streaming pass per smoothing phase (sweeps + restriction, prolongation +
    sweeps); 1: one streaming pass per sweep; 0: separate sweep / restriction /
@@ -280,6 +285,12 @@ int  mgb_dd_get_solution(const mgb_dd* d, int part, double* u_owned_dev, void* s
 /* fixed-count V(nu1, nu2) cycles of the decomposed solve (graph-replayed); history_dev
    (cycles + 1) as mgb_run_cycles, identical on every rank. */
 int  mgb_dd_run_cycles(mgb_dd* d, int nu1, int nu2, int cycles, int u_zero, double* history_dev, void* stream);
+
+/* Guard mode (environment MGB_GUARD=1 when the library is loaded; tests only): every
+   device allocation of the library carries a 4 KiB canary region on each side.  Reports
+   the number of live allocations and of those whose canaries were overwritten (their
+   sizes are listed in mgb_last_error).  MGB_CONFIG when guard mode is off. */
+int mgb_guard_check(int* allocations, int* corrupted);
 
 /* instrumentation for bench.py: number of kernel launches issued by the last
    mgb_run_cycles / mgb_vcycle call (graph replays count their nodes). */

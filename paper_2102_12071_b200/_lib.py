@@ -45,6 +45,7 @@ SIGNATURES = {
     "mgb_hier_depth": (I, [P, PI, PI]),
     "mgb_hier_level_info": (I, [P, I, PI, PI, PI, PI, PD]),
     "mgb_hier_stencil_points": (I, [P, I, PI]),
+    "mgb_hier_pass_kernel": (I, [P, I, I, PI]),
     "mgb_hier_get_operator": (I, [P, I, P]),
     "mgb_hier_get_kernels": (I, [P, I, P]),
     "mgb_hier_get_mask": (I, [P, I, P]),
@@ -81,6 +82,7 @@ SIGNATURES = {
     "mgb_dd_get_solution": (I, [P, I, P, P]),
     "mgb_dd_run_cycles": (I, [P, I, I, I, I, P, P]),
     "mgb_time_pass": (I, [P, P, I, I, I, P, P, I, PD, P]),
+    "mgb_guard_check": (I, [PI, PI]),
     "mgb_last_launch_count": (I64, [P]),
 }
 

@@ -724,6 +724,32 @@ extern "C" int mgb_hier_stencil_points(const mgb_hier* h, int level, int* a_poin
   return MGB_OK;
 }
 
+// forward declarations (defined with the cycle code below)
+static int pass_kind(const mgb_hier* h, int l, int nu1, int nu2);
+
+extern "C" int mgb_hier_pass_kernel(const mgb_hier* h, int level, int nu, int* kind) {
+  if (!h || !kind) return fail(MGB_CONTRACT, "null argument");
+  if (level < 0 || level + 1 >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  const int pk = pass_kind(h, level, nu, nu);
+  if (pk == 0) {
+    *kind = 0;
+  } else if (pk == 2) {
+    *kind = 4;
+  } else {
+    const LevelD& lv = h->lv[level];
+    StreamArgs a{};
+    a.g = h->grid(level);
+    a.A = lv.opA();
+    a.K = lv.opK();
+    a.mask = lv.mask;
+    a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
+    a.uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
+    a.kernel = h->stream_kernel;
+    *kind = stream_kernel_kind(a);
+  }
+  return MGB_OK;
+}
+
 // Constant-coefficient hierarchy held entirely as band-class tables (no per-point
 // planes): the Galerkin product and the coarsest materialisation read the fine
 // tables through the class accessor and evaluate one representative point per

@@ -70,15 +70,20 @@ struct DeviceGuard {
   }
 };
 
+// Guard mode (MGB_GUARD=1, tests only; compute-sanitizer is not available on every GPU
+// pool): every device allocation of the library gets a 4 KiB canary region on each side,
+// and mgb_guard_check() reports the allocations whose canaries were overwritten.
+cudaError_t guarded_malloc(void** p, size_t bytes);
+void guarded_free(void* p);
 template <typename T>
 inline cudaError_t dalloc(T** p, size_t count) {
   *p = nullptr;
   if (count == 0) return cudaSuccess;
-  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  return guarded_malloc(reinterpret_cast<void**>(p), count * sizeof(T));
 }
 template <typename T>
 inline void dfree(T*& p) {
-  if (p) cudaFree(p);
+  if (p) guarded_free(p);
   p = nullptr;
 }
 

@@ -16,6 +16,9 @@
 //   jacobi                smoothers.py:29-50
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "mgb_internal.h"
 
@@ -27,6 +30,75 @@ bool pdl_enabled() {
   static const bool off = getenv("MGB_NO_PDL") && atoi(getenv("MGB_NO_PDL")) != 0;
   return !off;
 }
+
+// ---- guard mode -----------------------------------------------------------------
+namespace {
+constexpr size_t GUARD_BYTES = 4096;
+constexpr unsigned char GUARD_PATTERN = 0xA5;
+std::mutex g_guard_mu;
+std::map<void*, size_t> g_guarded;   // user pointer -> user bytes
+bool guard_on() {
+  static const bool on = getenv("MGB_GUARD") && atoi(getenv("MGB_GUARD")) != 0;
+  return on;
+}
+}  // namespace
+
+cudaError_t guarded_malloc(void** p, size_t bytes) {
+  if (!guard_on()) return cudaMalloc(p, bytes);
+  const size_t user = (bytes + 255) / 256 * 256;
+  unsigned char* base = nullptr;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), user + 2 * GUARD_BYTES);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(base, GUARD_PATTERN, user + 2 * GUARD_BYTES);
+  if (e != cudaSuccess) return e;
+  *p = base + GUARD_BYTES;
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guarded[*p] = bytes;
+  return cudaSuccess;
+}
+
+void guarded_free(void* p) {
+  if (!guard_on()) {
+    cudaFree(p);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guarded.erase(p);
+  cudaFree(static_cast<unsigned char*>(p) - GUARD_BYTES);
+}
+
+}  // namespace mgb
+
+extern "C" int mgb_guard_check(int* allocations, int* corrupted) {
+  using namespace mgb;
+  if (!allocations || !corrupted) return fail(MGB_CONTRACT, "null argument");
+  *allocations = *corrupted = 0;
+  if (!guard_on()) return fail(MGB_CONFIG, "guard mode is off (set MGB_GUARD=1 before loading the library)");
+  MGB_CUDA_TRY(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  std::vector<unsigned char> buf(GUARD_BYTES);
+  std::string report;
+  for (auto& kv : g_guarded) {
+    ++*allocations;
+    unsigned char* user = static_cast<unsigned char*>(kv.first);
+    // the bytes right after the user region up to the rounded size belong to the back canary
+    const size_t back_off = kv.second;
+    const size_t back_len = GUARD_BYTES;
+    bool bad = false;
+    MGB_CUDA_TRY(cudaMemcpy(buf.data(), user - GUARD_BYTES, GUARD_BYTES, cudaMemcpyDeviceToHost));
+    for (size_t q = 0; q < GUARD_BYTES; ++q) bad |= buf[q] != GUARD_PATTERN;
+    MGB_CUDA_TRY(cudaMemcpy(buf.data(), user + (back_off + 255) / 256 * 256, back_len, cudaMemcpyDeviceToHost));
+    for (size_t q = 0; q < back_len; ++q) bad |= buf[q] != GUARD_PATTERN;
+    if (bad) {
+      ++*corrupted;
+      report += " [" + std::to_string(kv.second) + " B]";
+    }
+  }
+  if (*corrupted) set_error(MGB_OK, "guard canaries overwritten around allocations of" + report);
+  return MGB_OK;
+}
+
+namespace mgb {
 
 cudaError_t debug_sync(const char* what) {
   static const bool on = getenv("MGB_DEBUG_SYNC") && getenv("MGB_DEBUG_SYNC")[0] == '1';

@@ -589,6 +589,15 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   return cudaErrorInvalidValue;
 }
 
+int stream_kernel_kind(const StreamArgs& a) {
+  const int cm = (a.A.cls != nullptr && a.K.cls != nullptr && a.mask == nullptr) ? (a.ci_valid ? 2 : 1) : 0;
+  static const bool one_col = getenv("MGB_STREAM1") && atoi(getenv("MGB_STREAM1")) != 0;
+  const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() * a.g.batch >= 1000000);
+  if (cm == 2 && warp_strip_selected(a.kernel, a.g.n(), a.g.batch, a.uniform != 0) && stream3_ok(a)) return 3;
+  if (cm != 0 && (pairs || a.kernel == 3)) return 2;
+  return 1;
+}
+
 int stream_max_blocks(const Grid& g) {
   // upper bound on the CTAs of any streaming pass over g (seg >= 16, nsw >= 1)
   const int wout = SWT - 2 * 4 - 4;

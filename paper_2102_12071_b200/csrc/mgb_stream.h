@@ -54,6 +54,8 @@ inline int64_t pad_offset(int cols) { return (int64_t)PAD_ROWS * pad_pitch(cols)
 // (the number of history partials written when norm is set).
 cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 int stream_max_blocks(const Grid& g);
+// which streaming kernel launch_stream picks for these arguments: 1, 2 or 3
+int stream_kernel_kind(const StreamArgs& a);
 // Two-columns-per-thread variant for band-class levels without masks (mgb_stream2.cu);
 // launch_stream dispatches to it (MGB_STREAM1=1 keeps the one-column kernel).
 cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);

@@ -224,6 +224,15 @@ class MultigridHierarchy:
         _lib.call("mgb_hier_stencil_points", self._h, l, C.byref(p))
         return p.value
 
+    PASS_KERNELS = {0: "separate kernels", 1: "k_stream (one column per thread)", 2: "k_stream2 (column pairs)",
+                    3: "k_stream3 (one warp per 128-column strip, four columns per lane)", 4: "k_tile (tile-local passes)"}
+
+    def pass_kernel(self, l: int, nu: int) -> str:
+        """Name of the kernel that runs level l's fused V(nu, nu) passes."""
+        k = C.c_int()
+        _lib.call("mgb_hier_pass_kernel", self._h, l, int(nu), C.byref(k))
+        return self.PASS_KERNELS[k.value]
+
     # -- smoother bookkeeping ------------------------------------------------
     def _sweeps(self, nu1, nu2):
         """Resolve (nu1, nu2) and make sure the device holds each level's smoother."""
