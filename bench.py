@@ -14,10 +14,11 @@ Other configs: c1 (255^2, V(2,2) x 20), c3 (8191^2 GRF 5-point variable
 coefficients, per-point tables, V(2,2) x 10), c4 (256 problems at 511^2 with
 random (eps, theta), V(1,1) x 10, batched hierarchy).
 
-Multi-GPU (torchrun): c1-c3 place one replica per rank (weak scaling, no
-data-path collective); c4 splits its 256 problems across ranks (strong scaling);
-c5 (32767^2) is domain-decomposed in row blocks with NCCL halo exchange and
-agglomerated coarse levels (strong scaling of the one problem).
+Multi-GPU (torchrun): the single-problem configs c2 (the default), c3 and c5 are
+domain-decomposed in row blocks with NCCL halo exchange overlapped with the interior
+rows and agglomerated coarse levels (strong scaling of the one problem: the N = 1
+line is the same problem on one GPU); c4 splits its 256 problems across ranks (strong
+scaling, no data-path collective); c1 (255^2, L2-resident) places one replica per rank.
 The value is the job's unknowns / max-over-ranks device time.
 
 `--impl reference` times the CPU oracle port of the reference algorithm (NumPy,
@@ -472,8 +473,11 @@ def run_reference(args):
 
 
 def run_dd(args, world, rank, local, dev):
-    """Config 5 over N GPUs: row-block domain decomposition (NCCL halo exchange,
-    agglomerated coarse levels), strong scaling of the one 32767^2 problem."""
+    """A single-problem config over N GPUs (strong scaling of the one problem): row-block
+    domain decomposition of the fine levels (NCCL halo exchange overlapped with the
+    interior rows of every pass, coarse levels agglomerated below 1023 rows).  Every
+    rank builds the same hierarchy (the tables are replicated: band classes for configs
+    2 / 5, per-point planes for config 3) and owns a row block of u and f."""
     import torch
     import torch.distributed as dist
     from paper_2102_12071_b200 import dd, dist as D
@@ -488,23 +492,44 @@ def run_dd(args, world, rank, local, dev):
     stream = torch.cuda.current_stream(dev)
     hist = torch.empty(cycles + 1, dtype=torch.float64, device=dev)
     warm = max(3, args.warmup)
-    for _ in range(warm):
-        solver.run_cycles(cycles, nu, nu, True, hist)
-    dist.barrier()
-    torch.cuda.synchronize(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+
+    def timed(steps, sample_clocks=False):
+        for _ in range(warm if sample_clocks else 2):
+            solver.run_cycles(cycles, nu, nu, True, hist)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = ClockSampler(local) if sample_clocks else None
+        if clk:
+            clk.__enter__()
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             solver.run_cycles(cycles, nu, nu, True, hist)
         ev1.record(stream)
         dist.barrier()
         torch.cuda.synchronize(dev)
-    ms_max = D.max_over_ranks(ev0.elapsed_time(ev1) / args.steps, dev)
+        if clk:
+            clk.__exit__()
+        return D.max_over_ranks(ev0.elapsed_time(ev1) / steps, dev), clk
+
+    ms_max, clk = timed(args.steps, sample_clocks=True)
+    hist_last = float(hist[-1].item())
+    sent, xsteps = solver.stats()
     value = n * n * cycles / (ms_max * 1e-3)
+    # where the exchanges cost: the same schedule without overlap, and with the exchanges
+    # skipped altogether (wrong numbers, right timing: the exposed exchange time)
+    probe = max(1, min(args.steps, 3))
+    solver.set_option("overlap", False)
+    ms_serial, _ = timed(probe)
+    solver.set_option("overlap", True)
+    solver.set_option("exchange", False)
+    ms_noex, _ = timed(probe)
+    solver.set_option("exchange", True)
     # e2e: host block in, solution block out, inside the timed region
     f_pin = f_blk.cpu().pin_memory()
     u_pin = torch.empty_like(f_pin).pin_memory()
+    solver.set_rhs(rank, f_blk)
+    solver.run_cycles(cycles, nu, nu, True, hist)
     dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -528,11 +553,15 @@ def run_dd(args, world, rank, local, dev):
             "data": "synthetic (seeded generators; reference-trained seeded conv net fixture)",
             "config": {"workload": workload_desc(args.config), "unknowns_per_problem": n * n, "problems": 1,
                        "cycles_per_step": cycles, "l2": "inputs larger than L2",
-                       "parallelism": f"row-block domain decomposition x{world} (NCCL halos, "
-                                      f"{solver.distributed_levels} distributed levels, coarse levels agglomerated)"},
+                       "parallelism": f"row-block domain decomposition x{world} (NCCL halos overlapped with the "
+                                      f"interior rows, {solver.distributed_levels} distributed levels, coarse levels "
+                                      f"below 1023 rows agglomerated and solved on every rank)"},
+            "dd": {"rows_per_rank": r1 - r0, "sent_bytes_per_step_rank0": sent, "exchange_steps_per_step": xsteps,
+                   "ms_per_step_without_overlap": ms_serial, "ms_per_step_without_exchanges": ms_noex,
+                   "exchange_exposed_ms": ms_max - ms_noex, "exchange_hidden_by_overlap_ms": ms_serial - ms_max},
             "e2e": {"value": n * n * cycles / (e_ms * 1e-3), "unit": "unknowns/s",
                     "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 8 * n * n + 8 * (cycles + 1)},
-            "gpu_launches": None, "history_last": float(hist[-1].item()), "clocks": clk.summary(),
+            "gpu_launches": None, "history_last": hist_last, "clocks": clk.summary(),
             "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
@@ -551,8 +580,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     D.init("nccl", device=dev)
     cfg = CONFIGS[args.config]
-    if cfg["op"] == "rot_classed" and world > 1:
-        return run_dd(args, world, rank, local, dev)
+    if world > 1 and cfg["batch"] == 1 and cfg["n"] >= 2047:
+        return run_dd(args, world, rank, local, dev)   # one problem over the ranks: strong scaling
     batched = cfg["batch"] > 1
     lo, hi = D.shard(cfg["batch"], rank, world) if batched else (0, 1)
     h, f_host, info = build_problem(args.config, local, lo, hi)

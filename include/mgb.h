@@ -285,6 +285,22 @@ int  mgb_dd_get_solution(const mgb_dd* d, int part, double* u_owned_dev, void* s
 /* fixed-count V(nu1, nu2) cycles of the decomposed solve (graph-replayed); history_dev
    (cycles + 1) as mgb_run_cycles, identical on every rank. */
 int  mgb_dd_run_cycles(mgb_dd* d, int nu1, int nu2, int cycles, int u_zero, double* history_dev, void* stream);
+/* Callback exchange backend (one part per process, created with nccl_id == NULL): every
+   exchange of the rank-local schedule is handed to `fn` after the stream has been
+   synchronised (the cycles then run eagerly, without a graph).  op 0: send `count`
+   doubles at send_dev to rank `peer` and receive `count` doubles from it into recv_dev;
+   op 1: all-gather, `count` doubles at send_dev from every rank into recv_dev in rank
+   order (send_dev is this rank's slot of recv_dev); op 2: all-reduce (sum) of `count`
+   doubles in place at recv_dev.  All pointers are device pointers; return 0 on success. */
+typedef int (*mgb_dd_exchange_fn)(void* ctx, int op, int peer, const double* send_dev, double* recv_dev, int64_t count);
+int  mgb_dd_set_exchange(mgb_dd* d, mgb_dd_exchange_fn fn, void* ctx);
+/* "overlap" (default 1): split every pass into an interior launch that overlaps the halo
+   exchange (side stream) and an edge launch after it; "exchange" (default 1): 0 skips
+   every exchange — wrong results, for timing the exposed exchange cost only. */
+int  mgb_dd_set_option(mgb_dd* d, const char* key, int value);
+/* bytes this process sent (halos + its all-gather slot) and the number of exchange steps
+   in the last enqueued run (all cycles of it) */
+int  mgb_dd_stats(const mgb_dd* d, int64_t* sent_bytes, int* exchanges);
 
 /* Guard mode (environment MGB_GUARD=1 when the library is loaded; tests only): every
    device allocation of the library carries a 4 KiB canary region on each side.  Reports

@@ -82,6 +82,9 @@ SIGNATURES = {
     "mgb_dd_get_solution": (I, [P, I, P, P]),
     "mgb_dd_run_cycles": (I, [P, I, I, I, I, P, P]),
     "mgb_time_pass": (I, [P, P, I, I, I, P, P, I, PD, P]),
+    "mgb_dd_set_exchange": (I, [P, P, P]),
+    "mgb_dd_set_option": (I, [P, C.c_char_p, I]),
+    "mgb_dd_stats": (I, [P, C.POINTER(I64), PI]),
     "mgb_guard_check": (I, [PI, PI]),
     "mgb_last_launch_count": (I64, [P]),
 }

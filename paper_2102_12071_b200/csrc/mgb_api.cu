@@ -1921,6 +1921,9 @@ int hier_depth(const mgb_hier* h) { return h->depth(); }
 int hier_device(const mgb_hier* h) { return h->device; }
 int hier_level_ks(const mgb_hier* h, int l) { return h->lv[l].ks; }
 bool hier_level_classed(const mgb_hier* h, int l) { return h->lv[l].Acls && h->lv[l].Kcls && !h->lv[l].mask; }
+bool hier_level_conv(const mgb_hier* h, int l) { return h->lv[l].conv.nl > 0; }
+const uint8_t* hier_mask(const mgb_hier* h, int l) { return h->lv[l].mask; }
+int hier_a5(const mgb_hier* h, int l) { return h->lv[l].a5 && !h->lv[l].Acls; }
 Grid hier_grid(const mgb_hier* h, int l) { return h->grid(l); }
 Op hier_opA(const mgb_hier* h, int l) { return h->lv[l].opA(); }
 Op hier_opK(const mgb_hier* h, int l) { return h->lv[l].opK(); }

@@ -11,7 +11,17 @@
 //    row blocks on the solve stream, ncclAllGather for agglomeration,
 //    ncclAllReduce of the 8-byte history partial sums — all graph-capturable;
 //  * virtual (all parts in one process on one GPU): the same schedule with
-//    device-to-device copies; used to test the decomposition on a single B200.
+//    device-to-device copies; used to test the decomposition on a single B200;
+//  * callback (one part per process, mgb_dd_set_exchange): every exchange is handed
+//    to a host function after a stream synchronisation (no graph), e.g. a
+//    host-staged gloo exchange between processes that share one GPU — the test of
+//    the rank-local schedule itself where only one GPU exists.
+// Overlap: a pass over a block is split into an interior launch (rows that read no
+// ghost row) and an edge launch; the exchanges run on a side stream while the
+// interior launch runs, the edge launch waits for them (fork / join by events,
+// captured with the rest).  Per-point results do not depend on the split.
+// Levels may hold band-class tables or per-point planes and masks (the tables are
+// replicated on every rank and addressed by global row).
 // Per-point results are independent of the partition (every point runs the
 // same operation sequence), so u matches the single-domain solve bitwise; only
 // the history norms are summed in a different order.
@@ -137,6 +147,13 @@ struct mgb_dd {
   double* f2 = nullptr;          // total ||f||^2
   double* hist_scratch = nullptr;
   nccl::Comm comm = nullptr;
+  mgb_dd_exchange_fn xfn = nullptr;   // callback backend
+  void* xctx = nullptr;
+  bool overlap = true, do_exchange = true;
+  cudaStream_t side = nullptr;        // exchanges of the overlapped schedule
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int64_t halo_bytes = 0;             // bytes this rank sent in the last enqueued run (all cycles)
+  int exchanges = 0;
   cudaStream_t cap = nullptr;
   cudaGraphExec_t graph = nullptr;
   int gkey[4] = {-1, -1, -1, -1};
@@ -159,6 +176,9 @@ struct mgb_dd {
     if (cw) mgb_work_destroy(cw);
     if (comm && nccl::api().ok) nccl::api().CommDestroy(comm);
     if (cap) cudaStreamDestroy(cap);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
   int rows(int l) const { return hier_rows(h, l); }
   int cols(int l) const { return hier_cols(h, l); }
@@ -184,12 +204,12 @@ extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int 
   if (nparts < 1 || nlocal < 1 || first_part < 0 || first_part + nlocal > nparts)
     return fail(MGB_CONFIG, "invalid part layout");
   if (nlocal != nparts && nlocal != 1) return fail(MGB_CONFIG, "either all parts local (virtual) or one per rank");
-  if (nlocal == 1 && nparts > 1 && !nccl_id) return fail(MGB_CONFIG, "multi-rank decomposition needs an NCCL id");
+  // nlocal == 1, nparts > 1 without an NCCL id: the callback backend (mgb_dd_set_exchange)
   if (hier_batch(h) != 1) return fail(MGB_CONFIG, "domain decomposition takes a single problem");
   const int L = hier_depth(h);
   for (int l = 0; l + 1 < L; ++l)
-    if (hier_level_ks(h, l) != 1 || !hier_level_classed(h, l))
-      return fail(MGB_CONFIG, "domain decomposition needs band-class (constant-coefficient) levels with 1-stage smoothers");
+    if (hier_level_ks(h, l) != 1 || hier_level_conv(h, l))
+      return fail(MGB_CONFIG, "domain decomposition needs per-point (or band-class) 1-stage smoothers on every level");
   DeviceGuard dg(hier_device(h));
   std::unique_ptr<mgb_dd> d(new mgb_dd());
   d->h = h;
@@ -238,7 +258,7 @@ extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int 
   }
   d->max_blocks = stream_max_blocks(hier_grid(h, 0));
   for (auto& P : d->parts) {
-    MGB_CUDA_TRY(dalloc(&P.partials, (size_t)d->max_blocks));
+    MGB_CUDA_TRY(dalloc(&P.partials, (size_t)3 * d->max_blocks + 64));   // interior + edge launches
     MGB_CUDA_TRY(dalloc(&P.norm2, 1));
   }
   MGB_CUDA_TRY(dalloc(&d->norm_parts, (size_t)nlocal));
@@ -250,6 +270,13 @@ extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int 
   MGB_CUDA_TRY(dalloc(&d->gather, (size_t)nparts * d->Bc * d->cols(d->La)));
   MGB_CUDA_TRY(cudaMemset(d->gather, 0, sizeof(double) * nparts * d->Bc * d->cols(d->La)));
   MGB_CUDA_TRY(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
+  MGB_CUDA_TRY(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
+  MGB_CUDA_TRY(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
+  MGB_CUDA_TRY(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
+  {
+    static const char* e = getenv("MGB_DD_OVERLAP");
+    if (e) d->overlap = atoi(e) != 0;
+  }
   if (nlocal == 1 && nccl_id) {  // (a 1-rank communicator also takes the NCCL path: tested on one GPU)
     if (!nccl::api().ok) return fail(MGB_NCCL, "libnccl.so.2 not available");
     nccl::UniqueId id;
@@ -275,10 +302,11 @@ extern "C" int mgb_dd_info(const mgb_dd* d, int part, int* r0, int* r1, int* dis
 // ---- halo exchange of one level's field (ghost rows [R0-G, R0) and [R1, R1+G)) ----
 // which: 0 = u, 1 = t, 2 = f
 static int exchange(mgb_dd* d, int l, int which, cudaStream_t s) {
+  if (!d->do_exchange) return MGB_OK;   // timing runs only (results are wrong without the halos)
   const int cols = d->cols(l), rows = d->rows(l);
   auto buf = [&](DDPart& P) -> double* { return which == 0 ? P.u[l] : which == 1 ? P.t[l] : P.f[l]; };
   const size_t gcount = (size_t)G * cols;
-  if (d->comm == nullptr) {
+  if (d->comm == nullptr && d->xfn == nullptr) {
     // virtual: all parts local
     for (int q = 0; q < d->nlocal; ++q) {
       DDPart& P = d->parts[q];
@@ -288,6 +316,7 @@ static int exchange(mgb_dd* d, int l, int which, cudaStream_t s) {
         const double* va = mgb_dd::gview(buf(A), A.R0[l], cols);
         MGB_CUDA_TRY(cudaMemcpyAsync(v + (int64_t)(P.R0[l] - G) * cols, va + (int64_t)(P.R0[l] - G) * cols,
                                      gcount * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        d->halo_bytes += gcount * sizeof(double);
       }
       if (q + 1 < d->nlocal) {
         DDPart& B = d->parts[q + 1];
@@ -295,21 +324,37 @@ static int exchange(mgb_dd* d, int l, int which, cudaStream_t s) {
         const int n = std::min(G, rows - P.R1[l]);
         MGB_CUDA_TRY(cudaMemcpyAsync(v + (int64_t)P.R1[l] * cols, vb + (int64_t)P.R1[l] * cols,
                                      (size_t)n * cols * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        d->halo_bytes += (size_t)n * cols * sizeof(double);
       }
     }
+    ++d->exchanges;
     return MGB_OK;
   }
-  auto& A = nccl::api();
   DDPart& P = d->parts[0];
   double* v = mgb_dd::gview(buf(P), P.R0[l], cols);
   const int me = P.part;
+  const int nb = me + 1 < d->nparts ? std::min(G, rows - P.R1[l]) : 0;
+  ++d->exchanges;
+  d->halo_bytes += ((me > 0 ? gcount : 0) + (size_t)nb * cols) * sizeof(double);
+  if (d->xfn) {
+    // callback backend: the neighbour above first, then the one below (rank 0 starts the chain)
+    MGB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (me > 0)
+      if (d->xfn(d->xctx, 0, me - 1, v + (int64_t)P.R0[l] * cols, v + (int64_t)(P.R0[l] - G) * cols, (int64_t)gcount))
+        return fail(MGB_NCCL, "exchange callback failed (halo, upper neighbour)");
+    if (nb > 0)
+      if (d->xfn(d->xctx, 0, me + 1, v + (int64_t)(P.R1[l] - nb) * cols, v + (int64_t)P.R1[l] * cols,
+                 (int64_t)nb * cols))
+        return fail(MGB_NCCL, "exchange callback failed (halo, lower neighbour)");
+    return MGB_OK;
+  }
+  auto& A = nccl::api();
   MGB_NCCL_TRY(A.GroupStart());
   if (me > 0) {
     MGB_NCCL_TRY(A.Send(v + (int64_t)P.R0[l] * cols, gcount, nccl::Float64, me - 1, d->comm, s));
     MGB_NCCL_TRY(A.Recv(v + (int64_t)(P.R0[l] - G) * cols, gcount, nccl::Float64, me - 1, d->comm, s));
   }
-  if (me + 1 < d->nparts) {
-    const int nb = std::min(G, rows - P.R1[l]);
+  if (nb > 0) {
     MGB_NCCL_TRY(A.Send(v + (int64_t)(P.R1[l] - nb) * cols, (size_t)nb * cols, nccl::Float64, me + 1, d->comm, s));
     MGB_NCCL_TRY(A.Recv(v + (int64_t)P.R1[l] * cols, (size_t)nb * cols, nccl::Float64, me + 1, d->comm, s));
   }
@@ -324,6 +369,10 @@ static int reduce_norm(mgb_dd* d, double* dst, cudaStream_t s) {
   k_sum_norm<<<1, 32, 0, s>>>(d->norm_parts, d->nlocal, dst);
   MGB_CUDA_TRY(cudaGetLastError());
   if (d->comm) MGB_NCCL_TRY(nccl::api().AllReduce(dst, dst, 1, nccl::Float64, nccl::Sum, d->comm, s));
+  if (d->xfn) {
+    MGB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (d->xfn(d->xctx, 2, -1, nullptr, dst, 1)) return fail(MGB_NCCL, "exchange callback failed (all-reduce)");
+  }
   return MGB_OK;
 }
 
@@ -332,29 +381,100 @@ static StreamArgs dd_args(const mgb_dd* d, int l, cudaStream_t s) {
   a.g = hier_grid(d->h, l);
   a.A = hier_opA(d->h, l);
   a.K = hier_opK(d->h, l);
+  a.mask = hier_mask(d->h, l);
+  a.mask_c = hier_mask(d->h, l + 1);
+  a.a5 = hier_a5(d->h, l);
   a.stream = s;
   hier_interior(d->h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel);
   return a;
+}
+
+// Rows of a block's edge launches: a pass over rows [x, y) reads rows [x - 6, y + 5], so
+// the interior launch over [R0 + EDGE, R1 - EDGE) touches owned rows only.  Even, so the
+// sub-ranges start at even rows like the blocks themselves (coarse anchors 2c + 1 never
+// straddle a boundary).
+static constexpr int EDGE = 32;
+
+// One pass (PRE: res; POST: pro; or the plain norm sweep) over part P's rows of level l.
+// phase 0: the interior rows, 1: the edge rows, 2: the whole block in one launch.  With
+// norm, the launches' partial sums are appended at P.partials + *npart.
+static int launch_rows(mgb_dd* d, int l, DDPart& P, StreamArgs a, int nsw, bool res, bool pro, bool norm, int phase,
+                       int* npart) {
+  const int R0 = P.R0[l], R1 = P.R1[l];
+  // a block edge on the physical boundary needs no ghost rows: it belongs to the interior launch
+  const int lo = P.part == 0 ? R0 : R0 + EDGE, hi = P.part == d->nparts - 1 ? R1 : R1 - EDGE;
+  int ranges[2][2], nr = 0;
+  if (phase == 2) {
+    ranges[nr][0] = R0, ranges[nr++][1] = R1;
+  } else if (phase == 0) {
+    ranges[nr][0] = lo, ranges[nr++][1] = hi;
+  } else {
+    if (lo > R0) ranges[nr][0] = R0, ranges[nr++][1] = lo;
+    if (hi < R1) ranges[nr][0] = hi, ranges[nr++][1] = R1;
+  }
+  for (int q = 0; q < nr; ++q) {
+    a.own0 = ranges[q][0];
+    a.own1 = ranges[q][1];
+    if (a.own1 <= a.own0) continue;
+    a.partials = norm ? P.partials + *npart : nullptr;
+    int nb = 0;
+    MGB_CUDA_TRY(launch_stream(a, nsw, res, pro, norm, &nb));
+    if (norm) *npart += nb;
+  }
+  return MGB_OK;
+}
+
+static bool split_ok(const mgb_dd* d, int l) {
+  if (!d->overlap || d->nparts == 1) return false;
+  for (auto& P : d->parts)
+    if (P.R1[l] - P.R0[l] < 4 * EDGE) return false;
+  return true;
+}
+
+// Run `exchanges` (the halo exchanges a pass needs) and the pass `rows(phase)`.  Overlapped:
+// the exchanges go to the side stream while the interior rows run on s; the edge rows wait
+// for them.  Otherwise: exchanges, then the whole block.
+template <typename FX, typename FR>
+static int exchange_and_pass(mgb_dd* d, int l, cudaStream_t s, bool any_exchange, FX exchanges, FR rows) {
+  if (!any_exchange || !split_ok(d, l)) {
+    if (int st = exchanges(s)) return st;
+    return rows(2);
+  }
+  if (d->xfn) {   // callback backend: eager and synchronous, same launches
+    if (int st = exchanges(s)) return st;
+    if (int st = rows(0)) return st;
+    return rows(1);
+  }
+  MGB_CUDA_TRY(cudaEventRecord(d->ev_fork, s));
+  MGB_CUDA_TRY(cudaStreamWaitEvent(d->side, d->ev_fork, 0));
+  if (int st = exchanges(d->side)) return st;
+  MGB_CUDA_TRY(cudaEventRecord(d->ev_join, d->side));
+  if (int st = rows(0)) return st;
+  MGB_CUDA_TRY(cudaStreamWaitEvent(s, d->ev_join, 0));
+  return rows(1);
 }
 
 // residual norm^2 of the current level-0 u (or of f when u == null) per part, via a
 // streaming plain-sweep pass whose output goes to scratch
 static int norm_pass(mgb_dd* d, bool of_f, double* dst, cudaStream_t s) {
   const int cols = d->cols(0);
-  if (!of_f)
-    if (int st = exchange(d, 0, 0, s)) return st;
-  for (auto& P : d->parts) {
-    StreamArgs a = dd_args(d, 0, s);
-    a.f = mgb_dd::gview(P.f[0], P.R0[0], cols);
-    a.u = of_f ? nullptr : mgb_dd::gview(P.u[0], P.R0[0], cols);
-    a.uo = mgb_dd::gview(P.t[0], P.R0[0], cols);
-    a.partials = P.partials;
-    a.own0 = P.R0[0];
-    a.own1 = P.R1[0];
-    int nb = 0;
-    MGB_CUDA_TRY(launch_stream(a, 1, false, false, true, &nb));
-    MGB_CUDA_TRY(launch_finalize(1, nb, P.partials, P.norm2, nullptr, nullptr, 0, s));
-  }
+  std::vector<int> np(d->parts.size(), 0);
+  auto rows = [&](int phase) -> int {
+    for (size_t q = 0; q < d->parts.size(); ++q) {
+      DDPart& P = d->parts[q];
+      StreamArgs a = dd_args(d, 0, s);
+      a.f = mgb_dd::gview(P.f[0], P.R0[0], cols);
+      a.u = of_f ? nullptr : mgb_dd::gview(P.u[0], P.R0[0], cols);
+      a.uo = mgb_dd::gview(P.t[0], P.R0[0], cols);
+      if (int st = launch_rows(d, 0, P, a, 1, false, false, true, phase, &np[q])) return st;
+    }
+    return MGB_OK;
+  };
+  if (int st = exchange_and_pass(d, 0, s, !of_f, [&](cudaStream_t x) { return of_f ? MGB_OK : exchange(d, 0, 0, x); },
+                                 rows))
+    return st;
+  for (size_t q = 0; q < d->parts.size(); ++q)
+    MGB_CUDA_TRY(launch_finalize(1, np[q], d->parts[q].partials, d->parts[q].norm2, nullptr, nullptr, 0, s));
   return reduce_norm(d, dst, s);
 }
 
@@ -365,34 +485,42 @@ static int dd_cycle(mgb_dd* d, int nu1, int nu2, bool zero, double* hist, cudaSt
   for (int l = 0; l < Ld; ++l) {
     const int cols = d->cols(l);
     const bool z = zero || l > 0;
-    if (!z)
-      if (int st = exchange(d, l, 0, s)) return st;
-    if (l > 0)
-      if (int st = exchange(d, l, 2, s)) return st;
     const bool last = l + 1 == Ld;
-    for (auto& P : d->parts) {
-      StreamArgs a = dd_args(d, l, s);
-      a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
-      a.u = z ? nullptr : mgb_dd::gview(P.u[l], P.R0[l], cols);
-      a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
-      a.own0 = P.R0[l];
-      a.own1 = P.R1[l];
-      if (last) {
-        // restricted residual straight into this part's slot of the gather layout
-        const int cc = d->cols(La);
-        a.rc = d->gather + (int64_t)P.part * d->Bc * cc - (int64_t)(P.R0[l] / 2) * cc;
-      } else {
-        const int cc = d->cols(l + 1);
-        a.rc = mgb_dd::gview(P.f[l + 1], P.R0[l] / 2, cc);
+    const bool nrm = hist && l == 0;
+    std::vector<int> np(d->parts.size(), 0);
+    auto rows = [&](int phase) -> int {
+      for (size_t q = 0; q < d->parts.size(); ++q) {
+        DDPart& P = d->parts[q];
+        StreamArgs a = dd_args(d, l, s);
+        a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
+        a.u = z ? nullptr : mgb_dd::gview(P.u[l], P.R0[l], cols);
+        a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
+        if (last) {
+          // restricted residual straight into this part's slot of the gather layout
+          const int cc = d->cols(La);
+          a.rc = d->gather + (int64_t)P.part * d->Bc * cc - (int64_t)(P.R0[l] / 2) * cc;
+        } else {
+          const int cc = d->cols(l + 1);
+          a.rc = mgb_dd::gview(P.f[l + 1], P.R0[l] / 2, cc);
+        }
+        if (int st = launch_rows(d, l, P, a, nu1, true, false, nrm, phase, &np[q])) return st;
       }
-      const bool nrm = hist && l == 0;
-      a.partials = nrm ? P.partials : nullptr;
-      int nb = 0;
-      MGB_CUDA_TRY(launch_stream(a, nu1, true, false, nrm, &nb));
-      if (nrm) MGB_CUDA_TRY(launch_finalize(1, nb, P.partials, P.norm2, nullptr, nullptr, 0, s));
+      return MGB_OK;
+    };
+    auto xch = [&](cudaStream_t x) -> int {
+      if (!z)
+        if (int st = exchange(d, l, 0, x)) return st;
+      if (l > 0)
+        if (int st = exchange(d, l, 2, x)) return st;
+      return MGB_OK;
+    };
+    if (int st = exchange_and_pass(d, l, s, !z || l > 0, xch, rows)) return st;
+    for (size_t q = 0; q < d->parts.size(); ++q) {
+      DDPart& P = d->parts[q];
+      if (nrm) MGB_CUDA_TRY(launch_finalize(1, np[q], P.partials, P.norm2, nullptr, nullptr, 0, s));
       std::swap(P.u[l], P.t[l]);
     }
-    if (hist && l == 0) {
+    if (nrm) {
       if (int st = reduce_norm(d, d->r2, s)) return st;
       k_hist_entry<<<1, 32, 0, s>>>(d->r2, d->f2, hist);
       MGB_CUDA_TRY(cudaGetLastError());
@@ -401,10 +529,16 @@ static int dd_cycle(mgb_dd* d, int nu1, int nu2, bool zero, double* hist, cudaSt
   // agglomerate: every rank gets the whole restricted residual, solves the coarse part
   const int cc = d->cols(La);
   const size_t blkc = (size_t)d->Bc * cc;
-  if (d->comm) {
+  if (d->comm && d->do_exchange) {
     MGB_NCCL_TRY(nccl::api().AllGather(d->gather + (int64_t)d->first * blkc, d->gather, blkc, nccl::Float64,
                                        d->comm, s));
   }
+  if (d->xfn && d->do_exchange) {
+    MGB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (d->xfn(d->xctx, 1, -1, d->gather + (int64_t)d->first * blkc, d->gather, (int64_t)blkc))
+      return fail(MGB_NCCL, "exchange callback failed (all-gather)");
+  }
+  if (d->nparts > 1 && d->do_exchange) d->halo_bytes += blkc * sizeof(double) * (d->comm || d->xfn ? 1 : d->nparts);
   double* cf = work_level_f(d->cw, La);
   double* cu = work_level_u(d->cw, La);
   MGB_CUDA_TRY(cudaMemcpyAsync(cf, d->gather, sizeof(double) * d->rows(La) * cc, cudaMemcpyDeviceToDevice, s));
@@ -413,23 +547,55 @@ static int dd_cycle(mgb_dd* d, int nu1, int nu2, bool zero, double* hist, cudaSt
   // ascend
   for (int l = Ld - 1; l >= 0; --l) {
     const int cols = d->cols(l);
-    if (int st = exchange(d, l, 0, s)) return st;
-    if (l + 1 < Ld)
-      if (int st = exchange(d, l + 1, 0, s)) return st;
-    for (auto& P : d->parts) {
-      StreamArgs a = dd_args(d, l, s);
-      a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
-      a.u = mgb_dd::gview(P.u[l], P.R0[l], cols);
-      a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
-      a.own0 = P.R0[l];
-      a.own1 = P.R1[l];
-      if (l + 1 < Ld) a.ec = mgb_dd::gview(P.u[l + 1], P.R0[l + 1], d->cols(l + 1));
-      else a.ec = ec_full;
-      int nb = 0;
-      MGB_CUDA_TRY(launch_stream(a, nu2, false, true, false, &nb));
-      std::swap(P.u[l], P.t[l]);
-    }
+    int unused = 0;
+    auto rows = [&](int phase) -> int {
+      for (auto& P : d->parts) {
+        StreamArgs a = dd_args(d, l, s);
+        a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
+        a.u = mgb_dd::gview(P.u[l], P.R0[l], cols);
+        a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
+        if (l + 1 < Ld) a.ec = mgb_dd::gview(P.u[l + 1], P.R0[l + 1], d->cols(l + 1));
+        else a.ec = ec_full;
+        if (int st = launch_rows(d, l, P, a, nu2, false, true, false, phase, &unused)) return st;
+      }
+      return MGB_OK;
+    };
+    auto xch = [&](cudaStream_t x) -> int {
+      if (int st = exchange(d, l, 0, x)) return st;
+      if (l + 1 < Ld)
+        if (int st = exchange(d, l + 1, 0, x)) return st;
+      return MGB_OK;
+    };
+    if (int st = exchange_and_pass(d, l, s, true, xch, rows)) return st;
+    for (auto& P : d->parts) std::swap(P.u[l], P.t[l]);
   }
+  return MGB_OK;
+}
+
+extern "C" int mgb_dd_set_exchange(mgb_dd* d, mgb_dd_exchange_fn fn, void* ctx) {
+  if (!d) return fail(MGB_CONTRACT, "null decomposition");
+  if (d->comm) return fail(MGB_CONFIG, "this decomposition already exchanges through NCCL");
+  if (d->nlocal != 1) return fail(MGB_CONFIG, "the callback backend holds one part per process");
+  d->xfn = fn;
+  d->xctx = ctx;
+  return MGB_OK;
+}
+
+extern "C" int mgb_dd_set_option(mgb_dd* d, const char* key, int value) {
+  if (!d || !key) return fail(MGB_CONTRACT, "null argument");
+  const std::string k(key);
+  if (k == "overlap") d->overlap = value != 0;
+  else if (k == "exchange") d->do_exchange = value != 0;
+  else return fail(MGB_CONFIG, "unknown decomposition option " + k);
+  if (d->graph) cudaGraphExecDestroy(d->graph);   // the captured schedule depends on both
+  d->graph = nullptr;
+  return MGB_OK;
+}
+
+extern "C" int mgb_dd_stats(const mgb_dd* d, int64_t* sent_bytes, int* exchanges) {
+  if (!d) return fail(MGB_CONTRACT, "null decomposition");
+  if (sent_bytes) *sent_bytes = d->halo_bytes;
+  if (exchanges) *exchanges = d->exchanges;
   return MGB_OK;
 }
 
@@ -460,6 +626,8 @@ extern "C" int mgb_dd_get_solution(const mgb_dd* d, int part, double* u_owned_de
 }
 
 static int dd_enqueue(mgb_dd* d, int nu1, int nu2, int cycles, int u_zero, double* hist, cudaStream_t s) {
+  d->halo_bytes = 0;
+  d->exchanges = 0;
   if (int st = exchange(d, 0, 2, s)) return st;  // f ghosts of level 0
   if (int st = norm_pass(d, true, d->f2, s)) return st;
   for (int c = 0; c < cycles; ++c)
@@ -478,6 +646,9 @@ extern "C" int mgb_dd_run_cycles(mgb_dd* d, int nu1, int nu2, int cycles, int u_
   DeviceGuard dg(d->device);
   cudaStream_t s = S(stream);
   if (int st = work_prepare(d->cw)) return st;
+  if (d->nlocal == 1 && d->nparts > 1 && !d->comm && !d->xfn)
+    return fail(MGB_CONFIG, "this decomposition has neither an NCCL communicator nor an exchange callback");
+  if (d->xfn) return dd_enqueue(d, nu1, nu2, cycles, u_zero, history_dev, s);   // eager: host exchanges
   // one CUDA graph per (nu1, nu2, cycles, u_zero, history) (halo copies / NCCL ops are captured too)
   const int key[4] = {nu1, nu2, cycles, u_zero};
   if (!d->graph || std::memcmp(key, d->gkey, sizeof(key)) != 0 || d->ghist != history_dev) {

@@ -16,6 +16,9 @@ int hier_depth(const mgb_hier* h);
 int hier_device(const mgb_hier* h);
 int hier_level_ks(const mgb_hier* h, int l);
 bool hier_level_classed(const mgb_hier* h, int l);
+bool hier_level_conv(const mgb_hier* h, int l);
+const uint8_t* hier_mask(const mgb_hier* h, int l);
+int hier_a5(const mgb_hier* h, int l);
 Grid hier_grid(const mgb_hier* h, int l);
 Op hier_opA(const mgb_hier* h, int l);
 Op hier_opK(const mgb_hier* h, int l);
