@@ -484,7 +484,9 @@ def run_dd(args, world, rank, local, dev):
     cfg = CONFIGS[args.config]
     h, f_host, info = build_problem(args.config, local)
     n, nu, cycles = cfg["n"], cfg["nu"], cfg["cycles"]
-    solver = dd.from_process_group(h, agglomerate_rows=1023)
+    host_backend = dist.get_backend() == "gloo"
+    rdev = None if host_backend else dev   # device of the control-plane reductions
+    solver = dd.from_process_group(h, agglomerate_rows=1023, backend="host" if host_backend else "nccl")
     r0, r1 = solver.rows(rank)
     f_blk = torch.from_numpy(np.ascontiguousarray(f_host[0, r0:r1])).to(dev)
     del f_host
@@ -510,7 +512,7 @@ def run_dd(args, world, rank, local, dev):
         torch.cuda.synchronize(dev)
         if clk:
             clk.__exit__()
-        return D.max_over_ranks(ev0.elapsed_time(ev1) / steps, dev), clk
+        return D.max_over_ranks(ev0.elapsed_time(ev1) / steps, rdev), clk
 
     ms_max, clk = timed(args.steps, sample_clocks=True)
     hist_last = float(hist[-1].item())
@@ -544,7 +546,7 @@ def run_dd(args, world, rank, local, dev):
     e1.record(stream)
     dist.barrier()
     torch.cuda.synchronize(dev)
-    e_ms = D.max_over_ranks(e0.elapsed_time(e1) / e_steps, dev)
+    e_ms = D.max_over_ranks(e0.elapsed_time(e1) / e_steps, rdev)
     if rank == 0:
         line = {
             "metric": "unknowns/sec per V-cycle (fp64)", "value": value, "unit": "unknowns/s", "n_gpus": world,
@@ -576,9 +578,14 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_2102_12071_b200 import _lib, device as dv, dist as D
     world, rank, local = D.env()
+    # MGB_BENCH_BACKEND=gloo: the test of this script's multi-rank path on one GPU (ranks
+    # share cuda:0 and the decomposition exchanges through the host); never a measurement
+    backend = os.environ.get("MGB_BENCH_BACKEND", "nccl")
+    if backend == "gloo":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    D.init("nccl", device=dev)
+    D.init(backend, device=dev)
     cfg = CONFIGS[args.config]
     if world > 1 and cfg["batch"] == 1 and cfg["n"] >= 2047:
         return run_dd(args, world, rank, local, dev)   # one problem over the ranks: strong scaling
