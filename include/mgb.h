@@ -302,6 +302,51 @@ int  mgb_dd_set_option(mgb_dd* d, const char* key, int value);
    in the last enqueued run (all cycles of it) */
 int  mgb_dd_stats(const mgb_dd* d, int64_t* sent_bytes, int* exchanges);
 
+/* ---- training path: device kernels behind the Python tape ----------
+   The backward passes of the grid operations (autodiff.py:139-325), the small dense and
+   batched-convolution operations of the kernel-inference nets, the transposed coarsest
+   solve (dense.py:66-80) and Adam (training.py:73-93).  All pointers are device pointers,
+   fp64; reductions over points are deterministic.  `scratch_dev` buffers hold
+   mgb_ad_scratch_doubles(outputs) doubles. */
+int mgb_ad_scratch_doubles(int outputs);
+/* z = a x + b y (y == NULL: z = a x); a = 1, b = +-1 give x + y and x - y exactly */
+int mgb_ad_axpby(int64_t n, double a, const double* x_dev, double b, const double* y_dev, double* z_dev, void* stream);
+/* z[i] = x[i] * c[i / c_repeat] (c_repeat <= 1: c[i]) */
+int mgb_ad_mul(int64_t n, const double* x_dev, const double* c_dev, int64_t c_repeat, double* z_dev, void* stream);
+/* g_dev == NULL: z = leaky(x); else z = g * leaky'(x)  (autodiff.py:86-96) */
+int mgb_ad_leaky(int64_t n, const double* x_dev, double slope, const double* g_dev, double* z_dev, void* stream);
+/* x (n, c, inner) -> z (n, inner) summed over c; and its backward gx += broadcast(g)  (autodiff.py:109-115) */
+int mgb_ad_sum_axis1(int64_t n, int c, int inner, const double* x_dev, double* z_dev, void* stream);
+int mgb_ad_bcast_axis1(int64_t n, int c, int inner, const double* g_dev, double* gx_dev, void* stream);
+/* out_dev[0] = sum x y (y == NULL: sum x^2) */
+int mgb_ad_dot(int64_t n, const double* x_dev, const double* y_dev, double* scratch_dev, double* out_dev, void* stream);
+/* du(q) = sum_d T(q - d)[d] gm(q - d) with gm = g on mask_in, du zeroed off mask_out (either
+   mask may be NULL); T (rows, cols, 3, 3).  order 0: the backward of stencil_apply
+   (autodiff.py:183-190, T = the operator table), 1: the du of pointwise_conv (:274-279). */
+int mgb_ad_stencil_adjoint(int rows, int cols, const double* T_dev, const uint8_t* mask_in_dev,
+                           const uint8_t* mask_out_dev, const double* g_dev, int order, double* du_dev, void* stream);
+/* dK(p)[d] (+)= gm(p) u(p + d): the kernel gradient of pointwise_conv (autodiff.py:268-273) */
+int mgb_ad_pconv_kgrad(int rows, int cols, const uint8_t* mask_dev, const double* g_dev, const double* u_dev,
+                       int accumulate, double* dK_dev, void* stream);
+/* dk[d] (+)= sum_p gm(p) u(p + d): the kernel gradient of conv2d (autodiff.py:152-159) */
+int mgb_ad_conv_kgrad(int rows, int cols, int ksize, const uint8_t* mask_dev, const double* g_dev, const double* u_dev,
+                      double* scratch_dev, int accumulate, double* dk_dev, void* stream);
+/* conv_batch (autodiff.py:283-325): kern (c, 3, 3), img (n, 3, 3) -> out (n, c, 3, 3); backward
+   into dk_dev (c, 3, 3) and / or dimg_dev (n, 3, 3) (either may be NULL) */
+int mgb_ad_conv_batch(int64_t n, int c, const double* kern_dev, const double* img_dev, double* out_dev, void* stream);
+int mgb_ad_conv_batch_bwd(int64_t n, int c, const double* kern_dev, const double* img_dev, const double* g_dev,
+                          double* scratch_dev, int acc_k, double* dk_dev, int acc_img, double* dimg_dev, void* stream);
+/* C (M, N) (+)= op(A) op(B), row-major; trans_a: A stored (K, M); trans_b: B stored (N, K)
+   (autodiff.py:128-137 forward and both backward products) */
+int mgb_ad_matmul(int M, int K, int N, const double* A_dev, int trans_a, const double* B_dev, int trans_b,
+                  int accumulate, double* C_dev, double* scratch_dev, void* stream);
+/* dense.lu_solve_t (dense.py:66-80): A^T x = b from the factorisation of A; scratch_dev: n doubles */
+int mgb_lu_solve_t(int n, const double* lu_dev, const int32_t* perm_dev, const double* b_dev, double* x_dev,
+                   double* scratch_dev, void* stream);
+/* one Adam step of training.py:73-93 on a parameter array (g_dev == NULL: zero gradient) */
+int mgb_ad_adam(int64_t n, double* p_dev, const double* g_dev, double* m_dev, double* v_dev, double lr, double beta1,
+                double beta2, double eps, int step, void* stream);
+
 /* Guard mode (environment MGB_GUARD=1 when the library is loaded; tests only): every
    device allocation of the library carries a 4 KiB canary region on each side.  Reports
    the number of live allocations and of those whose canaries were overwritten (their

@@ -85,6 +85,21 @@ SIGNATURES = {
     "mgb_dd_set_exchange": (I, [P, P, P]),
     "mgb_dd_set_option": (I, [P, C.c_char_p, I]),
     "mgb_dd_stats": (I, [P, C.POINTER(I64), PI]),
+    "mgb_ad_scratch_doubles": (I, [I]),
+    "mgb_ad_axpby": (I, [I64, D, P, D, P, P, P]),
+    "mgb_ad_mul": (I, [I64, P, P, I64, P, P]),
+    "mgb_ad_leaky": (I, [I64, P, D, P, P, P]),
+    "mgb_ad_sum_axis1": (I, [I64, I, I, P, P, P]),
+    "mgb_ad_bcast_axis1": (I, [I64, I, I, P, P, P]),
+    "mgb_ad_dot": (I, [I64, P, P, P, P, P]),
+    "mgb_ad_stencil_adjoint": (I, [I, I, P, P, P, P, I, P, P]),
+    "mgb_ad_pconv_kgrad": (I, [I, I, P, P, P, I, P, P]),
+    "mgb_ad_conv_kgrad": (I, [I, I, I, P, P, P, P, I, P, P]),
+    "mgb_ad_conv_batch": (I, [I64, I, P, P, P, P]),
+    "mgb_ad_conv_batch_bwd": (I, [I64, I, P, P, P, P, I, P, I, P, P]),
+    "mgb_ad_matmul": (I, [I, I, I, P, I, P, I, I, P, P, P]),
+    "mgb_lu_solve_t": (I, [I, P, P, P, P, P, P]),
+    "mgb_ad_adam": (I, [I64, P, P, P, P, D, D, D, D, I, P]),
     "mgb_guard_check": (I, [PI, PI]),
     "mgb_last_launch_count": (I64, [P]),
 }

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmgb.so")
-SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_stream2.cu", "mgb_stream3.cu", "mgb_tile.cu", "mgb_coarse.cu", "mgb_dd.cu", "mgb_krylov.cu", "mgb_conv.cu", "mgb_cnn.cu", "mgb_api.cu"]
+SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_stream2.cu", "mgb_stream3.cu", "mgb_tile.cu", "mgb_coarse.cu", "mgb_dd.cu", "mgb_krylov.cu", "mgb_conv.cu", "mgb_cnn.cu", "mgb_train.cu", "mgb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
