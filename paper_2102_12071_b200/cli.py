@@ -19,8 +19,11 @@ and `--precision 64|32` (CNN inference arithmetic).  Every CSV row gains `device
 one when level 0 holds band-class tables) and `roofline_frac` (of the HBM peak in
 MEASURED_PEAKS.json, else the profiling recipe's fallback).
 
-`train` and `analyze` are not on the B200 path (SURVEY 8(f) row 4 / out of scope):
-they exit 1 with the reference's UnsupportedOperationError message format.
+`train` (cli.py:489-587) runs the GPU trainers of training.py: `--variant conv|fc` the
+staged kernel-inference-net training, else the adaptive / independent conv-smoother
+strategies; it writes model.json, loss.csv and manifest.json as the reference does
+(mixture `--thetas` and `--inject-k` are not on the B200 path).  `analyze` is out of
+scope: it exits 1 with the reference's UnsupportedOperationError message format.
 """
 
 from __future__ import annotations
@@ -106,6 +109,16 @@ _EXT = (("device", "str", "b200", ("b200",), "ext"), ("gpus", "int", 1, None, "e
         ("sweeps", "int", 1, None, "ext"), ("precision", "int", 64, (64, 32), "ext"))
 _OUT = (("out", "str", ".", None, "plain"), ("csv", "str", None, None, "plain"))
 OPTIONS = {
+    "train": _opts(
+        ("family", "str", "rotated", ("rotated", "variable")), ("n", "int", 16), ("geometry", "str", "square", _GEOS),
+        ("theta", "angle", 0.0), ("xi", "float", 100.0), ("kappa", "float", 1.0), ("levels", "int", 2),
+        ("scheme", "str", "full", ("full", "redblack")),
+        ("strategy", "str", "adaptive", ("adaptive", "independent")), ("variant", "str", None, ("fc", "conv")),
+        ("net_k", "int", 1), ("form", "str", "full", ("full", "rb")), ("omega", "float", 2.0 / 3.0),
+        ("activation", "str", "linear", ("linear", "leaky")), ("epochs", "int", 500), ("samples", "int", 50),
+        ("batch_size", "int", 10), ("learning_rate", "float", 1e-3), ("max_steps", "int", 4), ("inject_k", "int", 0),
+        ("thetas", "angles", None), ("seed", "int", 0), ("out", "str", ".", None, "plain"),
+        ("device", "str", "b200", ("b200",), "ext")),
     "solve": _opts(
         ("family", "str", "rotated", ("rotated", "variable")), ("n", "int", 16), ("geometry", "str", "square", _GEOS),
         ("theta", "angle", 0.0), ("xi", "float", 100.0), ("kappa", "float", 1.0), ("levels", "int", 2),
@@ -442,7 +455,84 @@ def _not_on_path(name: str):
     return run
 
 
-COMMANDS = {"solve": cmd_solve, "bench": cmd_bench, "train": _not_on_path("train"), "analyze": _not_on_path("analyze")}
+def stack_to_dict(problem, hier, metadata: dict) -> dict:
+    """cli.py:317-331: a hierarchy's conv smoothers with the problem they were trained on."""
+    from . import model_to_dict
+    return {"format_version": 1, "kind": "smoother_stack", "problem": problem.asdict(), "scheme": hier.scheme,
+            "levels": hier.depth, "metadata": metadata,
+            "smoothers": [model_to_dict(lev.smoother) for lev in hier.levels[:-1]]}
+
+
+def _stack_params(hier) -> int:
+    total = 0
+    for lev in hier.levels[:-1]:
+        sm = lev.smoother
+        total += sum(k.weights.size for k in sm.layers) + (sm.skip.weights.size if sm.skip is not None else 0)
+    return total
+
+
+def cmd_train(cfg: dict) -> int:
+    """cli.py:489-587 on the GPU trainers."""
+    from . import build_hierarchy, model_to_dict, training as tr
+    from .problems import ProblemSpec
+    _visible_gpus(dict(cfg, gpus=1))
+    chash = config_hash("train", cfg)
+    problem = ProblemSpec(cfg["family"], cfg["n"], cfg["geometry"], cfg["theta"], cfg["xi"], cfg["kappa"])
+    tc = tr.TrainConfig(samples=cfg["samples"], max_steps=cfg["max_steps"], batch_size=cfg["batch_size"],
+                        learning_rate=cfg["learning_rate"], epochs=cfg["epochs"], seed=cfg["seed"])
+    A = problem.assemble()
+    meta = {"config_hash": chash, "seed": cfg["seed"], "epochs": cfg["epochs"]}
+    notes = []
+    t0 = time.perf_counter()
+    if cfg["thetas"] is not None:
+        raise UnsupportedOperationError("mixture training (--thetas) is not on the B200 path")
+    if cfg["inject_k"] > 0:
+        raise UnsupportedOperationError("residual-injection retraining (--inject-k) is not on the B200 path")
+    if cfg["variant"] is not None:
+        net, hier, records = tr.train_inference_net(A, cfg["variant"], cfg["levels"], tc, k=cfg["net_k"])
+        params = net.parameter_count()
+        doc = model_to_dict(net, {**meta, "parameters": params, "problem": problem.asdict()})
+    elif cfg["strategy"] == "independent":
+        sm, record = tr.train_independent(A, tc, form=cfg["form"], omega=cfg["omega"], activation=cfg["activation"])
+        hier = build_hierarchy(A, 2, scheme=cfg["scheme"])   # saved as a depth-2 stack (cli.py:527-531)
+        hier.levels[0].smoother = sm
+        records = [record]
+        params = _stack_params(hier)
+        doc = stack_to_dict(problem, hier, {**meta, "parameters": params})
+    else:
+        hier, records = tr.train_adaptive(A, cfg["levels"], tc, scheme=cfg["scheme"], omega=cfg["omega"],
+                                          activation=cfg["activation"])
+        params = _stack_params(hier)
+        doc = stack_to_dict(problem, hier, {**meta, "parameters": params})
+    wall = time.perf_counter() - t0
+    if cfg["epochs"] < 500:
+        notes.append("epochs below the 500 default")
+    os.makedirs(cfg["out"], exist_ok=True)
+    model_path = os.path.join(cfg["out"], "model.json")
+    with open(model_path, "w") as fh:
+        json.dump(doc, fh, sort_keys=True)
+    loss_path = os.path.join(cfg["out"], "loss.csv")
+    write_csv(loss_path, ["config_hash", "seed", "level", "epoch", "loss"],
+              [{"config_hash": chash, "seed": cfg["seed"], "level": rec.level, "epoch": e, "loss": f"{v:.10e}"}
+               for rec in records for e, v in enumerate(rec.epochs)])
+    manifest = {"subcommand": "train",
+                "config": {k: render(OPTIONS["train"][k][0], v) for k, v in cfg.items() if v is not None},
+                "config_hash": chash, "seed": cfg["seed"], "problem": problem.asdict(), "parameters": params,
+                "records": [{"level": r.level, "epochs": len(r.epochs), "initial": r.initial if r.epochs else None,
+                             "final": r.final if r.epochs else None} for r in records],
+                "wall_time": wall, "notes": notes, "device": cfg["device"],
+                "outputs": {"model": model_path, "loss": loss_path}}
+    with open(os.path.join(cfg["out"], "manifest.json"), "w") as fh:
+        json.dump(manifest, fh, indent=2, sort_keys=True)
+    print(f"model: {model_path}")
+    print(f"parameters: {params}")
+    for r in records:
+        print(f"level {r.level}: loss {r.initial:.6f} -> {r.final:.6f} ({len(r.epochs)} epochs)" if r.epochs
+              else f"level {r.level}: initialization kept (0 epochs)")
+    return 0
+
+
+COMMANDS = {"train": cmd_train, "solve": cmd_solve, "bench": cmd_bench, "analyze": _not_on_path("analyze")}
 
 
 def main(argv=None) -> int:
@@ -450,7 +540,7 @@ def main(argv=None) -> int:
     parser = build_parser()
     args = sys.argv[1:] if argv is None else list(argv)
     try:
-        if args and args[0] in ("train", "analyze"):
+        if args and args[0] == "analyze":
             return COMMANDS[args[0]]({})
         ns = parser.parse_args(args)
         if ns.subcommand is None:

@@ -53,8 +53,9 @@ def test_angles_and_config_files(tmp_path, monkeypatch):
 
 
 def test_exit_codes_without_running(capsys):
-    assert cli.main(["train", "--n", "15"]) == 1                  # not on the B200 path
+    assert cli.main(["analyze", "--n", "15"]) == 1                # not on the B200 path
     assert "not on the B200 path" in capsys.readouterr().err
+    assert cli.main(["train", "--n", "15", "--thetas", "0.1,0.2"]) == 1   # mixture training: unsupported
     assert cli.main(["solve", "--device", "cpu"]) == 1            # no CPU fallback
     assert cli.main(["solve", "--n", "many"]) == 1
     assert cli.main([]) == 1
@@ -99,3 +100,37 @@ def test_sweeps_extension_and_trial_dealing(tmp_path, monkeypatch):
         its.append(int(list(csv.DictReader(open(path)))[0]["iterations"]))
     assert its[1] < its[0]
     assert cli.main(base + ["--gpus", "64"]) == 1
+
+
+TRAIN_ARGV = ["train", "--n", "15", "--theta", "pi/6", "--xi", "0.01", "--levels", "3", "--epochs", "2", "--samples", "4",
+              "--batch-size", "2", "--max-steps", "2"]
+
+
+def test_train_config_hash_is_the_references():
+    sub, cfg = _cfg(TRAIN_ARGV)
+    want = json.load(open(os.path.join(GOLD, "stack_model.json")))["metadata"]["config_hash"]
+    assert cli.config_hash(sub, cfg) == want
+
+
+@pytest.mark.gpu
+def test_train_reproduces_the_reference_model_file(tmp_path):
+    """`train` (adaptive strategy) on the GPU against stack_model.json, the model file the
+    reference CLI wrote for the same flags (make_golden_cli.py): same structure and
+    metadata, smoother weights to 1e-8; loss.csv and manifest.json are written."""
+    import numpy as np
+    assert cli.main(TRAIN_ARGV + ["--out", str(tmp_path)]) == 0
+    got = json.load(open(tmp_path / "model.json"))
+    want = json.load(open(os.path.join(GOLD, "stack_model.json")))
+    assert got["kind"] == want["kind"] == "smoother_stack" and got["levels"] == want["levels"]
+    assert got["metadata"] == want["metadata"] and got["problem"] == want["problem"]
+    for a, b in zip(got["smoothers"], want["smoothers"]):
+        assert a["form"] == b["form"] and a["activation"] == b["activation"] and a["gain"] == pytest.approx(b["gain"], rel=1e-13)
+        for x, y in zip(a["layers"] + a["skip"], b["layers"] + b["skip"]):
+            assert np.allclose(x["data"], y["data"], rtol=0, atol=1e-8 * max(1e-300, np.max(np.abs(y["data"]))))
+    rows = list(csv.DictReader(open(tmp_path / "loss.csv")))
+    assert len(rows) == 2 * 2 and rows[0]["config_hash"] == want["metadata"]["config_hash"]
+    man = json.load(open(tmp_path / "manifest.json"))
+    assert man["subcommand"] == "train" and man["parameters"] == want["metadata"]["parameters"]
+    # the trained stack deploys through `solve --model`
+    assert cli.main(["solve", "--n", "31", "--theta", "pi/6", "--xi", "0.01", "--levels", "4", "--model",
+                     str(tmp_path / "model.json"), "--csv", str(tmp_path / "s.csv")]) == 0
