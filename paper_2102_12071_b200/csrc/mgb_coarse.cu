@@ -9,7 +9,10 @@
 // Reference: v_cycle hierarchy.py:96-111 (V(nu1, nu2) as RepeatedSmoother,
 // cli.py:365-377), coarse_solve hierarchy.py:91-93 / lu_solve dense.py:50-63,
 // restrict transfer.py:108-121, prolong transfer.py:124-147.
+#include <cstdlib>
+
 #include "mgb_coarse.h"
+#include "mgb_dot.h"
 
 namespace mgb {
 namespace {
@@ -243,6 +246,204 @@ __global__ void __launch_bounds__(CT) k_coarse_block(CoarseArgs a) {
   }
 }
 
+
+// ---- fast path: band-class levels of at most 1024 points, no masks, zero start ---------
+// One point per thread on every level; every level's u, f, r sit in shared memory with a
+// zero ring around them (no bounds tests: the ring is the zero closure of grid.py:27-35),
+// a thread's class-table rows are looked up once per level visit, and every stage is the
+// stencil_dot chain of the tile / streaming passes (mgb_dot.h) in their stage order, so the
+// result is bitwise the per-level passes' (tested).  Replaces 2 launches per level plus the
+// LU launch by one launch: the levels up to 31^2 of a V(2,2) cycle cost ~19 us as separate
+// launches (launch latency) and run here in a few microseconds.
+struct TailLevel {
+  int rows, cols, P;     // P: padded pitch (cols + 2)
+  double *U, *F, *R;     // (rows + 2) x P each, interior at (+1, +1)
+  const double *tA, *tK; // 25 x 9 class tables in shared memory
+};
+
+__global__ void __launch_bounds__(CT) k_coarse_tail(CoarseArgs a) {
+  extern __shared__ double sm[];
+  pdl_trigger();
+  const int b = blockIdx.x, tid = threadIdx.x;
+  __shared__ TailLevel lv[COARSE_MAX_LEVELS];   // level descriptors (dynamic level index: not registers)
+  double* cur = sm;
+  size_t grid_doubles = 0;
+  for (int l = 0; l < a.nlev; ++l) {
+    const int P = a.lv[l].cols + 2, cnt = (a.lv[l].rows + 2) * P;
+    if (tid == 0) {
+      TailLevel& t = lv[l];
+      t.rows = a.lv[l].rows;
+      t.cols = a.lv[l].cols;
+      t.P = P;
+      t.U = cur;
+      t.F = cur + cnt;
+      t.R = cur + 2 * cnt;
+    }
+    cur += 3 * cnt;
+    grid_doubles += 3 * (size_t)cnt;
+  }
+  for (size_t q = tid; q < grid_doubles; q += CT) sm[q] = 0.0;   // fields and their zero rings
+  for (int l = 0; l < a.nlev; ++l) {
+    for (int q = tid; q < NCLS * 9; q += CT) {
+      cur[q] = a.lv[l].A.cls[(int64_t)b * NCLS * 9 + q];
+      if (l + 1 < a.nlev) cur[NCLS * 9 + q] = a.lv[l].K.cls[(int64_t)b * NCLS * 9 + q];
+    }
+    if (tid == 0) {
+      lv[l].tA = cur;
+      lv[l].tK = cur + NCLS * 9;
+    }
+    cur += 2 * NCLS * 9;
+  }
+  const int nn = a.nc;
+  double* slu = cur;            // coarsest factors
+  for (int q = tid; q < nn * nn; q += CT) slu[q] = a.lu[(int64_t)b * nn * nn + q];
+  pdl_wait();                   // f of the top level comes from the preceding pass
+  __syncthreads();
+  {
+    const TailLevel t = lv[0];
+    const int n = t.rows * t.cols;
+    if (tid < n) {
+      const int i = tid / t.cols, j = tid - i * t.cols;
+      t.F[(i + 1) * t.P + j + 1] = a.lv[0].f[(int64_t)b * n + tid];
+    }
+  }
+  __syncthreads();
+
+  // the thread's point on level l: padded index q and its class-table rows
+  struct Pt {
+    bool on;
+    int i, j, q;
+    const double *wA, *wK;
+  };
+  auto point = [&](int l) {
+    const TailLevel t = lv[l];
+    Pt p;
+    p.on = tid < t.rows * t.cols;
+    p.i = p.on ? tid / t.cols : 0;
+    p.j = p.on ? tid - p.i * t.cols : 0;
+    p.q = (p.i + 1) * t.P + p.j + 1;
+    const int cls = bandk(p.i, t.rows) * 5 + bandk(p.j, t.cols);
+    p.wA = t.tA + cls * 9;
+    p.wK = t.tK + cls * 9;
+    return p;
+  };
+  auto resid = [&](const TailLevel& t, const Pt& p) {   // R = F - A U
+    if (p.on) {
+      const double* s = t.U + p.q - t.P - 1;
+      t.R[p.q] = stencil_dot<true>(p.wA, s, s + t.P, s + 2 * t.P, t.F[p.q]);
+    }
+    __syncthreads();
+  };
+  auto update = [&](const TailLevel& t, const Pt& p, const double* src, bool from_zero) {   // U = U + K src
+    if (p.on) {
+      const double* s = src + p.q - t.P - 1;
+      t.U[p.q] = stencil_dot<false>(p.wK, s, s + t.P, s + 2 * t.P, from_zero ? 0.0 : t.U[p.q]);
+    }
+    __syncthreads();
+  };
+
+  // ---- down: nu1 sweeps from zero, residual, full weighting
+  for (int l = 0; l + 1 < a.nlev; ++l) {
+    const TailLevel t = lv[l];
+    const TailLevel c = lv[l + 1];
+    const Pt p = point(l);
+    update(t, p, t.F, true);           // r = f - A 0 = f: the first sweep reads f itself
+    for (int q = 1; q < a.nu1; ++q) {
+      resid(t, p);
+      update(t, p, t.R, false);
+    }
+    resid(t, p);
+    if (tid < c.rows * c.cols) {
+      const int ci = tid / c.cols, cj = tid - ci * c.cols;
+      const double* r0 = t.R + (2 * ci + 1) * t.P + 2 * cj + 1;
+      const double* r1 = r0 + t.P;
+      const double* r2 = r1 + t.P;
+      double s = 0.0625 * r0[0];
+      s = fma(0.125, r0[1], s);
+      s = fma(0.0625, r0[2], s);
+      s = fma(0.125, r1[0], s);
+      s = fma(0.25, r1[1], s);
+      s = fma(0.125, r1[2], s);
+      s = fma(0.0625, r2[0], s);
+      s = fma(0.125, r2[1], s);
+      s = fma(0.0625, r2[2], s);
+      c.F[(ci + 1) * c.P + cj + 1] = s;
+    }
+    __syncthreads();
+  }
+  // ---- coarsest: one warp, forward (unit lower) and back substitution (dense.py:50-63)
+  {
+    const TailLevel t = lv[a.nlev - 1];
+    const int32_t* pm = a.perm + (int64_t)b * nn;
+    auto padded = [&](int flat) { return (flat / t.cols + 1) * t.P + flat % t.cols + 1; };
+    if (tid < 32) {
+      const int i = tid;
+      double x = i < nn ? t.F[padded(a.actp[pm[i]])] : 0.0;
+      for (int k = 0; k < nn; ++k) {
+        const double xk = __shfl_sync(0xffffffffu, x, k);
+        if (i > k && i < nn) x = x - slu[i * nn + k] * xk;
+      }
+      for (int k = nn - 1; k >= 0; --k) {
+        if (i == k) x = x / slu[k * nn + k];
+        const double xk = __shfl_sync(0xffffffffu, x, k);
+        if (i < k) x = x - slu[i * nn + k] * xk;
+      }
+      if (i < nn) t.U[padded(a.actp[i])] = x;
+    }
+    __syncthreads();
+  }
+  // ---- up: u += P e (the tile pass's gather order), nu2 sweeps
+  for (int l = a.nlev - 2; l >= 0; --l) {
+    const TailLevel t = lv[l];
+    const TailLevel c = lv[l + 1];
+    const Pt p = point(l);
+    if (p.on) {
+      double s = 0.0;
+#pragma unroll
+      for (int di = -1; di <= 1; ++di) {
+        const int tt = p.i - 1 - di;
+        if (tt & 1) continue;
+#pragma unroll
+        for (int dj = -1; dj <= 1; ++dj) {
+          const int uu = p.j - 1 - dj;
+          if (uu & 1) continue;
+          const double wgt = (di == 0 ? 2.0 : 1.0) * (dj == 0 ? 2.0 : 1.0) * 0.125;
+          s = fma(wgt, c.U[((tt >> 1) + 1) * c.P + (uu >> 1) + 1], s);
+        }
+      }
+      t.U[p.q] = t.U[p.q] + s;
+    }
+    __syncthreads();
+    for (int q = 0; q < a.nu2; ++q) {
+      resid(t, p);
+      update(t, p, t.R, false);
+    }
+  }
+  {
+    const TailLevel t = lv[0];
+    const int n = t.rows * t.cols;
+    if (tid < n) {
+      const int i = tid / t.cols, j = tid - i * t.cols;
+      a.lv[0].u[(int64_t)b * n + tid] = t.U[(i + 1) * t.P + j + 1];
+    }
+  }
+}
+
+static bool tail_ok(const CoarseArgs& a) {
+  if (!a.zero_top || a.nc > 32 || a.nu1 < 1 || a.nu1 > 2 || a.nu2 < 1 || a.nu2 > 2) return false;
+  for (int l = 0; l < a.nlev; ++l) {
+    const CLevel& c = a.lv[l];
+    if (c.rows * c.cols > CT || c.mask || !c.A.cls || (l + 1 < a.nlev && !c.K.cls)) return false;
+  }
+  return true;
+}
+
+static size_t tail_smem(const CoarseArgs& a) {
+  size_t d = 0;
+  for (int l = 0; l < a.nlev; ++l) d += 3 * (size_t)(a.lv[l].rows + 2) * (a.lv[l].cols + 2) + 2 * NCLS * 9;
+  return (d + (size_t)a.nc * a.nc) * sizeof(double);
+}
+
 }  // namespace
 
 size_t coarse_block_smem(const CoarseArgs& a) {
@@ -257,6 +458,16 @@ size_t coarse_block_smem(const CoarseArgs& a) {
 }
 
 cudaError_t launch_coarse_block(const CoarseArgs& a, int batch, cudaStream_t s) {
+  static const bool no_tail = getenv("MGB_COARSE_TAIL") && atoi(getenv("MGB_COARSE_TAIL")) == 0;   // A/B experiments
+  if (!no_tail && tail_ok(a)) {
+    const size_t tsm = tail_smem(a);
+    cudaError_t e = cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+    e = launch_pdl(k_coarse_tail, dim3(batch), dim3(CT), tsm, s, a);
+    if (e != cudaSuccess) return e;
+    return MGB_DBG("k_coarse_tail");
+  }
   const size_t smem = coarse_block_smem(a);
   cudaError_t e = cudaFuncSetAttribute(k_coarse_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

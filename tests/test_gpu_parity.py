@@ -756,3 +756,24 @@ def test_virtual_decomposition_column_pair_kernel(n, nparts, monkeypatch):
     u = t.cat([s.solution(p) for p in range(nparts)])
     assert t.equal(u, u_ref), float((u - u_ref).abs().max())
     assert np.allclose(hist, hist_ref, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("n,theta,nu,net", [(255, math.pi / 6, 2, "conv"), (127, math.pi / 4, 1, "conv"),
+                                            (63, math.pi / 3, 2, "fc")])
+def test_coarse_tail_kernel_bitwise_equals_tile_passes(n, theta, nu, net):
+    """k_coarse_tail (band-class levels of at most 1024 points in one launch: the same
+    stencil_dot chains in the tile passes' stage order) against the per-level passes: u
+    and histories bit for bit."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    A = gen.rotated_fd(n, theta, 0.01)
+    h = mg.equip_inferred(mg.build_hierarchy(mg.StencilField(mg.full_spec(n), A), gen.levels_for(n)), net_of(net))
+    f = dv.to_dev(gen.uniform_rhs(n, 4))
+    out = []
+    for coarse_max in (0, 1024):
+        h.set_passes(coarse_max=coarse_max)
+        u = dv.zeros(f.shape)
+        hist = h.run_cycles(f, u, 4, nu, nu, u_zero=True).clone()
+        out.append((u, hist, h.last_launches))
+    assert t.equal(out[0][0], out[1][0]) and t.equal(out[0][1], out[1][1])
+    assert out[1][2] < out[0][2]          # fewer launches per solve
