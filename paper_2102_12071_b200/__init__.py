@@ -19,8 +19,10 @@ from .smoothers import (ConvSmoother, InferredSmoother, JacobiSmoother, KernelIn
 from .hierarchy import (Level, MultigridHierarchy, RepeatedSmoother, SolveReport, build_hierarchy,
                         build_hierarchy_batch, build_hierarchy_classed, coarse_solve, cycle_correction, equip_classical,
                         equip_conv_init, equip_inferred, equip_trained, retarget, solve, v_cycle)
-from .training import (LossRecord, TrainConfig, TrainingSample, forward_loss, make_dataset, train_adaptive,
-                       train_independent, train_inference_net, train_level)
+from .autodiff import grad_check
+from .problems import ProblemSpec, build_geometry
+from .training import (LossRecord, TrainConfig, TrainingSample, forward_loss, make_dataset, retrain_with_injection,
+                       train_adaptive, train_independent, train_inference_net, train_level, train_mixture)
 from .krylov import (CyclePreconditioner, FgmresConfig, GridAction, KrylovReport, cycle_preconditioner, fgmres,
                      gmres, grid_action)
 

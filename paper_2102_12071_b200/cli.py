@@ -22,7 +22,7 @@ MEASURED_PEAKS.json, else the profiling recipe's fallback).
 `train` (cli.py:489-587) runs the GPU trainers of training.py: `--variant conv|fc` the
 staged kernel-inference-net training, else the adaptive / independent conv-smoother
 strategies; it writes model.json, loss.csv and manifest.json as the reference does
-(mixture `--thetas` and `--inject-k` are not on the B200 path).  `analyze` is out of
+(including the `--thetas` mixture and `--inject-k` retraining).  `analyze` is out of
 scope: it exits 1 with the reference's UnsupportedOperationError message format.
 """
 
@@ -484,14 +484,21 @@ def cmd_train(cfg: dict) -> int:
     meta = {"config_hash": chash, "seed": cfg["seed"], "epochs": cfg["epochs"]}
     notes = []
     t0 = time.perf_counter()
-    if cfg["thetas"] is not None:
-        raise UnsupportedOperationError("mixture training (--thetas) is not on the B200 path")
-    if cfg["inject_k"] > 0:
-        raise UnsupportedOperationError("residual-injection retraining (--inject-k) is not on the B200 path")
     if cfg["variant"] is not None:
         net, hier, records = tr.train_inference_net(A, cfg["variant"], cfg["levels"], tc, k=cfg["net_k"])
         params = net.parameter_count()
         doc = model_to_dict(net, {**meta, "parameters": params, "problem": problem.asdict()})
+    elif cfg["thetas"] is not None:
+        if cfg["family"] != "rotated":
+            raise ConfigError("angle mixtures need the rotated family")
+        ops = [ProblemSpec(cfg["family"], cfg["n"], cfg["geometry"], t, cfg["xi"], cfg["kappa"]).assemble()
+               for t in cfg["thetas"]]
+        hiers, records = tr.train_mixture(ops, cfg["levels"], tc, scheme=cfg["scheme"], omega=cfg["omega"],
+                                          activation=cfg["activation"])
+        hier = hiers[0]
+        params = _stack_params(hier)
+        notes.append("mixture model; kernels shared across angles, saved against the first angle's operator")
+        doc = stack_to_dict(problem, hier, {**meta, "parameters": params})
     elif cfg["strategy"] == "independent":
         sm, record = tr.train_independent(A, tc, form=cfg["form"], omega=cfg["omega"], activation=cfg["activation"])
         hier = build_hierarchy(A, 2, scheme=cfg["scheme"])   # saved as a depth-2 stack (cli.py:527-531)
@@ -502,6 +509,10 @@ def cmd_train(cfg: dict) -> int:
     else:
         hier, records = tr.train_adaptive(A, cfg["levels"], tc, scheme=cfg["scheme"], omega=cfg["omega"],
                                           activation=cfg["activation"])
+        if cfg["inject_k"] > 0:
+            hier, more = tr.retrain_with_injection(hier, tc, cfg["inject_k"])
+            records = records + more
+            notes.append(f"retrained on residual probes after {cfg['inject_k']} cycles")
         params = _stack_params(hier)
         doc = stack_to_dict(problem, hier, {**meta, "parameters": params})
     wall = time.perf_counter() - t0

@@ -113,6 +113,18 @@ def run_cases():
     sm, rec = rt.train_independent(A15, cfg2, form="rb")
     out["run_independent_records"] = np.array(rec.epochs)
     out["run_independent_layers"] = np.stack([k.weights for k in sm.layers])
+    ops = [rp.ProblemSpec("rotated", 15, angle=t).assemble() for t in (np.pi / 6, np.pi / 4)]
+    hiers, recs = rt.train_mixture(ops, 3, cfg2)
+    out["run_mixture_records"] = np.array([r.epochs for r in recs])
+    for l in range(2):
+        out[f"run_mixture_layers{l}"] = np.stack([k.weights for k in hiers[1].levels[l].smoother.layers])
+        out[f"run_mixture_skip{l}"] = hiers[1].levels[l].smoother.skip.weights
+        out[f"run_mixture_gains{l}"] = np.array([h.levels[l].smoother.gain for h in hiers])
+    hier, _ = rt.train_adaptive(A15, 3, cfg2)
+    hier, recs = rt.retrain_with_injection(hier, cfg2, k_probe=2, probes=3)
+    out["run_injection_records"] = np.array([r.epochs for r in recs])
+    for l, lev in enumerate(hier.levels[:-1]):
+        out[f"run_injection_layers{l}"] = np.stack([k.weights for k in lev.smoother.layers])
     # forward-loss values of frozen hierarchies (graph == production cycle)
     h3 = build_hierarchy(A15, 3)
     equip_conv_init(h3)

@@ -55,7 +55,7 @@ def test_angles_and_config_files(tmp_path, monkeypatch):
 def test_exit_codes_without_running(capsys):
     assert cli.main(["analyze", "--n", "15"]) == 1                # not on the B200 path
     assert "not on the B200 path" in capsys.readouterr().err
-    assert cli.main(["train", "--n", "15", "--thetas", "0.1,0.2"]) == 1   # mixture training: unsupported
+    assert cli.main(["train", "--family", "variable", "--n", "15", "--thetas", "0.1,0.2", "--device", "cpu"]) == 1
     assert cli.main(["solve", "--device", "cpu"]) == 1            # no CPU fallback
     assert cli.main(["solve", "--n", "many"]) == 1
     assert cli.main([]) == 1

@@ -173,12 +173,33 @@ def test_train_independent_matches_the_reference(G):
     _close(np.stack([k.weights for k in sm.layers]), G["run_independent_layers"], 1e-8)
 
 
+def test_train_mixture_and_injection_match_the_reference(G):
+    """training.py:330-437: kernels shared across two rotation angles (per-operator gains),
+    and residual-injection retraining on top of an adaptively trained hierarchy."""
+    from paper_2102_12071_b200 import training as tr
+    cfg = tr.TrainConfig(samples=6, max_steps=2, batch_size=3, epochs=6, seed=42)
+    ops = [gen.ProblemSpec("rotated", 15, angle=t).assemble() for t in (np.pi / 6, np.pi / 4)]
+    hiers, recs = tr.train_mixture(ops, 3, cfg)
+    assert np.allclose(np.array([r.epochs for r in recs]), G["run_mixture_records"], rtol=1e-9, atol=0)
+    for l in range(2):
+        _close(np.stack([k.weights for k in hiers[1].levels[l].smoother.layers]), G[f"run_mixture_layers{l}"], 1e-8)
+        _close(hiers[1].levels[l].smoother.skip.weights, G[f"run_mixture_skip{l}"], 1e-8)
+        assert np.allclose([h.levels[l].smoother.gain for h in hiers], G[f"run_mixture_gains{l}"], rtol=1e-13)
+        assert hiers[0].levels[l].smoother.layers[0] is hiers[1].levels[l].smoother.layers[0]   # shared kernels
+    A15 = ops[0]
+    hier, _ = tr.train_adaptive(A15, 3, cfg)
+    hier, recs = tr.retrain_with_injection(hier, cfg, k_probe=2, probes=3)
+    assert np.allclose(np.array([r.epochs for r in recs]), G["run_injection_records"], rtol=1e-8, atol=0)
+    for l, lev in enumerate(hier.levels[:-1]):
+        _close(np.stack([k.weights for k in lev.smoother.layers]), G[f"run_injection_layers{l}"], 1e-7)
+
+
 def test_training_contract_errors():
     from paper_2102_12071_b200 import training as tr
     with pytest.raises(mg.ConfigError):
         tr.TrainConfig(samples=4, batch_size=5)
-    with pytest.raises(mg.UnsupportedOperationError):
-        tr.train_mixture([], 2, None)
+    with pytest.raises(mg.ConfigError):
+        tr.train_mixture([], 2, tr.TrainConfig())
     A = gen.ProblemSpec("rotated", 7, angle=0.3).assemble()
     h = mg.equip_classical(mg.build_hierarchy(A, 2), "jacobi")
     with pytest.raises(mg.ConfigError):
