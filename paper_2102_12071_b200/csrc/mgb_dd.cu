@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -130,7 +131,7 @@ using namespace mgb;
 struct DDPart {
   int part = 0;
   std::vector<int> R0, R1;       // owned rows per distributed level
-  std::vector<double*> u, t, f;  // ghosted blocks: rows [R0 - G, R1 + G) x cols
+  std::vector<double*> u, t, f;  // ghosted blocks: rows [R0 - ga, R1 + ga) x pitch (mgb_dd::view)
   double* partials = nullptr;
   double* norm2 = nullptr;       // per-part sum of squares (device scalar)
 };
@@ -182,8 +183,20 @@ struct mgb_dd {
   }
   int rows(int l) const { return hier_rows(h, l); }
   int cols(int l) const { return hier_cols(h, l); }
-  // pointer to global row 0 of a ghosted block whose first stored row is R0 - G
-  static double* gview(double* blk, int R0, int cols) { return blk - (int64_t)(R0 - DD_GHOST) * cols; }
+  // Block layout of a distributed level: stored rows [R0 - ga, R1 + ga), row pitch `pitch`,
+  // `lc` margin columns left of column 0.  Dense levels: ga = 6 (the ghost rows), pitch =
+  // cols, lc = 0.  Level 0 of a uniform band-class hierarchy (the warp-strip kernel) uses
+  // that kernel's padded layout: 16-byte aligned pitch, zero column margins, 16 allocated
+  // rows per edge (its unpredicated ring copies touch up to 11 rows beyond a block; only
+  // the 6 ghost rows next to the block carry data, the rest stay zero).
+  std::vector<int64_t> pitch;
+  std::vector<int> ga, lc;
+  std::vector<char> padded;
+  // pointer to global (row 0, column 0) of a block whose owned rows start at R0
+  double* view(double* blk, int R0, int l) const { return blk + lc[l] - (int64_t)(R0 - ga[l]) * pitch[l]; }
+  // start of stored row `row` (its left margin included) given the (0, 0) pointer
+  double* rowp(double* v0, int row, int l) const { return v0 + (int64_t)row * pitch[l] - lc[l]; }
+  size_t block_doubles(int r0, int r1, int l) const { return (size_t)(r1 - r0 + 2 * ga[l]) * pitch[l]; }
 };
 
 static constexpr int G = DD_GHOST;
@@ -234,6 +247,20 @@ extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int 
     if (r1 - r0 < 2 * G * align) return fail(MGB_CONFIG, "too many parts for this grid (blocks smaller than the halo)");
   }
   d->Bc = blk >> Ld;
+  for (int l = 0; l < Ld; ++l) {
+    StreamArgs a{};
+    a.g = hier_grid(h, l);
+    a.A = hier_opA(h, l);
+    a.K = hier_opK(h, l);
+    a.mask = hier_mask(h, l);
+    hier_interior(h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel);
+    static const bool no_pad = getenv("MGB_DD_PAD") && atoi(getenv("MGB_DD_PAD")) == 0;   // A/B experiments
+    const bool pad = !no_pad && a.uniform && stream_kernel_kind(a) == 3;
+    d->padded.push_back(pad ? 1 : 0);
+    d->pitch.push_back(pad ? pad_pitch(d->cols(l)) : d->cols(l));
+    d->ga.push_back(pad ? PAD_ROWS : G);
+    d->lc.push_back(pad ? PAD_LCOLS : 0);
+  }
   for (int q = 0; q < nlocal; ++q) {
     DDPart P;
     P.part = first_part + q;
@@ -242,7 +269,7 @@ extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int 
       const int r1 = P.part == nparts - 1 ? d->rows(l) : (std::min((P.part + 1) * blk, rows0) >> l);
       P.R0.push_back(r0);
       P.R1.push_back(r1);
-      const size_t cnt = (size_t)(r1 - r0 + 2 * G) * d->cols(l);
+      const size_t cnt = d->block_doubles(r0, r1, l);
       double *a = nullptr, *b = nullptr, *c = nullptr;
       MGB_CUDA_TRY(dalloc(&a, cnt));
       MGB_CUDA_TRY(dalloc(&b, cnt));
@@ -303,60 +330,64 @@ extern "C" int mgb_dd_info(const mgb_dd* d, int part, int* r0, int* r1, int* dis
 // which: 0 = u, 1 = t, 2 = f
 static int exchange(mgb_dd* d, int l, int which, cudaStream_t s) {
   if (!d->do_exchange) return MGB_OK;   // timing runs only (results are wrong without the halos)
-  const int cols = d->cols(l), rows = d->rows(l);
+  const int rows = d->rows(l);
+  const int64_t pitch = d->pitch[l];    // whole stored rows travel (margins included: they are zero)
   auto buf = [&](DDPart& P) -> double* { return which == 0 ? P.u[l] : which == 1 ? P.t[l] : P.f[l]; };
-  const size_t gcount = (size_t)G * cols;
+  const size_t gcount = (size_t)G * pitch;
   if (d->comm == nullptr && d->xfn == nullptr) {
     // virtual: all parts local
     for (int q = 0; q < d->nlocal; ++q) {
       DDPart& P = d->parts[q];
-      double* v = mgb_dd::gview(buf(P), P.R0[l], cols);
+      double* v = d->view(buf(P), P.R0[l], l);
       if (q > 0) {
         DDPart& A = d->parts[q - 1];
-        const double* va = mgb_dd::gview(buf(A), A.R0[l], cols);
-        MGB_CUDA_TRY(cudaMemcpyAsync(v + (int64_t)(P.R0[l] - G) * cols, va + (int64_t)(P.R0[l] - G) * cols,
-                                     gcount * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        double* va = d->view(buf(A), A.R0[l], l);
+        MGB_CUDA_TRY(cudaMemcpyAsync(d->rowp(v, P.R0[l] - G, l), d->rowp(va, P.R0[l] - G, l), gcount * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
         d->halo_bytes += gcount * sizeof(double);
       }
       if (q + 1 < d->nlocal) {
         DDPart& B = d->parts[q + 1];
-        const double* vb = mgb_dd::gview(buf(B), B.R0[l], cols);
+        double* vb = d->view(buf(B), B.R0[l], l);
         const int n = std::min(G, rows - P.R1[l]);
-        MGB_CUDA_TRY(cudaMemcpyAsync(v + (int64_t)P.R1[l] * cols, vb + (int64_t)P.R1[l] * cols,
-                                     (size_t)n * cols * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        d->halo_bytes += (size_t)n * cols * sizeof(double);
+        MGB_CUDA_TRY(cudaMemcpyAsync(d->rowp(v, P.R1[l], l), d->rowp(vb, P.R1[l], l), (size_t)n * pitch * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+        d->halo_bytes += (size_t)n * pitch * sizeof(double);
       }
     }
     ++d->exchanges;
     return MGB_OK;
   }
   DDPart& P = d->parts[0];
-  double* v = mgb_dd::gview(buf(P), P.R0[l], cols);
+  double* v = d->view(buf(P), P.R0[l], l);
   const int me = P.part;
   const int nb = me + 1 < d->nparts ? std::min(G, rows - P.R1[l]) : 0;
   ++d->exchanges;
-  d->halo_bytes += ((me > 0 ? gcount : 0) + (size_t)nb * cols) * sizeof(double);
+  d->halo_bytes += ((me > 0 ? gcount : 0) + (size_t)nb * pitch) * sizeof(double);
+  double* up_send = d->rowp(v, P.R0[l], l);
+  double* up_recv = d->rowp(v, P.R0[l] - G, l);
+  double* dn_send = d->rowp(v, P.R1[l] - nb, l);
+  double* dn_recv = d->rowp(v, P.R1[l], l);
   if (d->xfn) {
     // callback backend: the neighbour above first, then the one below (rank 0 starts the chain)
     MGB_CUDA_TRY(cudaStreamSynchronize(s));
     if (me > 0)
-      if (d->xfn(d->xctx, 0, me - 1, v + (int64_t)P.R0[l] * cols, v + (int64_t)(P.R0[l] - G) * cols, (int64_t)gcount))
+      if (d->xfn(d->xctx, 0, me - 1, up_send, up_recv, (int64_t)gcount))
         return fail(MGB_NCCL, "exchange callback failed (halo, upper neighbour)");
     if (nb > 0)
-      if (d->xfn(d->xctx, 0, me + 1, v + (int64_t)(P.R1[l] - nb) * cols, v + (int64_t)P.R1[l] * cols,
-                 (int64_t)nb * cols))
+      if (d->xfn(d->xctx, 0, me + 1, dn_send, dn_recv, (int64_t)nb * pitch))
         return fail(MGB_NCCL, "exchange callback failed (halo, lower neighbour)");
     return MGB_OK;
   }
   auto& A = nccl::api();
   MGB_NCCL_TRY(A.GroupStart());
   if (me > 0) {
-    MGB_NCCL_TRY(A.Send(v + (int64_t)P.R0[l] * cols, gcount, nccl::Float64, me - 1, d->comm, s));
-    MGB_NCCL_TRY(A.Recv(v + (int64_t)(P.R0[l] - G) * cols, gcount, nccl::Float64, me - 1, d->comm, s));
+    MGB_NCCL_TRY(A.Send(up_send, gcount, nccl::Float64, me - 1, d->comm, s));
+    MGB_NCCL_TRY(A.Recv(up_recv, gcount, nccl::Float64, me - 1, d->comm, s));
   }
   if (nb > 0) {
-    MGB_NCCL_TRY(A.Send(v + (int64_t)(P.R1[l] - nb) * cols, (size_t)nb * cols, nccl::Float64, me + 1, d->comm, s));
-    MGB_NCCL_TRY(A.Recv(v + (int64_t)P.R1[l] * cols, (size_t)nb * cols, nccl::Float64, me + 1, d->comm, s));
+    MGB_NCCL_TRY(A.Send(dn_send, (size_t)nb * pitch, nccl::Float64, me + 1, d->comm, s));
+    MGB_NCCL_TRY(A.Recv(dn_recv, (size_t)nb * pitch, nccl::Float64, me + 1, d->comm, s));
   }
   MGB_NCCL_TRY(A.GroupEnd());
   return MGB_OK;
@@ -386,6 +417,10 @@ static StreamArgs dd_args(const mgb_dd* d, int l, cudaStream_t s) {
   a.a5 = hier_a5(d->h, l);
   a.stream = s;
   hier_interior(d->h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel);
+  if (l < (int)d->padded.size() && d->padded[l]) {
+    a.ld = d->pitch[l];
+    a.padded = 1;
+  }
   return a;
 }
 
@@ -393,7 +428,10 @@ static StreamArgs dd_args(const mgb_dd* d, int l, cudaStream_t s) {
 // the interior launch over [R0 + EDGE, R1 - EDGE) touches owned rows only.  Even, so the
 // sub-ranges start at even rows like the blocks themselves (coarse anchors 2c + 1 never
 // straddle a boundary).
-static constexpr int EDGE = 32;
+#ifndef MGB_DD_EDGE
+#define MGB_DD_EDGE 8
+#endif
+static constexpr int EDGE = MGB_DD_EDGE;   // >= 6 and even; 8: the shortest edge launch (8 rows + pipeline fill)
 
 // One pass (PRE: res; POST: pro; or the plain norm sweep) over part P's rows of level l.
 // phase 0: the interior rows, 1: the edge rows, 2: the whole block in one launch.  With
@@ -427,7 +465,7 @@ static int launch_rows(mgb_dd* d, int l, DDPart& P, StreamArgs a, int nsw, bool 
 static bool split_ok(const mgb_dd* d, int l) {
   if (!d->overlap || d->nparts == 1) return false;
   for (auto& P : d->parts)
-    if (P.R1[l] - P.R0[l] < 4 * EDGE) return false;
+    if (P.R1[l] - P.R0[l] < 128) return false;
   return true;
 }
 
@@ -457,15 +495,14 @@ static int exchange_and_pass(mgb_dd* d, int l, cudaStream_t s, bool any_exchange
 // residual norm^2 of the current level-0 u (or of f when u == null) per part, via a
 // streaming plain-sweep pass whose output goes to scratch
 static int norm_pass(mgb_dd* d, bool of_f, double* dst, cudaStream_t s) {
-  const int cols = d->cols(0);
   std::vector<int> np(d->parts.size(), 0);
   auto rows = [&](int phase) -> int {
     for (size_t q = 0; q < d->parts.size(); ++q) {
       DDPart& P = d->parts[q];
       StreamArgs a = dd_args(d, 0, s);
-      a.f = mgb_dd::gview(P.f[0], P.R0[0], cols);
-      a.u = of_f ? nullptr : mgb_dd::gview(P.u[0], P.R0[0], cols);
-      a.uo = mgb_dd::gview(P.t[0], P.R0[0], cols);
+      a.f = d->view(P.f[0], P.R0[0], 0);
+      a.u = of_f ? nullptr : d->view(P.u[0], P.R0[0], 0);
+      a.uo = d->view(P.t[0], P.R0[0], 0);
       if (int st = launch_rows(d, 0, P, a, 1, false, false, true, phase, &np[q])) return st;
     }
     return MGB_OK;
@@ -483,7 +520,6 @@ static int dd_cycle(mgb_dd* d, int nu1, int nu2, bool zero, double* hist, cudaSt
   const int Ld = d->Ld, La = d->La;
   // descend over the distributed levels
   for (int l = 0; l < Ld; ++l) {
-    const int cols = d->cols(l);
     const bool z = zero || l > 0;
     const bool last = l + 1 == Ld;
     const bool nrm = hist && l == 0;
@@ -492,16 +528,15 @@ static int dd_cycle(mgb_dd* d, int nu1, int nu2, bool zero, double* hist, cudaSt
       for (size_t q = 0; q < d->parts.size(); ++q) {
         DDPart& P = d->parts[q];
         StreamArgs a = dd_args(d, l, s);
-        a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
-        a.u = z ? nullptr : mgb_dd::gview(P.u[l], P.R0[l], cols);
-        a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
+        a.f = d->view(P.f[l], P.R0[l], l);
+        a.u = z ? nullptr : d->view(P.u[l], P.R0[l], l);
+        a.uo = d->view(P.t[l], P.R0[l], l);
         if (last) {
           // restricted residual straight into this part's slot of the gather layout
           const int cc = d->cols(La);
           a.rc = d->gather + (int64_t)P.part * d->Bc * cc - (int64_t)(P.R0[l] / 2) * cc;
         } else {
-          const int cc = d->cols(l + 1);
-          a.rc = mgb_dd::gview(P.f[l + 1], P.R0[l] / 2, cc);
+          a.rc = d->view(P.f[l + 1], P.R0[l + 1], l + 1);   // (dense: levels >= 1 are never padded)
         }
         if (int st = launch_rows(d, l, P, a, nu1, true, false, nrm, phase, &np[q])) return st;
       }
@@ -546,15 +581,14 @@ static int dd_cycle(mgb_dd* d, int nu1, int nu2, bool zero, double* hist, cudaSt
   if (int st = work_vcycle_level(d->cw, La, cf, cu, true, nu1, nu2, s, &ec_full)) return st;
   // ascend
   for (int l = Ld - 1; l >= 0; --l) {
-    const int cols = d->cols(l);
     int unused = 0;
     auto rows = [&](int phase) -> int {
       for (auto& P : d->parts) {
         StreamArgs a = dd_args(d, l, s);
-        a.f = mgb_dd::gview(P.f[l], P.R0[l], cols);
-        a.u = mgb_dd::gview(P.u[l], P.R0[l], cols);
-        a.uo = mgb_dd::gview(P.t[l], P.R0[l], cols);
-        if (l + 1 < Ld) a.ec = mgb_dd::gview(P.u[l + 1], P.R0[l + 1], d->cols(l + 1));
+        a.f = d->view(P.f[l], P.R0[l], l);
+        a.u = d->view(P.u[l], P.R0[l], l);
+        a.uo = d->view(P.t[l], P.R0[l], l);
+        if (l + 1 < Ld) a.ec = d->view(P.u[l + 1], P.R0[l + 1], l + 1);
         else a.ec = ec_full;
         if (int st = launch_rows(d, l, P, a, nu2, false, true, false, phase, &unused)) return st;
       }
@@ -606,9 +640,9 @@ extern "C" int mgb_dd_set_rhs(mgb_dd* d, int part, const double* f_owned_dev, vo
   DeviceGuard dg(d->device);
   DDPart& P = d->parts[q];
   const int cols = d->cols(0);
-  MGB_CUDA_TRY(cudaMemcpyAsync(P.f[0] + (int64_t)G * cols, f_owned_dev,
-                               sizeof(double) * (size_t)(P.R1[0] - P.R0[0]) * cols, cudaMemcpyDeviceToDevice,
-                               S(stream)));
+  MGB_CUDA_TRY(cudaMemcpy2DAsync(d->view(P.f[0], P.R0[0], 0) + (int64_t)P.R0[0] * d->pitch[0], sizeof(double) * d->pitch[0],
+                                 f_owned_dev, sizeof(double) * cols, sizeof(double) * cols, (size_t)(P.R1[0] - P.R0[0]),
+                                 cudaMemcpyDeviceToDevice, S(stream)));
   return MGB_OK;
 }
 
@@ -619,9 +653,9 @@ extern "C" int mgb_dd_get_solution(const mgb_dd* d, int part, double* u_owned_de
   DeviceGuard dg(d->device);
   const DDPart& P = d->parts[q];
   const int cols = d->cols(0);
-  MGB_CUDA_TRY(cudaMemcpyAsync(u_owned_dev, P.u[0] + (int64_t)G * cols,
-                               sizeof(double) * (size_t)(P.R1[0] - P.R0[0]) * cols, cudaMemcpyDeviceToDevice,
-                               S(stream)));
+  MGB_CUDA_TRY(cudaMemcpy2DAsync(u_owned_dev, sizeof(double) * cols,
+                                 d->view(P.u[0], P.R0[0], 0) + (int64_t)P.R0[0] * d->pitch[0], sizeof(double) * d->pitch[0],
+                                 sizeof(double) * cols, (size_t)(P.R1[0] - P.R0[0]), cudaMemcpyDeviceToDevice, S(stream)));
   return MGB_OK;
 }
 
