@@ -683,6 +683,7 @@ def run_ours(args):
     if rank == 0:
         bpu = cycle_bytes_per_fine_unknown(n, levels, nu, nu)
         kname = h.pass_kernel(0, nu)   # the kernel launch_pass dispatches level 0 to
+        infer_pts = sum((25 if h.storage_info(l)[0] else (n >> l) ** 2) * nb for l in range(levels - 1))
         # compulsory traffic of one fused cycle: per level a PRE pass (u, f in; u out; the
         # restricted residual at 8 B per coarse point; on levels >= 1 the start is zero, so
         # u is not read) and a POST pass (u, f, coarse correction in; u out), plus the
@@ -736,7 +737,10 @@ def run_ours(args):
             "gpu_launches": int(launches_per_step * args.steps),
             "history_last": float(np.median(hl)) if batched else float(hl[0]),
             "history_last_stat": "median over problems" if batched else "single problem",
-            "setup_s": {"galerkin_lu": info["setup_rap_lu_s"], "cnn_inference": info["setup_infer_s"]},
+            "setup_s": {"galerkin_lu": info["setup_rap_lu_s"], "cnn_inference": info["setup_infer_s"],
+                        # points the stencil -> smoother CNN evaluated: every point of a level that keeps
+                        # per-point tables, 25 class representatives of a band-class level
+                        "cnn_points": infer_pts, "cnn_points_per_s": infer_pts / max(info["setup_infer_s"], 1e-12)},
             "clocks": clk.summary(),
             "cpu_baseline": None if cpu is None else {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         }
