@@ -1380,7 +1380,7 @@ static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, do
 
 // POST on level l: u <- u + P ec, then nu2 sweeps (result ends in *cur)
 static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, double** cur, double** oth, int nu2,
-                        cudaStream_t s) {
+                        cudaStream_t s, double* out_hist = nullptr, int64_t out_stride = 0) {
   const mgb_hier* h = w->h;
   StreamArgs a = stream_args(w, l, f, s);
   const bool split = h->fused == 1;
@@ -1388,6 +1388,13 @@ static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, d
   a.u = *cur;
   a.uo = *oth;
   a.ec = ec;
+  if (out_hist) {
+    // the relative residual of the pass's output folded into the pass (post_norm_ok checked by the caller)
+    a.partials = w->partials;
+    MGB_CUDA_TRY(launch_pass(h, l, a, nu2, true, true, false, &nb));
+    std::swap(*cur, *oth);
+    return finalize_pre(w, nb, false, out_hist, out_stride, s);
+  }
   MGB_CUDA_TRY(launch_pass(h, l, a, split ? 1 : nu2, false, true, false, &nb));
   std::swap(*cur, *oth);
   if (split && nu2 == 2) {
@@ -1404,8 +1411,13 @@ static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, d
 // the buffer holding the result (u_l or the level's ping-pong partner).  With
 // hist != null (level 0 only) the relative residual of the INPUT u is written to
 // hist[b * hstride], folded into the first pre-sweep when it is a fused sweep.
+// out_hist != null (level 0, post_norm_ok): the relative residual of the cycle's OUTPUT is
+// written there by the level's POST pass.
+static bool post_norm_ok(const mgb_work* w, int nu1, int nu2);
+
 static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero, int nu1, int nu2,
-                      cudaStream_t s, double** result, double* hist = nullptr, int64_t hstride = 0) {
+                      cudaStream_t s, double** result, double* hist = nullptr, int64_t hstride = 0,
+                      double* out_hist = nullptr, int64_t out_stride = 0) {
   const mgb_hier* h = w->h;
   const int L = h->depth();
   if (l == L - 1) {
@@ -1429,7 +1441,7 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
       return st;
     double* ec = nullptr;
     if (int st = vcycle_rec(w, l + 1, w->f[l + 1], w->u[l + 1], true, nu1, nu2, s, &ec)) return st;
-    if (int st = enqueue_post(w, l, f, ec, &cur, &oth, nu2, s)) return st;
+    if (int st = enqueue_post(w, l, f, ec, &cur, &oth, nu2, s, l == 0 ? out_hist : nullptr, out_stride)) return st;
     *result = cur;
     return MGB_OK;
   }
@@ -1460,9 +1472,10 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
 }
 
 static int enqueue_vcycle(mgb_work* w, int l, const double* f, double* u, int nu1, int nu2, cudaStream_t s,
-                          bool zero = false, double* hist = nullptr, int64_t hstride = 0) {
+                          bool zero = false, double* hist = nullptr, int64_t hstride = 0, double* out_hist = nullptr,
+                          int64_t out_stride = 0) {
   double* res = nullptr;
-  if (int st = vcycle_rec(w, l, f, u, zero, nu1, nu2, s, &res, hist, hstride)) return st;
+  if (int st = vcycle_rec(w, l, f, u, zero, nu1, nu2, s, &res, hist, hstride, out_hist, out_stride)) return st;
   if (res != u) {
     if (l == 0 && w->pad0) {   // both padded level-0 buffers: copy whole allocations (margins are zero)
       const int cols = w->h->lv[0].cols;
@@ -1483,6 +1496,15 @@ static bool level0_padded(const mgb_hier* h, int nu1, int nu2) {
   return h->batch == 1 && h->depth() > 1 && pass_kind(h, 0, nu1, nu2) == 1 && l0.ks == 1 && l0.Acls && l0.Kcls &&
          !l0.mask && l0.conv.nl == 0 && l0.uniform() &&
          warp_strip_selected(h->stream_kernel, l0.n, h->batch, true);
+}
+
+// The level-0 POST pass can carry the residual norm of its output: fused passes (not one
+// pass per sweep) in the warp-strip kernel.
+static bool post_norm_ok(const mgb_work* w, int nu1, int nu2) {
+  const mgb_hier* h = w->h;
+  static const bool off = getenv("MGB_NO_POST_NORM") && atoi(getenv("MGB_NO_POST_NORM")) != 0;   // A/B experiments
+  if (off || h->depth() < 2 || h->fused != 2 || pass_kind(h, 0, nu1, nu2) != 1) return false;
+  return stream_post_norm_ok(stream_args(w, 0, nullptr, nullptr));
 }
 
 static int ensure_pad0(mgb_work* w) {
@@ -1587,11 +1609,26 @@ static int enqueue_run(mgb_work* w, const GraphKey& key, cudaStream_t cs) {
     u = w->pu0;
   }
   w->pad0 = pad;
+  // the last history entry (residual of the final u): folded into the last cycle's level-0
+  // POST pass where that pass supports it, else a residual pass of its own
+  const bool fold = key.cycles > 0 && post_norm_ok(w, key.nu1, key.nu2);
   for (int c = 0; c < key.cycles && !st; ++c)
-    st = enqueue_vcycle(w, 0, f, u, key.nu1, key.nu2, cs, key.u_zero && c == 0, key.hist + c, key.cycles + 1);
-  if (!st) st = enqueue_resnorm(w, f, u, key.hist + key.cycles, key.cycles + 1, cs);
+    st = enqueue_vcycle(w, 0, f, u, key.nu1, key.nu2, cs, key.u_zero && c == 0, key.hist + c, key.cycles + 1,
+                        fold && c + 1 == key.cycles ? key.hist + key.cycles : nullptr, key.cycles + 1);
+  if (!st && !fold) st = enqueue_resnorm(w, f, u, key.hist + key.cycles, key.cycles + 1, cs);
   w->pad0 = false;
   if (!st && pad) MGB_CUDA_TRY(pad0_copy(h, key.u, false, w->pu0, true, cs));
+  return st;
+}
+
+// One solve() iteration (modes 1 / 2): a V-cycle and the relative residual of its result
+// into w->scratch.  Mode 2: key.f / key.u are the padded level-0 copies.
+static int enqueue_iteration(mgb_work* w, const GraphKey& key, cudaStream_t cs) {
+  w->pad0 = key.mode == 2;
+  const bool fold = post_norm_ok(w, key.nu1, key.nu2);
+  int st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, cs, false, nullptr, 0, fold ? w->scratch : nullptr, 4);
+  if (!st && !fold) st = enqueue_resnorm(w, key.f, key.u, w->scratch, 4, cs);
+  w->pad0 = false;
   return st;
 }
 
@@ -1616,8 +1653,7 @@ static int get_graph(mgb_work* w, const GraphKey& key, GraphEntry** out) {
       (void)nb;
       st = enqueue_run(w, key, w->cap);
     } else {
-      st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, w->cap);
-      if (!st) st = enqueue_resnorm(w, key.f, key.u, w->scratch, 4, w->cap);
+      st = enqueue_iteration(w, key, w->cap);
     }
     cudaError_t e = cudaStreamEndCapture(w->cap, &graph);
     if (st) {
@@ -1649,8 +1685,7 @@ static int enqueue_key(mgb_work* w, const GraphKey& key, cudaStream_t cs) {
     (void)nb;
     st = enqueue_run(w, key, cs);
   } else {
-    st = enqueue_vcycle(w, 0, key.f, key.u, key.nu1, key.nu2, cs);
-    if (!st) st = enqueue_resnorm(w, key.f, key.u, w->scratch, 4, cs);
+    st = enqueue_iteration(w, key, cs);
   }
   return st;
 }
@@ -1814,7 +1849,15 @@ extern "C" int mgb_solve(const mgb_hier* h, mgb_work* w, const double* f_dev, do
   int nh = 0;
   history_host[nh++] = r0;
   int it = 0;
-  GraphKey key{f_dev, u_dev, nu1, nu2, 1, 0, 1, nullptr};
+  // where level 0 runs the warp-strip passes, the loop iterates on the padded copies of f and
+  // u (staged once, as mgb_run_cycles does) and u is copied back when the loop ends
+  if (int st = prepare_work(w)) return st;
+  const bool pad = level0_padded(h, nu1, nu2) && w->pf0;
+  if (pad) {
+    MGB_CUDA_TRY(pad0_copy(h, w->pf0, true, f_dev, false, s));
+    MGB_CUDA_TRY(pad0_copy(h, w->pu0, true, u_dev, false, s));
+  }
+  GraphKey key{pad ? w->pf0 : f_dev, pad ? w->pu0 : u_dev, nu1, nu2, 1, 0, pad ? 2 : 1, nullptr};
   GraphEntry* pre = nullptr;
   if (int st = get_graph(w, key, &pre)) return st;  // capture outside the timed loop
   const auto t0 = std::chrono::steady_clock::now();
@@ -1829,8 +1872,13 @@ extern "C" int mgb_solve(const mgb_hier* h, mgb_work* w, const double* f_dev, do
       snprintf(buf, sizeof buf, "diverged at iteration %d: relative residual %.3e", it, rr);
       if (n_history) *n_history = nh;
       if (iterations) *iterations = it;
+      if (pad) pad0_copy(h, u_dev, false, w->pu0, true, s);
       return fail(MGB_NONCONVERGED, buf);
     }
+  }
+  if (pad) {
+    MGB_CUDA_TRY(pad0_copy(h, u_dev, false, w->pu0, true, s));
+    MGB_CUDA_TRY(cudaStreamSynchronize(s));
   }
   const auto t1 = std::chrono::steady_clock::now();
   if (n_history) *n_history = nh;

@@ -50,12 +50,16 @@ inline int64_t pad_offset(int cols) { return (int64_t)PAD_ROWS * pad_pitch(cols)
 
 // PRE: res = true, pro = false (norm optional, u null = zero start);
 // plain sweeps: res = pro = false, nsw = 1 (norm optional);
-// POST: res = false, pro = true.  nsw in {1, 2}.  *nblocks receives the CTA count
+// POST: res = false, pro = true; res = pro = true (warp-strip kernel only, see
+// stream_post_norm_ok): POST that also writes the partial sums of its output's residual.
+// nsw in {1, 2}.  *nblocks receives the CTA count
 // (the number of history partials written when norm is set).
 cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 int stream_max_blocks(const Grid& g);
 // which streaming kernel launch_stream picks for these arguments: 1, 2 or 3
 int stream_kernel_kind(const StreamArgs& a);
+// whether launch_stream(a, nsw, true, true, false, ..) — POST + output residual norm — is available
+inline bool stream_post_norm_ok(const StreamArgs& a) { return stream_kernel_kind(a) == 3; }
 // Two-columns-per-thread variant for band-class levels without masks (mgb_stream2.cu);
 // launch_stream dispatches to it (MGB_STREAM1=1 keeps the one-column kernel).
 cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);

@@ -3,7 +3,10 @@
 //
 // Same passes as k_stream / k_stream2 (PRE: [history norm] + nu sweeps + residual +
 // full-weighting restriction; POST: prolongation + nu sweeps; plain sweeps; the
-// residual-norm pass), same push-form FMA chains, hence bit-identical results.  The
+// residual-norm pass), same push-form FMA chains, hence bit-identical results.  One pass
+// more: POST with the norm of the residual of its own output (res && pro), which folds the
+// per-iteration residual of solve() and the last history entry of run_cycles into the
+// last pass instead of a separate pass over u and f.  The
 // design differs in three ways that remove what bounded k_stream2 (a CTA-wide
 // barrier and a shared-memory neighbour exchange per row step at 8 warps/SM):
 //
@@ -308,8 +311,20 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
       }
     }
   }
+  // ---- POST with RES: the norm of the last residual (field S) instead of a restriction: the
+  // relative residual of the pass's OUTPUT u, folded into the pass (hierarchy.py:135-141)
+  if (RES && PRO) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int y = t - S + j;
+      const bool orow = MODE == 0 || (y >= L.R0 && y < L.R1);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (orow && ((L.own >> c) & 1)) norm = fma(fld[S][j][c], fld[S][j][c], norm);
+    }
+  }
   // ---- restriction: push field S rows y = t - S + j (coarse anchors c0 + 1, c0 + 3)
-  if (RES) {
+  if (RES && !PRO) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       const int y = t - S + j;
@@ -545,7 +560,7 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
   }
 #undef MGB_STEP3
   cpa_wait<0>();
-  if (NORM) {
+  if (NORM || (RES && PRO)) {
     double v = norm;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -665,6 +680,7 @@ cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, boo
   MGB_ST3(1, false, false, false, true, false)  MGB_ST3(1, false, false, true, true, false)
   MGB_ST3(1, false, false, true, false, true)
   MGB_ST3(1, false, true, false, false, false) MGB_ST3(2, false, true, false, false, false)
+  MGB_ST3(1, true, true, false, false, false)  MGB_ST3(2, true, true, false, false, false)   // POST + output residual norm
 #undef MGB_ST3
   return cudaErrorInvalidValue;
 }
