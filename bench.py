@@ -652,7 +652,7 @@ def run_ours(args):
     f_pin = [torch.from_numpy(np.ascontiguousarray(f_host if batched else f_host[0])).pin_memory() for _ in range(2)]
     u_pin = [torch.zeros_like(f_pin[0]).pin_memory() for _ in range(2)]
     fh, uh = [x.numpy() for x in f_pin], [x.numpy() for x in u_pin]
-    e_steps = max(3, min(args.steps, 10))
+    e_steps = max(3, min(args.steps, 50))   # the same K steps as the device-timed region
     hist_hosts = [np.empty((nb, cycles + 1)) for _ in range(e_steps)]
     f_list = [fh[k % 2] for k in range(e_steps)]
     u_list = [uh[k % 2] for k in range(e_steps)]

@@ -598,7 +598,8 @@ static void choose_seg3(int rows, int cols, int S, int wout, int occ, bool unifo
   for (int nseg = 1; nseg <= maxseg; ++nseg) {
     const int seg = (rows + nseg - 1) / nseg;
     int nse = ne ? std::max(1, (int)std::ceil(rows / std::max(1.0, (seg + F) / r - F))) : 0;
-    nse = std::min(nse, maxseg);
+    static const int edge_min_rows = getenv("MGB_EDGE3_MINROWS") ? atoi(getenv("MGB_EDGE3_MINROWS")) : 8;   // measured: 8 beats 16 on c2 levels 1-2
+    nse = std::min(nse, std::max(1, (rows + edge_min_rows - 1) / edge_min_rows));
     const int sege = ne ? (rows + nse - 1) / nse : 0;
     const int64_t ctas = (int64_t)ni * nseg + (int64_t)ne * nse;
     const double w = (double)ctas / slots;
