@@ -54,9 +54,17 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         return LIB
     nvcc = nvcc_path()
 
+    hdr_t = max(os.path.getmtime(p) for p in [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".h")]
+                + [os.path.join(ROOT, "include", "mgb.h"), os.path.abspath(__file__)])
+
     def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         obj = obj if out == LIB else obj.replace(".o", f".{os.getpid()}.o")
+        # incremental: the default build keeps its objects (git-ignored) and recompiles a
+        # source only when it or a header changed
+        if out == LIB and not verbose and not force and not defines and os.path.exists(obj) and \
+                os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(os.path.join(CSRC, src))):
+            return src, obj, subprocess.CompletedProcess([], 0, "", "")
         cmd = [nvcc, *flags(), *defines, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
@@ -76,8 +84,9 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, out)
-    for o in objs:
-        os.remove(o)
+    if out != LIB:
+        for o in objs:
+            os.remove(o)
     return out
 
 

@@ -69,6 +69,42 @@ struct LevelD {
     }
     return true;
   }
+  // Quasi-uniform (single problem): the classes differ from the interior one only on the
+  // boundary rows / columns themselves (bands 1 and 3 equal band 2), and A differs there
+  // only in the entries that point out of the grid - which multiply the exact zeros of the
+  // zero closure (grid.py:27-35), so the interior A weights give the same values everywhere.
+  // What a constant-coefficient operator's Galerkin chain with kernels inferred from each
+  // point's own table looks like (config 2 / 5 levels >= 1): the warp-strip passes then need
+  // class weights only for the update stages of the boundary column of the two edge strips
+  // and for the steps that touch the first / last row.
+  bool quasi_uniform() const {
+    static const bool off = getenv("MGB_NO_QUASI") && atoi(getenv("MGB_NO_QUASI")) != 0;   // A/B experiments
+    if (off || hAcls.size() != 225 || hKcls.size() != 225 || cols % 2 == 0 || cols < 8 || rows < 8) return false;
+    for (int bi = 0; bi < 5; ++bi)
+      for (int bj = 0; bj < 5; ++bj) {
+        const int qi = bi == 1 || bi == 3 ? 2 : bi, qj = bj == 1 || bj == 3 ? 2 : bj;
+        for (int o = 0; o < 9; ++o) {
+          const int di = o / 3 - 1, dj = o % 3 - 1;
+          const bool outside = (bi == 0 && di < 0) || (bi == 4 && di > 0) || (bj == 0 && dj < 0) || (bj == 4 && dj > 0);
+          const double av = hAcls[(bi * 5 + bj) * 9 + o];
+          if (!std::isfinite(av) || (!outside && av != hAint()[o])) return false;
+          if (hKcls[(bi * 5 + bj) * 9 + o] != hKcls[(qi * 5 + qj) * 9 + o]) return false;
+        }
+      }
+    return true;
+  }
+  // StreamArgs::kq: the smoother's class tables of the row / column bands {first, interior, last}
+  void fill_kq(double* kq) const {
+    if (hKcls.size() < 225) return;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c)
+        for (int o = 0; o < 9; ++o) kq[(r * 3 + c) * 9 + o] = hKcls[((2 * r) * 5 + 2 * c) * 9 + o];
+  }
+  // StreamArgs::uniform: 1 uniform, 2 quasi-uniform, 0 neither
+  int uniformity() const {
+    if (!Acls || !Kcls || mask) return 0;
+    return uniform() ? 1 : (quasi_uniform() ? 2 : 0);
+  }
   std::vector<uint8_t> hmask;
   int64_t nact = 0;
   bool a5 = false;         // per-point A with all-zero corner planes (5-point operator)
@@ -743,7 +779,7 @@ extern "C" int mgb_hier_pass_kernel(const mgb_hier* h, int level, int nu, int* k
     a.K = lv.opK();
     a.mask = lv.mask;
     a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
-    a.uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
+    a.uniform = lv.uniformity();
     a.kernel = h->stream_kernel;
     *kind = stream_kernel_kind(a);
   }
@@ -1321,7 +1357,7 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   a.f = f;
   a.stream = s;
   a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
-  a.uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
+  a.uniform = lv.uniformity();
   a.kernel = h->stream_kernel;
   a.a5 = lv.a5 && !lv.Acls;
   if (l == 0 && w->pad0) {
@@ -1332,6 +1368,7 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
     a.ci[o] = lv.hAint()[o];
     a.ci[9 + o] = lv.hKint()[o];
   }
+  lv.fill_kq(a.kq);
   return a;
 }
 
@@ -1975,15 +2012,16 @@ int hier_a5(const mgb_hier* h, int l) { return h->lv[l].a5 && !h->lv[l].Acls; }
 Grid hier_grid(const mgb_hier* h, int l) { return h->grid(l); }
 Op hier_opA(const mgb_hier* h, int l) { return h->lv[l].opA(); }
 Op hier_opK(const mgb_hier* h, int l) { return h->lv[l].opK(); }
-void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform, int* kernel) {
+void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform, int* kernel, double* kq) {
   const LevelD& lv = h->lv[l];
   *valid = h->batch == 1 && lv.Acls && lv.Kcls;
-  if (uniform) *uniform = lv.Acls && lv.Kcls && !lv.mask && lv.uniform();
+  if (uniform) *uniform = lv.uniformity();
   if (kernel) *kernel = h->stream_kernel;
   for (int o = 0; o < 9; ++o) {
     ci[o] = lv.hAint()[o];
     ci[9 + o] = lv.hKint()[o];
   }
+  if (kq) lv.fill_kq(kq);
 }
 double* work_level_u(mgb_work* w, int l) { return w->u[l]; }
 double* work_level_f(mgb_work* w, int l) { return w->f[l]; }

@@ -253,9 +253,9 @@ extern "C" int mgb_dd_create(const mgb_hier* h, int nparts, int first_part, int 
     a.A = hier_opA(h, l);
     a.K = hier_opK(h, l);
     a.mask = hier_mask(h, l);
-    hier_interior(h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel);
+    hier_interior(h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel, a.kq);
     static const bool no_pad = getenv("MGB_DD_PAD") && atoi(getenv("MGB_DD_PAD")) == 0;   // A/B experiments
-    const bool pad = !no_pad && a.uniform && stream_kernel_kind(a) == 3;
+    const bool pad = !no_pad && a.uniform == 1 && stream_kernel_kind(a) == 3;
     d->padded.push_back(pad ? 1 : 0);
     d->pitch.push_back(pad ? pad_pitch(d->cols(l)) : d->cols(l));
     d->ga.push_back(pad ? PAD_ROWS : G);
@@ -416,7 +416,7 @@ static StreamArgs dd_args(const mgb_dd* d, int l, cudaStream_t s) {
   a.mask_c = hier_mask(d->h, l + 1);
   a.a5 = hier_a5(d->h, l);
   a.stream = s;
-  hier_interior(d->h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel);
+  hier_interior(d->h, l, &a.ci_valid, a.ci, &a.uniform, &a.kernel, a.kq);
   if (l < (int)d->padded.size() && d->padded[l]) {
     a.ld = d->pitch[l];
     a.padded = 1;

@@ -22,7 +22,8 @@ int hier_a5(const mgb_hier* h, int l);
 Grid hier_grid(const mgb_hier* h, int l);
 Op hier_opA(const mgb_hier* h, int l);
 Op hier_opK(const mgb_hier* h, int l);
-void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform = nullptr, int* kernel = nullptr);
+void hier_interior(const mgb_hier* h, int l, int* valid, double* ci, int* uniform = nullptr, int* kernel = nullptr,
+                   double* kq = nullptr);
 int work_create_from(const mgb_hier* h, int first, mgb_work** out);
 double* work_level_u(mgb_work* w, int l);
 double* work_level_f(mgb_work* w, int l);

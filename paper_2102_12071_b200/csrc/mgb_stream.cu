@@ -553,7 +553,8 @@ static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks)
 bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform) {
   static const int env = getenv("MGB_STREAM3") ? atoi(getenv("MGB_STREAM3")) : -1;
   if (kernel == 3) return true;
-  if (kernel != 0 || batch != 1 || n < 1000000 || env == 0) return false;
+  static const int64_t min_n = getenv("MGB_STREAM3_MIN") ? atoll(getenv("MGB_STREAM3_MIN")) : 1000000;
+  if (kernel != 0 || batch != 1 || n < min_n || env == 0) return false;
   return uniform || env == 1;
 }
 
@@ -599,9 +600,10 @@ int stream_kernel_kind(const StreamArgs& a) {
 }
 
 int stream_max_blocks(const Grid& g) {
-  // upper bound on the CTAs of any streaming pass over g (seg >= 16, nsw >= 1)
+  // upper bound on the CTAs of any streaming pass over g (segments of at least 16 rows; the
+  // warp-strip kernel's edge strips down to 8: counted with 8 for every strip)
   const int wout = SWT - 2 * 4 - 4;
-  return (int)(((g.cols + wout - 1) / wout) * ((g.rows + 15) / 16));
+  return (int)(((g.cols + wout - 1) / wout) * ((g.rows + 7) / 8));
 }
 
 }  // namespace mgb

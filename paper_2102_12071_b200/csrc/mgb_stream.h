@@ -22,7 +22,9 @@ struct StreamArgs {
                            // must be addressable: with domain decomposition the arrays are
                            // ghosted row blocks passed as pointers pre-offset to global rows.
   int ci_valid;            // 1: ci holds the interior-class weights (batch == 1, classed A and M)
-  int uniform;             // 1: every band class equals the interior one (ci valid everywhere)
+  int uniform;             // 1: every band class equals the interior one (ci valid everywhere);
+                           // 2: quasi-uniform (LevelD::quasi_uniform: the classes differ only on the boundary
+                           // rows / columns, A only in entries that point out of the grid)
   int kernel;              // streaming kernel: 0 auto, 1 one column per thread, 2 column pairs, 3 one warp per strip
   int a5;                  // per-point A with zero corner planes: their loads are skipped
   // two-column kernel CTA map (set by its launcher): edge strips (first / last) get
@@ -38,6 +40,8 @@ struct StreamArgs {
   int64_t ld;
   int padded;
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
+  double kq[81];           // quasi-uniform levels: M class tables [row band first / interior / last][column band
+                           // first / interior / last][9], read from the constant bank
   cudaStream_t stream;
 };
 

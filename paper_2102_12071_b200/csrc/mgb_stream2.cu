@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(T2, RES ? MINB_PRE : MINB) k_stream2(StreamArg
   // fast steps: every CTA column interior (band class 2) and in the grid, or a level
   // whose band classes are all equal (then only out-of-grid columns need zeroing)
   const bool cta_int = c.j0 - H >= 2 && c.j0 - H + c.sw - 1 <= g.cols - 3;
-  const bool cta_fast = cta_int || a.uniform;
+  const bool cta_fast = cta_int || a.uniform == 1;
 #ifdef MGB_CTA_PROF
   unsigned long long prof_t0 = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
@@ -754,7 +754,7 @@ static cudaError_t run_k2(KF kern, int nsw, bool res, bool pro, StreamArgs a, in
   }
   Grid go = a.g;
   go.rows = a.own1 - a.own0;
-  choose_seg2(go, nsw, res, occ, tw, a.uniform != 0, a.own0 == 0, a.own1 == a.g.rows, a);
+  choose_seg2(go, nsw, res, occ, tw, a.uniform == 1, a.own0 == 0, a.own1 == a.g.rows, a);
   const int ni = a.nstrips - a.nedge;
   const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
   const dim3 grid(nctas, 1, a.g.batch);

@@ -38,6 +38,11 @@
 
 #include "mgb_stream.h"
 
+#ifdef MGB_CTA_PROF
+// experiment builds only: per-CTA (smid, entry, loop start, end) of the last warp-strip launch
+__device__ unsigned long long g_cta_prof3[4 * 8192];
+#endif
+
 namespace mgb {
 namespace {
 
@@ -52,6 +57,24 @@ constexpr int SW3 = 32 * CPT;      // strip width
 #ifndef MGB_S3MINB
 #define MGB_S3MINB 12
 #endif
+#ifndef MGB_S3WPC
+#define MGB_S3WPC 1
+#endif
+#ifndef MGB_S3SYNC
+#define MGB_S3SYNC 0
+#endif
+// Experiment knobs (defaults: one warp per CTA, no pacing).  The warp schedulers serve the
+// lowest warp slot first: on config 2's level-0 PRE pass (per-warp %globaltimer,
+// scripts/cta_prof3.py) the three warps of a scheduler finish after 64 / 75 / 85 us.  Putting
+// WPC3 warps (each still owning its own strip and row segment) into one CTA per SM with a CTA
+// barrier every SYNC3 rows keeps them in step (a warp that has finished exits, the barrier
+// goes on with the rest) - and measured SLOWER (PRE 95 - 101 us for periods 16 - 2 against
+// 92.7 us unpaced): the schedulers lose nothing when the favoured warp finishes early, the
+// others speed up.
+constexpr int WPC3 = MGB_S3WPC;
+constexpr int SYNC3 = WPC3 > 1 ? MGB_S3SYNC : 0;   // rows between pacing barriers (a power of two; 0: none)
+static_assert((SYNC3 & (SYNC3 - 1)) == 0, "pacing period");
+static_assert(MGB_S3MINB % WPC3 == 0, "warps per SM must be a multiple of the warps per CTA");
 constexpr int NR3 = MGB_S3NR;      // rows entering per step
 constexpr int DG3 = MGB_S3DG;      // ring groups (of NR3 rows) in flight beyond the next one
 constexpr int pow2_at_least(int v) { return v <= 1 ? 1 : 2 * pow2_at_least((v + 1) / 2); }
@@ -110,6 +133,9 @@ struct Lane3 {
   int64_t ld;          // row pitch of f, u, uo
   unsigned cin, own;   // bit c: column c0 + c in the grid / owned
   int cb[4];           // band of column c0 + c (2 when outside the grid)
+  int ecol, eside;     // quasi-uniform levels: the lane's boundary column (0 or 2; -1 none: c0 is even, the
+                       // grid's first and last columns are even); the strip's boundary column band
+                       // (0 first strip, 2 last strip, -1 interior strip; warp-uniform)
   const double* tab;   // shared-memory class tables: A [25][9], then K [25][9]
   int lo_c, hi_c, mcol;  // POST: coarse rows that may be read, first coarse column of the lane
   double* uo_t;          // uo at (row t - 2 NSW, column c0) of the current step (advanced per step)
@@ -134,8 +160,18 @@ __device__ __forceinline__ void load_e3(const StreamArgs& a, const Lane3& L, int
 //         columns zeroed, output rows tested against the segment)
 //      2: interior rows, edge strip of a non-uniform level (per-column class weights)
 //      3: anything else (per row band and column class; rows and columns tested)
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, bool ZA, bool ALN, int NR, int MODE, int P0>
-__device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const int t,
+// Quasi-uniform levels (UNI == 2, StreamArgs::uniform == 2) use modes 0 and 1 and
+//      4: interior rows, edge strip: constant weights as in mode 1 (the residual stages'
+//         interior A weights are exact everywhere: the class tables differ only in entries
+//         that multiply the zero closure); the update stages' three chains of the grid's
+//         boundary column are redone with its class weights (a.kq, constant bank) in the one
+//         lane that holds it, in stencil_dot's term order, and replace the constant-weight ones
+//      5: rows at the grid's top / bottom: mode 4's scheme with the row-band class of each of
+//         the three rows an update stage pushes into (one warp-uniform table per row role),
+//         rows tested against the grid
+// instead of modes 2 and 3: no per-column class tables, no shared-memory table.
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, bool ZA, bool ALN, int NR, int MODE, int P0>
+__device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const int t, const int tq,
                                       double (&acc)[P3<NSW, RES, NOUT>::S][2][4], double (&racc)[2], double& norm,
                                       const double* ringF, const double* ringU, double (&e0)[3], double (&e1)[3],
                                       double (&eN)[3]) {
@@ -143,7 +179,8 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
   constexpr int S = P::S;
   const Grid& g = a.g;
   constexpr bool CMASK = MODE >= 1;            // zero out-of-grid columns
-  constexpr bool RTEST = MODE == 3;            // rows may leave the grid / the interior band
+  constexpr bool EFIX = MODE >= 4;             // boundary-column chains of the update stages
+  constexpr bool RTEST = MODE == 3 || MODE == 5;   // rows may leave the grid / the interior band
   const int lane = L.lane;
   double fld[S + 1][NR][4];
   // ---- field 0: u (+ P ec) at rows t + j
@@ -208,6 +245,19 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
     for (int j = 0; j < NR; ++j) {
       const int row = t - k + j;
       double* out = fld[k][j];
+#ifndef MGB_S3_NOGUARD
+      // (not on uniform levels: their segments are long, and the test costs config 2's level-0
+      // PRE pass 3 us; it saves 8 / 5 us on the PRE passes of levels 1 / 2)
+      // pipeline fill: stage k's first needed row (R0 - 1 - (S - k), or R0 - (S - k) without a
+      // restriction) starts its chain 2k - 2 steps after the segment's first step; before
+      // that the stage would only compute rows nothing reads (warp-uniform test; steps inside
+      // the segment, MODE 0, are past it)
+      if (UNI != 1 && MODE != 0 && k > 1 && tq + j < 2 * k - 2) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = 0.0;
+        continue;
+      }
+#endif
       if (ZU && k == 1) {
         // zero start: f - A 0 = f (the chain fma(-w, 0, f) returns f)
         ld_own(ringF + (row & (RF3 - 1)) * SW3, lane, out);
@@ -229,7 +279,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         }
         const int s_old = (P0 + j + k) & 1;   // slot of row t - k + j (completes now); static
         int bN = 2, bM = 2, bB = 2;
-        if (MODE == 3) {
+        if (MODE == 3 || MODE == 5) {
           const int x = row + 1;              // the input row
           bN = (unsigned)(x + 1) < (unsigned)g.rows ? band3(x + 1, g.rows) : 2;
           bM = (unsigned)x < (unsigned)g.rows ? band3(x, g.rows) : 2;
@@ -240,8 +290,13 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         const double* wB[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          if (MODE <= 1 || UNI) {
+          if (MODE <= 1 || MODE == 4 || UNI == 1 || (MODE == 5 && resid)) {
             wN[c] = wM[c] = wB[c] = resid ? a.ci : a.ci + 9;
+          } else if (MODE == 5) {
+            // the row band's table of the interior column band (bands 1 and 3 equal band 2)
+            wN[c] = a.kq + ((bN == 0 ? 0 : bN == 4 ? 2 : 1) * 3 + 1) * 9;
+            wM[c] = a.kq + ((bM == 0 ? 0 : bM == 4 ? 2 : 1) * 3 + 1) * 9;
+            wB[c] = a.kq + ((bB == 0 ? 0 : bB == 4 ? 2 : 1) * 3 + 1) * 9;
           } else if (MODE == 2) {
             wN[c] = wM[c] = wB[c] = tabk + (10 + L.cb[c]) * 9;
           } else {
@@ -252,6 +307,28 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         }
         double (&Ao)[4] = acc[k - 1][s_old];        // row t - k + j: its bottom terms complete it
         double (&Am)[4] = acc[k - 1][s_old ^ 1];    // row t - k + j + 1: middle terms
+        // mode 4: the boundary column's three chains (completing row, middle row, new row)
+        // with its own class weights, from the accumulators as they are before this stage
+        double eo = 0.0, em = 0.0, es = 0.0;
+        if (EFIX && !resid && (MODE == 4 || L.eside >= 0)) {
+          const bool e2 = L.ecol == 2;
+          // the boundary column's class per row role (interior rows: one table)
+          const double* weN = a.kq + ((MODE == 4 ? 1 : (bN == 0 ? 0 : bN == 4 ? 2 : 1)) * 3 + L.eside) * 9;
+          const double* weM = MODE == 4 ? weN : a.kq + ((bM == 0 ? 0 : bM == 4 ? 2 : 1) * 3 + L.eside) * 9;
+          const double* weB = MODE == 4 ? weN : a.kq + ((bB == 0 ? 0 : bB == 4 ? 2 : 1) * 3 + L.eside) * 9;
+          double xe[3];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) xe[q] = e2 ? in[2 + q] : in[q];
+          eo = e2 ? Ao[2] : Ao[0];
+          em = e2 ? Am[2] : Am[0];
+          es = e2 ? seed[2] : seed[0];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) eo = fma(weB[6 + q], xe[q], eo);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) em = fma(weM[3 + q], xe[q], em);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) es = fma(weN[q], xe[q], es);
+        }
 #define FMS(w_, x_, a_) fma(resid ? -(w_) : (w_), (x_), (a_))
         // critical path first (the completed row feeds the next stage through shuffles),
         // one wave of four independent chains per weight; every chain keeps
@@ -276,6 +353,15 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         // row t - k + j + 2 reuses the completed row's slot
 #pragma unroll
         for (int c = 0; c < 4; ++c) Ao[c] = seed[c];
+        if (EFIX && !resid && (MODE == 4 || L.eside >= 0)) {
+#pragma unroll
+          for (int c = 0; c < 4; c += 2) {
+            const bool fix = L.ecol == c;
+            out[c] = fix ? eo : out[c];
+            Am[c] = fix ? em : Am[c];
+            Ao[c] = fix ? es : Ao[c];
+          }
+        }
       }
       // zero the completed row outside the grid
       if (RTEST) {
@@ -378,24 +464,36 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
 // FMAs are skipped (adding an exact zero product leaves every chain's value unchanged).
 // ALN: f, u, uo use the padded layout (16-byte copies bypassing L1, 128-bit stores, no
 // column predicates: the margins read as zeros).
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, bool ZA, bool ALN>
-__global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, bool ZA, bool ALN>
+__global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(StreamArgs a) {
+#ifdef MGB_CTA_PROF
+  unsigned long long prof_t0 = 0, prof_t1 = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
+#endif
   pdl_trigger();
   using P = P3<NSW, RES, NOUT>;
   constexpr int S = P::S, H = P::H, WOUT = P::WOUT;
   constexpr int NR = NR3;
   extern __shared__ __align__(16) double sm3[];
-  double* ringF = sm3;                       // RF3 x SW3
+  // work item of this warp; warps beyond the last item leave before any barrier
+  // (the lane-0 broadcast tells the compiler that the warp index, and with it the strip, the
+  // segment and every row bound derived from it, is warp-uniform: uniform registers and
+  // uniform branches, as in a one-warp CTA)
+  const int wib = WPC3 > 1 ? __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0) : 0;
+  const int item = blockIdx.x * WPC3 + wib;
+  const int nitems = a.nedge * a.nseg_edge + (a.nstrips - a.nedge) * a.nseg;
+  if (WPC3 > 1 && item >= nitems) return;
+  double* ringF = sm3 + (size_t)wib * (RF3 * SW3 + (ZU ? 0 : RU3 * SW3) + (UNI != 0 ? 0 : 2 * NCLS3 * 9));  // RF3 x SW3
   double* ringU = ringF + RF3 * SW3;         // RU3 x SW3 (unused when ZU)
   double* tab = ringU + (ZU ? 0 : RU3 * SW3);  // 2 x 25 x 9 class tables (non-uniform levels)
   const Grid& g = a.g;
   Lane3 L;
-  L.lane = threadIdx.x;
+  L.lane = threadIdx.x & 31;
   // CTA -> (strip, row segment): the two edge strips' CTAs first (shorter segments on
   // non-uniform levels, whose edge steps read class weights), then the interior ones
   int strip, sy, seg, nseg;
   {
-    const int id = blockIdx.x, ne = a.nedge;
+    const int id = item, ne = a.nedge;
     if (id < ne * a.nseg_edge) {
       strip = (id % ne == 0) ? 0 : a.nstrips - 1;
       sy = id / ne;
@@ -420,13 +518,18 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
     L.own |= ((in && gc >= j0 && gc < j0 + WOUT) ? 1u : 0u) << c;
     L.cb[c] = in ? band3(gc, g.cols) : 2;
   }
+  L.ecol = -1;
+  L.eside = strip == 0 ? 0 : (strip == a.nstrips - 1 ? 2 : -1);
+#pragma unroll
+  for (int c = 0; c < 4; c += 2)
+    if (L.c0 + c == 0 || L.c0 + c == g.cols - 1) L.ecol = c;
   const int own0 = a.own1 > 0 ? a.own0 : 0, rend = a.own1 > 0 ? a.own1 : g.rows;
   L.R0 = own0 + sy * seg;
   L.R1 = sy == nseg - 1 ? rend : min(rend, L.R0 + seg);
   L.tab = tab;
   L.ld = a.ld > 0 ? a.ld : g.cols;
   const bool strip_int = j0 - H >= 2 && j0 - H + SW3 - 1 <= g.cols - 3;
-  if (!UNI) {
+  if (UNI == 0) {
     for (int q = L.lane; q < 2 * NCLS3 * 9; q += 32)
       tab[q] = q < NCLS3 * 9 ? a.A.cls[q] : a.K.cls[q - NCLS3 * 9];
     __syncwarp();
@@ -434,7 +537,8 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
   // rows: field S rows [ylo, yhi] are needed (restriction: one row beyond the owned
   // range on each side), field 0 rows [ylo - S, yhi + S]; steps start at a multiple of NR
   const int ylo = RES ? L.R0 - 1 : L.R0, yhi = RES ? L.R1 : L.R1 - 1;
-  int t0 = ylo - S;
+  const int tfirst = ylo - S;   // the first step that matters (stage k: 2k - 2 steps later)
+  int t0 = tfirst;
   t0 -= (t0 & 1);   // even: static row parities (NR = 2 steps, or the two-step unroll)
   const int t1 = yhi + S;
   const int lo_row = max(0, ylo - S), hi_row = min(g.rows - 1, t1);
@@ -528,10 +632,13 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
   }
   for (int s = s0; s <= sstart + DG3; ++s) issue(s, s >= sstart);
   L.uo_t = NOUT || !a.uo ? nullptr : a.uo + (int64_t)(t0 - 2 * NSW) * L.ld + L.c0;
+#ifdef MGB_CTA_PROF
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t1));
+#endif
 
 #define MGB_STEP3(P0_)                                                                                       \
   {                                                                                                          \
-    const int t = tb + (P0_) * NR;                                                                           \
+    const int t = tb + (P0_) * NR, tq = t - tfirst;                                                          \
     __syncwarp();                                                                                            \
     issue(t / NR + 1 + DG3, true);                                                                           \
     cpa_wait<DG3>(); /* f rows up to t + NR and u rows t .. t + NR - 1 have landed */                       \
@@ -539,39 +646,62 @@ __global__ void __launch_bounds__(32, MGB_S3MINB) k_stream3(StreamArgs a) {
     const bool rows_int = t - S >= 2 && t + NR <= g.rows - 3;                                                \
     /* core: every row an output of this step touches is owned (norm, u, coarse rows) */                    \
     const bool core = t - S - 2 >= L.R0 && t + NR <= L.R1 - 1;                                               \
-    if (rows_int && strip_int && core && (NOUT || a.uo))                                                     \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
-    else if (rows_int && (UNI || strip_int))                                                                 \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
-    else if (rows_int)                                                                                       \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 2, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
-    else                                                                                                     \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 3, (P0_) * NR & 1>(a, L, t, acc, racc, norm, ringF, ringU, e0, e1, eN); \
+    if (UNI == 2) {                                                                                                                                   \
+      if (!rows_int)                                                                                                                                  \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 5, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+      else if (!strip_int)                                                                                                                            \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 4, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+      else if (core && (NOUT || a.uo))                                                                                                                \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+      else                                                                                                                                            \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+    } else if (rows_int && strip_int && core && (NOUT || a.uo))                                                                                       \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
+    else if (rows_int && (UNI != 0 || strip_int))                                                                                                     \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
+    else if (rows_int)                                                                                                                                \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 2, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
+    else                                                                                                                                              \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 3, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
     L.uo_t += NR * L.ld;                                                                                     \
   }
   // t0 is even: with one row per step, unroll two steps so each step's parity is static
-  if (NR == 2) {
-    for (int tb = t0; tb <= t1; tb += NR) MGB_STEP3(0)
-  } else {
-    for (int tb = t0; tb <= t1; tb += 2 * NR) {
-      MGB_STEP3(0)
-      MGB_STEP3(1)
-    }
+  constexpr int ADV = NR == 2 ? NR : 2 * NR;
+#pragma unroll 1
+  for (int tb = t0; tb <= t1; tb += ADV) {
+    if (SYNC3 > 0 && (tb & ((SYNC3 > ADV ? SYNC3 : ADV) - 1)) == 0) __syncthreads();   // pacing only
+    MGB_STEP3(0)
+    if (NR != 2) MGB_STEP3(1)
   }
 #undef MGB_STEP3
   cpa_wait<0>();
+#ifdef MGB_CTA_PROF
+  if (L.lane == 0 && item < 8192) {
+    unsigned long long t2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    smid |= wid << 16;
+    g_cta_prof3[4 * item] = smid;
+    g_cta_prof3[4 * item + 1] = prof_t0;
+    g_cta_prof3[4 * item + 2] = prof_t1;
+    g_cta_prof3[4 * item + 3] = t2;
+  }
+#endif
   if (NORM || (RES && PRO)) {
     double v = norm;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (L.lane == 0) a.partials[blockIdx.x] = v;
+    if (L.lane == 0) a.partials[item] = v;
   }
 }
 
 }  // namespace
 
-static size_t stream3_smem(bool zu, bool uni) {
-  return sizeof(double) * ((size_t)(RF3 + (zu ? 0 : RU3)) * SW3 + (uni ? 0 : 2 * NCLS3 * 9));
+static size_t stream3_smem(bool zu, int uni) {
+  return sizeof(double) * ((size_t)(RF3 + (zu ? 0 : RU3)) * SW3 + (uni != 0 ? 0 : 2 * NCLS3 * 9));
 }
 
 static int sm_count3() {
@@ -584,17 +714,20 @@ static int sm_count3() {
 // Row segments: whole waves of the measured occupancy with the fewest pipeline fills
 // (2S + 3 steps per segment); the two edge strips of a non-uniform level get
 // segments shorter by the measured cost ratio of their class-weight steps.
-static void choose_seg3(int rows, int cols, int S, int wout, int occ, bool uniform, StreamArgs& a) {
+static void choose_seg3(int rows, int cols, int S, int wout, int occ, int uniform, StreamArgs& a) {
   const int strips = (cols + wout - 1) / wout;
-  const int ne = uniform ? 0 : std::min(strips, 2), ni = strips - ne;
+  const int ne = uniform == 1 ? 0 : std::min(strips, 2), ni = strips - ne;
   const int64_t slots = (int64_t)sm_count3() * std::max(occ, 1);
   static const double r_env = getenv("MGB_EDGE3") ? atof(getenv("MGB_EDGE3")) : 0.0;
-  const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : 1.8);
+  // edge-strip step cost relative to an interior strip's: class lookups for every column
+  // 1.8 (measured); the boundary-column fix-up of a quasi-uniform level ~1.25
+  const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : (uniform == 2 ? 1.25 : 1.8));
   const int F = 2 * S + 2 + NR3;
   double best_t = 1e300;
   a.nstrips = strips;
   a.nedge = ne;
-  const int maxseg = std::max(1, (rows + 15) / 16);
+  static const int min_rows = getenv("MGB_SEG3_MINROWS") ? std::max(1, atoi(getenv("MGB_SEG3_MINROWS"))) : 12;
+  const int maxseg = std::max(1, (rows + min_rows - 1) / min_rows);
   for (int nseg = 1; nseg <= maxseg; ++nseg) {
     const int seg = (rows + nseg - 1) / nseg;
     int nse = ne ? std::max(1, (int)std::ceil(rows / std::max(1.0, (seg + F) / r - F))) : 0;
@@ -622,7 +755,7 @@ static void choose_seg3(int rows, int cols, int S, int wout, int occ, bool unifo
   }
 }
 
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, bool UNI, bool ZA, bool ALN>
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, bool ZA, bool ALN>
 static cudaError_t run_k3(StreamArgs a, int* nblocks) {
   using P = P3<NSW, RES, NOUT>;
   auto kern = k_stream3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN>;
@@ -632,26 +765,27 @@ static cudaError_t run_k3(StreamArgs a, int* nblocks) {
   static thread_local std::vector<Occ> occ_cache;   // per instantiation, per device
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
-  const size_t smem = stream3_smem(ZU, UNI);
+  const size_t smem = WPC3 * stream3_smem(ZU, UNI);
   int occ = -1;
   for (auto& e : occ_cache)
     if (e.dev == dev) occ = e.occ;
   if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WPC3, smem);
     if (e != cudaSuccess) return e;
+    occ *= WPC3;   // warps (work items) per SM
     occ_cache.push_back({dev, occ});
   }
   if (a.own1 <= 0) {
     a.own0 = 0;
     a.own1 = a.g.rows;
   }
-  choose_seg3(a.own1 - a.own0, a.g.cols, P::S, P::WOUT, occ, a.uniform != 0, a);
+  choose_seg3(a.own1 - a.own0, a.g.cols, P::S, P::WOUT, occ, UNI == 2 ? 2 : (a.uniform == 1 ? 1 : 0), a);
   const int ni = a.nstrips - a.nedge;
   const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
   if (nblocks) *nblocks = nctas;
-  const cudaError_t e = launch_pdl(kern, dim3(nctas, 1, 1), dim3(32), smem, a.stream, a);
+  const cudaError_t e = launch_pdl(kern, dim3((nctas + WPC3 - 1) / WPC3, 1, 1), dim3(32 * WPC3), smem, a.stream, a);
   if (e != cudaSuccess) return e;
   return MGB_DBG("k_stream3");
 }
@@ -666,13 +800,21 @@ cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, boo
   const bool nout = a.uo == nullptr && !res && !pro;
   static const bool no_za = getenv("MGB_NO_ZA") && atoi(getenv("MGB_NO_ZA")) != 0;   // A/B experiments
   const bool za = !no_za && a.ci[2] == 0.0 && a.ci[6] == 0.0;   // uniform: every class is the interior one
+  // quasi-uniform flavour: the first and the last strip must be different strips
+  const bool quasi = a.uniform == 2 && a.g.cols > SW3;
 #define MGB_ST3(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                                \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_)    \
-    return !a.uniform  ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, false, false, false>(a, nblocks) \
-           : !a.padded ? (za ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, true, false>(a, nblocks)  \
-                             : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, false, false>(a, nblocks)) \
-           : za        ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, true, true>(a, nblocks)       \
-                       : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, true, false, true>(a, nblocks);
+    return quasi           ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 2, false, false>(a, nblocks) \
+           : a.uniform != 1 ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 0, false, false>(a, nblocks) \
+           : !a.padded ? (za ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, true, false>(a, nblocks)  \
+                             : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, false>(a, nblocks)) \
+           : za        ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, true, true>(a, nblocks)       \
+                       : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, true>(a, nblocks);
+#ifdef MGB_S3_FEW   // experiment builds only: config 2's level-0 passes (fast compile)
+  MGB_ST3(2, true, false, true, false, false) MGB_ST3(2, false, true, false, false, false)
+  MGB_ST3(2, true, true, false, false, false) MGB_ST3(2, true, false, true, true, false)
+  MGB_ST3(2, true, false, false, false, false) MGB_ST3(2, true, false, false, true, false)
+#else
   MGB_ST3(1, true, false, false, false, false) MGB_ST3(1, true, false, true, false, false)
   MGB_ST3(1, true, false, false, true, false)  MGB_ST3(1, true, false, true, true, false)
   MGB_ST3(2, true, false, false, false, false) MGB_ST3(2, true, false, true, false, false)
@@ -682,8 +824,15 @@ cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, boo
   MGB_ST3(1, false, false, true, false, true)
   MGB_ST3(1, false, true, false, false, false) MGB_ST3(2, false, true, false, false, false)
   MGB_ST3(1, true, true, false, false, false)  MGB_ST3(2, true, true, false, false, false)   // POST + output residual norm
+#endif
 #undef MGB_ST3
   return cudaErrorInvalidValue;
 }
 
 }  // namespace mgb
+
+#ifdef MGB_CTA_PROF
+extern "C" __attribute__((visibility("default"))) int mgb_debug_cta_prof3(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_cta_prof3, sizeof(unsigned long long) * 4 * n);
+}
+#endif
