@@ -149,6 +149,14 @@ int mgb_hier_storage_info(const mgb_hier* h, int level, int* a_classed, int* k_c
    per-point A: 5 when its corner planes are zero everywhere (a 5-point operator,
    checked on the device at build), else 9 (0 for class-compact A). */
 int mgb_hier_stencil_points(const mgb_hier* h, int level, int* a_points);
+/* How far level `level`'s band-class tables are from constant: 1 uniform (every class equals
+   the interior one: the level-0 operator of a constant-coefficient problem, grid.py:163-206),
+   2 quasi-uniform (the classes differ only on the first / last row and column, A only in
+   entries that point out of the grid: the Galerkin chain of such a problem,
+   transfer.py:150-222, with kernels inferred from each point's own table,
+   smoothers.py:302-322), 0 neither (or per-point planes / masked).  The warp-strip passes
+   use constant-bank weights everywhere on 1, and everywhere but the boundary column / rows on 2. */
+int mgb_hier_level_uniformity(const mgb_hier* h, int level, int* uniformity);
 /* Which kernel runs level `level`'s fused V(nu, nu) passes (measurement labels):
    0 separate sweep / restriction / prolongation kernels, 1 k_stream (one column per
    thread), 2 k_stream2 (column pairs), 3 k_stream3 (one warp per 128-column strip),

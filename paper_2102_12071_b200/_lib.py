@@ -45,6 +45,7 @@ SIGNATURES = {
     "mgb_hier_depth": (I, [P, PI, PI]),
     "mgb_hier_level_info": (I, [P, I, PI, PI, PI, PI, PD]),
     "mgb_hier_stencil_points": (I, [P, I, PI]),
+    "mgb_hier_level_uniformity": (I, [P, I, PI]),
     "mgb_hier_pass_kernel": (I, [P, I, I, PI]),
     "mgb_hier_get_operator": (I, [P, I, P]),
     "mgb_hier_get_kernels": (I, [P, I, P]),

@@ -760,6 +760,13 @@ extern "C" int mgb_hier_stencil_points(const mgb_hier* h, int level, int* a_poin
   return MGB_OK;
 }
 
+extern "C" int mgb_hier_level_uniformity(const mgb_hier* h, int level, int* uniformity) {
+  if (!h || !uniformity) return fail(MGB_CONTRACT, "null argument");
+  if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
+  *uniformity = h->batch == 1 ? h->lv[level].uniformity() : 0;
+  return MGB_OK;
+}
+
 // forward declarations (defined with the cycle code below)
 static int pass_kind(const mgb_hier* h, int l, int nu1, int nu2);
 

@@ -82,6 +82,17 @@ constexpr int RU3 = pow2_at_least(NR3 * (DG3 + 2));       // u ring rows (t .. t
 constexpr int RF3 = pow2_at_least(NR3 * (DG3 + 2) + 4);   // f ring rows (t - 4 .. t + NR (DG + 2) - 1)
 static_assert(NR3 * (DG3 + 2) <= RU3 && NR3 * (DG3 + 2) + 4 <= RF3, "ring depths");
 constexpr int NCLS3 = 25;
+// One stage lag (experiment knob, default off: measured no faster, see DESIGN): stages 3.. consume the field-2 row that stage 2 completed in
+// the PREVIOUS step (kept in four registers), so a step holds two independent stage chains
+// (1-2 and 3-5) instead of one chain through all five.  A warp issues in order, and a
+// dependent stage costs a shuffle plus three dependent DFMAs (~100 cycles): the single chain
+// kept a lone warp at ~1,000 cycles per step for ~470 cycles of issue.
+#ifndef MGB_S3LAG
+#define MGB_S3LAG 0
+#endif
+constexpr bool LAG3 = MGB_S3LAG != 0;
+static_assert(!LAG3 || NR3 == 1, "the stage lag is written for one row per step");
+__host__ __device__ constexpr int lag3(int k) { return LAG3 && k >= 3 ? 1 : 0; }
 
 template <int NSW, bool RES, bool NOUT>
 struct P3 {
@@ -174,7 +185,7 @@ template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, b
 __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const int t, const int tq,
                                       double (&acc)[P3<NSW, RES, NOUT>::S][2][4], double (&racc)[2], double& norm,
                                       const double* ringF, const double* ringU, double (&e0)[3], double (&e1)[3],
-                                      double (&eN)[3]) {
+                                      double (&eN)[3], double (&prev)[4]) {
   using P = P3<NSW, RES, NOUT>;
   constexpr int S = P::S;
   const Grid& g = a.g;
@@ -236,14 +247,15 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
       }
     }
   }
-  // ---- stages k = 1..S: push field k-1 rows t - k + 1 + j, complete rows t - k + j
+  // ---- stages k = 1..S: push field k-1 rows t - k - lag + 1 + j, complete rows t - k - lag + j
 #pragma unroll
   for (int k = 1; k <= S; ++k) {
     const bool resid = k & 1;
     const double* tabk = L.tab + (resid ? 0 : NCLS3 * 9);
+    const int dk = lag3(k);
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      const int row = t - k + j;
+      const int row = t - k - dk + j;
       double* out = fld[k][j];
 #ifndef MGB_S3_NOGUARD
       // (not on uniform levels: their segments are long, and the test costs config 2's level-0
@@ -252,7 +264,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
       // restriction) starts its chain 2k - 2 steps after the segment's first step; before
       // that the stage would only compute rows nothing reads (warp-uniform test; steps inside
       // the segment, MODE 0, are past it)
-      if (UNI != 1 && MODE != 0 && k > 1 && tq + j < 2 * k - 2) {
+      if (UNI != 1 && MODE != 0 && k > 1 && tq + j < 2 * k - 2 + dk) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) out[c] = 0.0;
         continue;
@@ -262,7 +274,8 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         // zero start: f - A 0 = f (the chain fma(-w, 0, f) returns f)
         ld_own(ringF + (row & (RF3 - 1)) * SW3, lane, out);
       } else {
-        const double* v = fld[k - 1][j];
+        // the lagged stage's input is last step's field-2 row
+        const double* v = (LAG3 && k == 3) ? prev : fld[k - 1][j];
         double in[6];
         in[0] = __shfl_up_sync(0xffffffffu, v[3], 1);     // column c0 - 1 (lane 0: strip halo)
         in[1] = v[0];
@@ -275,9 +288,9 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
           ld_own(ringF + ((row + 2) & (RF3 - 1)) * SW3, lane, seed);
         } else {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) seed[c] = fld[k - 2][j][c];
+          for (int c = 0; c < 4; ++c) seed[c] = (LAG3 && k == 4) ? prev[c] : fld[k - 2][j][c];
         }
-        const int s_old = (P0 + j + k) & 1;   // slot of row t - k + j (completes now); static
+        const int s_old = (P0 + j + k + dk) & 1;   // slot of row t - k - lag + j (completes now); static
         int bN = 2, bM = 2, bB = 2;
         if (MODE == 3 || MODE == 5) {
           const int x = row + 1;              // the input row
@@ -397,12 +410,16 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
       }
     }
   }
+  if (LAG3 && S >= 3) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) prev[c] = fld[2][NR - 1][c];
+  }
   // ---- POST with RES: the norm of the last residual (field S) instead of a restriction: the
   // relative residual of the pass's OUTPUT u, folded into the pass (hierarchy.py:135-141)
   if (RES && PRO) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      const int y = t - S + j;
+      const int y = t - S - lag3(S) + j;
       const bool orow = MODE == 0 || (y >= L.R0 && y < L.R1);
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -413,10 +430,10 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
   if (RES && !PRO) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      const int y = t - S + j;
+      const int y = t - S - lag3(S) + j;
       const double* xs = fld[S][j];
       const double xr = __shfl_down_sync(0xffffffffu, xs[0], 1);
-      if ((P0 + j + S) & 1) {   // y odd: middle row of coarse row (y - 1) / 2
+      if ((P0 + j + S + lag3(S)) & 1) {   // y odd: middle row of coarse row (y - 1) / 2
         racc[0] = fma(0.125, xs[0], racc[0]);
         racc[0] = fma(0.25, xs[1], racc[0]);
         racc[0] = fma(0.125, xs[2], racc[0]);
@@ -540,8 +557,8 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   const int tfirst = ylo - S;   // the first step that matters (stage k: 2k - 2 steps later)
   int t0 = tfirst;
   t0 -= (t0 & 1);   // even: static row parities (NR = 2 steps, or the two-step unroll)
-  const int t1 = yhi + S;
-  const int lo_row = max(0, ylo - S), hi_row = min(g.rows - 1, t1);
+  const int t1 = yhi + S + lag3(S);   // the lagged stages finish one step later
+  const int lo_row = max(0, ylo - S), hi_row = min(g.rows - 1, yhi + S);
   L.lo_c = (lo_row - 2) >> 1;
   L.hi_c = (hi_row >> 1) + 1;
   L.mcol = (L.c0 >> 1) - 1;
@@ -618,6 +635,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   double norm = 0.0;
   // POST: coarse rows (t >> 1) - 1, t >> 1 (e0, e1) and the next one in flight (eN)
   double e0[3] = {0.0, 0.0, 0.0}, e1[3] = {0.0, 0.0, 0.0}, eN[3] = {0.0, 0.0, 0.0};
+  double prev[4] = {0.0, 0.0, 0.0, 0.0};   // field 2's newest row (the stage lag)
   pdl_wait();  // u, f, ec come from the preceding kernels; uo / rc may still be read there
   if (PRO) {
     load_e3(a, L, (t0 >> 1) - 1, e1);
@@ -631,7 +649,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
     if (!ZU) unx = ub + (int64_t)t0 * L.ld + colq;
   }
   for (int s = s0; s <= sstart + DG3; ++s) issue(s, s >= sstart);
-  L.uo_t = NOUT || !a.uo ? nullptr : a.uo + (int64_t)(t0 - 2 * NSW) * L.ld + L.c0;
+  L.uo_t = NOUT || !a.uo ? nullptr : a.uo + (int64_t)(t0 - 2 * NSW - lag3(2 * NSW)) * L.ld + L.c0;
 #ifdef MGB_CTA_PROF
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t1));
 #endif
@@ -643,26 +661,26 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
     issue(t / NR + 1 + DG3, true);                                                                           \
     cpa_wait<DG3>(); /* f rows up to t + NR and u rows t .. t + NR - 1 have landed */                       \
     __syncwarp();                                                                                            \
-    const bool rows_int = t - S >= 2 && t + NR <= g.rows - 3;                                                \
+    const bool rows_int = t - S - lag3(S) >= 2 && t + NR <= g.rows - 3;                                      \
     /* core: every row an output of this step touches is owned (norm, u, coarse rows) */                    \
-    const bool core = t - S - 2 >= L.R0 && t + NR <= L.R1 - 1;                                               \
+    const bool core = t - S - lag3(S) - 2 >= L.R0 && t + NR <= L.R1 - 1;                                     \
     if (UNI == 2) {                                                                                                                                   \
       if (!rows_int)                                                                                                                                  \
-        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 5, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 5, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
       else if (!strip_int)                                                                                                                            \
-        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 4, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 4, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
       else if (core && (NOUT || a.uo))                                                                                                                \
-        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
       else                                                                                                                                            \
-        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);            \
+        step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
     } else if (rows_int && strip_int && core && (NOUT || a.uo))                                                                                       \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);              \
     else if (rows_int && (UNI != 0 || strip_int))                                                                                                     \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);              \
     else if (rows_int)                                                                                                                                \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 2, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 2, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);              \
     else                                                                                                                                              \
-      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 3, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN);              \
+      step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 3, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);              \
     L.uo_t += NR * L.ld;                                                                                     \
   }
   // t0 is even: with one row per step, unroll two steps so each step's parity is static
@@ -722,7 +740,7 @@ static void choose_seg3(int rows, int cols, int S, int wout, int occ, int unifor
   // edge-strip step cost relative to an interior strip's: class lookups for every column
   // 1.8 (measured); the boundary-column fix-up of a quasi-uniform level ~1.25
   const double r = ni == 0 ? 1.0 : (r_env > 0.0 ? r_env : (uniform == 2 ? 1.25 : 1.8));
-  const int F = 2 * S + 2 + NR3;
+  const int F = 2 * S + 2 + NR3 + lag3(S);
   double best_t = 1e300;
   a.nstrips = strips;
   a.nedge = ne;

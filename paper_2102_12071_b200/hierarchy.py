@@ -224,6 +224,13 @@ class MultigridHierarchy:
         _lib.call("mgb_hier_stencil_points", self._h, l, C.byref(p))
         return p.value
 
+    def level_uniformity(self, l: int) -> int:
+        """1: level l's band classes all equal the interior one; 2: they differ only on the
+        first / last row and column (A only in entries that point out of the grid); 0 neither."""
+        p = C.c_int()
+        _lib.call("mgb_hier_level_uniformity", self._h, l, C.byref(p))
+        return p.value
+
     PASS_KERNELS = {0: "separate kernels", 1: "k_stream (one column per thread)", 2: "k_stream2 (column pairs)",
                     3: "k_stream3 (one warp per 128-column strip, four columns per lane)", 4: "k_tile (tile-local passes)"}
 

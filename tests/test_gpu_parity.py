@@ -618,6 +618,8 @@ def test_facade_rejects_bad_device_buffers():
     (97, 1201, math.pi / 4, 2, "conv_c2"),     # short and wide: many strips, few rows
     (2047, 130, math.pi / 5, 2, "conv"),       # tall and narrow: two strips, long segments
     (40, 40, 0.3, 1, "fc"),                    # one strip, one segment
+    (1023, 2047, math.pi / 4, 2, "conv_c2"),   # quasi-uniform coarse levels with several strips (modes 4 / 5)
+    (767, 515, 1.1, 1, "conv_c5"),             # the same, sizes that are not 2^k - 1, V(1,1)
 ])
 def test_warp_strip_stream_kernel_bit_identical(rows, cols, theta, nu, net):
     """The one-warp-per-strip kernel (k_stream3: four columns per lane, shuffle
@@ -631,6 +633,12 @@ def test_warp_strip_stream_kernel_bit_identical(rows, cols, theta, nu, net):
     levels = gen.levels_for(min(rows, cols))
     h = mg.equip_inferred(mg.build_hierarchy_classed(rows, cols, table, levels), net_of(net))
     h.set_passes(0, 1)
+    if (rows, cols) == (1023, 2047):
+        # level 0 uniform; the Galerkin levels with conv-net kernels quasi-uniform (an fc net's
+        # kernels see the neighbours' tables: two boundary bands differ)
+        assert [h.level_uniformity(l) for l in range(3)] == [1, 2, 2]
+    if net == "fc" and rows == 1023:
+        assert h.level_uniformity(1) == 0
     f = dv.to_dev(np.random.default_rng(9).uniform(-1, 1, (rows, cols)))
     out = []
     for kind in (2, 3):
