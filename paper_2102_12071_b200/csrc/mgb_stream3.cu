@@ -91,6 +91,10 @@ constexpr int NCLS3 = 25;
 #define MGB_S3LAG 0
 #endif
 constexpr bool LAG3 = MGB_S3LAG != 0;
+// quasi-uniform flavour: whether steps inside the segment get their own (test-free) body
+#ifndef MGB_S3Q_MODE0
+#define MGB_S3Q_MODE0 0
+#endif
 static_assert(!LAG3 || NR3 == 1, "the stage lag is written for one row per step");
 __host__ __device__ constexpr int lag3(int k) { return LAG3 && k >= 3 ? 1 : 0; }
 
@@ -669,7 +673,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
         step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 5, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
       else if (!strip_int)                                                                                                                            \
         step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 4, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
-      else if (core && (NOUT || a.uo))                                                                                                                \
+      else if (MGB_S3Q_MODE0 && core && (NOUT || a.uo))                                                                                                                \
         step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 0, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
       else                                                                                                                                            \
         step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 1, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);            \
