@@ -188,6 +188,7 @@ struct mgb_work {
   // enqueued (stream_args / vcycle_rec then address level 0 through them)
   double *pf0 = nullptr, *pu0 = nullptr, *pt0 = nullptr;
   bool pad0 = false;
+  double* plain_out = nullptr;   // while enqueuing the last cycle of a padded run_cycles solve: the caller's u
   std::vector<GraphEntry> graphs;
   int graph_version = -1;   // hierarchy version the cached graphs were captured against
   int64_t last_launches = 0;
@@ -1432,6 +1433,12 @@ static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, d
   a.u = *cur;
   a.uo = *oth;
   a.ec = ec;
+  if (l == 0 && w->pad0 && w->plain_out && !split) {
+    // the last POST pass of a run_cycles solve: straight into the caller's dense u instead of
+    // the padded copy plus a 2-D copy back (nothing reads the padded u afterwards)
+    a.uo = w->plain_out;
+    a.ld_out = h->lv[0].cols;
+  }
   if (out_hist) {
     // the relative residual of the pass's output folded into the pass (post_norm_ok checked by the caller)
     a.partials = w->partials;
@@ -1563,12 +1570,35 @@ static int ensure_pad0(mgb_work* w) {
   return MGB_OK;
 }
 
-// dense <-> padded level-0 copies (2-D copies: the margins are never touched)
+// dense <-> padded level-0 copies (the margins are never touched).  A copy kernel of our own:
+// the dense rows of an odd-width grid are only 8-byte aligned, and cudaMemcpy2DAsync moved
+// config 2's 134 MB in 136 us (2 TB/s) where 256-column x 8-row tiles of coalesced 8-byte
+// accesses run at the HBM rate.
+__global__ void __launch_bounds__(256) k_pitch_copy(double* __restrict__ dst, int64_t dp, const double* __restrict__ src,
+                                                    int64_t sp, int rows, int cols) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  const int r0 = blockIdx.y * 8;
+  if (c >= cols) return;
+  double v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (r0 + q < rows) v[q] = src[(int64_t)(r0 + q) * sp + c];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (r0 + q < rows) dst[(int64_t)(r0 + q) * dp + c] = v[q];
+}
+
 static cudaError_t pad0_copy(const mgb_hier* h, double* dst, bool dst_padded, const double* src, bool src_padded,
                              cudaStream_t s) {
   const LevelD& l0 = h->lv[0];
-  const size_t P = sizeof(double) * pad_pitch(l0.cols), D = sizeof(double) * l0.cols;
-  return cudaMemcpy2DAsync(dst, dst_padded ? P : D, src, src_padded ? P : D, D, l0.rows, cudaMemcpyDeviceToDevice, s);
+  const int64_t P = pad_pitch(l0.cols), D = l0.cols;
+  static const bool memcpy2d = getenv("MGB_PAD_MEMCPY2D") && atoi(getenv("MGB_PAD_MEMCPY2D")) != 0;   // A/B experiments
+  if (memcpy2d)
+    return cudaMemcpy2DAsync(dst, sizeof(double) * (dst_padded ? P : D), src, sizeof(double) * (src_padded ? P : D),
+                             sizeof(double) * D, l0.rows, cudaMemcpyDeviceToDevice, s);
+  k_pitch_copy<<<dim3((l0.cols + 255) / 256, (l0.rows + 7) / 8), 256, 0, s>>>(dst, dst_padded ? P : D, src,
+                                                                            src_padded ? P : D, l0.rows, l0.cols);
+  return cudaGetLastError();
 }
 
 static int check_equipped(const mgb_hier* h) {
@@ -1656,12 +1686,19 @@ static int enqueue_run(mgb_work* w, const GraphKey& key, cudaStream_t cs) {
   // the last history entry (residual of the final u): folded into the last cycle's level-0
   // POST pass where that pass supports it, else a residual pass of its own
   const bool fold = key.cycles > 0 && post_norm_ok(w, key.nu1, key.nu2);
-  for (int c = 0; c < key.cycles && !st; ++c)
+  // padded solve whose last history entry rides on the last POST pass: that pass writes the
+  // caller's u itself (the separate residual pass of the other case reads the padded u)
+  static const bool no_direct = getenv("MGB_NO_DIRECT_OUT") && atoi(getenv("MGB_NO_DIRECT_OUT")) != 0;   // A/B experiments
+  const bool direct = pad && fold && h->fused == 2 && key.nu2 > 0 && !no_direct;
+  for (int c = 0; c < key.cycles && !st; ++c) {
+    w->plain_out = direct && c + 1 == key.cycles ? key.u : nullptr;
     st = enqueue_vcycle(w, 0, f, u, key.nu1, key.nu2, cs, key.u_zero && c == 0, key.hist + c, key.cycles + 1,
                         fold && c + 1 == key.cycles ? key.hist + key.cycles : nullptr, key.cycles + 1);
+  }
+  w->plain_out = nullptr;
   if (!st && !fold) st = enqueue_resnorm(w, f, u, key.hist + key.cycles, key.cycles + 1, cs);
   w->pad0 = false;
-  if (!st && pad) MGB_CUDA_TRY(pad0_copy(h, key.u, false, w->pu0, true, cs));
+  if (!st && pad && !direct) MGB_CUDA_TRY(pad0_copy(h, key.u, false, w->pu0, true, cs));
   return st;
 }
 

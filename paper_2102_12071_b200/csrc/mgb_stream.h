@@ -39,6 +39,8 @@ struct StreamArgs {
   // PAD_ROWS rows and PAD_LCOLS / >= 122 columns around the grid, margins never written)
   int64_t ld;
   int padded;
+  int64_t ld_out;          // > 0: uo is a dense array of this pitch (the caller's own u) although f and u use
+                           // the padded layout: the last POST pass of a solve writes its result there directly
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank
   double kq[81];           // quasi-uniform levels: M class tables [row band first / interior / last][column band
                            // first / interior / last][9], read from the constant bank

@@ -146,6 +146,7 @@ __device__ __forceinline__ void ld_own(const double* row, int lane, double v[4])
 struct Lane3 {
   int lane, c0, R0, R1;
   int64_t ld;          // row pitch of f, u, uo
+  int64_t ldo;         // row pitch of uo when it is a dense array beside padded inputs (0: ld)
   unsigned cin, own;   // bit c: column c0 + c in the grid / owned
   int cb[4];           // band of column c0 + c (2 when outside the grid)
   int ecol, eside;     // quasi-uniform levels: the lane's boundary column (0 or 2; -1 none: c0 is even, the
@@ -398,11 +399,11 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
           if (orow && ((L.own >> c) & 1)) norm = fma(out[c], out[c], norm);
       }
       if (!NOUT && k == 2 * NSW && orow && (MODE == 0 || a.uo)) {
-        double* dst = L.uo_t + (int64_t)j * L.ld;   // row t - 2 NSW + j
+        double* dst = L.uo_t + (int64_t)j * (L.ldo ? L.ldo : L.ld);   // row t - 2 NSW - lag + j
 #ifdef MGB_S3_NOSTORE
         if (out[0] == 1.2345e300)   // experiment builds only: (practically) no HBM writes
 #endif
-        if (ALN) {
+        if (ALN && L.ldo == 0) {
           // padded layout: 16-byte aligned pairs (c0 even), owned pairs whole (even bounds)
           if (L.own & 1) *reinterpret_cast<double2*>(dst) = make_double2(out[0], out[1]);
           if (L.own & 4) *reinterpret_cast<double2*>(dst + 2) = make_double2(out[2], out[3]);
@@ -549,6 +550,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   L.R1 = sy == nseg - 1 ? rend : min(rend, L.R0 + seg);
   L.tab = tab;
   L.ld = a.ld > 0 ? a.ld : g.cols;
+  L.ldo = ALN && a.ld_out > 0 ? a.ld_out : 0;
   const bool strip_int = j0 - H >= 2 && j0 - H + SW3 - 1 <= g.cols - 3;
   if (UNI == 0) {
     for (int q = L.lane; q < 2 * NCLS3 * 9; q += 32)
@@ -653,7 +655,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
     if (!ZU) unx = ub + (int64_t)t0 * L.ld + colq;
   }
   for (int s = s0; s <= sstart + DG3; ++s) issue(s, s >= sstart);
-  L.uo_t = NOUT || !a.uo ? nullptr : a.uo + (int64_t)(t0 - 2 * NSW - lag3(2 * NSW)) * L.ld + L.c0;
+  L.uo_t = NOUT || !a.uo ? nullptr : a.uo + (int64_t)(t0 - 2 * NSW - lag3(2 * NSW)) * (L.ldo ? L.ldo : L.ld) + L.c0;
 #ifdef MGB_CTA_PROF
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t1));
 #endif
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
       step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 2, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);              \
     else                                                                                                                                              \
       step3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, NR, 3, (P0_) * NR & 1>(a, L, t, tq, acc, racc, norm, ringF, ringU, e0, e1, eN, prev);              \
-    L.uo_t += NR * L.ld;                                                                                     \
+    L.uo_t += NR * (L.ldo ? L.ldo : L.ld);                                                                                     \
   }
   // t0 is even: with one row per step, unroll two steps so each step's parity is static
   constexpr int ADV = NR == 2 ? NR : 2 * NR;
