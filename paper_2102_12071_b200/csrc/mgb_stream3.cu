@@ -805,6 +805,10 @@ static cudaError_t run_k3(StreamArgs a, int* nblocks) {
     a.own0 = 0;
     a.own1 = a.g.rows;
   }
+  static const int occ_env = getenv("MGB_S3_OCC") ? atoi(getenv("MGB_S3_OCC")) : 0;   // experiments: warps per SM the segments are sized for
+  static const int occ_env_q = getenv("MGB_S3_OCC_Q") ? atoi(getenv("MGB_S3_OCC_Q")) : 0;   // the same, quasi-uniform flavour only
+  if (occ_env > 0) occ = std::min(occ, occ_env);
+  if (UNI == 2 && occ_env_q > 0) occ = std::min(occ, occ_env_q);
   choose_seg3(a.own1 - a.own0, a.g.cols, P::S, P::WOUT, occ, UNI == 2 ? 2 : (a.uniform == 1 ? 1 : 0), a);
   const int ni = a.nstrips - a.nedge;
   const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
