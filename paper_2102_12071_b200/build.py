@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmgb.so")
-SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_stream2.cu", "mgb_stream3.cu", "mgb_tile.cu", "mgb_coarse.cu", "mgb_dd.cu", "mgb_krylov.cu", "mgb_conv.cu", "mgb_cnn.cu", "mgb_train.cu", "mgb_api.cu"]
+SOURCES = ["mgb_kernels.cu", "mgb_cycle.cu", "mgb_stream.cu", "mgb_stream2.cu", "mgb_stream3.cu", "mgb_stream3b.cu", "mgb_tile.cu", "mgb_coarse.cu", "mgb_dd.cu", "mgb_krylov.cu", "mgb_conv.cu", "mgb_cnn.cu", "mgb_train.cu", "mgb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -63,7 +63,8 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         # incremental: the default build keeps its objects (git-ignored) and recompiles a
         # source only when it or a header changed
         if out == LIB and not verbose and not force and not defines and os.path.exists(obj) and \
-                os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(os.path.join(CSRC, src))):
+                os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(os.path.join(CSRC, src)),
+                                                os.path.getmtime(os.path.join(CSRC, "mgb_stream3.cu")) if src == "mgb_stream3b.cu" else 0):
             return src, obj, subprocess.CompletedProcess([], 0, "", "")
         cmd = [nvcc, *flags(), *defines, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)

@@ -38,6 +38,16 @@
 
 #include "mgb_stream.h"
 
+// This file is compiled twice to halve the build's critical path: as itself (the NSW = 1
+// passes, stream3_ok and the launch_stream3 dispatcher) and through mgb_stream3b.cu with
+// MGB_S3_PART 2 (the NSW = 2 passes behind launch_stream3_nsw2).
+#ifndef MGB_S3_PART
+#define MGB_S3_PART 1
+#endif
+#if defined(MGB_CTA_PROF) && MGB_S3_PART != 2
+#undef MGB_CTA_PROF   // the per-warp timeline probe lives with the NSW = 2 passes
+#endif
+
 #ifdef MGB_CTA_PROF
 // experiment builds only: per-CTA (smid, entry, loop start, end) of the last warp-strip launch
 __device__ unsigned long long g_cta_prof3[4 * 8192];
@@ -818,12 +828,22 @@ static cudaError_t run_k3(StreamArgs a, int* nblocks) {
   return MGB_DBG("k_stream3");
 }
 
+cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool norm, int* nblocks);
+
+#if MGB_S3_PART == 1
 bool stream3_ok(const StreamArgs& a) {
   return a.g.batch == 1 && a.ci_valid && a.mask == nullptr && a.A.cls != nullptr && a.K.cls != nullptr &&
          a.A.ks == 1 && a.K.ks == 1;
 }
+#endif
 
+#if MGB_S3_PART == 1
 cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks) {
+  if (nsw == 2) return launch_stream3_nsw2(a, res, pro, norm, nblocks);
+#else
+cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool norm, int* nblocks) {
+  const int nsw = 2;
+#endif
   const bool zu = a.u == nullptr;
   const bool nout = a.uo == nullptr && !res && !pro;
   static const bool no_za = getenv("MGB_NO_ZA") && atoi(getenv("MGB_NO_ZA")) != 0;   // A/B experiments
@@ -838,20 +858,19 @@ cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, boo
                              : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, false>(a, nblocks)) \
            : za        ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, true, true>(a, nblocks)       \
                        : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, true>(a, nblocks);
-#ifdef MGB_S3_FEW   // experiment builds only: config 2's level-0 passes (fast compile)
-  MGB_ST3(2, true, false, true, false, false) MGB_ST3(2, false, true, false, false, false)
-  MGB_ST3(2, true, true, false, false, false) MGB_ST3(2, true, false, true, true, false)
-  MGB_ST3(2, true, false, false, false, false) MGB_ST3(2, true, false, false, true, false)
-#else
-  MGB_ST3(1, true, false, false, false, false) MGB_ST3(1, true, false, true, false, false)
-  MGB_ST3(1, true, false, false, true, false)  MGB_ST3(1, true, false, true, true, false)
+#if MGB_S3_PART == 2
   MGB_ST3(2, true, false, false, false, false) MGB_ST3(2, true, false, true, false, false)
   MGB_ST3(2, true, false, false, true, false)  MGB_ST3(2, true, false, true, true, false)
+  MGB_ST3(2, false, true, false, false, false)
+  MGB_ST3(2, true, true, false, false, false)   // POST + output residual norm
+#elif !defined(MGB_S3_FEW)   // MGB_S3_FEW (experiment builds): the NSW = 2 passes only (fast compile)
+  MGB_ST3(1, true, false, false, false, false) MGB_ST3(1, true, false, true, false, false)
+  MGB_ST3(1, true, false, false, true, false)  MGB_ST3(1, true, false, true, true, false)
   MGB_ST3(1, false, false, false, false, false) MGB_ST3(1, false, false, true, false, false)
   MGB_ST3(1, false, false, false, true, false)  MGB_ST3(1, false, false, true, true, false)
   MGB_ST3(1, false, false, true, false, true)
-  MGB_ST3(1, false, true, false, false, false) MGB_ST3(2, false, true, false, false, false)
-  MGB_ST3(1, true, true, false, false, false)  MGB_ST3(2, true, true, false, false, false)   // POST + output residual norm
+  MGB_ST3(1, false, true, false, false, false)
+  MGB_ST3(1, true, true, false, false, false)   // POST + output residual norm
 #endif
 #undef MGB_ST3
   return cudaErrorInvalidValue;

@@ -16,7 +16,9 @@ def cc(s, out, defs=()):
     if r.returncode:
         raise RuntimeError(r.stderr)
     return r.stderr
-others = [s for s in B.SOURCES if s != src]
+# sources that are compiled with the variant's defines: mgb_stream3b.cu is mgb_stream3.cu's second half
+group = ["mgb_stream3.cu", "mgb_stream3b.cu"] if src == "mgb_stream3.cu" else [src]
+others = [s for s in B.SOURCES if s not in group]
 def base(s):
     o = os.path.join(obj_dir, s.replace(".cu", ".o"))
     if not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(os.path.join(B.CSRC, f)) for f in os.listdir(B.CSRC)):
@@ -26,10 +28,13 @@ with ThreadPoolExecutor(8) as ex:
     objs = list(ex.map(base, others))
 def variant(v):
     name, defs = v
-    o = os.path.join(obj_dir, f"{src[:-3]}_{name}.o")
-    log = cc(src, o, [d for d in defs.split(",") if d])
+    vobjs, log = [], ""
+    for g in group:
+        o = os.path.join(obj_dir, f"{g[:-3]}_{name}.o")
+        log += cc(g, o, [d for d in defs.split(",") if d])
+        vobjs.append(o)
     lib = os.path.join(B.ROOT, "experiments", f"libmgb_{name}.so")
-    r = subprocess.run([nvcc, *B.ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, o, "-ldl"], capture_output=True, text=True)
+    r = subprocess.run([nvcc, *B.ARCH, "-shared", "-cudart", "static", "-o", lib, *objs, *vobjs, "-ldl"], capture_output=True, text=True)
     if r.returncode:
         raise RuntimeError(r.stderr)
     regs = [l for l in log.splitlines() if "registers" in l]
