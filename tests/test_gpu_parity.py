@@ -655,6 +655,38 @@ def test_warp_strip_stream_kernel_bit_identical(rows, cols, theta, nu, net):
     assert np.allclose(ha, hb, rtol=1e-13, atol=0) and np.allclose(hwa, hwb, rtol=1e-13, atol=0)
 
 
+@pytest.mark.parametrize("rows,cols,nu,cycles,net", [
+    (1023, 1025, 2, 3, "conv_c2"),      # odd x odd, just above the 1 M point threshold
+    (1024, 1301, 1, 2, "conv"),         # even rows, V(1,1)
+    (2047, 1025, 2, 1, "conv_c5"),      # one cycle: the first PRE and the last POST are the same cycle's
+    (1100, 1100, 2, 2, "conv_c2"),      # even x even (no quasi-uniform levels: the column bands sit on odd columns)
+])
+def test_default_path_padded_level0_direct_output(rows, cols, nu, cycles, net):
+    """The default pass selection on levels of at least 1 M points — padded level-0 copies
+    staged by the copy kernel, the last POST pass writing the caller's dense u directly, the
+    quasi-uniform flavour below — against the column-pair kernel on the caller's arrays:
+    u bitwise equal for zero and warm starts, histories to summation order."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    table = gen.rotated_fd(1, math.pi / 4, 1e-2, h=1.0 / (max(rows, cols) + 1))[0, 0]
+    h = mg.equip_inferred(mg.build_hierarchy_classed(rows, cols, table, gen.levels_for(min(rows, cols))), net_of(net))
+    assert "k_stream3" in h.pass_kernel(0, nu)
+    f = dv.to_dev(np.random.default_rng(3).uniform(-1, 1, (rows, cols)))
+    out = []
+    for kind in (2, 0):
+        h.set_stream_kernel(kind)
+        u = dv.zeros(f.shape)
+        hh = h.run_cycles(f, u, cycles, nu, nu, u_zero=True)
+        u2 = u.clone()
+        hw = h.run_cycles(f, u2, cycles, nu, nu, u_zero=False)
+        out.append((u, dv.host(hh)[0], u2, dv.host(hw)[0]))
+    h.set_stream_kernel(0)
+    (ua, ha, wa, hwa), (ub, hb, wb, hwb) = out
+    assert t.equal(ua, ub), float((ua - ub).abs().max())
+    assert t.equal(wa, wb), float((wa - wb).abs().max())
+    assert np.allclose(ha, hb, rtol=1e-13, atol=0) and np.allclose(hwa, hwb, rtol=1e-13, atol=0)
+
+
 def test_warp_strip_kernel_full_size_c2():
     """Config 2 at 4095^2 (uniform level 0, non-uniform levels 1-2): the warp-strip
     kernel equals the column-pair kernel bitwise over 3 V(2,2) cycles."""
