@@ -789,7 +789,7 @@ extern "C" int mgb_hier_pass_kernel(const mgb_hier* h, int level, int nu, int* k
     a.ci_valid = h->batch == 1 && lv.Acls && lv.Kcls;
     a.uniform = lv.uniformity();
     a.kernel = h->stream_kernel;
-    *kind = stream_kernel_kind(a);
+    *kind = stream_kernel_kind(a, nu);
   }
   return MGB_OK;
 }
@@ -1555,7 +1555,7 @@ static bool post_norm_ok(const mgb_work* w, int nu1, int nu2) {
   const mgb_hier* h = w->h;
   static const bool off = getenv("MGB_NO_POST_NORM") && atoi(getenv("MGB_NO_POST_NORM")) != 0;   // A/B experiments
   if (off || h->depth() < 2 || h->fused != 2 || pass_kind(h, 0, nu1, nu2) != 1) return false;
-  return stream_post_norm_ok(stream_args(w, 0, nullptr, nullptr));
+  return stream_post_norm_ok(stream_args(w, 0, nullptr, nullptr), nu2);
 }
 
 static int ensure_pad0(mgb_work* w) {

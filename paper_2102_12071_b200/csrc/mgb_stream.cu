@@ -550,11 +550,13 @@ static cudaError_t run_k(KF kern, int nsw, bool res, StreamArgs a, int* nblocks)
 // default, on single-problem uniform band-class levels of at least 1M points (config
 // 2 / 5 level 0); MGB_STREAM3=0 / 1 turns the default off / extends it to every
 // single-problem band-class level of that size (A/B experiments).
-bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform) {
+bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform, int nsw) {
   static const int env = getenv("MGB_STREAM3") ? atoi(getenv("MGB_STREAM3")) : -1;
+  static const bool no_batch = getenv("MGB_STREAM3_BATCH") && atoi(getenv("MGB_STREAM3_BATCH")) == 0;   // A/B experiments
+  if (batch > 1 && (nsw != 1 || !uniform || no_batch)) return false;   // batched flavour: uniform levels, one sweep per pass
   if (kernel == 3) return true;
   static const int64_t min_n = getenv("MGB_STREAM3_MIN") ? atoll(getenv("MGB_STREAM3_MIN")) : 1000000;
-  if (kernel != 0 || batch != 1 || n < min_n || env == 0) return false;
+  if (kernel != 0 || n * batch < min_n || env == 0) return false;
   return uniform || env == 1;
 }
 
@@ -567,7 +569,8 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   // column-pair kernel: band-class levels of >= 1M points (batch included; interior
   // weights from the constant bank or, batched, from registers)
   const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() * a.g.batch >= 1000000);
-  if (cm == 2 && warp_strip_selected(a.kernel, a.g.n(), a.g.batch, a.uniform != 0) && stream3_ok(a))
+  if ((cm == 2 || (cm == 1 && a.g.batch > 1)) && warp_strip_selected(a.kernel, a.g.n(), a.g.batch, a.uniform != 0, nsw) &&
+      stream3_ok(a, nsw))
     return launch_stream3(a, nsw, res, pro, norm, nblocks);
   if (cm != 0 && (pairs || a.kernel == 3)) return launch_stream2(a, nsw, res, pro, norm, nblocks);
 #define MGB_ST(NSW_, RES_, PRO_, NORM_, ZU_)                                                           \
@@ -590,11 +593,13 @@ cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool
   return cudaErrorInvalidValue;
 }
 
-int stream_kernel_kind(const StreamArgs& a) {
+int stream_kernel_kind(const StreamArgs& a, int nsw) {
   const int cm = (a.A.cls != nullptr && a.K.cls != nullptr && a.mask == nullptr) ? (a.ci_valid ? 2 : 1) : 0;
   static const bool one_col = getenv("MGB_STREAM1") && atoi(getenv("MGB_STREAM1")) != 0;
   const bool pairs = a.kernel == 2 || (a.kernel == 0 && !one_col && a.g.n() * a.g.batch >= 1000000);
-  if (cm == 2 && warp_strip_selected(a.kernel, a.g.n(), a.g.batch, a.uniform != 0) && stream3_ok(a)) return 3;
+  if ((cm == 2 || (cm == 1 && a.g.batch > 1)) && warp_strip_selected(a.kernel, a.g.n(), a.g.batch, a.uniform != 0, nsw) &&
+      stream3_ok(a, nsw))
+    return 3;
   if (cm != 0 && (pairs || a.kernel == 3)) return 2;
   return 1;
 }

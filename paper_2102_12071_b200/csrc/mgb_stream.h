@@ -63,17 +63,18 @@ inline int64_t pad_offset(int cols) { return (int64_t)PAD_ROWS * pad_pitch(cols)
 cudaError_t launch_stream(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 int stream_max_blocks(const Grid& g);
 // which streaming kernel launch_stream picks for these arguments: 1, 2 or 3
-int stream_kernel_kind(const StreamArgs& a);
+int stream_kernel_kind(const StreamArgs& a, int nsw = 0);
 // whether launch_stream(a, nsw, true, true, false, ..) — POST + output residual norm — is available
-inline bool stream_post_norm_ok(const StreamArgs& a) { return stream_kernel_kind(a) == 3; }
+inline bool stream_post_norm_ok(const StreamArgs& a, int nsw = 0) { return stream_kernel_kind(a, nsw) == 3; }
 // Two-columns-per-thread variant for band-class levels without masks (mgb_stream2.cu);
 // launch_stream dispatches to it (MGB_STREAM1=1 keeps the one-column kernel).
 cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 // One warp per strip, four columns per lane (mgb_stream3.cu): single-problem band-class
 // levels without masks (stream3_ok); launch_stream dispatches to it for kernel == 3
 // (and for kernel == 0 on large levels, see launch_stream).
-bool stream3_ok(const StreamArgs& a);
-bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform);
+// (nsw: sweeps per pass; a batch of problems runs there only on a uniform level with nsw == 1)
+bool stream3_ok(const StreamArgs& a, int nsw = 0);
+bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform, int nsw = 0);
 cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 
 }  // namespace mgb

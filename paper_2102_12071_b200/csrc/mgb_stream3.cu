@@ -157,6 +157,9 @@ struct Lane3 {
   int lane, c0, R0, R1;
   int64_t ld;          // row pitch of f, u, uo
   int64_t ldo;         // row pitch of uo when it is a dense array beside padded inputs (0: ld)
+  int64_t boffc;       // batched levels: the problem's offset into the coarse arrays rc / ec (0: one problem)
+  const double* wci;   // interior-class A (9) and M (9) weights: a.ci (constant bank), or the problem's own in
+                       // registers (batched uniform levels)
   unsigned cin, own;   // bit c: column c0 + c in the grid / owned
   int cb[4];           // band of column c0 + c (2 when outside the grid)
   int ecol, eside;     // quasi-uniform levels: the lane's boundary column (0 or 2; -1 none: c0 is even, the
@@ -174,7 +177,7 @@ __device__ __forceinline__ void load_e3(const StreamArgs& a, const Lane3& L, int
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     const int cj = L.mcol + q;
-    dst[q] = (rv && (unsigned)cj < (unsigned)cols_c) ? __ldg(a.ec + (int64_t)ci * cols_c + cj) : 0.0;
+    dst[q] = (rv && (unsigned)cj < (unsigned)cols_c) ? __ldg(a.ec + L.boffc + (int64_t)ci * cols_c + cj) : 0.0;
   }
 }
 
@@ -319,7 +322,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (MODE <= 1 || MODE == 4 || UNI == 1 || (MODE == 5 && resid)) {
-            wN[c] = wM[c] = wB[c] = resid ? a.ci : a.ci + 9;
+            wN[c] = wM[c] = wB[c] = resid ? L.wci : L.wci + 9;
           } else if (MODE == 5) {
             // the row band's table of the interior column band (bands 1 and 3 equal band 2)
             wN[c] = a.kq + ((bN == 0 ? 0 : bN == 4 ? 2 : 1) * 3 + 1) * 9;
@@ -467,7 +470,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         const int rows_c = g.rows / 2, cols_c = g.cols / 2;
         if (MODE == 0 || (y >= 2 && ci >= (L.R0 >> 1) && 2 * ci + 1 < L.R1 && ci < rows_c)) {
           const int cj = L.c0 >> 1;
-          double* dst = a.rc + (int64_t)ci * cols_c + cj;
+          double* dst = a.rc + L.boffc + (int64_t)ci * cols_c + cj;
           if ((L.own & 1) && cj < cols_c) {
             const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj];
             dst[0] = act ? sA : 0.0;
@@ -496,7 +499,10 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
 // FMAs are skipped (adding an exact zero product leaves every chain's value unchanged).
 // ALN: f, u, uo use the padded layout (16-byte copies bypassing L1, 128-bit stores, no
 // column predicates: the margins read as zeros).
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, bool ZA, bool ALN>
+// BAT: a batch of problems on a uniform level (config 4's level 0, V(1,1)): a work item is
+// (problem, strip, segment), and the problem's own interior weights live in registers instead
+// of the constant bank (36 registers: the NSW = 1 passes have room for them).
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, bool ZA, bool ALN, bool BAT = false>
 __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(StreamArgs a) {
 #ifdef MGB_CTA_PROF
   unsigned long long prof_t0 = 0, prof_t1 = 0;
@@ -513,8 +519,10 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   // uniform branches, as in a one-warp CTA)
   const int wib = WPC3 > 1 ? __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0) : 0;
   const int item = blockIdx.x * WPC3 + wib;
-  const int nitems = a.nedge * a.nseg_edge + (a.nstrips - a.nedge) * a.nseg;
+  const int nitems1 = a.nedge * a.nseg_edge + (a.nstrips - a.nedge) * a.nseg;   // per problem
+  const int nitems = BAT ? nitems1 * a.g.batch : nitems1;
   if (WPC3 > 1 && item >= nitems) return;
+  const int bprob = BAT ? item / nitems1 : 0;
   double* ringF = sm3 + (size_t)wib * (RF3 * SW3 + (ZU ? 0 : RU3 * SW3) + (UNI != 0 ? 0 : 2 * NCLS3 * 9));  // RF3 x SW3
   double* ringU = ringF + RF3 * SW3;         // RU3 x SW3 (unused when ZU)
   double* tab = ringU + (ZU ? 0 : RU3 * SW3);  // 2 x 25 x 9 class tables (non-uniform levels)
@@ -525,7 +533,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   // non-uniform levels, whose edge steps read class weights), then the interior ones
   int strip, sy, seg, nseg;
   {
-    const int id = item, ne = a.nedge;
+    const int id = BAT ? item - bprob * nitems1 : item, ne = a.nedge;
     if (id < ne * a.nseg_edge) {
       strip = (id % ne == 0) ? 0 : a.nstrips - 1;
       sy = id / ne;
@@ -561,6 +569,16 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   L.tab = tab;
   L.ld = a.ld > 0 ? a.ld : g.cols;
   L.ldo = ALN && a.ld_out > 0 ? a.ld_out : 0;
+  L.boffc = BAT ? (int64_t)bprob * (g.rows / 2) * (g.cols / 2) : 0;
+  double wreg[18];
+  if (BAT) {
+#pragma unroll
+    for (int o = 0; o < 9; ++o) {
+      wreg[o] = __ldg(a.A.cls + (int64_t)bprob * NCLS3 * 9 + 12 * 9 + o);
+      wreg[9 + o] = __ldg(a.K.cls + (int64_t)bprob * NCLS3 * 9 + 12 * 9 + o);
+    }
+  }
+  L.wci = BAT ? wreg : a.ci;
   const bool strip_int = j0 - H >= 2 && j0 - H + SW3 - 1 <= g.cols - 3;
   if (UNI == 0) {
     for (int q = L.lane; q < 2 * NCLS3 * 9; q += 32)
@@ -590,8 +608,9 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   unsigned cq = 0;
 #pragma unroll
   for (int m = 0; m < 4; ++m) cq |= (((unsigned)(colq + 32 * m) < (unsigned)g.cols) ? 1u : 0u) << m;
-  const double* fb = a.f;
-  const double* ub = a.u;
+  const int64_t boff = BAT ? (int64_t)bprob * g.n() : 0;
+  const double* fb = a.f + boff;
+  const double* ub = a.u ? a.u + boff : nullptr;
   // padded layout: every row a segment touches ([-11, rows + 8], inside the PAD_ROWS margins)
   // and every strip column is addressable and the margins hold zeros, so the copies need no
   // predicate; rows are issued in sequence, so the source pointers just advance by the pitch
@@ -665,7 +684,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
     if (!ZU) unx = ub + (int64_t)t0 * L.ld + colq;
   }
   for (int s = s0; s <= sstart + DG3; ++s) issue(s, s >= sstart);
-  L.uo_t = NOUT || !a.uo ? nullptr : a.uo + (int64_t)(t0 - 2 * NSW - lag3(2 * NSW)) * (L.ldo ? L.ldo : L.ld) + L.c0;
+  L.uo_t = NOUT || !a.uo ? nullptr : a.uo + boff + (int64_t)(t0 - 2 * NSW - lag3(2 * NSW)) * (L.ldo ? L.ldo : L.ld) + L.c0;
 #ifdef MGB_CTA_PROF
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t1));
 #endif
@@ -748,7 +767,7 @@ static int sm_count3() {
 // Row segments: whole waves of the measured occupancy with the fewest pipeline fills
 // (2S + 3 steps per segment); the two edge strips of a non-uniform level get
 // segments shorter by the measured cost ratio of their class-weight steps.
-static void choose_seg3(int rows, int cols, int S, int wout, int occ, int uniform, StreamArgs& a) {
+static void choose_seg3(int rows, int cols, int S, int wout, int occ, int uniform, StreamArgs& a, int batch = 1) {
   const int strips = (cols + wout - 1) / wout;
   const int ne = uniform == 1 ? 0 : std::min(strips, 2), ni = strips - ne;
   const int64_t slots = (int64_t)sm_count3() * std::max(occ, 1);
@@ -768,7 +787,7 @@ static void choose_seg3(int rows, int cols, int S, int wout, int occ, int unifor
     static const int edge_min_rows = getenv("MGB_EDGE3_MINROWS") ? atoi(getenv("MGB_EDGE3_MINROWS")) : 8;   // measured: 8 beats 16 on c2 levels 1-2
     nse = std::min(nse, std::max(1, (rows + edge_min_rows - 1) / edge_min_rows));
     const int sege = ne ? (rows + nse - 1) / nse : 0;
-    const int64_t ctas = (int64_t)ni * nseg + (int64_t)ne * nse;
+    const int64_t ctas = ((int64_t)ni * nseg + (int64_t)ne * nse) * batch;
     const double w = (double)ctas / slots;
     const double waves = w <= 2.0 ? std::ceil(w) : w + 0.5;
     const double t = waves * std::max((double)(seg + F), ne ? r * (sege + F) : 0.0);
@@ -789,10 +808,10 @@ static void choose_seg3(int rows, int cols, int S, int wout, int occ, int unifor
   }
 }
 
-template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, bool ZA, bool ALN>
+template <int NSW, bool RES, bool PRO, bool NORM, bool ZU, bool NOUT, int UNI, bool ZA, bool ALN, bool BAT = false>
 static cudaError_t run_k3(StreamArgs a, int* nblocks) {
   using P = P3<NSW, RES, NOUT>;
-  auto kern = k_stream3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN>;
+  auto kern = k_stream3<NSW, RES, PRO, NORM, ZU, NOUT, UNI, ZA, ALN, BAT>;
   struct Occ {
     int dev, occ;
   };
@@ -819,11 +838,13 @@ static cudaError_t run_k3(StreamArgs a, int* nblocks) {
   static const int occ_env_q = getenv("MGB_S3_OCC_Q") ? atoi(getenv("MGB_S3_OCC_Q")) : 0;   // the same, quasi-uniform flavour only
   if (occ_env > 0) occ = std::min(occ, occ_env);
   if (UNI == 2 && occ_env_q > 0) occ = std::min(occ, occ_env_q);
-  choose_seg3(a.own1 - a.own0, a.g.cols, P::S, P::WOUT, occ, UNI == 2 ? 2 : (a.uniform == 1 ? 1 : 0), a);
+  choose_seg3(a.own1 - a.own0, a.g.cols, P::S, P::WOUT, occ, UNI == 2 ? 2 : (a.uniform == 1 ? 1 : 0), a,
+              BAT ? a.g.batch : 1);
   const int ni = a.nstrips - a.nedge;
   const int nctas = a.nedge * a.nseg_edge + ni * a.nseg;
-  if (nblocks) *nblocks = nctas;
-  const cudaError_t e = launch_pdl(kern, dim3((nctas + WPC3 - 1) / WPC3, 1, 1), dim3(32 * WPC3), smem, a.stream, a);
+  if (nblocks) *nblocks = nctas;   // per problem (the history partials are [problem][item])
+  const int64_t total = (int64_t)nctas * (BAT ? a.g.batch : 1);
+  const cudaError_t e = launch_pdl(kern, dim3((unsigned)((total + WPC3 - 1) / WPC3), 1, 1), dim3(32 * WPC3), smem, a.stream, a);
   if (e != cudaSuccess) return e;
   return MGB_DBG("k_stream3");
 }
@@ -831,9 +852,10 @@ static cudaError_t run_k3(StreamArgs a, int* nblocks) {
 cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool norm, int* nblocks);
 
 #if MGB_S3_PART == 1
-bool stream3_ok(const StreamArgs& a) {
-  return a.g.batch == 1 && a.ci_valid && a.mask == nullptr && a.A.cls != nullptr && a.K.cls != nullptr &&
-         a.A.ks == 1 && a.K.ks == 1;
+bool stream3_ok(const StreamArgs& a, int nsw) {
+  const bool tabs = a.mask == nullptr && a.A.cls != nullptr && a.K.cls != nullptr && a.A.ks == 1 && a.K.ks == 1;
+  if (a.g.batch > 1) return tabs && a.uniform == 1 && nsw == 1 && !a.padded && a.own1 <= 0;   // the batched flavour
+  return tabs && a.ci_valid;
 }
 #endif
 
@@ -850,7 +872,15 @@ cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool no
   const bool za = !no_za && a.ci[2] == 0.0 && a.ci[6] == 0.0;   // uniform: every class is the interior one
   // quasi-uniform flavour: the first and the last strip must be different strips
   const bool quasi = a.uniform == 2 && a.g.cols > SW3;
+#if MGB_S3_PART == 1
+#define MGB_ST3B(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                              \
+  if (a.g.batch > 1 && nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_) \
+    return run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, false, true>(a, nblocks);
+#else
+#define MGB_ST3B(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)
+#endif
 #define MGB_ST3(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                                \
+  MGB_ST3B(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                                     \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_)    \
     return quasi           ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 2, false, false>(a, nblocks) \
            : a.uniform != 1 ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 0, false, false>(a, nblocks) \
@@ -873,6 +903,7 @@ cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool no
   MGB_ST3(1, true, true, false, false, false)   // POST + output residual norm
 #endif
 #undef MGB_ST3
+#undef MGB_ST3B
   return cudaErrorInvalidValue;
 }
 

@@ -687,6 +687,38 @@ def test_default_path_padded_level0_direct_output(rows, cols, nu, cycles, net):
     assert np.allclose(ha, hb, rtol=1e-13, atol=0) and np.allclose(hwa, hwb, rtol=1e-13, atol=0)
 
 
+def test_warp_strip_kernel_batched_uniform_level():
+    """Config 4's path: a batch of constant-coefficient problems, V(1,1).  Level 0 (uniform per
+    problem) runs the warp-strip kernel's batched flavour — work items (problem, strip, segment),
+    the problem's interior weights in registers — against the column-pair kernel: u bitwise
+    equal for every problem, histories to summation order; V(2,2) stays on column pairs."""
+    from paper_2102_12071_b200 import device as dv
+    t = dv.torch()
+    rows, cols, nb = 300, 391, 5
+    rng = np.random.default_rng(5)
+    tabs = np.stack([np.broadcast_to(gen.rotated_fd(1, th, eps, h=1.0 / (cols + 1))[0, 0], (25, 3, 3))
+                     for th, eps in zip(rng.uniform(0, math.pi, nb), 10.0 ** rng.uniform(-3, 0, nb))])
+    h = mg.equip_inferred(mg.build_hierarchy_classed(rows, cols, tabs, gen.levels_for(rows)), net_of("conv"))
+    h.set_passes(0, 1)
+    f = dv.to_dev(rng.uniform(-1, 1, (nb, rows, cols)))
+    out = []
+    for kind in (2, 3):
+        h.set_stream_kernel(kind)
+        if kind == 3:
+            assert "k_stream3" in h.pass_kernel(0, 1) and "k_stream2" in h.pass_kernel(0, 2)
+            assert "k_stream2" in h.pass_kernel(1, 1)      # Galerkin levels of a batch: column pairs
+        u = dv.zeros(f.shape)
+        hh = h.run_cycles(f, u, 3, 1, 1, u_zero=True)
+        u2 = u.clone()
+        hw = h.run_cycles(f, u2, 2, 1, 1, u_zero=False)
+        out.append((u, dv.host(hh), u2, dv.host(hw)))
+    h.set_stream_kernel(0)
+    (ua, ha, wa, hwa), (ub, hb, wb, hwb) = out
+    assert t.equal(ua, ub), float((ua - ub).abs().max())
+    assert t.equal(wa, wb), float((wa - wb).abs().max())
+    assert np.allclose(ha, hb, rtol=1e-13, atol=0) and np.allclose(hwa, hwb, rtol=1e-13, atol=0)
+
+
 def test_warp_strip_kernel_full_size_c2():
     """Config 2 at 4095^2 (uniform level 0, non-uniform levels 1-2): the warp-strip
     kernel equals the column-pair kernel bitwise over 3 V(2,2) cycles."""
