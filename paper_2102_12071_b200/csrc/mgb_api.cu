@@ -188,6 +188,9 @@ struct mgb_work {
   // enqueued (stream_args / vcycle_rec then address level 0 through them)
   double *pf0 = nullptr, *pu0 = nullptr, *pt0 = nullptr;
   bool pad0 = false;
+  // padded buffers of the levels >= 1 that a warp-strip parent feeds (level_padded): f, u and the
+  // ping-pong partner; vcycle_rec / stream_args recognise them by address
+  std::vector<double*> pf, pu, pt;
   double* plain_out = nullptr;   // while enqueuing the last cycle of a padded run_cycles solve: the caller's u
   std::vector<GraphEntry> graphs;
   int graph_version = -1;   // hierarchy version the cached graphs were captured against
@@ -213,6 +216,13 @@ struct mgb_work {
         dfree(base);
         *p = nullptr;
       }
+    for (auto* vec : {&pf, &pu, &pt})
+      for (size_t l = 0; l < vec->size(); ++l)
+        if ((*vec)[l]) {
+          double* base = (*vec)[l] - pad_offset(h->lv[l].cols);
+          dfree(base);
+          (*vec)[l] = nullptr;
+        }
     if (hist_pinned) cudaFreeHost(hist_pinned);
     for (int b = 0; b < 2; ++b)
       for (cudaEvent_t e : {ev_in[b], ev_done[b], ev_out[b]})
@@ -1368,7 +1378,7 @@ static StreamArgs stream_args(const mgb_work* w, int l, const double* f, cudaStr
   a.uniform = lv.uniformity();
   a.kernel = h->stream_kernel;
   a.a5 = lv.a5 && !lv.Acls;
-  if (l == 0 && w->pad0) {
+  if ((l == 0 && w->pad0) || (l > 0 && f && l < (int)w->pf.size() && w->pf[l] && f == w->pf[l])) {
     a.ld = pad_pitch(lv.cols);
     a.padded = 1;
   }
@@ -1398,7 +1408,7 @@ static bool pre_gives_fnorm(const mgb_hier* h, int nu1, int nu2) {
 // into w->f[l+1].  in == null: zero initial guess.  *cur / *oth: ping-pong buffers
 // (the result ends in *cur).  hist != null: relative residual of the input.
 static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, double** cur, double** oth, int nu1,
-                       double* hist, int64_t hstride, cudaStream_t s) {
+                       double* hist, int64_t hstride, cudaStream_t s, bool child_padded = false) {
   const mgb_hier* h = w->h;
   StreamArgs a = stream_args(w, l, f, s);
   const bool split = h->fused == 1;
@@ -1416,6 +1426,10 @@ static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, do
   a.u = in;
   a.uo = *oth;
   a.rc = w->f[l + 1];
+  if (child_padded) {   // the next level runs on its padded buffers (level_padded)
+    a.rc = w->pf[l + 1];
+    a.ldc = pad_pitch(h->lv[l + 1].cols);
+  }
   a.partials = hist ? w->partials : nullptr;
   MGB_CUDA_TRY(launch_pass(h, l, a, split ? 1 : nu1, true, false, hist != nullptr, &nb));
   if (hist) MGB_CUDA_TRY(finalize_pre(w, nb, in == nullptr, hist, hstride, s));
@@ -1425,9 +1439,10 @@ static int enqueue_pre(mgb_work* w, int l, const double* f, const double* in, do
 
 // POST on level l: u <- u + P ec, then nu2 sweeps (result ends in *cur)
 static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, double** cur, double** oth, int nu2,
-                        cudaStream_t s, double* out_hist = nullptr, int64_t out_stride = 0) {
+                        cudaStream_t s, double* out_hist = nullptr, int64_t out_stride = 0, bool child_padded = false) {
   const mgb_hier* h = w->h;
   StreamArgs a = stream_args(w, l, f, s);
+  if (child_padded) a.ldc = pad_pitch(h->lv[l + 1].cols);
   const bool split = h->fused == 1;
   int nb = 0;
   a.u = *cur;
@@ -1465,6 +1480,7 @@ static int enqueue_post(mgb_work* w, int l, const double* f, const double* ec, d
 // out_hist != null (level 0, post_norm_ok): the relative residual of the cycle's OUTPUT is
 // written there by the level's POST pass.
 static bool post_norm_ok(const mgb_work* w, int nu1, int nu2);
+static bool level_padded(const mgb_hier* h, int l, int nu1, int nu2);
 
 static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero, int nu1, int nu2,
                       cudaStream_t s, double** result, double* hist = nullptr, int64_t hstride = 0,
@@ -1484,15 +1500,20 @@ static int vcycle_rec(mgb_work* w, int l, const double* f, double* u, bool zero,
     return MGB_OK;
   }
   double* cur = u;
-  double* oth = (l == 0 && w->pad0) ? w->pt0 : w->t[l];
+  const bool padl = l > 0 && l < (int)w->pf.size() && w->pf[l] && f == w->pf[l];   // this level on its padded buffers
+  double* oth = (l == 0 && w->pad0) ? w->pt0 : (padl ? w->pt[l] : w->t[l]);
   const Grid g = h->grid(l);
   const bool fuse_norm = hist && nu1 > 0 && lv.ks == 1;
   if (use_stream(h, l, nu1, nu2)) {
-    if (int st = enqueue_pre(w, l, f, zero ? nullptr : cur, &cur, &oth, nu1, fuse_norm ? hist : nullptr, hstride, s))
+    // the next level's buffers: padded when both levels run warp-strip passes
+    const bool cp = level_padded(h, l + 1, nu1, nu2) && l + 1 < (int)w->pf.size() && w->pf[l + 1];
+    if (int st = enqueue_pre(w, l, f, zero ? nullptr : cur, &cur, &oth, nu1, fuse_norm ? hist : nullptr, hstride, s, cp))
       return st;
     double* ec = nullptr;
-    if (int st = vcycle_rec(w, l + 1, w->f[l + 1], w->u[l + 1], true, nu1, nu2, s, &ec)) return st;
-    if (int st = enqueue_post(w, l, f, ec, &cur, &oth, nu2, s, l == 0 ? out_hist : nullptr, out_stride)) return st;
+    if (int st = vcycle_rec(w, l + 1, cp ? w->pf[l + 1] : w->f[l + 1], cp ? w->pu[l + 1] : w->u[l + 1], true, nu1,
+                            nu2, s, &ec))
+      return st;
+    if (int st = enqueue_post(w, l, f, ec, &cur, &oth, nu2, s, l == 0 ? out_hist : nullptr, out_stride, cp)) return st;
     *result = cur;
     return MGB_OK;
   }
@@ -1543,10 +1564,52 @@ static int enqueue_vcycle(mgb_work* w, int l, const double* f, double* u, int nu
 // Level 0 of a run_cycles solve runs on padded copies when its passes are the
 // warp-strip kernel's (single problem, uniform band classes, streamed, fused).
 static bool level0_padded(const mgb_hier* h, int nu1, int nu2) {
+  static const bool off = getenv("MGB_NO_PAD0") && atoi(getenv("MGB_NO_PAD0")) != 0;   // A/B experiments
+  if (off) return false;
   const LevelD& l0 = h->lv[0];
   return h->batch == 1 && h->depth() > 1 && pass_kind(h, 0, nu1, nu2) == 1 && l0.ks == 1 && l0.Acls && l0.Kcls &&
          !l0.mask && l0.conv.nl == 0 && l0.uniform() &&
          warp_strip_selected(h->stream_kernel, l0.n, h->batch, true);
+}
+
+// Level l >= 1 runs on padded buffers (16-byte aligned pitch, zero margins: the warp-strip
+// kernel's aligned path, as level 0 of a run_cycles solve) when it and its parent level both
+// run fused warp-strip passes: the parent's PRE pass restricts straight into the padded f and
+// its POST pass prolongs from the padded u (StreamArgs::ldc), so no staging copy exists.
+static bool level_padded(const mgb_hier* h, int l, int nu1, int nu2) {
+  static const bool off = getenv("MGB_NO_PADL") && atoi(getenv("MGB_NO_PADL")) != 0;   // A/B experiments
+  if (off || l < 1 || l + 1 >= h->depth() || h->batch != 1 || h->fused != 2 || l == coarse_first_level(h)) return false;
+  for (int q = l - 1; q <= l; ++q) {
+    const LevelD& lv = h->lv[q];
+    if (pass_kind(h, q, nu1, nu2) != 1 || lv.ks != 1 || !lv.Acls || !lv.Kcls || lv.mask || lv.conv.nl != 0) return false;
+    const int uni = lv.uniformity();
+    if (uni == 0 || (uni == 2 && lv.cols <= 128)) return false;   // generic flavour: no aligned path
+    if (!warp_strip_selected(h->stream_kernel, lv.n, h->batch, true)) return false;
+  }
+  return true;
+}
+
+static int ensure_padl(mgb_work* w) {
+  const mgb_hier* h = w->h;
+  const int L = h->depth();
+  if ((int)w->pf.size() != L) {
+    w->pf.assign(L, nullptr);
+    w->pu.assign(L, nullptr);
+    w->pt.assign(L, nullptr);
+  }
+  for (int l = 1; l + 1 < L; ++l) {
+    if (!w->t[l] || !w->t[l - 1]) continue;   // a workspace that starts below this level's parent (work_create_from)
+    if (!(level_padded(h, l, 2, 2) || level_padded(h, l, 1, 1))) continue;
+    for (std::vector<double*>* vec : {&w->pf, &w->pu, &w->pt}) {
+      if ((*vec)[l]) continue;
+      double* base = nullptr;
+      const size_t cnt = (size_t)pad_elems(h->lv[l].rows, h->lv[l].cols);
+      MGB_CUDA_TRY(dalloc(&base, cnt));
+      MGB_CUDA_TRY(cudaMemset(base, 0, sizeof(double) * cnt));
+      (*vec)[l] = base + pad_offset(h->lv[l].cols);
+    }
+  }
+  return MGB_OK;
 }
 
 // The level-0 POST pass can carry the residual norm of its output: fused passes (not one
@@ -1649,6 +1712,7 @@ static int coarse_first_level(const mgb_hier* h);
 int prepare_work(mgb_work* w) {
   if (level0_padded(w->h, 2, 2) || level0_padded(w->h, 1, 1))
     if (int st = ensure_pad0(w)) return st;
+  if (int st = ensure_padl(w)) return st;
   for (int l = 0; l + 1 < w->h->depth(); ++l)
     if (w->h->lv[l].ks > 1 || w->h->lv[l].conv.nl > 0)
       if (int st = ensure_generic(w, l)) return st;

@@ -39,6 +39,8 @@ struct StreamArgs {
   // PAD_ROWS rows and PAD_LCOLS / >= 122 columns around the grid, margins never written)
   int64_t ld;
   int padded;
+  int64_t ldc;             // > 0: row pitch of the coarse arrays rc (PRE) and ec (POST): the next level's padded
+                           // buffers (warp-strip kernel only; 0: cols / 2)
   int64_t ld_out;          // > 0: uo is a dense array of this pitch (the caller's own u) although f and u use
                            // the padded layout: the last POST pass of a solve writes its result there directly
   double ci[18];           // interior-class A (9) and M (9) weights, read from the constant bank

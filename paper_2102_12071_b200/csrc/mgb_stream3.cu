@@ -157,6 +157,7 @@ struct Lane3 {
   int lane, c0, R0, R1;
   int64_t ld;          // row pitch of f, u, uo
   int64_t ldo;         // row pitch of uo when it is a dense array beside padded inputs (0: ld)
+  int64_t ldc;         // row pitch of the coarse arrays rc / ec (cols / 2, or the next level's padded pitch)
   int64_t boffc;       // batched levels: the problem's offset into the coarse arrays rc / ec (0: one problem)
   const double* wci;   // interior-class A (9) and M (9) weights: a.ci (constant bank), or the problem's own in
                        // registers (batched uniform levels)
@@ -177,7 +178,7 @@ __device__ __forceinline__ void load_e3(const StreamArgs& a, const Lane3& L, int
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     const int cj = L.mcol + q;
-    dst[q] = (rv && (unsigned)cj < (unsigned)cols_c) ? __ldg(a.ec + L.boffc + (int64_t)ci * cols_c + cj) : 0.0;
+    dst[q] = (rv && (unsigned)cj < (unsigned)cols_c) ? __ldg(a.ec + L.boffc + (int64_t)ci * L.ldc + cj) : 0.0;
   }
 }
 
@@ -470,7 +471,7 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         const int rows_c = g.rows / 2, cols_c = g.cols / 2;
         if (MODE == 0 || (y >= 2 && ci >= (L.R0 >> 1) && 2 * ci + 1 < L.R1 && ci < rows_c)) {
           const int cj = L.c0 >> 1;
-          double* dst = a.rc + L.boffc + (int64_t)ci * cols_c + cj;
+          double* dst = a.rc + L.boffc + (int64_t)ci * L.ldc + cj;
           if ((L.own & 1) && cj < cols_c) {
             const bool act = a.mask_c == nullptr || a.mask_c[(int64_t)ci * cols_c + cj];
             dst[0] = act ? sA : 0.0;
@@ -570,6 +571,7 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   L.ld = a.ld > 0 ? a.ld : g.cols;
   L.ldo = ALN && a.ld_out > 0 ? a.ld_out : 0;
   L.boffc = BAT ? (int64_t)bprob * (g.rows / 2) * (g.cols / 2) : 0;
+  L.ldc = a.ldc > 0 ? a.ldc : g.cols / 2;
   double wreg[18];
   if (BAT) {
 #pragma unroll
@@ -882,7 +884,8 @@ cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool no
 #define MGB_ST3(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                                \
   MGB_ST3B(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                                     \
   if (nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_)    \
-    return quasi           ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 2, false, false>(a, nblocks) \
+    return quasi           ? (a.padded ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 2, false, true>(a, nblocks)   \
+                                       : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 2, false, false>(a, nblocks)) \
            : a.uniform != 1 ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 0, false, false>(a, nblocks) \
            : !a.padded ? (za ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, true, false>(a, nblocks)  \
                              : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, false>(a, nblocks)) \
