@@ -1,7 +1,8 @@
 """Small solves that drive every cycle kernel family once (for compute-sanitizer):
 k_stream / k_stream2 / k_stream3 (forced on every level), k_tile, the single-CTA coarse
-kernel, per-point planes, a masked domain, the batched hierarchy, and the padded level-0
-path of run_cycles.  Prints the final relative residuals (must be finite)."""
+kernel, per-point planes, a masked domain, the batched hierarchy (column pairs and the
+warp-strip kernel's batched flavour), the padded level-0 path of run_cycles and the padded
+quasi-uniform levels below it.  Prints the final relative residuals (must be finite)."""
 import math, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -83,6 +84,20 @@ eps, theta = gen.batch_parameters(3, seed=3)
 Ab = np.stack([gen.rotated_fd(n, theta[i], eps[i]) for i in range(3)])
 hb = mg.equip_inferred(mg.build_hierarchy_batch(Ab, lv), net)
 run("batch of 3, V(1,1)", hb, np.stack([gen.uniform_rhs(n, [4, i]) for i in range(3)]), nu=1)
+hb.set_stream_kernel(3)               # the warp-strip kernel's batched flavour on the uniform level 0
+hb.set_passes(1, 1, 0)
+run("batch of 3, V(1,1), warp strips", hb, np.stack([gen.uniform_rhs(n, [4, i]) for i in range(3)]), nu=1)
+# quasi-uniform Galerkin levels wider than one strip: the padded buffers below level 0 (a warp-strip
+# parent restricting into / prolonging from them) and the aligned quasi-uniform flavour
+if n >= 255:
+    m = 2 * n + 1
+    hq = mg.equip_inferred(mg.build_hierarchy(mg.StencilField(mg.full_spec(m), gen.rotated_fd(m, math.pi / 5, 0.02)),
+                                              gen.levels_for(m)), net)
+    hq.set_stream_kernel(3)
+    hq.set_passes(1, 1, 0)
+    assert hq.level_uniformity(0) == 1 and hq.level_uniformity(1) == 2
+    run(f"warp strips, {m}^2, padded levels", hq, gen.uniform_rhs(m, 6))
+    run(f"warp strips, {m}^2, V(1,1)", hq, gen.uniform_rhs(m, 7), nu=1, cycles=3)
 if "--guard" in sys.argv:
     import ctypes as C
     from paper_2102_12071_b200 import _lib
