@@ -79,18 +79,21 @@ struct LevelD {
   // and for the steps that touch the first / last row.
   bool quasi_uniform() const {
     static const bool off = getenv("MGB_NO_QUASI") && atoi(getenv("MGB_NO_QUASI")) != 0;   // A/B experiments
-    if (off || hAcls.size() != 225 || hKcls.size() != 225 || cols % 2 == 0 || cols < 8 || rows < 8) return false;
-    for (int bi = 0; bi < 5; ++bi)
-      for (int bj = 0; bj < 5; ++bj) {
-        const int qi = bi == 1 || bi == 3 ? 2 : bi, qj = bj == 1 || bj == 3 ? 2 : bj;
-        for (int o = 0; o < 9; ++o) {
-          const int di = o / 3 - 1, dj = o % 3 - 1;
-          const bool outside = (bi == 0 && di < 0) || (bi == 4 && di > 0) || (bj == 0 && dj < 0) || (bj == 4 && dj > 0);
-          const double av = hAcls[(bi * 5 + bj) * 9 + o];
-          if (!std::isfinite(av) || (!outside && av != hAint()[o])) return false;
-          if (hKcls[(bi * 5 + bj) * 9 + o] != hKcls[(qi * 5 + qj) * 9 + o]) return false;
+    if (off || hAcls.size() != hKcls.size() || hAcls.size() % 225 != 0 || hAcls.empty() || cols % 2 == 0 || cols < 8 ||
+        rows < 8)
+      return false;
+    for (size_t pb = 0; pb < hAcls.size(); pb += 225)   // every problem of a batch
+      for (int bi = 0; bi < 5; ++bi)
+        for (int bj = 0; bj < 5; ++bj) {
+          const int qi = bi == 1 || bi == 3 ? 2 : bi, qj = bj == 1 || bj == 3 ? 2 : bj;
+          for (int o = 0; o < 9; ++o) {
+            const int di = o / 3 - 1, dj = o % 3 - 1;
+            const bool outside = (bi == 0 && di < 0) || (bi == 4 && di > 0) || (bj == 0 && dj < 0) || (bj == 4 && dj > 0);
+            const double av = hAcls[pb + (bi * 5 + bj) * 9 + o];
+            if (!std::isfinite(av) || (!outside && av != hAcls[pb + 12 * 9 + o])) return false;
+            if (hKcls[pb + (bi * 5 + bj) * 9 + o] != hKcls[pb + (qi * 5 + qj) * 9 + o]) return false;
+          }
         }
-      }
     return true;
   }
   // StreamArgs::kq: the smoother's class tables of the row / column bands {first, interior, last}
@@ -774,7 +777,7 @@ extern "C" int mgb_hier_stencil_points(const mgb_hier* h, int level, int* a_poin
 extern "C" int mgb_hier_level_uniformity(const mgb_hier* h, int level, int* uniformity) {
   if (!h || !uniformity) return fail(MGB_CONTRACT, "null argument");
   if (level < 0 || level >= h->depth()) return fail(MGB_CONFIG, "level out of range");
-  *uniformity = h->batch == 1 ? h->lv[level].uniformity() : 0;
+  *uniformity = h->lv[level].uniformity();
   return MGB_OK;
 }
 

@@ -159,6 +159,8 @@ struct Lane3 {
   int64_t ldo;         // row pitch of uo when it is a dense array beside padded inputs (0: ld)
   int64_t ldc;         // row pitch of the coarse arrays rc / ec (cols / 2, or the next level's padded pitch)
   int64_t boffc;       // batched levels: the problem's offset into the coarse arrays rc / ec (0: one problem)
+  const double* kq;    // quasi-uniform levels: the nine M class tables (a.kq in the constant bank; a batch: the
+                       // problem's own, in shared memory)
   const double* wci;   // interior-class A (9) and M (9) weights: a.ci (constant bank), or the problem's own in
                        // registers (batched uniform levels)
   unsigned cin, own;   // bit c: column c0 + c in the grid / owned
@@ -326,9 +328,9 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
             wN[c] = wM[c] = wB[c] = resid ? L.wci : L.wci + 9;
           } else if (MODE == 5) {
             // the row band's table of the interior column band (bands 1 and 3 equal band 2)
-            wN[c] = a.kq + ((bN == 0 ? 0 : bN == 4 ? 2 : 1) * 3 + 1) * 9;
-            wM[c] = a.kq + ((bM == 0 ? 0 : bM == 4 ? 2 : 1) * 3 + 1) * 9;
-            wB[c] = a.kq + ((bB == 0 ? 0 : bB == 4 ? 2 : 1) * 3 + 1) * 9;
+            wN[c] = L.kq + ((bN == 0 ? 0 : bN == 4 ? 2 : 1) * 3 + 1) * 9;
+            wM[c] = L.kq + ((bM == 0 ? 0 : bM == 4 ? 2 : 1) * 3 + 1) * 9;
+            wB[c] = L.kq + ((bB == 0 ? 0 : bB == 4 ? 2 : 1) * 3 + 1) * 9;
           } else if (MODE == 2) {
             wN[c] = wM[c] = wB[c] = tabk + (10 + L.cb[c]) * 9;
           } else {
@@ -345,9 +347,9 @@ __device__ __forceinline__ void step3(const StreamArgs& a, const Lane3& L, const
         if (EFIX && !resid && (MODE == 4 || L.eside >= 0)) {
           const bool e2 = L.ecol == 2;
           // the boundary column's class per row role (interior rows: one table)
-          const double* weN = a.kq + ((MODE == 4 ? 1 : (bN == 0 ? 0 : bN == 4 ? 2 : 1)) * 3 + L.eside) * 9;
-          const double* weM = MODE == 4 ? weN : a.kq + ((bM == 0 ? 0 : bM == 4 ? 2 : 1) * 3 + L.eside) * 9;
-          const double* weB = MODE == 4 ? weN : a.kq + ((bB == 0 ? 0 : bB == 4 ? 2 : 1) * 3 + L.eside) * 9;
+          const double* weN = L.kq + ((MODE == 4 ? 1 : (bN == 0 ? 0 : bN == 4 ? 2 : 1)) * 3 + L.eside) * 9;
+          const double* weM = MODE == 4 ? weN : L.kq + ((bM == 0 ? 0 : bM == 4 ? 2 : 1) * 3 + L.eside) * 9;
+          const double* weB = MODE == 4 ? weN : L.kq + ((bB == 0 ? 0 : bB == 4 ? 2 : 1) * 3 + L.eside) * 9;
           double xe[3];
 #pragma unroll
           for (int q = 0; q < 3; ++q) xe[q] = e2 ? in[2 + q] : in[q];
@@ -524,7 +526,8 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
   const int nitems = BAT ? nitems1 * a.g.batch : nitems1;
   if (WPC3 > 1 && item >= nitems) return;
   const int bprob = BAT ? item / nitems1 : 0;
-  double* ringF = sm3 + (size_t)wib * (RF3 * SW3 + (ZU ? 0 : RU3 * SW3) + (UNI != 0 ? 0 : 2 * NCLS3 * 9));  // RF3 x SW3
+  double* ringF = sm3 + (size_t)wib * (RF3 * SW3 + (ZU ? 0 : RU3 * SW3) + (UNI != 0 ? 0 : 2 * NCLS3 * 9) +
+                                       (BAT && UNI == 2 ? 82 : 0));  // RF3 x SW3
   double* ringU = ringF + RF3 * SW3;         // RU3 x SW3 (unused when ZU)
   double* tab = ringU + (ZU ? 0 : RU3 * SW3);  // 2 x 25 x 9 class tables (non-uniform levels)
   const Grid& g = a.g;
@@ -581,6 +584,17 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
     }
   }
   L.wci = BAT ? wreg : a.ci;
+  L.kq = a.kq;
+  if (BAT && UNI == 2) {
+    // the problem's class tables of the row / column bands {first, interior, last} (StreamArgs::kq's layout)
+    double* kqs = ringU + (ZU ? 0 : RU3 * SW3);
+    for (int q = L.lane; q < 81; q += 32) {
+      const int cls = q / 9, o = q - 9 * cls, r = cls / 3, c = cls - 3 * r;
+      kqs[q] = __ldg(a.K.cls + (int64_t)bprob * NCLS3 * 9 + ((2 * r) * 5 + 2 * c) * 9 + o);
+    }
+    __syncwarp();
+    L.kq = kqs;
+  }
   const bool strip_int = j0 - H >= 2 && j0 - H + SW3 - 1 <= g.cols - 3;
   if (UNI == 0) {
     for (int q = L.lane; q < 2 * NCLS3 * 9; q += 32)
@@ -755,8 +769,8 @@ __global__ void __launch_bounds__(32 * WPC3, MGB_S3MINB / WPC3) k_stream3(Stream
 
 }  // namespace
 
-static size_t stream3_smem(bool zu, int uni) {
-  return sizeof(double) * ((size_t)(RF3 + (zu ? 0 : RU3)) * SW3 + (uni != 0 ? 0 : 2 * NCLS3 * 9));
+static size_t stream3_smem(bool zu, int uni, bool bat) {
+  return sizeof(double) * ((size_t)(RF3 + (zu ? 0 : RU3)) * SW3 + (uni != 0 ? 0 : 2 * NCLS3 * 9) + (bat && uni == 2 ? 82 : 0));
 }
 
 static int sm_count3() {
@@ -820,7 +834,7 @@ static cudaError_t run_k3(StreamArgs a, int* nblocks) {
   static thread_local std::vector<Occ> occ_cache;   // per instantiation, per device
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
-  const size_t smem = WPC3 * stream3_smem(ZU, UNI);
+  const size_t smem = WPC3 * stream3_smem(ZU, UNI, BAT);
   int occ = -1;
   for (auto& e : occ_cache)
     if (e.dev == dev) occ = e.occ;
@@ -856,7 +870,8 @@ cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool no
 #if MGB_S3_PART == 1
 bool stream3_ok(const StreamArgs& a, int nsw) {
   const bool tabs = a.mask == nullptr && a.A.cls != nullptr && a.K.cls != nullptr && a.A.ks == 1 && a.K.ks == 1;
-  if (a.g.batch > 1) return tabs && a.uniform == 1 && nsw == 1 && !a.padded && a.own1 <= 0;   // the batched flavour
+  if (a.g.batch > 1)   // the batched flavours: uniform, or quasi-uniform with the first and last strip distinct
+    return tabs && (a.uniform == 1 || (a.uniform == 2 && a.g.cols > SW3)) && nsw == 1 && !a.padded && a.own1 <= 0;
   return tabs && a.ci_valid;
 }
 #endif
@@ -877,7 +892,8 @@ cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool no
 #if MGB_S3_PART == 1
 #define MGB_ST3B(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                              \
   if (a.g.batch > 1 && nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_) \
-    return run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, false, true>(a, nblocks);
+    return a.uniform == 2 ? run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 2, false, false, true>(a, nblocks) \
+                          : run_k3<NSW_, RES_, PRO_, NORM_, ZU_, NOUT_, 1, false, false, true>(a, nblocks);
 #else
 #define MGB_ST3B(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)
 #endif

@@ -689,12 +689,12 @@ def test_default_path_padded_level0_direct_output(rows, cols, nu, cycles, net):
 
 def test_warp_strip_kernel_batched_uniform_level():
     """Config 4's path: a batch of constant-coefficient problems, V(1,1).  Level 0 (uniform per
-    problem) runs the warp-strip kernel's batched flavour — work items (problem, strip, segment),
+    problem) and level 1 (quasi-uniform per problem) run the warp-strip kernel's batched flavours — work items (problem, strip, segment),
     the problem's interior weights in registers — against the column-pair kernel: u bitwise
     equal for every problem, histories to summation order; V(2,2) stays on column pairs."""
     from paper_2102_12071_b200 import device as dv
     t = dv.torch()
-    rows, cols, nb = 300, 391, 5
+    rows, cols, nb = 303, 391, 5
     rng = np.random.default_rng(5)
     tabs = np.stack([np.broadcast_to(gen.rotated_fd(1, th, eps, h=1.0 / (cols + 1))[0, 0], (25, 3, 3))
                      for th, eps in zip(rng.uniform(0, math.pi, nb), 10.0 ** rng.uniform(-3, 0, nb))])
@@ -706,7 +706,11 @@ def test_warp_strip_kernel_batched_uniform_level():
         h.set_stream_kernel(kind)
         if kind == 3:
             assert "k_stream3" in h.pass_kernel(0, 1) and "k_stream2" in h.pass_kernel(0, 2)
-            assert "k_stream2" in h.pass_kernel(1, 1)      # Galerkin levels of a batch: column pairs
+            # the batch's first Galerkin level (151 x 195: quasi-uniform per problem, two strips): the
+            # batched quasi-uniform flavour, class tables per problem in shared memory; the next one
+            # (75 x 97: one strip) stays on column pairs
+            assert [h.level_uniformity(l) for l in range(3)] == [1, 2, 2]
+            assert "k_stream3" in h.pass_kernel(1, 1) and "k_stream2" in h.pass_kernel(2, 1)
         u = dv.zeros(f.shape)
         hh = h.run_cycles(f, u, 3, 1, 1, u_zero=True)
         u2 = u.clone()
