@@ -1586,7 +1586,7 @@ static bool level_padded(const mgb_hier* h, int l, int nu1, int nu2) {
     const LevelD& lv = h->lv[q];
     if (pass_kind(h, q, nu1, nu2) != 1 || lv.ks != 1 || !lv.Acls || !lv.Kcls || lv.mask || lv.conv.nl != 0) return false;
     const int uni = lv.uniformity();
-    if (uni == 0 || (uni == 2 && lv.cols <= 128)) return false;   // generic flavour: no aligned path
+    if (uni == 0 || (uni == 2 && !quasi_cols_ok(lv.cols))) return false;   // generic flavour: no aligned path
     if (!warp_strip_selected(h->stream_kernel, lv.n, h->batch, true)) return false;
   }
   return true;

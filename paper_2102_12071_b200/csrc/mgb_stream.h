@@ -76,6 +76,9 @@ cudaError_t launch_stream2(const StreamArgs& a, int nsw, bool res, bool pro, boo
 // (and for kernel == 0 on large levels, see launch_stream).
 // (nsw: sweeps per pass; a batch of problems runs there only on a uniform level with nsw == 1)
 bool stream3_ok(const StreamArgs& a, int nsw = 0);
+// quasi-uniform flavour: the grid's first and last column must lie in different strips of
+// every pass (a strip owns at most 124 columns)
+inline bool quasi_cols_ok(int cols) { return cols > 124; }
 bool warp_strip_selected(int kernel, int64_t n, int batch, bool uniform, int nsw = 0);
 cudaError_t launch_stream3(const StreamArgs& a, int nsw, bool res, bool pro, bool norm, int* nblocks);
 

@@ -871,7 +871,7 @@ cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool no
 bool stream3_ok(const StreamArgs& a, int nsw) {
   const bool tabs = a.mask == nullptr && a.A.cls != nullptr && a.K.cls != nullptr && a.A.ks == 1 && a.K.ks == 1;
   if (a.g.batch > 1)   // the batched flavours: uniform, or quasi-uniform with the first and last strip distinct
-    return tabs && (a.uniform == 1 || (a.uniform == 2 && a.g.cols > SW3)) && nsw == 1 && !a.padded && a.own1 <= 0;
+    return tabs && (a.uniform == 1 || (a.uniform == 2 && quasi_cols_ok(a.g.cols))) && nsw == 1 && !a.padded && a.own1 <= 0;
   return tabs && a.ci_valid;
 }
 #endif
@@ -888,7 +888,7 @@ cudaError_t launch_stream3_nsw2(const StreamArgs& a, bool res, bool pro, bool no
   static const bool no_za = getenv("MGB_NO_ZA") && atoi(getenv("MGB_NO_ZA")) != 0;   // A/B experiments
   const bool za = !no_za && a.ci[2] == 0.0 && a.ci[6] == 0.0;   // uniform: every class is the interior one
   // quasi-uniform flavour: the first and the last strip must be different strips
-  const bool quasi = a.uniform == 2 && a.g.cols > SW3;
+  const bool quasi = a.uniform == 2 && quasi_cols_ok(a.g.cols);
 #if MGB_S3_PART == 1
 #define MGB_ST3B(NSW_, RES_, PRO_, NORM_, ZU_, NOUT_)                                              \
   if (a.g.batch > 1 && nsw == NSW_ && res == RES_ && pro == PRO_ && norm == NORM_ && zu == ZU_ && nout == NOUT_) \
